@@ -1,0 +1,160 @@
+/*
+ * diffreg.h -- C ABI of the B200 Gauss-Newton Hessian-matvec library (paper_1608_03630_b200).
+ *
+ * The library implements the data-parallel hot path of the Gauss-Newton-Krylov diffeomorphic
+ * registration solver of arXiv 1608.03630 ("the paper"; citations "P:Lnnn" are lines of
+ * /root/reference/PAPER.md with the section / equation they fall in):
+ *
+ *   - RK2 semi-Lagrangian departure points along the characteristics of +v and -v
+ *     (Eq. 6), computed once per velocity;
+ *   - tricubic (cubic Lagrange, 4x4x4 stencil) interpolation at those points;
+ *   - the state / adjoint / incremental-state / incremental-adjoint transport solves
+ *     (Eq. 2b-c, Eq. 3, Eqs. 5a-5d; Eq. 7; Algorithm 2);
+ *   - FFT spectral operators: gradient, divergence, regularisation beta*A with A = Laplacian^2
+ *     (H2) or -Laplacian (H1), its inverse as preconditioner, and the Leray
+ *     projection for the isochoric variant;
+ *   - the Gauss-Newton Hessian matvec H(v) vt = beta A vt + P b~ (Eq. 5e).
+ *
+ * The exact discrete operator every call computes is SURVEY.md §8(c) D0-D14 (listed in DESIGN.md);
+ * an fp64 CPU oracle under oracle/ computes the same quantities for the parity tests.
+ *
+ * DATA LAYOUT (all calls).  Grid n = (N1, N2, N3), periodic on [0, 2pi)^3, x_a = 2 pi i_a / N_a.
+ *   scalar field : N3*N2*N1 values, index i1 + N1*(i2 + N2*i3)  (x1 fastest)
+ *   vector field : 3 consecutive scalar fields (SoA): component a at offset a*N1*N2*N3
+ *   value type   : float, or double when the context was created with DR_FP64.
+ * GPU grid restriction (this build): every N_a is a power of two in [4, 1024].
+ *
+ * POINTERS.  Every field pointer of the main path (set_images, set_velocity, forward_solve,
+ * adjoint_solve, hessian_matvec, precond_apply) may be a device pointer or a host pointer
+ * (pinned or pageable); the library detects which with cudaPointerGetAttributes.  Host inputs
+ * are copied into the workspace on the context stream; host outputs are copied back and the call
+ * synchronises the stream before it returns.  Device-pointer calls are asynchronous w.r.t. the
+ * host and ordered on the context stream (like cuBLAS).  The dr_op_* / dr_get_* test hooks take
+ * device pointers only.
+ *
+ * OWNERSHIP.  The caller owns every input, output and the workspace.  Inputs are only read;
+ * images and the velocity are copied into the workspace (retained).  Outputs are fully
+ * overwritten.  The library allocates no device memory after dr_create (and none at all when a
+ * workspace is passed in).
+ *
+ * ERRORS.  Every call returns a dr_status; no exception crosses the ABI.  On error, outputs are
+ * unspecified and dr_last_error(ctx) describes the failure.  Calls made out of order (e.g. a matvec
+ * before dr_forward_solve) return DR_ERR_ORDER.  A context is bound to one device and one stream
+ * and is not thread-safe.
+ */
+#ifndef DIFFREG_H
+#define DIFFREG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dr_status {
+    DR_OK = 0,
+    DR_ERR_ARG = 1,        /* NULL / aliasing / bad enum argument                                */
+    DR_ERR_GRID = 2,       /* N_a not a power of two in [4, 1024]                                */
+    DR_ERR_PARAM = 3,      /* beta <= 0, nt < 1 or nt > 64, reg not H1/H2                        */
+    DR_ERR_ORDER = 4,      /* call sequence violated (see each function)                         */
+    DR_ERR_CUDA = 5,       /* CUDA runtime error (message in dr_last_error)                      */
+    DR_ERR_NCCL = 6,       /* reserved: multi-GPU communicator error                             */
+    DR_ERR_OOM = 7,        /* workspace smaller than dr_workspace_bytes / cudaMalloc failed       */
+    DR_ERR_NONFINITE = 8,  /* reserved                                                           */
+    DR_ERR_PLAN = 9        /* reserved: scatter-plan capacity exceeded (multi-GPU)               */
+} dr_status;
+
+enum { DR_REG_H1 = 1,      /* A = -Laplacian   (H1 seminorm, beta/2 |grad v|^2), a(k) = |k|^2   */
+       DR_REG_H2 = 2 };    /* A = Laplacian^2  (H2 seminorm, beta/2 |Lap v|^2), |k|^4   */
+
+enum { DR_ISOCHORIC = 1u,  /* incompressible variant: v Leray-projected, P = Leray  */
+       DR_FP64 = 2u };     /* all fields are double instead of float                             */
+
+typedef struct dr_config {
+    int32_t n[3];   /* N1 (x1, fastest), N2, N3                                                   */
+    int32_t nt;     /* number of time steps n_t, dt = 1/n_t; 1 <= nt <= 64          */
+    int32_t reg;    /* DR_REG_H1 or DR_REG_H2                                                     */
+    uint32_t flags; /* DR_ISOCHORIC | DR_FP64                                                     */
+    double beta;    /* regularisation parameter beta > 0 (Eq. 2a)                      */
+} dr_config;
+
+typedef struct dr_ctx dr_ctx;
+
+/* Bytes of device workspace a context for cfg needs (0 if cfg is invalid). */
+size_t dr_workspace_bytes(const dr_config* cfg);
+
+/* Create a context on the current CUDA device.  workspace: device buffer of >= dr_workspace_bytes
+ * bytes, or NULL to let dr_create cudaMalloc it (freed by dr_destroy).  stream: a cudaStream_t
+ * (NULL = legacy default stream).  Errors: DR_ERR_ARG, DR_ERR_GRID, DR_ERR_PARAM, DR_ERR_OOM. */
+dr_status dr_create(const dr_config* cfg, void* workspace, size_t workspace_bytes, void* stream,
+                    dr_ctx** out);
+dr_status dr_destroy(dr_ctx* ctx);
+
+/* Template rho_T and reference rho_R images (scalar fields).  Copied.  Invalidates the
+ * adjoint solve (and the forward solve, whose initial condition is rho_T). */
+dr_status dr_set_images(dr_ctx* ctx, const void* rho_T, const void* rho_R);
+
+/* Velocity v (vector field, stationary).  Copied.  Isochoric contexts replace v by L v
+ * (P:L157).  Builds, once per velocity (the "interpolation planner"): the RK2
+ * departure displacements for +v and -v (Eq. 6), their per-tile gather plans, and (non-isochoric)
+ * div v and the adjoint multiplier m (Eq. 7 with f = nu div v).  Invalidates all solves. */
+dr_status dr_set_velocity(dr_ctx* ctx, const void* v);
+
+/* State solve (Eqs. 2b-2c): rho_0 = rho_T, rho_{j+1} = I[rho_j](X+), all n_t+1 slices
+ * kept, plus the state gradients grad rho_j cached for the matvec.  rho1_out (nullable) receives
+ * rho(1) = rho_{n_t}.  Requires dr_set_images and dr_set_velocity, else DR_ERR_ORDER. */
+dr_status dr_forward_solve(dr_ctx* ctx, void* rho1_out);
+
+/* Adjoint solve (Eq. 3): lambda(1) = rho_R - rho(1), transported backward with -v
+ * (P:L275); lambda0_out (nullable) receives lambda(0).  Requires dr_forward_solve. */
+dr_status dr_adjoint_solve(dr_ctx* ctx, void* lambda0_out);
+
+/* Gauss-Newton Hessian matvec Hvt = H(v) vt (Eqs. 5a-5e with the lambda terms
+ * dropped): incremental state forward (Algorithm 2), incremental adjoint backward,
+ * b~ = int lambda~ grad rho dt (trapezoid), Hvt = beta A vt + P b~.  vt, Hvt: vector fields,
+ * must not alias.  Requires dr_forward_solve. */
+dr_status dr_hessian_matvec(dr_ctx* ctx, const void* vt, void* Hvt);
+
+/* Spectral preconditioner z = (beta A)^{-1} r with a_hat(0) = 1, followed by the Leray
+ * projection in isochoric contexts.  r, z: vector fields, may alias.  Requires only the context. */
+dr_status dr_precond_apply(dr_ctx* ctx, const void* r, void* z);
+
+/* Wait for all work of the context; surfaces asynchronous CUDA errors. */
+dr_status dr_sync(dr_ctx* ctx);
+
+/* Human-readable description of the last error of ctx (owned by ctx, valid until the next call). */
+const char* dr_last_error(const dr_ctx* ctx);
+const char* dr_status_string(dr_status s);
+
+/* ---------------------------------------------------------------- per-operator test hooks
+ * Device pointers only.  They run the same kernels as the main path. */
+enum { DR_OP_GRAD = 0,    /* in: scalar   out: vector   grad f  (i k' per axis)       */
+       DR_OP_DIV = 1,     /* in: vector   out: scalar   div u                                  */
+       DR_OP_REG = 2,     /* in: vector   out: vector   beta A u                               */
+       DR_OP_PRECOND = 3, /* in: vector   out: vector   same as dr_precond_apply               */
+       DR_OP_LERAY = 4 }; /* in: vector   out: vector   L u = u - grad Lap^{-1} div u          */
+dr_status dr_op_spectral(dr_ctx* ctx, int op, const void* in, void* out);
+
+/* out[p] = I[f](s_p): tricubic interpolation of the scalar field f at npts points given
+ * in CELL coordinates s (x = h*s), laid out as s[0..npts) = s1, s[npts..2npts) = s2, then s3. */
+dr_status dr_op_interp(dr_ctx* ctx, const void* f, int64_t npts, const void* s, void* out);
+
+/* Copy of the departure displacement field d^sigma (sigma = +1 or -1), cell units: the departure
+ * point of node i is s_i = i - d_i.  Requires dr_set_velocity. */
+dr_status dr_get_departure(dr_ctx* ctx, int sigma, void* d_out);
+
+enum { DR_FIELD_STATE = 0,       /* scalar rho_j, j = 0..nt           (after forward_solve)    */
+       DR_FIELD_STATE_GRAD = 1,  /* vector grad rho_j, j = 0..nt      (after forward_solve)    */
+       DR_FIELD_ADJOINT = 2,     /* scalar lambda_j, j = 0..nt        (after adjoint_solve)    */
+       DR_FIELD_INC_STATE = 3,   /* scalar rho~(1), j ignored         (after hessian_matvec)   */
+       DR_FIELD_INC_ADJOINT = 4, /* scalar lambda~_j, j = 0..nt       (after hessian_matvec)   */
+       DR_FIELD_BTILDE = 5,      /* vector b~, j ignored              (after hessian_matvec)   */
+       DR_FIELD_MULTIPLIER = 6,  /* scalar m (1 when isochoric)       (after set_velocity)     */
+       DR_FIELD_VELOCITY = 7 };  /* vector v as used (projected if isochoric)                   */
+dr_status dr_get_field(dr_ctx* ctx, int which, int j, void* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIFFREG_H */

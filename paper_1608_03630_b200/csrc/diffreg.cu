@@ -1,0 +1,855 @@
+// diffreg.cu -- C-ABI implementation (include/diffreg.h) of the B200 Gauss-Newton Hessian matvec of
+// arXiv 1608.03630.  Host orchestration of the CUDA kernels in fft.cuh / sl.cuh / pointwise.cuh:
+// every step of the hot path runs in those kernels; this file only sizes the workspace, validates
+// arguments and call order, and launches.  See DESIGN.md for the data layout and the dataflow.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "diffreg.h"
+#include "common.cuh"
+#include "fft.cuh"
+#include "pointwise.cuh"
+#include "sl.cuh"
+
+using namespace dr;
+
+namespace {
+
+struct DrError {
+    dr_status s;
+    std::string msg;
+};
+
+[[noreturn]] void fail(dr_status s, const std::string& m) { throw DrError{s, m}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(DR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+#define CKL(name) ck(cudaGetLastError(), name)
+
+int ilog2(int n) {
+    int l = 0;
+    while ((1 << l) < n) ++l;
+    return l;
+}
+bool pow2_in_range(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
+
+dr_status validate(const dr_config* c) {
+    if (!c) return DR_ERR_ARG;
+    for (int a = 0; a < 3; ++a)
+        if (!pow2_in_range(c->n[a])) return DR_ERR_GRID;
+    if (c->nt < 1 || c->nt > 64) return DR_ERR_PARAM;
+    if (c->reg != DR_REG_H1 && c->reg != DR_REG_H2) return DR_ERR_PARAM;
+    if (!(c->beta > 0.0) || !std::isfinite(c->beta)) return DR_ERR_PARAM;
+    if (c->flags & ~(uint32_t)(DR_ISOCHORIC | DR_FP64)) return DR_ERR_PARAM;
+    return DR_OK;
+}
+
+Grid make_grid(const dr_config* c) {
+    Grid g;
+    g.n1 = c->n[0];
+    g.n2 = c->n[1];
+    g.n3 = c->n[2];
+    g.l1 = ilog2(g.n1);
+    g.l2 = ilog2(g.n2);
+    g.l3 = ilog2(g.n3);
+    g.M = (int64_t)g.n1 * g.n2 * g.n3;
+    g.n1c = g.n1 / 2 + 1;
+    g.n1p = ((g.n1c + 15) / 16) * 16;
+    g.S = (int64_t)g.n3 * g.n2 * g.n1p;
+    return g;
+}
+
+int64_t n_tiles(const Grid& g) {
+    return (int64_t)((g.n1 + SL_TX - 1) / SL_TX) * ((g.n2 + SL_TY - 1) / SL_TY) * ((g.n3 + SL_TZ - 1) / SL_TZ);
+}
+
+// Workspace layout (byte offsets, 256-aligned).  Field counts in units of M values of type T.
+struct Layout {
+    size_t rhoT, rhoR, v, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, spec, plan_p, plan_m, plan_t,
+        maxext, twx, twy, twz, total;
+};
+
+Layout layout(const dr_config* c) {
+    const Grid g = make_grid(c);
+    const size_t es = (c->flags & DR_FP64) ? 8 : 4;
+    const size_t F = (size_t)g.M * es;
+    const int nt = c->nt;
+    Layout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    L.rhoT = take(F);
+    L.rhoR = take(F);
+    L.v = take(3 * F);
+    L.dp = take(3 * F);
+    L.dm = take(3 * F);
+    L.m = take(F);
+    L.D = take(F);
+    L.rho = take((size_t)nt * F);             // rho_1..rho_nt (rho_0 is rhoT)
+    L.G = take((size_t)(nt + 1) * 3 * F);     // grad rho_j
+    L.lam = take((size_t)(nt + 1) * F);       // lambda_j
+    L.lt = take((size_t)nt * F);              // lambda~_0..lambda~_{nt-1} (also g_j scratch)
+    L.rt1 = take(F);                          // rho~(1)
+    L.bt = take(3 * F);                       // b~
+    L.tmp3 = take(3 * F);                     // d* and scratch
+    L.stin = take(3 * F);                     // host staging in
+    L.stout = take(3 * F);                    // host staging out
+    L.spec = take(6 * (size_t)g.S * 2 * es);  // six half spectra
+    const size_t pb = (size_t)n_tiles(g) * PLAN_INTS * sizeof(int);
+    L.plan_p = take(pb);
+    L.plan_m = take(pb);
+    L.plan_t = take(pb);
+    L.maxext = take(16 * sizeof(int));
+    L.twx = take((size_t)g.n1 * 2 * es);
+    L.twy = take((size_t)g.n2 * 2 * es);
+    L.twz = take((size_t)g.n3 * 2 * es);
+    L.total = off;
+    return L;
+}
+
+}  // namespace
+
+struct dr_ctx {
+    dr_config cfg;
+    Grid g;
+    Layout L;
+    cudaStream_t stream = nullptr;
+    char* ws = nullptr;
+    bool own_ws = false;
+    bool have_images = false, have_velocity = false, have_state = false, have_adjoint = false, have_matvec = false;
+    int cap_p[3] = {0, 0, 0}, cap_m[3] = {0, 0, 0};
+    std::string err;
+    template <typename T>
+    T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+};
+
+namespace {
+
+template <typename T>
+struct Impl {
+    dr_ctx& c;
+    const Grid& g;
+    cudaStream_t s;
+    explicit Impl(dr_ctx& cc) : c(cc), g(cc.g), s(cc.stream) {}
+
+    T dt() const { return T(1) / T(c.cfg.nt); }
+    T* rhoT() { return c.at<T>(c.L.rhoT); }
+    T* rhoR() { return c.at<T>(c.L.rhoR); }
+    T* v() { return c.at<T>(c.L.v); }
+    T* dplus() { return c.at<T>(c.L.dp); }
+    T* dminus() { return c.at<T>(c.L.dm); }
+    T* mult() { return c.at<T>(c.L.m); }
+    T* Dv() { return c.at<T>(c.L.D); }
+    T* rho(int j) { return j == 0 ? rhoT() : c.at<T>(c.L.rho) + (size_t)(j - 1) * g.M; }
+    T* G(int j) { return c.at<T>(c.L.G) + (size_t)j * 3 * g.M; }
+    T* lam(int j) { return c.at<T>(c.L.lam) + (size_t)j * g.M; }
+    T* lt(int j) { return c.at<T>(c.L.lt) + (size_t)j * g.M; }
+    T* rt1() { return c.at<T>(c.L.rt1); }
+    T* bt() { return c.at<T>(c.L.bt); }
+    T* tmp3() { return c.at<T>(c.L.tmp3); }
+    T* stin() { return c.at<T>(c.L.stin); }
+    T* stout() { return c.at<T>(c.L.stout); }
+    Cx<T>* spec(int i) { return c.at<Cx<T>>(c.L.spec) + (size_t)i * g.S; }
+    const Cx<T>* twx() { return c.at<Cx<T>>(c.L.twx); }
+    const Cx<T>* twy() { return c.at<Cx<T>>(c.L.twy); }
+    const Cx<T>* twz() { return c.at<Cx<T>>(c.L.twz); }
+    T* mult_or_null() { return (c.cfg.flags & DR_ISOCHORIC) ? nullptr : mult(); }
+
+    int grid_1d(int64_t n, int block = 256) const {
+        int64_t b = (n + block - 1) / block;
+        return (int)std::min<int64_t>(b, 148 * 16);
+    }
+
+    // -------------------------------------------------------------------- twiddle tables
+    void init_twiddles() {
+        auto fill = [&](int n, size_t off) {
+            std::vector<Cx<T>> h(n);
+            for (int m = 0; m < n; ++m) {
+                const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)n;
+                h[m].re = (T)std::cos(a);
+                h[m].im = (T)std::sin(a);
+            }
+            CK(cudaMemcpyAsync(c.ws + off, h.data(), sizeof(Cx<T>) * n, cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+        };
+        fill(g.n1, c.L.twx);
+        fill(g.n2, c.L.twy);
+        fill(g.n3, c.L.twz);
+    }
+
+    // -------------------------------------------------------------------- FFT pass launchers
+    template <int L>
+    static constexpr int row_rb() { return (256 / LineGeom<L>::TPL) > 0 ? 256 / LineGeom<L>::TPL : 1; }
+    template <int L>
+    static size_t row_smem() { return (size_t)row_rb<L>() * LineGeom<L>::LP * sizeof(Cx<T>); }
+    template <int L>
+    int row_blocks() const { return (int)(((int64_t)g.n2 * g.n3 + row_rb<L>() - 1) / row_rb<L>()); }
+
+    template <typename K>
+    static void set_smem(K kernel, size_t bytes) {
+        if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    }
+
+    template <int L>
+    void row_deriv_L(const T* f, T* out, int acc) {
+        auto k = k_row_deriv<T, L>;
+        set_smem(k, row_smem<L>());
+        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, f, out, acc, twx());
+        CKL("k_row_deriv");
+    }
+    template <int L>
+    void row_r2c_L(const T* f, Cx<T>* sp) {
+        auto k = k_row_r2c<T, L>;
+        set_smem(k, row_smem<L>());
+        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, f, sp, twx());
+        CKL("k_row_r2c");
+    }
+    template <int L>
+    void row_c2r_L(const Cx<T>* sp, T* out, const T* add) {
+        auto k = k_row_c2r<T, L>;
+        set_smem(k, row_smem<L>());
+        RowOut<T> e{out, add};
+        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, sp, e, twx());
+        CKL("k_row_c2r");
+    }
+
+#define DR_SWITCH_ROW(Lval, call)                          \
+    switch (Lval) {                                        \
+        case 2: call(2); break;                            \
+        case 4: call(4); break;                            \
+        case 8: call(8); break;                            \
+        case 16: call(16); break;                          \
+        case 32: call(32); break;                          \
+        case 64: call(64); break;                          \
+        case 128: call(128); break;                        \
+        case 256: call(256); break;                        \
+        case 512: call(512); break;                        \
+        default: fail(DR_ERR_GRID, "unsupported row length"); \
+    }
+#define DR_SWITCH_COL(Lval, call)                          \
+    switch (Lval) {                                        \
+        case 4: call(4); break;                            \
+        case 8: call(8); break;                            \
+        case 16: call(16); break;                          \
+        case 32: call(32); break;                          \
+        case 64: call(64); break;                          \
+        case 128: call(128); break;                        \
+        case 256: call(256); break;                        \
+        case 512: call(512); break;                        \
+        case 1024: call(1024); break;                      \
+        default: fail(DR_ERR_GRID, "unsupported column length"); \
+    }
+
+    void row_deriv(const T* f, T* out, int acc) {
+#define CALL(LL) row_deriv_L<LL>(f, out, acc)
+        DR_SWITCH_ROW(g.n1 / 2, CALL)
+#undef CALL
+    }
+    void row_r2c(const T* f, Cx<T>* sp) {
+#define CALL(LL) row_r2c_L<LL>(f, sp)
+        DR_SWITCH_ROW(g.n1 / 2, CALL)
+#undef CALL
+    }
+    void row_c2r(const Cx<T>* sp, T* out, const T* add) {
+#define CALL(LL) row_c2r_L<LL>(sp, out, add)
+        DR_SWITCH_ROW(g.n1 / 2, CALL)
+#undef CALL
+    }
+
+    // columns per CTA: keep NC components of the CTA's lines within ~64 KB of shared memory
+    template <int L, int NC>
+    static constexpr int pick_xc() {
+        return (NC * 16 * LineGeom<L>::LP * (int)sizeof(Cx<T>) <= 72 * 1024)  ? 16
+               : (NC * 8 * LineGeom<L>::LP * (int)sizeof(Cx<T>) <= 72 * 1024) ? 8
+               : (NC * 4 * LineGeom<L>::LP * (int)sizeof(Cx<T>) <= 72 * 1024) ? 4
+                                                                              : 2;
+    }
+    template <int L, int XC>
+    static size_t col_smem(int nc) {
+        return (size_t)nc * ColCfg<L, XC>::LINES * LineGeom<L>::LP * sizeof(Cx<T>);
+    }
+    template <int L, int XC>
+    int col_blocks(const ColGeom& cg, int nother) const {
+        const int nxb = (cg.nx + XC - 1) / XC;
+        return nxb * ((nother + ColCfg<L, XC>::OL - 1) / ColCfg<L, XC>::OL);
+    }
+
+    ColGeom spec_geom() const { return ColGeom{g.n1p, g.n1c, g.n2, g.n3}; }
+    ColGeom pair_geom() const { return ColGeom{g.n1 / 2, g.n1 / 2, g.n2, g.n3}; }
+
+    template <int L, int AX>
+    void col_deriv_L(const T* f, T* out, int acc) {
+        constexpr int XC = pick_xc<L, 1>();
+        const ColGeom cg = pair_geom();
+        auto k = k_col_deriv<T, L, XC, AX>;
+        const size_t sm = col_smem<L, XC>(1);
+        set_smem(k, sm);
+        k<<<col_blocks<L, XC>(cg, AX == 2 ? g.n3 : g.n2), ColCfg<L, XC>::NT, sm, s>>>(
+            cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, AX == 2 ? twy() : twz());
+        CKL("k_col_deriv");
+    }
+    void col_deriv(int ax, const T* f, T* out, int acc) {
+        if (ax == 2) {
+#define CALL(LL) col_deriv_L<LL, 2>(f, out, acc)
+            DR_SWITCH_COL(g.n2, CALL)
+#undef CALL
+        } else {
+#define CALL(LL) col_deriv_L<LL, 3>(f, out, acc)
+            DR_SWITCH_COL(g.n3, CALL)
+#undef CALL
+        }
+    }
+
+    template <int L, int DIR>
+    void col_fft_L(Cx<T>* sp) {
+        constexpr int XC = pick_xc<L, 1>();
+        const ColGeom cg = spec_geom();
+        auto k = k_col_fft<T, L, XC, DIR>;
+        const size_t sm = col_smem<L, XC>(1);
+        set_smem(k, sm);
+        k<<<col_blocks<L, XC>(cg, g.n3), ColCfg<L, XC>::NT, sm, s>>>(cg, sp, twy());
+        CKL("k_col_fft");
+    }
+    void col_fft(Cx<T>* sp, int dir) {
+        if (dir < 0) {
+#define CALL(LL) col_fft_L<LL, -1>(sp)
+            DR_SWITCH_COL(g.n2, CALL)
+#undef CALL
+        } else {
+#define CALL(LL) col_fft_L<LL, +1>(sp)
+            DR_SWITCH_COL(g.n2, CALL)
+#undef CALL
+        }
+    }
+
+    template <int L, int KIND>
+    void middle_L(Cx<T>* const* sp) {
+        constexpr int NCI = Sym<T, KIND>::NCI;
+        constexpr int XC = pick_xc<L, NCI>();
+        const ColGeom cg = spec_geom();
+        SpecPtrs<T, NCI> io;
+        for (int i = 0; i < NCI; ++i) io.p[i] = sp[i];
+        SymInfo si{c.cfg.reg, c.cfg.beta, 2.0 / (double)g.M};
+        auto k = k_col_middle<T, L, XC, KIND>;
+        const size_t sm = col_smem<L, XC>(NCI);
+        set_smem(k, sm);
+        k<<<col_blocks<L, XC>(cg, g.n2), ColCfg<L, XC>::NT, sm, s>>>(cg, io, si, twz());
+        CKL("k_col_middle");
+    }
+    template <int KIND>
+    void middle(Cx<T>* const* sp) {
+#define CALL(LL) middle_L<LL, KIND>(sp)
+        DR_SWITCH_COL(g.n3, CALL)
+#undef CALL
+    }
+
+    // -------------------------------------------------------------------- spectral operators
+    void grad(const T* f, T* out3) {
+        row_deriv(f, out3, 0);
+        col_deriv(2, f, out3 + g.M, 0);
+        col_deriv(3, f, out3 + 2 * g.M, 0);
+    }
+    void div(const T* u3, T* out) {
+        row_deriv(u3, out, 0);
+        col_deriv(2, u3 + g.M, out, 1);
+        col_deriv(3, u3 + 2 * g.M, out, 1);
+    }
+    // out_c = F^-1[sym F in_c] (+ add_c), componentwise symbol KIND 0/1
+    template <int KIND>
+    void scalar_symbol3(const T* in3, T* out3, const T* add3) {
+        for (int cc = 0; cc < 3; ++cc) {
+            Cx<T>* sp = spec(0);
+            row_r2c(in3 + cc * g.M, sp);
+            col_fft(sp, -1);
+            middle<KIND>(&sp);
+            col_fft(sp, +1);
+            row_c2r(sp, out3 + cc * g.M, add3 ? add3 + cc * g.M : nullptr);
+        }
+    }
+    // coupled 3-component symbol (KIND 2, 3): out = F^-1[sym F in]
+    template <int KIND>
+    void vector_symbol3(const T* in3, T* out3) {
+        Cx<T>* sp[3] = {spec(0), spec(1), spec(2)};
+        for (int cc = 0; cc < 3; ++cc) {
+            row_r2c(in3 + cc * g.M, sp[cc]);
+            col_fft(sp[cc], -1);
+        }
+        middle<KIND>(sp);
+        for (int cc = 0; cc < 3; ++cc) {
+            col_fft(sp[cc], +1);
+            row_c2r(sp[cc], out3 + cc * g.M, nullptr);
+        }
+    }
+    void reg_apply(const T* in3, T* out3) { scalar_symbol3<0>(in3, out3, nullptr); }
+    void leray(const T* in3, T* out3) { vector_symbol3<2>(in3, out3); }
+    void precond(const T* r3, T* z3) {
+        if (c.cfg.flags & DR_ISOCHORIC) vector_symbol3<3>(r3, z3);
+        else scalar_symbol3<1>(r3, z3, nullptr);
+    }
+
+    // -------------------------------------------------------------------- semi-Lagrangian
+    void plan(const T* d, int* plan_buf, int* cap, int nc) {
+        int* mx = c.at<int>(c.L.maxext);
+        const int init[3] = {INT_MIN, INT_MIN, INT_MIN};
+        CK(cudaMemcpyAsync(mx, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        k_sl_plan<T><<<(unsigned)n_tiles(g), SL_THREADS, 0, s>>>(g, d, plan_buf, mx);
+        CKL("k_sl_plan");
+        int h[3];
+        CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        // capacity: the largest box if it fits the budget, else shrink the most generous axis;
+        // tiles beyond the capacity gather from global memory.
+        const size_t budget = (size_t)96 * 1024;
+        const int tile[3] = {SL_TX, SL_TY, SL_TZ};
+        for (int a = 0; a < 3; ++a) cap[a] = std::max(h[a], 4);
+        while ((size_t)nc * cap[0] * cap[1] * cap[2] * sizeof(T) > budget) {
+            int a_best = 0;
+            double r_best = -1;
+            for (int a = 0; a < 3; ++a) {
+                const double r = (double)cap[a] / (tile[a] + 3);
+                if (cap[a] > tile[a] + 3 && r > r_best) { r_best = r; a_best = a; }
+            }
+            if (r_best < 0) break;
+            cap[a_best]--;
+        }
+        while ((size_t)nc * cap[0] * cap[1] * cap[2] * sizeof(T) > budget) {  // still too large: shrink all
+            for (int a = 0; a < 3; ++a) cap[a] = std::max(4, cap[a] - 1);
+        }
+    }
+
+    template <int NC, class Epi>
+    void gather(Src<T, NC> src, const T* d, const int* plan_buf, const int* cap, Epi epi) {
+        const size_t sm = (size_t)NC * cap[0] * cap[1] * cap[2] * sizeof(T);
+        auto k = k_sl_gather<T, NC, Epi>;
+        set_smem(k, sm);
+        k<<<(unsigned)n_tiles(g), SL_THREADS, sm, s>>>(g, src, d, plan_buf, cap[0], cap[1], cap[2], epi);
+        CKL("k_sl_gather");
+    }
+    int* plan_p() { return c.at<int>(c.L.plan_p); }
+    int* plan_m() { return c.at<int>(c.L.plan_m); }
+    int* plan_t() { return c.at<int>(c.L.plan_t); }
+
+    void gather_scalar_p(const T* f, T* out) {
+        gather<1>(Src<T, 1>{{f}}, dplus(), plan_p(), c.cap_p, EpiStore<T>{out});
+    }
+
+    // -------------------------------------------------------------------- API steps
+    void set_velocity(const T* vin) {
+        CK(cudaMemcpyAsync(v(), vin, 3 * g.M * sizeof(T), cudaMemcpyDefault, s));
+        if (c.cfg.flags & DR_ISOCHORIC) leray(v(), v());
+        const double h[3] = {2.0 * M_PI / g.n1, 2.0 * M_PI / g.n2, 2.0 * M_PI / g.n3};
+        const double dtt = 1.0 / c.cfg.nt;
+        for (int sg = 1; sg >= -1; sg -= 2) {
+            T* dout = sg > 0 ? dplus() : dminus();
+            k_dstar<T><<<grid_1d(3 * g.M), 256, 0, s>>>(g, v(), tmp3(), (T)(sg * dtt / h[0]), (T)(sg * dtt / h[1]),
+                                                        (T)(sg * dtt / h[2]));
+            CKL("k_dstar");
+            int capt[3];
+            plan(tmp3(), plan_t(), capt, 3);
+            EpiDeparture<T> e;
+            e.d = dout;
+            e.v = v();
+            e.M = g.M;
+            for (int a = 0; a < 3; ++a) e.c[a] = (T)(sg * 0.5 * dtt / h[a]);
+            gather<3>(Src<T, 3>{{v(), v() + g.M, v() + 2 * g.M}}, tmp3(), plan_t(), capt, e);
+            plan(dout, sg > 0 ? plan_p() : plan_m(), sg > 0 ? c.cap_p : c.cap_m, 1);
+        }
+        if (!(c.cfg.flags & DR_ISOCHORIC)) {
+            div(v(), Dv());
+            gather<1>(Src<T, 1>{{Dv()}}, dminus(), plan_m(), c.cap_m, EpiMultiplier<T>{mult(), Dv(), dt()});
+        }
+    }
+
+    void forward_solve() {
+        for (int j = 0; j < c.cfg.nt; ++j) gather_scalar_p(rho(j), rho(j + 1));
+        for (int j = 0; j <= c.cfg.nt; ++j) grad(rho(j), G(j));
+    }
+
+    void adjoint_solve() {
+        const int nt = c.cfg.nt;
+        k_sub<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, rhoR(), rho(nt), lam(nt));
+        CKL("k_sub");
+        for (int k = nt; k >= 1; --k)
+            gather<1>(Src<T, 1>{{lam(k)}}, dminus(), plan_m(), c.cap_m, EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)});
+    }
+
+    void hessian_matvec(const T* vt, T* Hvt) {
+        const int nt = c.cfg.nt;
+        const T dtt = dt();
+        // incremental state (Algorithm 2, merged gather g_j = rho~_j + dt/2 f_j)
+        k_inc_init<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, vt, G(0), lt(0), T(0.5) * dtt);
+        CKL("k_inc_init");
+        for (int j = 0; j < nt; ++j) {
+            const bool last = (j == nt - 1);
+            EpiIncState<T> e{last ? rt1() : lt(j + 1), vt, G(j + 1), last ? T(0.5) * dtt : dtt, g.M};
+            gather<1>(Src<T, 1>{{lt(j)}}, dplus(), plan_p(), c.cap_p, e);
+        }
+        // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-)
+        for (int k = nt; k >= 1; --k) {
+            const T* src = (k == nt) ? rt1() : lt(k);
+            gather<1>(Src<T, 1>{{src}}, dminus(), plan_m(), c.cap_m,
+                      EpiAdjoint<T>{lt(k - 1), mult_or_null(), k == nt ? T(-1) : T(1)});
+        }
+        k_quadrature<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, nt, lt(0), rt1(), T(-1), G(0), bt(), dtt);
+        CKL("k_quadrature");
+        // spectral tail: H vt = beta A vt + P b~
+        if (c.cfg.flags & DR_ISOCHORIC) {
+            Cx<T>* sp[6] = {spec(0), spec(1), spec(2), spec(3), spec(4), spec(5)};
+            for (int cc = 0; cc < 3; ++cc) {
+                row_r2c(vt + cc * g.M, sp[cc]);
+                col_fft(sp[cc], -1);
+                row_r2c(bt() + cc * g.M, sp[3 + cc]);
+                col_fft(sp[3 + cc], -1);
+            }
+            middle<4>(sp);
+            for (int cc = 0; cc < 3; ++cc) {
+                col_fft(sp[cc], +1);
+                row_c2r(sp[cc], Hvt + cc * g.M, nullptr);
+            }
+        } else {
+            scalar_symbol3<0>(vt, Hvt, bt());
+        }
+    }
+};
+
+dr_status guard(dr_ctx* c, dr_status st, const std::string& m) {
+    if (c) c->err = m;
+    return st;
+}
+
+template <typename F>
+dr_status run(dr_ctx* c, F&& f) {
+    if (!c) return DR_ERR_ARG;
+    try {
+        f();
+        c->err.clear();
+        return DR_OK;
+    } catch (const DrError& e) {
+        c->err = e.msg;
+        return e.s;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        return DR_ERR_CUDA;
+    }
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+size_t elem_size(const dr_ctx* c) { return (c->cfg.flags & DR_FP64) ? 8 : 4; }
+
+// input: device pointers are used in place, host pointers are staged into `stage`
+const void* stage_in(dr_ctx* c, const void* p, size_t bytes, void* stage) {
+    if (is_device_ptr(p)) return p;
+    CK(cudaMemcpyAsync(stage, p, bytes, cudaMemcpyHostToDevice, c->stream));
+    return stage;
+}
+
+template <typename F>
+void with_output(dr_ctx* c, void* out, size_t bytes, void* stage, F&& f) {
+    if (is_device_ptr(out)) {
+        f(out);
+        return;
+    }
+    f(stage);
+    CK(cudaMemcpyAsync(out, stage, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+template <typename F>
+void dispatch(dr_ctx* c, F&& f) {
+    if (c->cfg.flags & DR_FP64) {
+        Impl<double> im(*c);
+        f(im);
+    } else {
+        Impl<float> im(*c);
+        f(im);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dr_workspace_bytes(const dr_config* cfg) {
+    if (validate(cfg) != DR_OK) return 0;
+    return layout(cfg).total;
+}
+
+dr_status dr_create(const dr_config* cfg, void* workspace, size_t workspace_bytes, void* stream, dr_ctx** out) {
+    if (!out) return DR_ERR_ARG;
+    *out = nullptr;
+    const dr_status v = validate(cfg);
+    if (v != DR_OK) return v;
+    dr_ctx* c = new dr_ctx();
+    c->cfg = *cfg;
+    c->g = make_grid(cfg);
+    c->L = layout(cfg);
+    c->stream = reinterpret_cast<cudaStream_t>(stream);
+    if (workspace) {
+        if (workspace_bytes < c->L.total) {
+            delete c;
+            return DR_ERR_OOM;
+        }
+        c->ws = static_cast<char*>(workspace);
+    } else {
+        if (cudaMalloc(&c->ws, c->L.total) != cudaSuccess) {
+            cudaGetLastError();
+            delete c;
+            return DR_ERR_OOM;
+        }
+        c->own_ws = true;
+    }
+    const dr_status st = run(c, [&] { dispatch(c, [](auto& im) { im.init_twiddles(); }); });
+    if (st != DR_OK) {
+        if (c->own_ws) cudaFree(c->ws);
+        delete c;
+        return st;
+    }
+    *out = c;
+    return DR_OK;
+}
+
+dr_status dr_destroy(dr_ctx* c) {
+    if (!c) return DR_ERR_ARG;
+    if (c->own_ws) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(c->ws);
+    }
+    delete c;
+    return DR_OK;
+}
+
+dr_status dr_set_images(dr_ctx* c, const void* rho_T, const void* rho_R) {
+    return run(c, [&] {
+        if (!rho_T || !rho_R) fail(DR_ERR_ARG, "rho_T and rho_R must be non-NULL");
+        const size_t F = c->g.M * elem_size(c);
+        CK(cudaMemcpyAsync(c->ws + c->L.rhoT, rho_T, F, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(c->ws + c->L.rhoR, rho_R, F, cudaMemcpyDefault, c->stream));
+        c->have_images = true;
+        c->have_state = c->have_adjoint = c->have_matvec = false;
+    });
+}
+
+dr_status dr_set_velocity(dr_ctx* c, const void* v) {
+    return run(c, [&] {
+        if (!v) fail(DR_ERR_ARG, "v must be non-NULL");
+        c->have_velocity = false;
+        c->have_state = c->have_adjoint = c->have_matvec = false;
+        dispatch(c, [&](auto& im) {
+            using T = std::remove_pointer_t<decltype(im.v())>;
+            im.set_velocity(static_cast<const T*>(v));
+        });
+        c->have_velocity = true;
+    });
+}
+
+dr_status dr_forward_solve(dr_ctx* c, void* rho1_out) {
+    return run(c, [&] {
+        if (!c->have_images || !c->have_velocity) fail(DR_ERR_ORDER, "forward_solve needs set_images and set_velocity");
+        dispatch(c, [&](auto& im) { im.forward_solve(); });
+        c->have_state = true;
+        c->have_adjoint = c->have_matvec = false;
+        if (rho1_out) {
+            const size_t F = c->g.M * elem_size(c);
+            CK(cudaMemcpyAsync(rho1_out, c->ws + c->L.rho + (size_t)(c->cfg.nt - 1) * F, F,
+                               cudaMemcpyDefault, c->stream));
+            if (!is_device_ptr(rho1_out)) CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+dr_status dr_adjoint_solve(dr_ctx* c, void* lambda0_out) {
+    return run(c, [&] {
+        if (!c->have_state) fail(DR_ERR_ORDER, "adjoint_solve needs forward_solve");
+        dispatch(c, [&](auto& im) { im.adjoint_solve(); });
+        c->have_adjoint = true;
+        if (lambda0_out) {
+            const size_t F = c->g.M * elem_size(c);
+            CK(cudaMemcpyAsync(lambda0_out, c->ws + c->L.lam, F, cudaMemcpyDefault, c->stream));
+            if (!is_device_ptr(lambda0_out)) CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+dr_status dr_hessian_matvec(dr_ctx* c, const void* vt, void* Hvt) {
+    return run(c, [&] {
+        if (!vt || !Hvt) fail(DR_ERR_ARG, "vt and Hvt must be non-NULL");
+        if (vt == Hvt) fail(DR_ERR_ARG, "vt and Hvt must not alias");
+        if (!c->have_state) fail(DR_ERR_ORDER, "hessian_matvec needs forward_solve");
+        const size_t V = 3 * c->g.M * elem_size(c);
+        const void* in = stage_in(c, vt, V, c->ws + c->L.stin);
+        with_output(c, Hvt, V, c->ws + c->L.stout, [&](void* out) {
+            dispatch(c, [&](auto& im) {
+                using T = std::remove_pointer_t<decltype(im.v())>;
+                im.hessian_matvec(static_cast<const T*>(in), static_cast<T*>(out));
+            });
+        });
+        c->have_matvec = true;
+    });
+}
+
+dr_status dr_precond_apply(dr_ctx* c, const void* r, void* z) {
+    return run(c, [&] {
+        if (!r || !z) fail(DR_ERR_ARG, "r and z must be non-NULL");
+        const size_t V = 3 * c->g.M * elem_size(c);
+        const void* in = stage_in(c, r, V, c->ws + c->L.stin);
+        with_output(c, z, V, c->ws + c->L.stout, [&](void* out) {
+            dispatch(c, [&](auto& im) {
+                using T = std::remove_pointer_t<decltype(im.v())>;
+                im.precond(static_cast<const T*>(in), static_cast<T*>(out));
+            });
+        });
+    });
+}
+
+dr_status dr_sync(dr_ctx* c) {
+    return run(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+const char* dr_last_error(const dr_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+const char* dr_status_string(dr_status s) {
+    switch (s) {
+        case DR_OK: return "DR_OK";
+        case DR_ERR_ARG: return "DR_ERR_ARG";
+        case DR_ERR_GRID: return "DR_ERR_GRID";
+        case DR_ERR_PARAM: return "DR_ERR_PARAM";
+        case DR_ERR_ORDER: return "DR_ERR_ORDER";
+        case DR_ERR_CUDA: return "DR_ERR_CUDA";
+        case DR_ERR_NCCL: return "DR_ERR_NCCL";
+        case DR_ERR_OOM: return "DR_ERR_OOM";
+        case DR_ERR_NONFINITE: return "DR_ERR_NONFINITE";
+        case DR_ERR_PLAN: return "DR_ERR_PLAN";
+    }
+    return "unknown";
+}
+
+dr_status dr_op_spectral(dr_ctx* c, int op, const void* in, void* out) {
+    return run(c, [&] {
+        if (!in || !out) fail(DR_ERR_ARG, "in/out must be non-NULL");
+        dispatch(c, [&](auto& im) {
+            using T = std::remove_pointer_t<decltype(im.v())>;
+            const T* i = static_cast<const T*>(in);
+            T* o = static_cast<T*>(out);
+            switch (op) {
+                case DR_OP_GRAD: im.grad(i, o); break;
+                case DR_OP_DIV: im.div(i, o); break;
+                case DR_OP_REG: im.reg_apply(i, o); break;
+                case DR_OP_PRECOND: im.precond(i, o); break;
+                case DR_OP_LERAY: im.leray(i, o); break;
+                default: fail(DR_ERR_ARG, "unknown spectral op");
+            }
+        });
+    });
+}
+
+dr_status dr_op_interp(dr_ctx* c, const void* f, int64_t npts, const void* s, void* out) {
+    return run(c, [&] {
+        if (!f || !s || !out || npts < 0) fail(DR_ERR_ARG, "bad interp arguments");
+        if (npts == 0) return;
+        dispatch(c, [&](auto& im) {
+            using T = std::remove_pointer_t<decltype(im.v())>;
+            k_interp_points<T><<<im.grid_1d(npts), 256, 0, c->stream>>>(c->g, static_cast<const T*>(f), npts,
+                                                                          static_cast<const T*>(s), static_cast<T*>(out));
+            CKL("k_interp_points");
+        });
+    });
+}
+
+dr_status dr_get_departure(dr_ctx* c, int sigma, void* d_out) {
+    return run(c, [&] {
+        if (!d_out || (sigma != 1 && sigma != -1)) fail(DR_ERR_ARG, "bad departure arguments");
+        if (!c->have_velocity) fail(DR_ERR_ORDER, "get_departure needs set_velocity");
+        CK(cudaMemcpyAsync(d_out, c->ws + (sigma > 0 ? c->L.dp : c->L.dm), 3 * c->g.M * elem_size(c),
+                           cudaMemcpyDeviceToDevice, c->stream));
+    });
+}
+
+dr_status dr_get_field(dr_ctx* c, int which, int j, void* out) {
+    return run(c, [&] {
+        if (!out) fail(DR_ERR_ARG, "out must be non-NULL");
+        const size_t F = c->g.M * elem_size(c);
+        const int nt = c->cfg.nt;
+        size_t off = 0, bytes = F;
+        auto need = [&](bool ok, const char* m) {
+            if (!ok) fail(DR_ERR_ORDER, m);
+        };
+        auto jrange = [&]() {
+            if (j < 0 || j > nt) fail(DR_ERR_ARG, "slice index out of range");
+        };
+        switch (which) {
+            case DR_FIELD_STATE:
+                need(c->have_state, "needs forward_solve");
+                jrange();
+                off = (j == 0) ? c->L.rhoT : c->L.rho + (size_t)(j - 1) * F;
+                break;
+            case DR_FIELD_STATE_GRAD:
+                need(c->have_state, "needs forward_solve");
+                jrange();
+                off = c->L.G + (size_t)j * 3 * F;
+                bytes = 3 * F;
+                break;
+            case DR_FIELD_ADJOINT:
+                need(c->have_adjoint, "needs adjoint_solve");
+                jrange();
+                off = c->L.lam + (size_t)j * F;
+                break;
+            case DR_FIELD_INC_STATE:
+                need(c->have_matvec, "needs hessian_matvec");
+                off = c->L.rt1;
+                break;
+            case DR_FIELD_INC_ADJOINT:
+                need(c->have_matvec, "needs hessian_matvec");
+                jrange();
+                if (j == nt) {  // lambda~(1) = -rho~(1) (Eq. 5d); materialise it
+                    dispatch(c, [&](auto& im) {
+                        using T = std::remove_pointer_t<decltype(im.v())>;
+                        k_scale<T><<<im.grid_1d(c->g.M), 256, 0, c->stream>>>(c->g.M, im.rt1(), static_cast<T*>(out), T(-1));
+                        CKL("k_scale");
+                    });
+                    return;
+                }
+                off = c->L.lt + (size_t)j * F;
+                break;
+            case DR_FIELD_BTILDE:
+                need(c->have_matvec, "needs hessian_matvec");
+                off = c->L.bt;
+                bytes = 3 * F;
+                break;
+            case DR_FIELD_MULTIPLIER:
+                need(c->have_velocity, "needs set_velocity");
+                if (c->cfg.flags & DR_ISOCHORIC) fail(DR_ERR_ARG, "isochoric contexts have m == 1");
+                off = c->L.m;
+                break;
+            case DR_FIELD_VELOCITY:
+                need(c->have_velocity, "needs set_velocity");
+                off = c->L.v;
+                bytes = 3 * F;
+                break;
+            default:
+                fail(DR_ERR_ARG, "unknown field");
+        }
+        CK(cudaMemcpyAsync(out, c->ws + off, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    });
+}
+
+}  // extern "C"

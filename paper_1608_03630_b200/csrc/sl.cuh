@@ -1,0 +1,315 @@
+// sl.cuh -- semi-Lagrangian gather kernels: RK2 departure points (Eq. 6) and the
+// tricubic interpolation at those points (reading A6: tensor cubic Lagrange on the
+// 4x4x4 nodes q-1..q+2 with periodic wrap) fused with the epilogue of each transport step
+// (state, adjoint, incremental state / adjoint: Eq. 7, Algorithm 2).
+//
+// Layout and plan.  Output tiles are TX x TY x TZ = 32 x 8 x 8 voxels (one 256-thread CTA; lane =
+// x1, warp = x2, each thread walks TZ points along x3).  Because departure points move with the
+// (stationary) velocity, the input box a tile reads is fixed once per velocity and direction:
+// the plan kernel (the analogue of the paper's "interpolation planner") stores per tile the
+// box origin (min floor(s) - 1, unwrapped) and extents.  Each transport step then stages that box
+// from L2/HBM into shared memory with coalesced row loads (periodic wrap on the fly) and gathers all
+// 64 stencil values from shared memory.  Tiles whose box exceeds the shared-memory capacity chosen
+// for the launch fall back to gathering straight from global memory (same arithmetic).
+#pragma once
+#include "common.cuh"
+
+namespace dr {
+
+constexpr int SL_TX = 32, SL_TY = 8, SL_TZ = 8, SL_THREADS = SL_TX * SL_TY;
+constexpr int PLAN_INTS = 8;  // ox, oy, oz, ex, ey, ez, pad, pad
+
+// Lagrange weights for nodes -1, 0, 1, 2 at t in [0, 1) (reading A6)
+template <typename T>
+__device__ __forceinline__ void lagrange4(T t, T w[4]) {
+    const T tm1 = t - T(1), tm2 = t - T(2), tp1 = t + T(1);
+    const T sixth = T(1) / T(6);
+    w[0] = -t * tm1 * tm2 * sixth;
+    w[1] = tp1 * tm1 * tm2 * T(0.5);
+    w[2] = -tp1 * t * tm2 * T(0.5);
+    w[3] = tp1 * t * tm1 * sixth;
+}
+
+template <typename T>
+__device__ __forceinline__ T floor_t(T x);
+template <>
+__device__ __forceinline__ float floor_t<float>(float x) { return floorf(x); }
+template <>
+__device__ __forceinline__ double floor_t<double>(double x) { return floor(x); }
+
+// Departure point of node i with displacement d (cells): s = i - d, q = i + floor(-d), t = -d - floor(-d)
+// (exact in floating point: subtracting the integer floor(-d) from -d loses nothing).
+template <typename T>
+__device__ __forceinline__ void cell_of(int i, T d, int& q, T& t) {
+    const T e = -d;
+    const T fl = floor_t(e);
+    t = e - fl;
+    q = i + (int)fl;
+}
+
+template <typename T>
+__device__ __forceinline__ T interp_smem(const T* __restrict__ b, int sy, int sz, const T w1[4], const T w2[4],
+                                         const T w3[4]) {
+    T acc = T(0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        T accb = T(0);
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            const T* r = b + c * sz + bb * sy;
+            const T row = w1[0] * r[0] + w1[1] * r[1] + w1[2] * r[2] + w1[3] * r[3];
+            accb += w2[bb] * row;
+        }
+        acc += w3[c] * accb;
+    }
+    return acc;
+}
+
+template <typename T>
+__device__ __forceinline__ T interp_global(const T* __restrict__ f, const Grid& g, int q1, int q2, int q3,
+                                           const T w1[4], const T w2[4], const T w3[4]) {
+    T acc = T(0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int j3 = wrapi(q3 + c - 1, g.n3);
+        T accb = T(0);
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            const int j2 = wrapi(q2 + bb - 1, g.n2);
+            const T* r = f + ((int64_t)j3 * g.n2 + j2) * g.n1;
+            T row = T(0);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) row += w1[a] * __ldg(r + wrapi(q1 + a - 1, g.n1));
+            accb += w2[bb] * row;
+        }
+        acc += w3[c] * accb;
+    }
+    return acc;
+}
+
+__device__ __forceinline__ void tile_coords(const Grid& g, int tile, int& x0, int& y0, int& z0) {
+    const int ntx = (g.n1 + SL_TX - 1) / SL_TX, nty = (g.n2 + SL_TY - 1) / SL_TY;
+    x0 = (tile % ntx) * SL_TX;
+    y0 = ((tile / ntx) % nty) * SL_TY;
+    z0 = (tile / (ntx * nty)) * SL_TZ;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Plan: per tile, the unwrapped box [min q - 1, max q + 2] of the stencil nodes of its departure
+// points, and the running maximum extents over all tiles (for sizing shared memory).
+template <typename T>
+__global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restrict__ d, int* __restrict__ plan,
+                                                        int* __restrict__ maxext) {
+    __shared__ int red[6];
+    if (threadIdx.x < 6) red[threadIdx.x] = (threadIdx.x < 3) ? INT_MAX : INT_MIN;
+    __syncthreads();
+    int x0, y0, z0;
+    tile_coords(g, blockIdx.x, x0, y0, z0);
+    const int x = x0 + (threadIdx.x % SL_TX), y = y0 + threadIdx.x / SL_TX;
+    int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+    if (x < g.n1 && y < g.n2) {
+        for (int k = 0; k < SL_TZ; ++k) {
+            const int z = z0 + k;
+            if (z >= g.n3) break;
+            const int64_t id = ((int64_t)z * g.n2 + y) * g.n1 + x;
+            const int ii[3] = {x, y, z};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                int q;
+                T t;
+                cell_of<T>(ii[a], d[a * g.M + id], q, t);
+                mn[a] = min(mn[a], q);
+                mx[a] = max(mx[a], q);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&red[a], mn[a]);
+            atomicMax(&red[3 + a], mx[a]);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int* p = plan + (int64_t)blockIdx.x * PLAN_INTS;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            p[a] = red[a] - 1;
+            p[3 + a] = red[3 + a] - red[a] + 4;
+            atomicMax(&maxext[a], p[3 + a]);
+        }
+        p[6] = p[7] = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Epilogues of the fused gather kernel.  `val` holds the NC interpolated components at the
+// departure point of voxel id.
+template <typename T>
+struct EpiStore {  // state solve: rho_{j+1} = I[rho_j](X+)   (Eq. 7 with f = 0)
+    T* out;
+    __device__ __forceinline__ void operator()(int64_t id, const T* val) const { out[id] = val[0]; }
+};
+
+template <typename T>
+struct EpiAdjoint {  // adjoint-like step: nu_{k-1} = scale * m * I[nu_k](X-)  (Eq. 7, f = nu div v; D7)
+    T* out;
+    const T* m;  // nullable (isochoric: m == 1)
+    T scale;
+    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
+        T r = scale * val[0];
+        if (m) r *= __ldg(m + id);
+        out[id] = r;
+    }
+};
+
+template <typename T>
+struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+) + c f_{j+1}, f = -vt.G_{j+1}
+    T* out;
+    const T* vt;  // vector field
+    const T* G;   // vector field grad rho_{j+1}
+    T c;
+    int64_t M;
+    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
+        const T f = -(__ldg(vt + id) * __ldg(G + id) + __ldg(vt + M + id) * __ldg(G + M + id) +
+                      __ldg(vt + 2 * M + id) * __ldg(G + 2 * M + id));
+        out[id] = val[0] + c * f;
+    }
+};
+
+template <typename T>
+struct EpiMultiplier {  // m = 1 + dt/2 (Dbar + D + dt Dbar D), Dbar = I[div v](X-)  (D7)
+    T* m;
+    const T* D;
+    T dt;
+    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
+        const T Db = val[0], Dv = __ldg(D + id);
+        m[id] = T(1) + T(0.5) * dt * (Db + Dv + dt * Db * Dv);
+    }
+};
+
+template <typename T>
+struct EpiDeparture {  // d = sigma dt/2 (v(x) + I[v](X*)) / h  (Eq. 6, cell units)
+    T* d;
+    const T* v;
+    T c[3];  // sigma * dt / (2 h_a)
+    int64_t M;
+    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) d[a * M + id] = c[a] * (__ldg(v + a * M + id) + val[a]);
+    }
+};
+
+template <typename T, int NC>
+struct Src {
+    const T* p[NC];
+};
+
+// Fused gather + epilogue.  Grid: one CTA per tile.  Dynamic smem: NC * capx * capy * capz values.
+template <typename T, int NC, class Epi>
+__global__ void __launch_bounds__(SL_THREADS) k_sl_gather(Grid g, Src<T, NC> src, const T* __restrict__ d,
+                                                          const int* __restrict__ plan, int capx, int capy, int capz,
+                                                          Epi epi) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* box = reinterpret_cast<T*>(smem_raw);
+    int x0, y0, z0;
+    tile_coords(g, blockIdx.x, x0, y0, z0);
+    const int* pl = plan + (int64_t)blockIdx.x * PLAN_INTS;
+    const int ox = pl[0], oy = pl[1], oz = pl[2], ex = pl[3], ey = pl[4], ez = pl[5];
+    const bool fits = ex <= capx && ey <= capy && ez <= capz;
+    const int lane = threadIdx.x % SL_TX, wy = threadIdx.x / SL_TX;
+    const int x = x0 + lane, y = y0 + wy;
+    const bool xyok = x < g.n1 && y < g.n2;
+
+    // displacements of this thread's points (issued before the box load so they overlap it)
+    T dd[SL_TZ][3];
+#pragma unroll
+    for (int k = 0; k < SL_TZ; ++k) {
+        const int z = z0 + k;
+        const int64_t id = ((int64_t)z * g.n2 + y) * g.n1 + x;
+        const bool ok = xyok && z < g.n3;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) dd[k][a] = ok ? __ldg(d + a * g.M + id) : T(0);
+    }
+
+    const int sy = capx, sz = capx * capy, sc = capx * capy * capz;
+    if (fits) {
+        const int rows = ey * ez;
+        for (int r = wy; r < rows; r += SL_THREADS / 32) {
+            const int yy = r % ey, zz = r / ey;
+            const int gy = wrapi(oy + yy, g.n2), gz = wrapi(oz + zz, g.n3);
+            const int64_t rowbase = ((int64_t)gz * g.n2 + gy) * g.n1;
+            for (int xx = lane; xx < ex; xx += 32) {
+                const int gx = wrapi(ox + xx, g.n1);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) box[c * sc + zz * sz + yy * sy + xx] = __ldg(src.p[c] + rowbase + gx);
+            }
+        }
+    }
+    __syncthreads();
+    if (!xyok) return;
+#pragma unroll
+    for (int k = 0; k < SL_TZ; ++k) {
+        const int z = z0 + k;
+        if (z >= g.n3) break;
+        const int64_t id = ((int64_t)z * g.n2 + y) * g.n1 + x;
+        int q1, q2, q3;
+        T t1, t2, t3;
+        cell_of<T>(x, dd[k][0], q1, t1);
+        cell_of<T>(y, dd[k][1], q2, t2);
+        cell_of<T>(z, dd[k][2], q3, t3);
+        T w1[4], w2[4], w3[4];
+        lagrange4(t1, w1);
+        lagrange4(t2, w2);
+        lagrange4(t3, w3);
+        T val[NC];
+        if (fits) {
+            const T* b = box + (q3 - 1 - oz) * sz + (q2 - 1 - oy) * sy + (q1 - 1 - ox);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) val[c] = interp_smem(b + c * sc, sy, sz, w1, w2, w3);
+        } else {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) val[c] = interp_global(src.p[c], g, q1, q2, q3, w1, w2, w3);
+        }
+        epi(id, val);
+    }
+}
+
+// First-stage displacement of Eq. 6: d* = sigma dt v / h (cells), X* = x - h d*.
+template <typename T>
+__global__ void k_dstar(Grid g, const T* __restrict__ v, T* __restrict__ dstar, T c0, T c1, T c2) {
+    const int64_t n = 3 * g.M;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int a = (int)(e / g.M);
+        const T c = a == 0 ? c0 : (a == 1 ? c1 : c2);
+        dstar[e] = c * v[e];
+    }
+}
+
+// Interpolation at arbitrary points (test hook dr_op_interp): s in cell coordinates.
+template <typename T>
+__global__ void k_interp_points(Grid g, const T* __restrict__ f, int64_t npts, const T* __restrict__ s,
+                                T* __restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npts; p += (int64_t)gridDim.x * blockDim.x) {
+        T w[3][4];
+        int q[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const T sa = s[a * npts + p];
+            const T fl = floor_t(sa);
+            q[a] = (int)fl;
+            lagrange4(sa - fl, w[a]);
+        }
+        out[p] = interp_global(f, g, q[0], q[1], q[2], w[0], w[1], w[2]);
+    }
+}
+
+}  // namespace dr

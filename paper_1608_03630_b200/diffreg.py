@@ -1,0 +1,212 @@
+"""Thin ctypes binding of the C ABI in include/diffreg.h (argument marshalling only).
+
+Every function here forwards to the CUDA library `libdiffreg.so`; no step of the hot path runs in
+Python.  Fields are torch tensors (CUDA, or CPU for the host-buffer entry points), float32 by default
+or float64 for DR_FP64 contexts, shaped (N3, N2, N1) for scalars and (3, N3, N2, N1) for vectors.
+Importing this module never falls back to anything: if the library is missing or cannot be loaded,
+`lib()` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdiffreg.so")
+
+DR_OK, DR_ERR_ARG, DR_ERR_GRID, DR_ERR_PARAM, DR_ERR_ORDER, DR_ERR_CUDA, DR_ERR_NCCL, DR_ERR_OOM, \
+    DR_ERR_NONFINITE, DR_ERR_PLAN = range(10)
+DR_REG_H1, DR_REG_H2 = 1, 2
+DR_ISOCHORIC, DR_FP64 = 1, 2
+DR_OP_GRAD, DR_OP_DIV, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY = range(5)
+(DR_FIELD_STATE, DR_FIELD_STATE_GRAD, DR_FIELD_ADJOINT, DR_FIELD_INC_STATE, DR_FIELD_INC_ADJOINT,
+ DR_FIELD_BTILDE, DR_FIELD_MULTIPLIER, DR_FIELD_VELOCITY) = range(8)
+
+# every symbol include/diffreg.h declares (checked by tests/test_abi.py)
+EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr_set_velocity",
+           "dr_forward_solve", "dr_adjoint_solve", "dr_hessian_matvec", "dr_precond_apply", "dr_sync",
+           "dr_last_error", "dr_status_string", "dr_op_spectral", "dr_op_interp", "dr_get_departure",
+           "dr_get_field"]
+
+
+class dr_config(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32 * 3), ("nt", ctypes.c_int32), ("reg", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("beta", ctypes.c_double)]
+
+
+class DiffRegError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libdiffreg.so (raises if absent: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() or paper_1608_03630_b200/build.py")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+        L.dr_workspace_bytes.argtypes = [ctypes.POINTER(dr_config)]
+        L.dr_workspace_bytes.restype = ctypes.c_size_t
+        L.dr_create.argtypes = [ctypes.POINTER(dr_config), vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
+        for name, args in [("dr_destroy", [vp]), ("dr_set_images", [vp, vp, vp]), ("dr_set_velocity", [vp, vp]),
+                           ("dr_forward_solve", [vp, vp]), ("dr_adjoint_solve", [vp, vp]),
+                           ("dr_hessian_matvec", [vp, vp, vp]), ("dr_precond_apply", [vp, vp, vp]),
+                           ("dr_sync", [vp]), ("dr_op_spectral", [vp, i32, vp, vp]),
+                           ("dr_op_interp", [vp, vp, i64, vp, vp]), ("dr_get_departure", [vp, i32, vp]),
+                           ("dr_get_field", [vp, i32, i32, vp])]:
+            getattr(L, name).argtypes = args
+            getattr(L, name).restype = ctypes.c_int
+        L.dr_create.restype = ctypes.c_int
+        L.dr_last_error.argtypes = [vp]
+        L.dr_last_error.restype = ctypes.c_char_p
+        L.dr_status_string.argtypes = [ctypes.c_int]
+        L.dr_status_string.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class Config:
+    n: tuple  # (N1, N2, N3)
+    nt: int = 4
+    reg: int = DR_REG_H2
+    beta: float = 1e-2
+    isochoric: bool = False
+    fp64: bool = False
+
+    def c(self) -> dr_config:
+        n = (self.n,) * 3 if isinstance(self.n, int) else tuple(self.n)
+        flags = (DR_ISOCHORIC if self.isochoric else 0) | (DR_FP64 if self.fp64 else 0)
+        cfg = dr_config()
+        cfg.n[:] = list(n)
+        cfg.nt, cfg.reg, cfg.flags, cfg.beta = self.nt, self.reg, flags, self.beta
+        return cfg
+
+    @property
+    def dtype(self):
+        return torch.float64 if self.fp64 else torch.float32
+
+    @property
+    def shape(self):
+        n = (self.n,) * 3 if isinstance(self.n, int) else tuple(self.n)
+        return (n[2], n[1], n[0])
+
+
+def dr_workspace_bytes(cfg: Config) -> int:
+    c = cfg.c()
+    return int(lib().dr_workspace_bytes(ctypes.byref(c)))
+
+
+class Context:
+    """One dr_ctx: owns its workspace tensor (torch device memory) and uses the given CUDA stream."""
+
+    def __init__(self, cfg: Config, device="cuda", stream: torch.cuda.Stream | None = None):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        nbytes = dr_workspace_bytes(cfg)
+        if nbytes == 0:
+            raise DiffRegError(DR_ERR_PARAM, f"invalid config {cfg}")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        c = cfg.c()
+        h = ctypes.c_void_p()
+        st = lib().dr_create(ctypes.byref(c), _ptr(self.workspace), nbytes,
+                             ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        if st != DR_OK:
+            raise DiffRegError(st, lib().dr_status_string(st).decode())
+        self.h = h
+
+    def _check(self, st):
+        if st != DR_OK:
+            raise DiffRegError(st, lib().dr_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().dr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # allocation helpers (on the context device)
+    def scalar(self, device=None):
+        return torch.empty(self.cfg.shape, dtype=self.cfg.dtype, device=device or self.device)
+
+    def vector(self, device=None):
+        return torch.empty((3,) + self.cfg.shape, dtype=self.cfg.dtype, device=device or self.device)
+
+    def _in(self, t):
+        assert t.dtype == self.cfg.dtype and t.is_contiguous(), (t.dtype, self.cfg.dtype)
+        return _ptr(t)
+
+    # ---- main path (same names as the C ABI) ----
+    def set_images(self, rho_T, rho_R):
+        self._check(lib().dr_set_images(self.h, self._in(rho_T), self._in(rho_R)))
+
+    def set_velocity(self, v):
+        self._check(lib().dr_set_velocity(self.h, self._in(v)))
+
+    def forward_solve(self, rho1_out=None):
+        self._check(lib().dr_forward_solve(self.h, _ptr(rho1_out)))
+        return rho1_out
+
+    def adjoint_solve(self, lambda0_out=None):
+        self._check(lib().dr_adjoint_solve(self.h, _ptr(lambda0_out)))
+        return lambda0_out
+
+    def hessian_matvec(self, vt, Hvt=None):
+        if Hvt is None:
+            Hvt = self.vector(vt.device)
+        self._check(lib().dr_hessian_matvec(self.h, self._in(vt), _ptr(Hvt)))
+        return Hvt
+
+    def precond_apply(self, r, z=None):
+        if z is None:
+            z = self.vector(r.device)
+        self._check(lib().dr_precond_apply(self.h, self._in(r), _ptr(z)))
+        return z
+
+    def sync(self):
+        self._check(lib().dr_sync(self.h))
+
+    # ---- test hooks ----
+    def op_spectral(self, op: int, x, out=None):
+        if out is None:
+            out = self.vector() if op in (DR_OP_GRAD, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY) else self.scalar()
+        self._check(lib().dr_op_spectral(self.h, op, self._in(x), _ptr(out)))
+        return out
+
+    def op_interp(self, f, s, out=None):
+        s = s.contiguous()
+        npts = s.shape[-1]
+        if out is None:
+            out = torch.empty(npts, dtype=self.cfg.dtype, device=self.device)
+        self._check(lib().dr_op_interp(self.h, self._in(f), npts, self._in(s), _ptr(out)))
+        return out
+
+    def get_departure(self, sigma: int):
+        out = self.vector()
+        self._check(lib().dr_get_departure(self.h, sigma, _ptr(out)))
+        return out
+
+    def get_field(self, which: int, j: int = 0):
+        vec = which in (DR_FIELD_STATE_GRAD, DR_FIELD_BTILDE, DR_FIELD_VELOCITY)
+        out = self.vector() if vec else self.scalar()
+        self._check(lib().dr_get_field(self.h, which, j, _ptr(out)))
+        return out

@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): relative L2 <= 1e-5 per operator and <= 1e-4 per Hessian matvec for
+the fp32 build; the data term P b~ is checked on its own as well (SURVEY P16'), since beta A vt
+dominates |H vt| for H2.  The fp64 build (DR_FP64, BASELINE config 1) is held to 1e-12 / 1e-11.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL32_OP, TOL32_MV = 1e-5, 1e-4
+TOL64_OP, TOL64_MV = 1e-12, 1e-11
+
+
+@pytest.fixture(scope="module")
+def dr():
+    from paper_1608_03630_b200 import build
+    build.build()
+    import paper_1608_03630_b200 as m
+    m.lib()
+    return m
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def np64(t):
+    return t.detach().to("cpu", torch.float64).numpy()
+
+
+def prep(x, fp64):
+    """Round once to the GPU dtype; the oracle gets the rounded values."""
+    g = x if fp64 else synth.round32(x)
+    return g.contiguous(), synth.promote64(g)
+
+
+def tols(fp64):
+    return (TOL64_OP, TOL64_MV) if fp64 else (TOL32_OP, TOL32_MV)
+
+
+# ------------------------------------------------------------------ spectral operators
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("n", [(32, 16, 64), (64, 64, 64), (8, 4, 16)])
+def test_spectral_ops(dr, n, fp64):
+    tol = tols(fp64)[0]
+    for reg in (1, 2):
+        cfg = dr.Config(n=n, nt=2, reg=reg, beta=0.37, fp64=fp64)
+        ctx = dr.Context(cfg)
+        f, f64 = prep(synth.blobs(5, n, kcut=min(n) // 3), fp64)
+        u, u64 = prep(synth.smooth_vec(6, n, kmax=min(n) // 3), fp64)
+        f, u = f.cuda(), u.cuda()
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_GRAD, f)), O.grad(f64)) < tol
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_DIV, u)), O.div(u64)) < tol
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_REG, u)), O.reg_apply(u64, reg, 0.37)) < tol
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, False)) < tol
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, u)), O.leray(u64)) < tol
+        ci = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37, fp64=fp64, isochoric=True))
+        assert rel(np64(ci.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, True)) < tol
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_spectral_white_noise_nyquist(dr, fp64):
+    """White noise carries Nyquist content: both sides must zero it in odd symbols (reading A2)."""
+    n = (16, 32, 8)
+    tol = tols(fp64)[0]
+    ctx = dr.Context(dr.Config(n=n, nt=2, fp64=fp64))
+    g = torch.Generator().manual_seed(3)
+    f, f64 = prep(torch.randn((8, 32, 16), generator=g, dtype=torch.float64), fp64)
+    u, u64 = prep(torch.randn((3, 8, 32, 16), generator=g, dtype=torch.float64), fp64)
+    assert rel(np64(ctx.op_spectral(dr.DR_OP_GRAD, f.cuda())), O.grad(f64)) < tol
+    assert rel(np64(ctx.op_spectral(dr.DR_OP_DIV, u.cuda())), O.div(u64)) < tol
+    assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, u.cuda())), O.leray(u64)) < tol
+    assert rel(np64(ctx.op_spectral(dr.DR_OP_REG, u.cuda())), O.reg_apply(u64, 2, 1e-2)) < tol
+
+
+# ------------------------------------------------------------------ interpolation
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_interp_points(dr, fp64):
+    n = (32, 16, 64)
+    ctx = dr.Context(dr.Config(n=n, nt=2, fp64=fp64))
+    f, f64 = prep(synth.blobs(7, n, kcut=6), fp64)
+    rng = np.random.default_rng(0)
+    s = np.concatenate([rng.uniform(-40, 100, (3, 5000)),
+                        np.array([[0, 31, 5], [0, 15, 3], [0, 63, 7]], dtype=np.float64)], axis=1)  # + exact nodes
+    st = torch.tensor(s, dtype=torch.float64 if fp64 else torch.float32)
+    out = np64(ctx.op_interp(f.cuda(), st.cuda()))
+    ref = O.interp(f64, synth.promote64(st))
+    assert rel(out, ref) < tols(fp64)[0]
+    # node exactness: t = 0 reproduces the node value exactly
+    fv = np64(f)
+    assert out[-3] == fv[0, 0, 0] and out[-2] == fv[3, 15, 31] and out[-1] == fv[7, 3, 5]
+    # empty input is a no-op
+    ctx.op_interp(f.cuda(), torch.zeros((3, 0), dtype=f.dtype, device="cuda"))
+
+
+# ------------------------------------------------------------------ transport, departure points, state/adjoint
+
+CASES = [
+    # name, n, nt, velocity generator, iso
+    ("cfg1", 32, 4, lambda n: synth.v_cfg1(n), True),
+    ("vstar64", 64, 8, lambda n: synth.v_star(n), False),
+    ("smooth_aniso", (64, 32, 16), 4, lambda n: synth.smooth_vec(9, n, kmax=4, cells_per_step=2.0, nt=4), False),
+    # large displacement (~9 cells/step): boxes exceed the shared-memory capacity -> global fallback tiles
+    ("stress", 64, 4, lambda n: synth.smooth_vec(10, n, kmax=6, cells_per_step=9.0, nt=4), False),
+]
+
+
+def setup_case(dr, name, n, nt, vgen, iso, fp64, reg=2, beta=1e-2):
+    cfg = dr.Config(n=n, nt=nt, reg=reg, beta=beta, isochoric=iso, fp64=fp64)
+    ctx = dr.Context(cfg)
+    rT, rT64 = prep(synth.blobs(11, n, kcut=10) if name != "cfg1" else synth.rho_t_paper(n), fp64)
+    rR, rR64 = prep(synth.blobs(12, n, kcut=10), fp64)
+    v, v64 = prep(vgen(n), fp64)
+    ctx.set_images(rT.cuda(), rR.cuda())
+    ctx.set_velocity(v.cuda())
+    prob = O.Problem(rho_T=rT64, rho_R=rR64, nt=nt, reg=reg, beta=beta, iso=iso)
+    return ctx, prob, v64
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_departure_state_adjoint(dr, case, fp64):
+    name, n, nt, vgen, iso = case
+    tol = tols(fp64)[0]
+    ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, fp64)
+    st = O.set_velocity(prob, v64)
+    if iso:
+        assert rel(np64(ctx.get_field(dr.DR_FIELD_VELOCITY)), st.v) < tol
+    assert rel(np64(ctx.get_departure(+1)), st.d_plus) < tol
+    assert rel(np64(ctx.get_departure(-1)), st.d_minus) < tol
+    if not iso:
+        Db = O.sl_gather(st.Dv, st.d_minus)
+        m_ref = 1 + 0.5 / nt * (Db + st.Dv + Db * st.Dv / nt)
+        assert rel(np64(ctx.get_field(dr.DR_FIELD_MULTIPLIER)) - 1, m_ref - 1) < 10 * tol
+    ctx.forward_solve()
+    for j in range(nt + 1):
+        assert rel(np64(ctx.get_field(dr.DR_FIELD_STATE, j)), st.rho[j]) < tol, j
+        assert rel(np64(ctx.get_field(dr.DR_FIELD_STATE_GRAD, j)), st.G[j]) < tol, j
+    ctx.adjoint_solve()
+    lam = O.adjoint_solve(prob, st)
+    for j in range(nt + 1):
+        assert rel(np64(ctx.get_field(dr.DR_FIELD_ADJOINT, j)), lam[j]) < tol, j
+
+
+def test_departure_single_step_on_gpu_inputs(dr):
+    """Exact per-step parity: oracle interpolation of the GPU's own rho_j at the GPU's departure points
+    reproduces the GPU's rho_{j+1} (isolates the gather kernel from accumulated rounding)."""
+    ctx, prob, v64 = setup_case(dr, "stress", 64, 4, CASES[3][3], False, False)
+    ctx.forward_solve()
+    d = np64(ctx.get_departure(+1))
+    for j in range(4):
+        rj = np64(ctx.get_field(dr.DR_FIELD_STATE, j))
+        ref = O.sl_gather(rj, d)
+        assert rel(np64(ctx.get_field(dr.DR_FIELD_STATE, j + 1)), ref) < 1e-6
+
+
+# ------------------------------------------------------------------ Hessian matvec
+
+def check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, iso):
+    top, tmv = tols(fp64)
+    st = O.set_velocity(prob, v64)
+    ctx.forward_solve()
+    Hv = np64(ctx.hessian_matvec(vt.cuda()))
+    ref, parts = O.hessian_matvec(prob, st, vt64, parts=True)
+    # per term (SURVEY P16'): the data term P b~ on its own, then beta A vt, then the sum
+    bt_gpu = ctx.get_field(dr.DR_FIELD_BTILDE)
+    bt = np64(bt_gpu)
+    assert rel(bt, parts["btilde"]) < tmv
+    if iso:
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, bt_gpu)), parts["data"]) < tmv
+    assert rel(np64(ctx.get_field(dr.DR_FIELD_INC_STATE)), parts["rho_tilde"][-1]) < tmv
+    for j in range(prob.nt + 1):
+        assert rel(np64(ctx.get_field(dr.DR_FIELD_INC_ADJOINT, j)), parts["lam_tilde"][j]) < tmv, j
+    reg = np64(ctx.op_spectral(dr.DR_OP_REG, vt.cuda()))
+    assert rel(reg, parts["reg"]) < top
+    assert rel(Hv, ref) < tmv
+    return Hv
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("zero_residual", [True, False])
+def test_matvec_config2(dr, zero_residual, fp64):
+    """BASELINE config 2: 64^3, nt = 8, H1, beta = 1e-2, v* (div v != 0 -> multiplier path), random smooth
+    vt (|k| <= 8, unit RMS); rho_R = rho(1)[v] (zero residual, GN == Newton; reading A13) or rho_R = rho_T."""
+    n, nt = 64, 8
+    cfg = dr.Config(n=n, nt=nt, reg=dr.DR_REG_H1, beta=1e-2, fp64=fp64)
+    ctx = dr.Context(cfg)
+    rT, rT64 = prep(synth.rho_t_paper(n), fp64)
+    v, v64 = prep(synth.v_star(n), fp64)
+    ctx.set_images(rT.cuda(), rT.cuda())
+    ctx.set_velocity(v.cuda())
+    if zero_residual:
+        rho1 = ctx.forward_solve(torch.empty_like(rT).cuda())
+        rR, rR64 = rho1.cpu().contiguous(), synth.promote64(rho1.cpu())
+        ctx.set_images(rT.cuda(), rho1)
+    else:
+        rR, rR64 = rT, rT64
+    prob = O.Problem(rho_T=rT64, rho_R=rR64, nt=nt, reg=1, beta=1e-2)
+    vt, vt64 = prep(synth.smooth_vec(2, n, kmax=8), fp64)
+    check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, False)
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_matvec_cases(dr, case, fp64):
+    name, n, nt, vgen, iso = case
+    ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, fp64)
+    vt, vt64 = prep(synth.smooth_vec(21, n, kmax=6, divfree=iso), fp64)
+    check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, iso)
+
+
+@pytest.mark.parametrize("iso", [False, True])
+def test_precond_apply(dr, iso):
+    n = (32, 64, 16)
+    ctx = dr.Context(dr.Config(n=n, nt=2, reg=2, beta=1e-2, isochoric=iso))
+    r, r64 = prep(synth.smooth_vec(31, n, kmax=8), False)
+    z = np64(ctx.precond_apply(r.cuda()))
+    assert rel(z, O.precond(r64, 2, 1e-2, iso)) < TOL32_OP
+    # in-place (r and z may alias)
+    rc = r.cuda().clone()
+    ctx.precond_apply(rc, rc)
+    assert rel(np64(rc), z) < 1e-7
+
+
+# ------------------------------------------------------------------ ABI behaviour on the GPU
+
+def test_host_buffers_match_device_buffers(dr):
+    n, nt = 32, 4
+    ctx = dr.Context(dr.Config(n=n, nt=nt))
+    rT = synth.round32(synth.blobs(1, n, kcut=8))
+    v = synth.round32(synth.smooth_vec(2, n, kmax=4, cells_per_step=1.0, nt=nt))
+    vt = synth.round32(synth.smooth_vec(3, n, kmax=4))
+    ctx.set_images(rT, rT)  # host pointers
+    ctx.set_velocity(v.pin_memory())
+    ctx.forward_solve()
+    h_host = ctx.hessian_matvec(vt.pin_memory(), torch.empty_like(vt).pin_memory())
+    h_pageable = ctx.hessian_matvec(vt, torch.empty_like(vt))
+    h_dev = ctx.hessian_matvec(vt.cuda()).cpu()
+    assert torch.equal(h_host, h_dev) and torch.equal(h_pageable, h_dev)
+    z_host = ctx.precond_apply(vt, torch.empty_like(vt))
+    assert torch.equal(z_host, ctx.precond_apply(vt.cuda()).cpu())
+
+
+def test_call_order_and_argument_errors(dr):
+    n = 16
+    ctx = dr.Context(dr.Config(n=n, nt=2))
+    vt = torch.zeros((3, n, n, n), device="cuda")
+    with pytest.raises(dr.DiffRegError) as e:
+        ctx.hessian_matvec(vt)
+    assert e.value.status == dr.DR_ERR_ORDER
+    with pytest.raises(dr.DiffRegError) as e:
+        ctx.forward_solve()
+    assert e.value.status == dr.DR_ERR_ORDER
+    with pytest.raises(dr.DiffRegError) as e:
+        ctx.adjoint_solve()
+    assert e.value.status == dr.DR_ERR_ORDER
+    f = torch.zeros((n, n, n), device="cuda")
+    ctx.set_images(f, f)
+    ctx.set_velocity(vt)
+    ctx.forward_solve()
+    with pytest.raises(dr.DiffRegError) as e:
+        ctx.hessian_matvec(vt, vt)  # aliasing
+    assert e.value.status == dr.DR_ERR_ARG
+    # zero velocity, zero probe: H 0 = 0 exactly
+    assert torch.count_nonzero(ctx.hessian_matvec(vt)) == 0
+    ctx.set_velocity(vt)  # invalidates the state
+    with pytest.raises(dr.DiffRegError) as e:
+        ctx.hessian_matvec(vt)
+    assert e.value.status == dr.DR_ERR_ORDER
+
+
+def test_matvec_linearity_and_determinism(dr):
+    n, nt = 32, 4
+    ctx = dr.Context(dr.Config(n=n, nt=nt))
+    rT = synth.round32(synth.blobs(1, n, kcut=8)).cuda()
+    ctx.set_images(rT, rT)
+    ctx.set_velocity(synth.round32(synth.smooth_vec(2, n, kmax=4, cells_per_step=1.5, nt=nt)).cuda())
+    ctx.forward_solve()
+    x = synth.round32(synth.smooth_vec(3, n, kmax=4)).cuda()
+    y = synth.round32(synth.smooth_vec(4, n, kmax=4)).cuda()
+    hx, hy = ctx.hessian_matvec(x), ctx.hessian_matvec(y)
+    h = ctx.hessian_matvec((2 * x - 3 * y).contiguous())
+    assert rel(np64(h), np64(2 * hx - 3 * hy)) < 1e-6
+    assert torch.equal(ctx.hessian_matvec(x), hx)  # bitwise deterministic
