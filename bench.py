@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Gauss-Newton Hessian matvec (arXiv 1608.03630), BASELINE.json config 3.
+
+Workload (one "step" = one pass of the whole hot path, i.e. what one
+Newton iteration with 10 Krylov iterations asks of the library):
+    set_velocity(v)            RK2 departure points for +v and -v, plans, div v, multiplier m
+    forward_solve()            state transport + cached state gradients
+    adjoint_solve()            adjoint transport
+    10 x { hessian_matvec(vt_i) ; precond_apply(H vt_i) }
+Grid 256^3, n_t = 4, fp32, H2 (biharmonic) regularisation, beta = 1e-2, Gauss-Newton, non-isochoric.
+Inputs: rho_T = blobs(100), rho_R = blobs(101) (16 anisotropic Gaussians, |k| <= 64), v = smooth_vec(3)
+scaled to 2 cells / step, vt_i = smooth_vec(1000 + i) (unit RMS, |k| <= 8).  All synthetic, seeded.
+
+Metric: Hessian matvecs/s (value) and voxel-steps/s.  One JSON line on rank 0.
+`--impl reference` times the fp64 CPU oracle (the only reference this paper-only task has).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+NT = 4
+N = 256
+NMV = 10
+METRIC = "Hessian matvecs/s at 256^3 (fp32, n_t=4, H2, GN; step = setup + fwd/adj solves + 10x(matvec+precond))"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=N)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile-out", default=None, help="write the per-kernel table (JSON) here")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- inputs
+
+def make_inputs(n, device):
+    import synth
+    rT = synth.round32(synth.blobs(100, n, device=device)).contiguous()
+    rR = synth.round32(synth.blobs(101, n, device=device)).contiguous()
+    v = synth.round32(synth.smooth_vec(3, n, kmax=8, cells_per_step=2.0, nt=NT, device=device)).contiguous()
+    vts = [synth.round32(synth.smooth_vec(1000 + i, n, kmax=8, device=device)).contiguous() for i in range(NMV)]
+    return rT, rR, v, vts
+
+
+# ----------------------------------------------------------------------------- algorithmic bytes per launch
+
+def algo_bytes(tag, n, nt, es=4):
+    """SURVEY.md §8(d) reference dataflow: each kernel reads each operand once and writes each produced
+    field once.  Spectra: forward half spectra complex128 (16 B), inverse complex64 (8 B)."""
+    M = n ** 3
+    Sc = (n // 2 + 1) * n * n
+    table = {
+        "sl_inc_state": 11 * es * M,      # gather g_j 1, d+ 3, vt 3, G_{j+1} 3, write 1
+        "sl_inc_adjoint": 6 * es * M,     # gather 1, d- 3, m 1, write 1
+        "sl_state": 5 * es * M,           # gather 1, d+ 3, write 1
+        "sl_adjoint": 6 * es * M,
+        "sl_multiplier": 6 * es * M,      # gather D 1, d- 3, D 1, write m 1
+        "sl_departure": 12 * es * M,      # gather v 3, d* 3, v 3, write d 3
+        "quadrature": (4 * (nt + 1) + 3) * es * M,
+        "inc_init": 7 * es * M,
+        "sub": 3 * es * M,
+        "dstar": 6 * es * M,
+        "row_deriv": 2 * es * M,
+        "col_deriv": 2 * es * M,          # (+1 read when accumulating; counted as 2)
+        "row_r2c": es * M + 16 * Sc,
+        "col_fft_fwd": 2 * 16 * Sc,       # forward x2 pass, complex128 in and out
+        "col_fft_inv": 2 * 8 * Sc,        # inverse x2 pass, complex64 in and out
+        "col_middle": 16 * Sc + 8 * Sc,
+        "row_c2r": 8 * Sc + 2 * es * M,   # spectrum in, (b~ in), real out
+    }
+    return table.get(tag)
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- distributed plumbing
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- oracle timing (CPU)
+
+def oracle_matvec_sample(n, rT, rR, v, vt, setup_from=None):
+    """Time one fp64 oracle GN matvec on the 256^3 workload.  If `setup_from` (a GPU context) is given,
+    the per-velocity state (departure points, multiplier source, state gradients) is copied from it so
+    that the bounded sample is the matvec alone; otherwise the oracle computes its own setup (untimed)."""
+    import synth
+    from oracle import oracle as O
+    prob = O.Problem(rho_T=synth.promote64(rT), rho_R=synth.promote64(rR), nt=NT, reg=2, beta=1e-2)
+    if setup_from is None:
+        st = O.set_velocity(prob, synth.promote64(v))
+    else:
+        import paper_1608_03630_b200 as dr
+        ctx = setup_from
+        st = O.VelocityState(v=synth.promote64(v), d_plus=synth.promote64(ctx.get_departure(+1)),
+                             d_minus=synth.promote64(ctx.get_departure(-1)), Dv=None)
+        # the oracle's adjoint source needs div v; recompute it with the oracle (cheap, untimed)
+        st.Dv = O.div(st.v)
+        st.G = [synth.promote64(ctx.get_field(dr.DR_FIELD_STATE_GRAD, j)) for j in range(NT + 1)]
+    vt64 = synth.promote64(vt)
+    t0 = time.perf_counter()
+    O.hessian_matvec(prob, st, vt64)
+    return time.perf_counter() - t0, O.num_threads(), prob, st, vt64
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import synth
+    from oracle import oracle as O
+    n = args.n
+    rT, rR, v, vts = make_inputs(n, "cuda" if torch.cuda.is_available() else "cpu")
+    rT, rR, v, vts = rT.cpu(), rR.cpu(), v.cpu(), [x.cpu() for x in vts]
+    prob = O.Problem(rho_T=synth.promote64(rT), rho_R=synth.promote64(rR), nt=NT, reg=2, beta=1e-2)
+    t0 = time.perf_counter()
+    st = O.set_velocity(prob, synth.promote64(v))
+    setup_s = time.perf_counter() - t0
+    vt64 = [synth.promote64(x) for x in vts[:2]]
+    for i in range(args.warmup):
+        O.hessian_matvec(prob, st, vt64[i % 2])
+    ts = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        O.hessian_matvec(prob, st, vt64[i % 2])
+        ts.append(time.perf_counter() - t0)
+    T = sum(ts)
+    value = args.steps / T
+    cores = O.num_threads()
+    sample = (f"one fp64 oracle GN matvec per step at {n}^3 (n_t={NT}, H2); the per-velocity setup "
+              f"(departure points, state solve, gradients: {setup_s:.1f} s) is untimed")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"cfg3 {n}^3 nt={NT} H2 beta=1e-2 GN non-isochoric (oracle sample)",
+                      "grid": [n] * 3, "nt": NT},
+           "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, ws, rank, local):
+    import paper_1608_03630_b200 as dr
+    n = args.n
+    dev = torch.device("cuda", local)
+    M = n ** 3
+    cfg = dr.Config(n=n, nt=NT, reg=dr.DR_REG_H2, beta=1e-2)
+    ctx = dr.Context(cfg, device=dev)
+    rT, rR, v, vts = make_inputs(n, dev)
+    ctx.set_images(rT, rR)
+    Hv = [torch.empty_like(vts[0]) for _ in range(NMV)]
+    Z = [torch.empty_like(vts[0]) for _ in range(NMV)]
+    stream = ctx.stream
+
+    def step(v_, vts_, Hv_, Z_):
+        ctx.set_velocity(v_)
+        ctx.forward_solve()
+        ctx.adjoint_solve()
+        for i in range(NMV):
+            ctx.hessian_matvec(vts_[i], Hv_[i])
+            ctx.precond_apply(Hv_[i], Z_[i])
+
+    for _ in range(args.warmup):
+        step(v, vts, Hv, Z)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs)
+    ctx.profile_reset()
+    ctx.profile_enable(True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(v, vts, Hv, Z)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    prof, launches = ctx.profile()
+    ctx.profile_enable(False)
+    ms_max = max_over_ranks(ms, ws)
+    T = ms_max / 1e3
+    value = ws * args.steps * NMV / T
+    vox_steps = ws * args.steps * (NT * M + NT * M + NMV * 2 * NT * M) / T
+
+    # ---- matvec-only throughput (secondary)
+    torch.cuda.synchronize()
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m0.record(stream)
+    for i in range(NMV):
+        ctx.hessian_matvec(vts[i], Hv[i])
+    m1.record(stream)
+    torch.cuda.synchronize()
+    mv_ms = m0.elapsed_time(m1) / NMV
+
+    # ---- dominant kernel roofline (algorithmic bytes / live CUDA-event duration)
+    peak, peak_kind = peaks()
+    table = []
+    for tag, (k, tms) in prof.items():
+        b = algo_bytes(tag, n, NT)
+        avg = tms / k
+        table.append({"tag": tag, "launches": k, "total_ms": tms, "avg_ms": avg, "share": tms / ms,
+                      "algo_bytes": b, "gbs": (b / (avg / 1e3) / 1e9) if b else None})
+    table.sort(key=lambda r: -r["total_ms"])
+    dom = table[0]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom["tag"])
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": dom["tag"], "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+            "frac": dom["gbs"] / peak if dom["gbs"] else None, "traffic": traffic,
+            "peak_kind": peak_kind, "algo_bytes_per_launch": dom["algo_bytes"], "avg_launch_ms": dom["avg_ms"],
+            "share_of_step": dom["share"]}
+    if args.profile_out and rank == 0:
+        with open(args.profile_out, "w") as f:
+            json.dump({"step_ms": ms / args.steps, "kernels": table, "matvec_ms": mv_ms}, f, indent=1)
+
+    # ---- e2e: the same step through the C ABI with host buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hT, hR, hv = rT.cpu().pin_memory(), rR.cpu().pin_memory(), v.cpu().pin_memory()
+        hvts = [x.cpu().pin_memory() for x in vts]
+        hHv = [torch.empty_like(x).pin_memory() for x in hvts]
+        hZ = [torch.empty_like(x).pin_memory() for x in hvts]
+
+        def step_host():
+            ctx.set_images(hT, hR)
+            step(hv, hvts, hHv, hZ)
+
+        step_host()
+        torch.cuda.synchronize()
+        barrier(ws)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        ksteps = max(1, min(args.steps, 3))
+        for _ in range(ksteps):
+            step_host()
+        h1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        hms = max_over_ranks(h0.elapsed_time(h1), ws)
+        fb = 4 * M
+        e2e = {"value": ws * ksteps * NMV / (hms / 1e3), "unit": "matvec/s",
+               "h2d_bytes_per_step": 2 * fb + 3 * fb + NMV * (3 * fb + 3 * fb),
+               "d2h_bytes_per_step": NMV * (3 * fb + 3 * fb), "steps": ksteps}
+
+    # ---- CPU baseline: the oracle, rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            secs, cores, *_ = oracle_matvec_sample(n, rT.cpu(), rR.cpu(), v.cpu(), vts[0].cpu(), setup_from=ctx)
+            cpu = {"value": 1.0 / secs, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+                   "sample": f"one fp64 oracle GN matvec at {n}^3 (n_t={NT}, H2) on {cores} OpenMP threads; "
+                             f"its per-velocity inputs (departure points, state gradients) copied from the GPU "
+                             f"setup; {secs:.1f} s"}
+        except Exception as ex:  # the baseline must not take the bench line down
+            cpu = {"value": None, "unit": "matvec/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {ex!r}"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "config": {"workload": f"cfg3: {n}^3 nt={NT} H2 beta=1e-2 GN non-isochoric; step = set_velocity + "
+                                      f"forward_solve + adjoint_solve + {NMV} x (hessian_matvec + precond_apply)",
+                          "grid": [n] * 3, "nt": NT, "reg": "H2", "beta": 1e-2, "isochoric": False,
+                          "matvecs_per_step": NMV,
+                          "l2": "inputs larger than L2 (working set ~%.1f GB >> 126 MB)" % (
+                              dr.dr_workspace_bytes(cfg) / 1e9),
+                          "parallelism": "single" if ws == 1 else f"replicas x{ws}"},
+               "voxel_steps_per_s": vox_steps, "matvec_only_ms": mv_ms,
+               "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu}
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args) if torch.cuda.is_available() else (1, 0, 0)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

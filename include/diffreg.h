@@ -127,6 +127,18 @@ dr_status dr_sync(dr_ctx* ctx);
 const char* dr_last_error(const dr_ctx* ctx);
 const char* dr_status_string(dr_status s);
 
+/* ---------------------------------------------------------------- tracing
+ * Launch accounting is always on: every kernel launch of the context is counted.  With profiling
+ * enabled, each launch is additionally bracketed by two CUDA events on the context stream and the
+ * elapsed GPU time is accumulated per kernel tag (e.g. "sl_inc_state", "col_middle").  Reading the
+ * profile synchronises the stream.  dr_profile_reset clears the tags and the launch counter. */
+dr_status dr_profile_enable(dr_ctx* ctx, int enable);
+dr_status dr_profile_reset(dr_ctx* ctx);
+/* number of distinct tags so far, and the total number of kernel launches since the last reset */
+dr_status dr_profile_count(dr_ctx* ctx, int* n_entries, int64_t* launches);
+/* entry i: tag (copied into name[name_len], NUL-terminated), launches and summed GPU milliseconds */
+dr_status dr_profile_entry(dr_ctx* ctx, int i, char* name, int name_len, int64_t* launches, double* total_ms);
+
 /* ---------------------------------------------------------------- per-operator test hooks
  * Device pointers only.  They run the same kernels as the main path. */
 enum { DR_OP_GRAD = 0,    /* in: scalar   out: vector   grad f  (i k' per axis)       */

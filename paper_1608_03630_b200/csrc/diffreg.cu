@@ -30,10 +30,14 @@ struct DrError {
 [[noreturn]] void fail(dr_status s, const std::string& m) { throw DrError{s, m}; }
 
 void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) fail(DR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear the non-sticky error so the next call starts clean
+        fail(DR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
 }
 #define CK(x) ck((x), #x)
 #define CKL(name) ck(cudaGetLastError(), name)
+// launch bracketing: PB() before a kernel launch, PE(tag) after it (error check + accounting + profiling)
 
 int ilog2(int n) {
     int l = 0;
@@ -74,8 +78,8 @@ int64_t n_tiles(const Grid& g) {
 
 // Workspace layout (byte offsets, 256-aligned).  Field counts in units of M values of type T.
 struct Layout {
-    size_t rhoT, rhoR, v, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, spec, plan_p, plan_m, plan_t,
-        maxext, twx, twy, twz, total;
+    size_t rhoT, rhoR, v, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, plan_p, plan_m,
+        plan_t, maxext, twx, twy, twz, twxd, twyd, twzd, total;
 };
 
 Layout layout(const dr_config* c) {
@@ -106,7 +110,8 @@ Layout layout(const dr_config* c) {
     L.tmp3 = take(3 * F);                     // d* and scratch
     L.stin = take(3 * F);                     // host staging in
     L.stout = take(3 * F);                    // host staging out
-    L.spec = take(6 * (size_t)g.S * 2 * es);  // six half spectra
+    L.specD = take(6 * (size_t)g.S * 16);     // six forward half spectra, complex<double>
+    L.specF = take(3 * (size_t)g.S * 2 * es); // three inverse-direction half spectra, complex<T>
     const size_t pb = (size_t)n_tiles(g) * PLAN_INTS * sizeof(int);
     L.plan_p = take(pb);
     L.plan_m = take(pb);
@@ -115,6 +120,9 @@ Layout layout(const dr_config* c) {
     L.twx = take((size_t)g.n1 * 2 * es);
     L.twy = take((size_t)g.n2 * 2 * es);
     L.twz = take((size_t)g.n3 * 2 * es);
+    L.twxd = take((size_t)g.n1 * 16);
+    L.twyd = take((size_t)g.n2 * 16);
+    L.twzd = take((size_t)g.n3 * 16);
     L.total = off;
     return L;
 }
@@ -131,9 +139,63 @@ struct dr_ctx {
     bool have_images = false, have_velocity = false, have_state = false, have_adjoint = false, have_matvec = false;
     int cap_p[3] = {0, 0, 0}, cap_m[3] = {0, 0, 0};
     std::string err;
+    // launch accounting and optional per-kernel CUDA-event profiling (dr_profile_*)
+    int64_t launches = 0;
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Pending { const char* tag; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    struct Acc { std::string tag; int64_t n = 0; double ms = 0; };
+    std::vector<Acc> acc;
+    cudaEvent_t cur_start = nullptr;
+    cudaEvent_t take_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+    void prof_begin() {
+        if (prof) {
+            cur_start = take_event();
+            cudaEventRecord(cur_start, stream);
+        }
+    }
+    void prof_end(const char* tag);
+    void prof_flush();
     template <typename T>
     T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
 };
+
+void dr_ctx::prof_end(const char* tag) {
+    ck(cudaGetLastError(), tag);
+    ++launches;
+    if (prof) {
+        cudaEvent_t e = take_event();
+        cudaEventRecord(e, stream);
+        pending.push_back(Pending{tag, cur_start, e});
+    }
+}
+
+void dr_ctx::prof_flush() {
+    if (pending.empty()) return;
+    CK(cudaEventSynchronize(pending.back().b));
+    for (const Pending& p : pending) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, p.a, p.b));
+        auto it = std::find_if(acc.begin(), acc.end(), [&](const Acc& a) { return a.tag == p.tag; });
+        if (it == acc.end()) {
+            acc.push_back(Acc{p.tag, 0, 0});
+            it = acc.end() - 1;
+        }
+        it->n += 1;
+        it->ms += ms;
+    }
+    pending.clear();
+    ev_used = 0;
+}
 
 namespace {
 
@@ -143,6 +205,8 @@ struct Impl {
     const Grid& g;
     cudaStream_t s;
     explicit Impl(dr_ctx& cc) : c(cc), g(cc.g), s(cc.stream) {}
+    void PB() { c.prof_begin(); }
+    void PE(const char* tag) { c.prof_end(tag); }
 
     T dt() const { return T(1) / T(c.cfg.nt); }
     T* rhoT() { return c.at<T>(c.L.rhoT); }
@@ -161,10 +225,14 @@ struct Impl {
     T* tmp3() { return c.at<T>(c.L.tmp3); }
     T* stin() { return c.at<T>(c.L.stin); }
     T* stout() { return c.at<T>(c.L.stout); }
-    Cx<T>* spec(int i) { return c.at<Cx<T>>(c.L.spec) + (size_t)i * g.S; }
+    Cx<double>* specD(int i) { return c.at<Cx<double>>(c.L.specD) + (size_t)i * g.S; }
+    Cx<T>* specF(int i) { return c.at<Cx<T>>(c.L.specF) + (size_t)i * g.S; }
     const Cx<T>* twx() { return c.at<Cx<T>>(c.L.twx); }
     const Cx<T>* twy() { return c.at<Cx<T>>(c.L.twy); }
     const Cx<T>* twz() { return c.at<Cx<T>>(c.L.twz); }
+    const Cx<double>* twxd() { return c.at<Cx<double>>(c.L.twxd); }
+    const Cx<double>* twyd() { return c.at<Cx<double>>(c.L.twyd); }
+    const Cx<double>* twzd() { return c.at<Cx<double>>(c.L.twzd); }
     T* mult_or_null() { return (c.cfg.flags & DR_ISOCHORIC) ? nullptr : mult(); }
 
     int grid_1d(int64_t n, int block = 256) const {
@@ -173,27 +241,31 @@ struct Impl {
     }
 
     // -------------------------------------------------------------------- twiddle tables
+    template <typename U>
+    void fill_twiddles(int n, size_t off) {
+        std::vector<Cx<U>> h(n);
+        for (int m = 0; m < n; ++m) {
+            const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)n;
+            h[m].re = (U)std::cos(a);
+            h[m].im = (U)std::sin(a);
+        }
+        CK(cudaMemcpyAsync(c.ws + off, h.data(), sizeof(Cx<U>) * n, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
     void init_twiddles() {
-        auto fill = [&](int n, size_t off) {
-            std::vector<Cx<T>> h(n);
-            for (int m = 0; m < n; ++m) {
-                const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)n;
-                h[m].re = (T)std::cos(a);
-                h[m].im = (T)std::sin(a);
-            }
-            CK(cudaMemcpyAsync(c.ws + off, h.data(), sizeof(Cx<T>) * n, cudaMemcpyHostToDevice, s));
-            CK(cudaStreamSynchronize(s));
-        };
-        fill(g.n1, c.L.twx);
-        fill(g.n2, c.L.twy);
-        fill(g.n3, c.L.twz);
+        fill_twiddles<T>(g.n1, c.L.twx);
+        fill_twiddles<T>(g.n2, c.L.twy);
+        fill_twiddles<T>(g.n3, c.L.twz);
+        fill_twiddles<double>(g.n1, c.L.twxd);
+        fill_twiddles<double>(g.n2, c.L.twyd);
+        fill_twiddles<double>(g.n3, c.L.twzd);
     }
 
     // -------------------------------------------------------------------- FFT pass launchers
     template <int L>
     static constexpr int row_rb() { return (256 / LineGeom<L>::TPL) > 0 ? 256 / LineGeom<L>::TPL : 1; }
-    template <int L>
-    static size_t row_smem() { return (size_t)row_rb<L>() * LineGeom<L>::LP * sizeof(Cx<T>); }
+    template <int L, typename U = T>
+    static size_t row_smem() { return (size_t)row_rb<L>() * LineGeom<L>::LP * sizeof(Cx<U>); }
     template <int L>
     int row_blocks() const { return (int)(((int64_t)g.n2 * g.n3 + row_rb<L>() - 1) / row_rb<L>()); }
 
@@ -206,23 +278,26 @@ struct Impl {
     void row_deriv_L(const T* f, T* out, int acc) {
         auto k = k_row_deriv<T, L>;
         set_smem(k, row_smem<L>());
+        PB();
         k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, f, out, acc, twx());
-        CKL("k_row_deriv");
+        PE("row_deriv");
     }
     template <int L>
-    void row_r2c_L(const T* f, Cx<T>* sp) {
-        auto k = k_row_r2c<T, L>;
-        set_smem(k, row_smem<L>());
-        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, f, sp, twx());
-        CKL("k_row_r2c");
+    void row_r2c_L(const T* f, Cx<double>* sp) {
+        auto k = k_row_r2c<T, double, L>;
+        set_smem(k, row_smem<L, double>());
+        PB();
+        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L, double>(), s>>>(g, f, sp, twxd());
+        PE("row_r2c");
     }
     template <int L>
     void row_c2r_L(const Cx<T>* sp, T* out, const T* add) {
         auto k = k_row_c2r<T, L>;
         set_smem(k, row_smem<L>());
         RowOut<T> e{out, add};
+        PB();
         k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, sp, e, twx());
-        CKL("k_row_c2r");
+        PE("row_c2r");
     }
 
 #define DR_SWITCH_ROW(Lval, call)                          \
@@ -257,7 +332,7 @@ struct Impl {
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
     }
-    void row_r2c(const T* f, Cx<T>* sp) {
+    void row_r2c(const T* f, Cx<double>* sp) {
 #define CALL(LL) row_r2c_L<LL>(f, sp)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
@@ -269,21 +344,24 @@ struct Impl {
     }
 
     // columns per CTA: keep NC components of the CTA's lines within ~64 KB of shared memory
-    template <int L, int NC>
+    template <int L, int NC, typename U = T>
     static constexpr int pick_xc() {
-        return (NC * 16 * LineGeom<L>::LP * (int)sizeof(Cx<T>) <= 72 * 1024)  ? 16
-               : (NC * 8 * LineGeom<L>::LP * (int)sizeof(Cx<T>) <= 72 * 1024) ? 8
-               : (NC * 4 * LineGeom<L>::LP * (int)sizeof(Cx<T>) <= 72 * 1024) ? 4
+        return (NC * 16 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024)  ? 16
+               : (NC * 8 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 8
+               : (NC * 4 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 4
                                                                               : 2;
     }
-    template <int L, int XC>
-    static size_t col_smem(int nc) {
-        return (size_t)nc * ColCfg<L, XC>::LINES * LineGeom<L>::LP * sizeof(Cx<T>);
+    template <int L, int XC, int NC, typename U>
+    using CCfg = ColCfg<L, XC, NC, (int)sizeof(Cx<U>)>;
+    template <int L, int XC, int NC, typename U>
+    static size_t col_smem() {
+        return (size_t)NC * CCfg<L, XC, NC, U>::LINES * LineGeom<L>::LP * sizeof(Cx<U>);
     }
-    template <int L, int XC>
+    template <int L, int XC, int NC, typename U>
     int col_blocks(const ColGeom& cg, int nother) const {
         const int nxb = (cg.nx + XC - 1) / XC;
-        return nxb * ((nother + ColCfg<L, XC>::OL - 1) / ColCfg<L, XC>::OL);
+        constexpr int OL = CCfg<L, XC, NC, U>::OL;
+        return nxb * ((nother + OL - 1) / OL);
     }
 
     ColGeom spec_geom() const { return ColGeom{g.n1p, g.n1c, g.n2, g.n3}; }
@@ -294,11 +372,12 @@ struct Impl {
         constexpr int XC = pick_xc<L, 1>();
         const ColGeom cg = pair_geom();
         auto k = k_col_deriv<T, L, XC, AX>;
-        const size_t sm = col_smem<L, XC>(1);
+        const size_t sm = col_smem<L, XC, 1, T>();
         set_smem(k, sm);
-        k<<<col_blocks<L, XC>(cg, AX == 2 ? g.n3 : g.n2), ColCfg<L, XC>::NT, sm, s>>>(
+        PB();
+        k<<<col_blocks<L, XC, 1, T>(cg, AX == 2 ? g.n3 : g.n2), CCfg<L, XC, 1, T>::NT, sm, s>>>(
             cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, AX == 2 ? twy() : twz());
-        CKL("k_col_deriv");
+        PE("col_deriv");
     }
     void col_deriv(int ax, const T* f, T* out, int acc) {
         if (ax == 2) {
@@ -312,45 +391,49 @@ struct Impl {
         }
     }
 
-    template <int L, int DIR>
-    void col_fft_L(Cx<T>* sp) {
-        constexpr int XC = pick_xc<L, 1>();
+    template <typename U, int L, int DIR>
+    void col_fft_L(Cx<U>* sp, const Cx<U>* tw) {
+        const char* tag = DIR < 0 ? "col_fft_fwd" : "col_fft_inv";
+        constexpr int XC = pick_xc<L, 1, U>();
         const ColGeom cg = spec_geom();
-        auto k = k_col_fft<T, L, XC, DIR>;
-        const size_t sm = col_smem<L, XC>(1);
+        auto k = k_col_fft<U, L, XC, DIR>;
+        const size_t sm = col_smem<L, XC, 1, U>();
         set_smem(k, sm);
-        k<<<col_blocks<L, XC>(cg, g.n3), ColCfg<L, XC>::NT, sm, s>>>(cg, sp, twy());
-        CKL("k_col_fft");
+        PB();
+        k<<<col_blocks<L, XC, 1, U>(cg, g.n3), CCfg<L, XC, 1, U>::NT, sm, s>>>(cg, sp, tw);
+        PE(tag);
     }
-    void col_fft(Cx<T>* sp, int dir) {
-        if (dir < 0) {
-#define CALL(LL) col_fft_L<LL, -1>(sp)
-            DR_SWITCH_COL(g.n2, CALL)
+    void col_fft_fwd(Cx<double>* sp) {  // forward along x2, in double
+#define CALL(LL) col_fft_L<double, LL, -1>(sp, twyd())
+        DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
-        } else {
-#define CALL(LL) col_fft_L<LL, +1>(sp)
-            DR_SWITCH_COL(g.n2, CALL)
+    }
+    void col_fft_inv(Cx<T>* sp) {  // inverse along x2, in T
+#define CALL(LL) col_fft_L<T, LL, +1>(sp, twy())
+        DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
-        }
     }
 
     template <int L, int KIND>
-    void middle_L(Cx<T>* const* sp) {
-        constexpr int NCI = Sym<T, KIND>::NCI;
-        constexpr int XC = pick_xc<L, NCI>();
+    void middle_L(Cx<double>* const* in, Cx<T>* const* out) {
+        constexpr int NCI = Sym<double, KIND>::NCI, NCO = Sym<double, KIND>::NCO;
+        constexpr int XC = pick_xc<L, NCI, double>();
         const ColGeom cg = spec_geom();
-        SpecPtrs<T, NCI> io;
-        for (int i = 0; i < NCI; ++i) io.p[i] = sp[i];
+        SpecPtrs<double, NCI> pi;
+        SpecPtrs<T, NCO> po;
+        for (int i = 0; i < NCI; ++i) pi.p[i] = in[i];
+        for (int i = 0; i < NCO; ++i) po.p[i] = out[i];
         SymInfo si{c.cfg.reg, c.cfg.beta, 2.0 / (double)g.M};
-        auto k = k_col_middle<T, L, XC, KIND>;
-        const size_t sm = col_smem<L, XC>(NCI);
+        auto k = k_col_middle<double, T, L, XC, KIND>;
+        const size_t sm = col_smem<L, XC, NCI, double>();
         set_smem(k, sm);
-        k<<<col_blocks<L, XC>(cg, g.n2), ColCfg<L, XC>::NT, sm, s>>>(cg, io, si, twz());
-        CKL("k_col_middle");
+        PB();
+        k<<<col_blocks<L, XC, NCI, double>(cg, g.n2), CCfg<L, XC, NCI, double>::NT, sm, s>>>(cg, pi, po, si, twzd());
+        PE("col_middle");
     }
     template <int KIND>
-    void middle(Cx<T>* const* sp) {
-#define CALL(LL) middle_L<LL, KIND>(sp)
+    void middle(Cx<double>* const* in, Cx<T>* const* out) {
+#define CALL(LL) middle_L<LL, KIND>(in, out)
         DR_SWITCH_COL(g.n3, CALL)
 #undef CALL
     }
@@ -366,30 +449,33 @@ struct Impl {
         col_deriv(2, u3 + g.M, out, 1);
         col_deriv(3, u3 + 2 * g.M, out, 1);
     }
-    // out_c = F^-1[sym F in_c] (+ add_c), componentwise symbol KIND 0/1
+    // out_c = F^-1[sym F in_c] (+ add_c), componentwise symbol KIND 0/1.  Forward passes (x1 r2c, x2)
+    // and the x3 middle pass run in double; the inverse x2 / x1 passes in T.
     template <int KIND>
     void scalar_symbol3(const T* in3, T* out3, const T* add3) {
         for (int cc = 0; cc < 3; ++cc) {
-            Cx<T>* sp = spec(0);
-            row_r2c(in3 + cc * g.M, sp);
-            col_fft(sp, -1);
-            middle<KIND>(&sp);
-            col_fft(sp, +1);
-            row_c2r(sp, out3 + cc * g.M, add3 ? add3 + cc * g.M : nullptr);
+            Cx<double>* sd = specD(0);
+            Cx<T>* sf = specF(0);
+            row_r2c(in3 + cc * g.M, sd);
+            col_fft_fwd(sd);
+            middle<KIND>(&sd, &sf);
+            col_fft_inv(sf);
+            row_c2r(sf, out3 + cc * g.M, add3 ? add3 + cc * g.M : nullptr);
         }
     }
     // coupled 3-component symbol (KIND 2, 3): out = F^-1[sym F in]
     template <int KIND>
     void vector_symbol3(const T* in3, T* out3) {
-        Cx<T>* sp[3] = {spec(0), spec(1), spec(2)};
+        Cx<double>* sd[3] = {specD(0), specD(1), specD(2)};
+        Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
         for (int cc = 0; cc < 3; ++cc) {
-            row_r2c(in3 + cc * g.M, sp[cc]);
-            col_fft(sp[cc], -1);
+            row_r2c(in3 + cc * g.M, sd[cc]);
+            col_fft_fwd(sd[cc]);
         }
-        middle<KIND>(sp);
+        middle<KIND>(sd, sf);
         for (int cc = 0; cc < 3; ++cc) {
-            col_fft(sp[cc], +1);
-            row_c2r(sp[cc], out3 + cc * g.M, nullptr);
+            col_fft_inv(sf[cc]);
+            row_c2r(sf[cc], out3 + cc * g.M, nullptr);
         }
     }
     void reg_apply(const T* in3, T* out3) { scalar_symbol3<0>(in3, out3, nullptr); }
@@ -404,45 +490,54 @@ struct Impl {
         int* mx = c.at<int>(c.L.maxext);
         const int init[3] = {INT_MIN, INT_MIN, INT_MIN};
         CK(cudaMemcpyAsync(mx, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        PB();
         k_sl_plan<T><<<(unsigned)n_tiles(g), SL_THREADS, 0, s>>>(g, d, plan_buf, mx);
-        CKL("k_sl_plan");
+        PE("sl_plan");
         int h[3];
         CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         // capacity: the largest box if it fits the budget, else shrink the most generous axis;
         // tiles beyond the capacity gather from global memory.
         const size_t budget = (size_t)96 * 1024;
+        const int VEC = 16 / (int)sizeof(T);
         const int tile[3] = {SL_TX, SL_TY, SL_TZ};
+        // x extent after aligning the origin down to VEC and the length up to VEC
+        h[0] = ((h[0] + 2 * (VEC - 1)) / VEC) * VEC;
         for (int a = 0; a < 3; ++a) cap[a] = std::max(h[a], 4);
-        while ((size_t)nc * cap[0] * cap[1] * cap[2] * sizeof(T) > budget) {
-            int a_best = 0;
+        auto bytes = [&] { return (size_t)nc * cap[0] * cap[1] * cap[2] * sizeof(T); };
+        while (bytes() > budget) {  // shrink the most generous axis (x in steps of VEC)
+            int a_best = -1;
             double r_best = -1;
             for (int a = 0; a < 3; ++a) {
-                const double r = (double)cap[a] / (tile[a] + 3);
-                if (cap[a] > tile[a] + 3 && r > r_best) { r_best = r; a_best = a; }
+                const int minimum = tile[a] + 3 + (a == 0 ? VEC : 0);
+                const double r = (double)cap[a] / minimum;
+                if (cap[a] > minimum && r > r_best) { r_best = r; a_best = a; }
             }
-            if (r_best < 0) break;
-            cap[a_best]--;
+            if (a_best < 0) break;
+            cap[a_best] -= (a_best == 0) ? VEC : 1;
         }
-        while ((size_t)nc * cap[0] * cap[1] * cap[2] * sizeof(T) > budget) {  // still too large: shrink all
-            for (int a = 0; a < 3; ++a) cap[a] = std::max(4, cap[a] - 1);
+        while (bytes() > budget) {  // still too large: everything falls back to global gathers
+            cap[0] = std::max(VEC, cap[0] - VEC);
+            cap[1] = std::max(1, cap[1] - 1);
+            cap[2] = std::max(1, cap[2] - 1);
         }
     }
 
     template <int NC, class Epi>
-    void gather(Src<T, NC> src, const T* d, const int* plan_buf, const int* cap, Epi epi) {
+    void gather(const char* tag, Src<T, NC> src, const T* d, const int* plan_buf, const int* cap, Epi epi) {
         const size_t sm = (size_t)NC * cap[0] * cap[1] * cap[2] * sizeof(T);
         auto k = k_sl_gather<T, NC, Epi>;
         set_smem(k, sm);
+        PB();
         k<<<(unsigned)n_tiles(g), SL_THREADS, sm, s>>>(g, src, d, plan_buf, cap[0], cap[1], cap[2], epi);
-        CKL("k_sl_gather");
+        PE(tag);
     }
     int* plan_p() { return c.at<int>(c.L.plan_p); }
     int* plan_m() { return c.at<int>(c.L.plan_m); }
     int* plan_t() { return c.at<int>(c.L.plan_t); }
 
     void gather_scalar_p(const T* f, T* out) {
-        gather<1>(Src<T, 1>{{f}}, dplus(), plan_p(), c.cap_p, EpiStore<T>{out});
+        gather<1>("sl_state", Src<T, 1>{{f}}, dplus(), plan_p(), c.cap_p, EpiStore<T>{out});
     }
 
     // -------------------------------------------------------------------- API steps
@@ -453,9 +548,10 @@ struct Impl {
         const double dtt = 1.0 / c.cfg.nt;
         for (int sg = 1; sg >= -1; sg -= 2) {
             T* dout = sg > 0 ? dplus() : dminus();
+            PB();
             k_dstar<T><<<grid_1d(3 * g.M), 256, 0, s>>>(g, v(), tmp3(), (T)(sg * dtt / h[0]), (T)(sg * dtt / h[1]),
                                                         (T)(sg * dtt / h[2]));
-            CKL("k_dstar");
+            PE("dstar");
             int capt[3];
             plan(tmp3(), plan_t(), capt, 3);
             EpiDeparture<T> e;
@@ -463,12 +559,12 @@ struct Impl {
             e.v = v();
             e.M = g.M;
             for (int a = 0; a < 3; ++a) e.c[a] = (T)(sg * 0.5 * dtt / h[a]);
-            gather<3>(Src<T, 3>{{v(), v() + g.M, v() + 2 * g.M}}, tmp3(), plan_t(), capt, e);
+            gather<3>("sl_departure", Src<T, 3>{{v(), v() + g.M, v() + 2 * g.M}}, tmp3(), plan_t(), capt, e);
             plan(dout, sg > 0 ? plan_p() : plan_m(), sg > 0 ? c.cap_p : c.cap_m, 1);
         }
         if (!(c.cfg.flags & DR_ISOCHORIC)) {
             div(v(), Dv());
-            gather<1>(Src<T, 1>{{Dv()}}, dminus(), plan_m(), c.cap_m, EpiMultiplier<T>{mult(), Dv(), dt()});
+            gather<1>("sl_multiplier", Src<T, 1>{{Dv()}}, dminus(), plan_m(), c.cap_m, EpiMultiplier<T>{mult(), Dv(), dt()});
         }
     }
 
@@ -479,44 +575,48 @@ struct Impl {
 
     void adjoint_solve() {
         const int nt = c.cfg.nt;
+        PB();
         k_sub<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, rhoR(), rho(nt), lam(nt));
-        CKL("k_sub");
+        PE("sub");
         for (int k = nt; k >= 1; --k)
-            gather<1>(Src<T, 1>{{lam(k)}}, dminus(), plan_m(), c.cap_m, EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)});
+            gather<1>("sl_adjoint", Src<T, 1>{{lam(k)}}, dminus(), plan_m(), c.cap_m, EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)});
     }
 
     void hessian_matvec(const T* vt, T* Hvt) {
         const int nt = c.cfg.nt;
         const T dtt = dt();
         // incremental state (Algorithm 2, merged gather g_j = rho~_j + dt/2 f_j)
+        PB();
         k_inc_init<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, vt, G(0), lt(0), T(0.5) * dtt);
-        CKL("k_inc_init");
+        PE("inc_init");
         for (int j = 0; j < nt; ++j) {
             const bool last = (j == nt - 1);
             EpiIncState<T> e{last ? rt1() : lt(j + 1), vt, G(j + 1), last ? T(0.5) * dtt : dtt, g.M};
-            gather<1>(Src<T, 1>{{lt(j)}}, dplus(), plan_p(), c.cap_p, e);
+            gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), c.cap_p, e);
         }
         // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-)
         for (int k = nt; k >= 1; --k) {
             const T* src = (k == nt) ? rt1() : lt(k);
-            gather<1>(Src<T, 1>{{src}}, dminus(), plan_m(), c.cap_m,
+            gather<1>("sl_inc_adjoint", Src<T, 1>{{src}}, dminus(), plan_m(), c.cap_m,
                       EpiAdjoint<T>{lt(k - 1), mult_or_null(), k == nt ? T(-1) : T(1)});
         }
+        PB();
         k_quadrature<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, nt, lt(0), rt1(), T(-1), G(0), bt(), dtt);
-        CKL("k_quadrature");
+        PE("quadrature");
         // spectral tail: H vt = beta A vt + P b~
         if (c.cfg.flags & DR_ISOCHORIC) {
-            Cx<T>* sp[6] = {spec(0), spec(1), spec(2), spec(3), spec(4), spec(5)};
+            Cx<double>* sd[6] = {specD(0), specD(1), specD(2), specD(3), specD(4), specD(5)};
+            Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
             for (int cc = 0; cc < 3; ++cc) {
-                row_r2c(vt + cc * g.M, sp[cc]);
-                col_fft(sp[cc], -1);
-                row_r2c(bt() + cc * g.M, sp[3 + cc]);
-                col_fft(sp[3 + cc], -1);
+                row_r2c(vt + cc * g.M, sd[cc]);
+                col_fft_fwd(sd[cc]);
+                row_r2c(bt() + cc * g.M, sd[3 + cc]);
+                col_fft_fwd(sd[3 + cc]);
             }
-            middle<4>(sp);
+            middle<4>(sd, sf);
             for (int cc = 0; cc < 3; ++cc) {
-                col_fft(sp[cc], +1);
-                row_c2r(sp[cc], Hvt + cc * g.M, nullptr);
+                col_fft_inv(sf[cc]);
+                row_c2r(sf[cc], Hvt + cc * g.M, nullptr);
             }
         } else {
             scalar_symbol3<0>(vt, Hvt, bt());
@@ -630,6 +730,8 @@ dr_status dr_create(const dr_config* cfg, void* workspace, size_t workspace_byte
 
 dr_status dr_destroy(dr_ctx* c) {
     if (!c) return DR_ERR_ARG;
+    cudaStreamSynchronize(c->stream);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_ws) {
         cudaStreamSynchronize(c->stream);
         cudaFree(c->ws);
@@ -721,6 +823,43 @@ dr_status dr_precond_apply(dr_ctx* c, const void* r, void* z) {
     });
 }
 
+dr_status dr_profile_enable(dr_ctx* c, int enable) {
+    return run(c, [&] {
+        c->prof_flush();
+        c->prof = enable != 0;
+    });
+}
+
+dr_status dr_profile_reset(dr_ctx* c) {
+    return run(c, [&] {
+        c->prof_flush();
+        c->acc.clear();
+        c->launches = 0;
+    });
+}
+
+dr_status dr_profile_count(dr_ctx* c, int* n_entries, int64_t* launches) {
+    return run(c, [&] {
+        c->prof_flush();
+        if (n_entries) *n_entries = (int)c->acc.size();
+        if (launches) *launches = c->launches;
+    });
+}
+
+dr_status dr_profile_entry(dr_ctx* c, int i, char* name, int name_len, int64_t* launches, double* total_ms) {
+    return run(c, [&] {
+        c->prof_flush();
+        if (i < 0 || i >= (int)c->acc.size()) fail(DR_ERR_ARG, "profile entry out of range");
+        const auto& a = c->acc[i];
+        if (name && name_len > 0) {
+            std::strncpy(name, a.tag.c_str(), name_len - 1);
+            name[name_len - 1] = 0;
+        }
+        if (launches) *launches = a.n;
+        if (total_ms) *total_ms = a.ms;
+    });
+}
+
 dr_status dr_sync(dr_ctx* c) {
     return run(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
 }
@@ -764,13 +903,15 @@ dr_status dr_op_spectral(dr_ctx* c, int op, const void* in, void* out) {
 
 dr_status dr_op_interp(dr_ctx* c, const void* f, int64_t npts, const void* s, void* out) {
     return run(c, [&] {
-        if (!f || !s || !out || npts < 0) fail(DR_ERR_ARG, "bad interp arguments");
+        if (npts < 0) fail(DR_ERR_ARG, "bad interp arguments");
         if (npts == 0) return;
+        if (!f || !s || !out) fail(DR_ERR_ARG, "bad interp arguments");
         dispatch(c, [&](auto& im) {
             using T = std::remove_pointer_t<decltype(im.v())>;
+            im.PB();
             k_interp_points<T><<<im.grid_1d(npts), 256, 0, c->stream>>>(c->g, static_cast<const T*>(f), npts,
                                                                           static_cast<const T*>(s), static_cast<T*>(out));
-            CKL("k_interp_points");
+            im.PE("interp_points");
         });
     });
 }
@@ -823,8 +964,9 @@ dr_status dr_get_field(dr_ctx* c, int which, int j, void* out) {
                 if (j == nt) {  // lambda~(1) = -rho~(1) (Eq. 5d); materialise it
                     dispatch(c, [&](auto& im) {
                         using T = std::remove_pointer_t<decltype(im.v())>;
+                        im.PB();
                         k_scale<T><<<im.grid_1d(c->g.M), 256, 0, c->stream>>>(c->g.M, im.rt1(), static_cast<T*>(out), T(-1));
-                        CKL("k_scale");
+                        im.PE("scale");
                     });
                     return;
                 }

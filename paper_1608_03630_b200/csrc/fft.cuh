@@ -194,24 +194,29 @@ __global__ void __launch_bounds__(256) k_row_deriv(Grid g, const T* __restrict__
     }
 }
 
-// Row pass: real rows -> half-spectrum rows (r2c along x1), spectrum row stride g.n1p.
-template <typename T, int L>
-__global__ void __launch_bounds__(256) k_row_r2c(Grid g, const T* __restrict__ f, Cx<T>* __restrict__ spec,
-                                                 const Cx<T>* __restrict__ twN) {
+// Row pass: real rows (type Ti) -> half-spectrum rows (r2c along x1) computed and stored in Tc,
+// spectrum row stride g.n1p.  Ti = float, Tc = double keeps the forward spectrum exact enough for the
+// high-wavenumber amplification of beta*A.
+template <typename Ti, typename Tc, int L>
+__global__ void __launch_bounds__(256) k_row_r2c(Grid g, const Ti* __restrict__ f, Cx<Tc>* __restrict__ spec,
+                                                 const Cx<Tc>* __restrict__ twN) {
     constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
     constexpr int RB = (256 / TPL) > 0 ? 256 / TPL : 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
+    Cx<Tc>* sm = reinterpret_cast<Cx<Tc>*>(smem_raw);
     const int64_t nrows = (int64_t)g.n2 * g.n3;
     const int64_t row0 = (int64_t)blockIdx.x * RB;
-    const Cx<T>* src = reinterpret_cast<const Cx<T>*>(f) + row0 * L;
+    const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f) + row0 * L;
     const int nvalid = (int)((nrows - row0) < RB ? (nrows - row0) : RB);
-    for (int e = threadIdx.x; e < nvalid * L; e += blockDim.x) sm[(e / L) * LP + P(e % L)] = src[e];
+    for (int e = threadIdx.x; e < nvalid * L; e += blockDim.x) {
+        const Cx<Ti> v = src[e];
+        sm[(e / L) * LP + P(e % L)] = cx<Tc>((Tc)v.re, (Tc)v.im);
+    }
     __syncthreads();
     const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    Cx<T>* buf = sm + line * LP;
-    fft_line<T, L, -1>(buf, t, twN, 2);
-    r2c_post<T, L>(buf, t, twN);
+    Cx<Tc>* buf = sm + line * LP;
+    fft_line<Tc, L, -1>(buf, t, twN, 2);
+    r2c_post<Tc, L>(buf, t, twN);
     constexpr int NC = L + 1;
     for (int e = threadIdx.x; e < nvalid * NC; e += blockDim.x) {
         const int r = e / NC, k = e % NC;
@@ -219,14 +224,14 @@ __global__ void __launch_bounds__(256) k_row_r2c(Grid g, const T* __restrict__ f
     }
 }
 
-// Row pass epilogues for the c2r inverse: out = s * x (+ add)
+// Row pass epilogue for the c2r inverse: out = x (+ add)
 template <typename T>
 struct RowOut {
     T* out;
     const T* add;  // nullable: field added after the inverse (b~ in the non-isochoric matvec)
 };
 
-// Row pass: half-spectrum rows -> real rows (c2r along x1) with epilogue out = x + add.
+// Row pass: half-spectrum rows -> real rows (c2r along x1) in T with epilogue out = x + add.
 // The spectrum already carries the full inverse normalisation.
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_row_c2r(Grid g, const Cx<T>* __restrict__ spec, RowOut<T> epi,
@@ -273,19 +278,23 @@ __device__ __forceinline__ int64_t col_addr(const ColGeom& c, int x, int other, 
     return ((int64_t)p * c.n2 + other) * c.W + x;               // other = i2, p = i3
 }
 
-template <int L, int XC>
+// CTA shape of a column pass: XC columns x OL transverse lines, TPL threads per line.  OL is chosen for
+// ~256 threads but capped so that NC components of ES-byte complex values fit in ~72 KB of smem.
+template <int L, int XC, int NC = 1, int ES = 16>
 struct ColCfg {
     static constexpr int TPL = LineGeom<L>::TPL;
-    static constexpr int OL = (XC * TPL >= 256) ? 1 : 256 / (XC * TPL);
+    static constexpr int OLT = (XC * TPL >= 256) ? 1 : 256 / (XC * TPL);
+    static constexpr int MAXL = (72 * 1024) / (NC * LineGeom<L>::LP * ES);
+    static constexpr int OLS = (MAXL / XC) >= 1 ? MAXL / XC : 1;
+    static constexpr int OL = OLT < OLS ? OLT : OLS;
     static constexpr int NT = XC * OL * TPL;
     static constexpr int LINES = XC * OL;
 };
 
-template <typename T, int L, int XC, int AX>
+template <typename T, int L, int XC, int OL, int AX>
 __device__ __forceinline__ void col_load(Cx<T>* sm, const Cx<T>* __restrict__ src, const ColGeom& c, int x0, int o0,
                                          int nother) {
     constexpr int LP = LineGeom<L>::LP;
-    constexpr int OL = ColCfg<L, XC>::OL;
     for (int e = threadIdx.x; e < XC * L * OL; e += blockDim.x) {
         const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
         const int x = x0 + xi, o = o0 + oi;
@@ -295,16 +304,16 @@ __device__ __forceinline__ void col_load(Cx<T>* sm, const Cx<T>* __restrict__ sr
     }
 }
 
-template <typename T, int L, int XC, int AX, bool ACC>
-__device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<T>* __restrict__ dst, const ColGeom& c, int x0, int o0,
+template <typename T, int L, int XC, int OL, int AX, bool ACC, typename To = T>
+__device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<To>* __restrict__ dst, const ColGeom& c, int x0, int o0,
                                           int nother) {
     constexpr int LP = LineGeom<L>::LP;
-    constexpr int OL = ColCfg<L, XC>::OL;
     for (int e = threadIdx.x; e < XC * L * OL; e += blockDim.x) {
         const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
         const int x = x0 + xi, o = o0 + oi;
         if (x < c.nx && o < nother) {
-            Cx<T> v = sm[(oi * XC + xi) * LP + P(p)];
+            const Cx<T> w = sm[(oi * XC + xi) * LP + P(p)];
+            Cx<To> v = cx<To>((To)w.re, (To)w.im);
             const int64_t a = col_addr<AX>(c, x, o, p);
             if (ACC) v = v + dst[a];
             dst[a] = v;
@@ -314,18 +323,18 @@ __device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<T>* __restrict__ d
 
 // Derivative along x2 / x3 of a real field (viewed as complex pairs): out (+)= d f / dx_AX.
 template <typename T, int L, int XC, int AX>
-__global__ void __launch_bounds__(ColCfg<L, XC>::NT) k_col_deriv(ColGeom c, const Cx<T>* __restrict__ src,
+__global__ void __launch_bounds__(ColCfg<L, XC, 1, sizeof(Cx<T>)>::NT) k_col_deriv(ColGeom c, const Cx<T>* __restrict__ src,
                                                                  Cx<T>* __restrict__ dst, int accumulate,
                                                                  const Cx<T>* __restrict__ tw) {
     constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int OL = ColCfg<L, XC>::OL;
+    constexpr int OL = ColCfg<L, XC, 1, sizeof(Cx<T>)>::OL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
     const int nxb = (c.nx + XC - 1) / XC;
     const int x0 = (blockIdx.x % nxb) * XC;
     const int o0 = (blockIdx.x / nxb) * OL;
     const int nother = (AX == 2) ? c.n3 : c.n2;
-    col_load<T, L, XC, AX>(sm, src, c, x0, o0, nother);
+    col_load<T, L, XC, OL, AX>(sm, src, c, x0, o0, nother);
     __syncthreads();
     const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
     Cx<T>* buf = sm + line * LP;
@@ -336,26 +345,26 @@ __global__ void __launch_bounds__(ColCfg<L, XC>::NT) k_col_deriv(ColGeom c, cons
     }
     __syncthreads();
     fft_line<T, L, +1>(buf, t, tw, 1);
-    if (accumulate) col_store<T, L, XC, AX, true>(sm, dst, c, x0, o0, nother);
-    else col_store<T, L, XC, AX, false>(sm, dst, c, x0, o0, nother);
+    if (accumulate) col_store<T, L, XC, OL, AX, true>(sm, dst, c, x0, o0, nother);
+    else col_store<T, L, XC, OL, AX, false>(sm, dst, c, x0, o0, nother);
 }
 
 // Plain complex FFT of spectrum columns along x2 (forward DIR=-1 or inverse DIR=+1), in place.
 template <typename T, int L, int XC, int DIR>
-__global__ void __launch_bounds__(ColCfg<L, XC>::NT) k_col_fft(ColGeom c, Cx<T>* __restrict__ spec,
+__global__ void __launch_bounds__(ColCfg<L, XC, 1, sizeof(Cx<T>)>::NT) k_col_fft(ColGeom c, Cx<T>* __restrict__ spec,
                                                                const Cx<T>* __restrict__ tw) {
     constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int OL = ColCfg<L, XC>::OL;
+    constexpr int OL = ColCfg<L, XC, 1, sizeof(Cx<T>)>::OL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
     const int nxb = (c.nx + XC - 1) / XC;
     const int x0 = (blockIdx.x % nxb) * XC;
     const int o0 = (blockIdx.x / nxb) * OL;
-    col_load<T, L, XC, 2>(sm, spec, c, x0, o0, c.n3);
+    col_load<T, L, XC, OL, 2>(sm, spec, c, x0, o0, c.n3);
     __syncthreads();
     const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
     fft_line<T, L, DIR>(sm + line * LP, t, tw, 1);
-    col_store<T, L, XC, 2, false>(sm, spec, c, x0, o0, c.n3);
+    col_store<T, L, XC, OL, 2, false>(sm, spec, c, x0, o0, c.n3);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -421,20 +430,25 @@ struct SpecPtrs {
     Cx<T>* p[NC];
 };
 
-// x3 middle pass: forward FFT of NCI spectra along x3, symbol, inverse FFT of NCO spectra.
-template <typename T, int L, int XC, int KIND>
-__global__ void __launch_bounds__(ColCfg<L, XC>::NT) k_col_middle(ColGeom c, SpecPtrs<T, Sym<T, KIND>::NCI> io,
-                                                                  SymInfo s, const Cx<T>* __restrict__ tw) {
+// x3 middle pass: forward FFT of NCI spectra along x3, symbol, inverse FFT of NCO spectra, all in Ti;
+// results are stored in To (the inverse passes after the symbol may run in the I/O precision: their
+// rounding is relative to the already-amplified signal).
+template <typename Ti, typename To, int L, int XC, int KIND>
+__global__ void __launch_bounds__(ColCfg<L, XC, Sym<Ti, KIND>::NCI, sizeof(Cx<Ti>)>::NT) k_col_middle(ColGeom c, SpecPtrs<Ti, Sym<Ti, KIND>::NCI> in,
+                                                                  SpecPtrs<To, Sym<Ti, KIND>::NCO> out, SymInfo s,
+                                                                  const Cx<Ti>* __restrict__ tw) {
+    using T = Ti;
     constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int OL = ColCfg<L, XC>::OL, LINES = ColCfg<L, XC>::LINES;
     constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
+    using CC = ColCfg<L, XC, NCI, sizeof(Cx<T>)>;
+    constexpr int OL = CC::OL, LINES = CC::LINES;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
     const int nxb = (c.nx + XC - 1) / XC;
     const int x0 = (blockIdx.x % nxb) * XC;
     const int o0 = (blockIdx.x / nxb) * OL;
 #pragma unroll
-    for (int ci = 0; ci < NCI; ++ci) col_load<T, L, XC, 3>(sm + ci * LINES * LP, io.p[ci], c, x0, o0, c.n2);
+    for (int ci = 0; ci < NCI; ++ci) col_load<T, L, XC, OL, 3>(sm + ci * LINES * LP, in.p[ci], c, x0, o0, c.n2);
     __syncthreads();
     const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
 #pragma unroll
@@ -459,7 +473,8 @@ __global__ void __launch_bounds__(ColCfg<L, XC>::NT) k_col_middle(ColGeom c, Spe
 #pragma unroll
     for (int co = 0; co < NCO; ++co) fft_line<T, L, +1>(sm + co * LINES * LP + line * LP, t, tw, 1);
 #pragma unroll
-    for (int co = 0; co < NCO; ++co) col_store<T, L, XC, 3, false>(sm + co * LINES * LP, io.p[co], c, x0, o0, c.n2);
+    for (int co = 0; co < NCO; ++co)
+        col_store<T, L, XC, OL, 3, false, To>(sm + co * LINES * LP, out.p[co], c, x0, o0, c.n2);
 }
 
 }  // namespace dr

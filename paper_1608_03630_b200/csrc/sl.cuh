@@ -151,12 +151,15 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restr
 }
 
 // ---------------------------------------------------------------------------------------------
-// Epilogues of the fused gather kernel.  `val` holds the NC interpolated components at the
-// departure point of voxel id.
+// Epilogues of the fused gather kernel.  `load(id)` fetches (and pre-reduces) the voxel's pointwise
+// operands before the box wait, so their latency overlaps the shared-memory staging; `store(id, val,
+// pre)` finishes the step with the NC interpolated components `val` at the departure point.
 template <typename T>
 struct EpiStore {  // state solve: rho_{j+1} = I[rho_j](X+)   (Eq. 7 with f = 0)
     T* out;
-    __device__ __forceinline__ void operator()(int64_t id, const T* val) const { out[id] = val[0]; }
+    struct Pre {};
+    __device__ __forceinline__ Pre load(int64_t) const { return Pre{}; }
+    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre&) const { out[id] = val[0]; }
 };
 
 template <typename T>
@@ -164,11 +167,9 @@ struct EpiAdjoint {  // adjoint-like step: nu_{k-1} = scale * m * I[nu_k](X-)  (
     T* out;
     const T* m;  // nullable (isochoric: m == 1)
     T scale;
-    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
-        T r = scale * val[0];
-        if (m) r *= __ldg(m + id);
-        out[id] = r;
-    }
+    struct Pre { T m; };
+    __device__ __forceinline__ Pre load(int64_t id) const { return Pre{m ? scale * __ldg(m + id) : scale}; }
+    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const { out[id] = p.m * val[0]; }
 };
 
 template <typename T>
@@ -178,11 +179,13 @@ struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+
     const T* G;   // vector field grad rho_{j+1}
     T c;
     int64_t M;
-    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
+    struct Pre { T cf; };
+    __device__ __forceinline__ Pre load(int64_t id) const {
         const T f = -(__ldg(vt + id) * __ldg(G + id) + __ldg(vt + M + id) * __ldg(G + M + id) +
                       __ldg(vt + 2 * M + id) * __ldg(G + 2 * M + id));
-        out[id] = val[0] + c * f;
+        return Pre{c * f};
     }
+    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const { out[id] = val[0] + p.cf; }
 };
 
 template <typename T>
@@ -190,9 +193,11 @@ struct EpiMultiplier {  // m = 1 + dt/2 (Dbar + D + dt Dbar D), Dbar = I[div v](
     T* m;
     const T* D;
     T dt;
-    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
-        const T Db = val[0], Dv = __ldg(D + id);
-        m[id] = T(1) + T(0.5) * dt * (Db + Dv + dt * Db * Dv);
+    struct Pre { T D; };
+    __device__ __forceinline__ Pre load(int64_t id) const { return Pre{__ldg(D + id)}; }
+    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const {
+        const T Db = val[0];
+        m[id] = T(1) + T(0.5) * dt * (Db + p.D + dt * Db * p.D);
     }
 };
 
@@ -202,9 +207,13 @@ struct EpiDeparture {  // d = sigma dt/2 (v(x) + I[v](X*)) / h  (Eq. 6, cell uni
     const T* v;
     T c[3];  // sigma * dt / (2 h_a)
     int64_t M;
-    __device__ __forceinline__ void operator()(int64_t id, const T* val) const {
+    struct Pre { T v[3]; };
+    __device__ __forceinline__ Pre load(int64_t id) const {
+        return Pre{{__ldg(v + id), __ldg(v + M + id), __ldg(v + 2 * M + id)}};
+    }
+    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) d[a * M + id] = c[a] * (__ldg(v + a * M + id) + val[a]);
+        for (int a = 0; a < 3; ++a) d[a * M + id] = c[a] * (p.v[a] + val[a]);
     }
 };
 
@@ -213,24 +222,58 @@ struct Src {
     const T* p[NC];
 };
 
-// Fused gather + epilogue.  Grid: one CTA per tile.  Dynamic smem: NC * capx * capy * capz values.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// Fused gather + epilogue.  Grid: one CTA per tile.  Dynamic smem: NC * capx * capy * capz values,
+// capx a multiple of VEC = 16 B / sizeof(T) so every staged row is 16-byte aligned.
+// Phases: (A) stage the tile's box with 16-byte cp.async (periodic wrap per chunk; x origin aligned
+// down to VEC, which never straddles the wrap since N1 is a multiple of VEC); (B) meanwhile load the
+// displacements and the epilogue operands of the thread's 8 points; (C) wait + barrier; (D) gather
+// 64 stencil values per point from shared memory and finish the step.
 template <typename T, int NC, class Epi>
 __global__ void __launch_bounds__(SL_THREADS) k_sl_gather(Grid g, Src<T, NC> src, const T* __restrict__ d,
                                                           const int* __restrict__ plan, int capx, int capy, int capz,
                                                           Epi epi) {
+    constexpr int VEC = 16 / (int)sizeof(T);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* box = reinterpret_cast<T*>(smem_raw);
     int x0, y0, z0;
     tile_coords(g, blockIdx.x, x0, y0, z0);
     const int* pl = plan + (int64_t)blockIdx.x * PLAN_INTS;
-    const int ox = pl[0], oy = pl[1], oz = pl[2], ex = pl[3], ey = pl[4], ez = pl[5];
+    const int ox = pl[0] & ~(VEC - 1), oy = pl[1], oz = pl[2];
+    const int ex = ((pl[0] + pl[3] - ox) + VEC - 1) & ~(VEC - 1), ey = pl[4], ez = pl[5];
     const bool fits = ex <= capx && ey <= capy && ez <= capz;
     const int lane = threadIdx.x % SL_TX, wy = threadIdx.x / SL_TX;
     const int x = x0 + lane, y = y0 + wy;
     const bool xyok = x < g.n1 && y < g.n2;
+    const int sy = capx, sz = capx * capy, sc = capx * capy * capz;
 
-    // displacements of this thread's points (issued before the box load so they overlap it)
+    // (A) asynchronous staging of the box
+    if (fits) {
+        const int nch = ex / VEC;
+        int yy = wy, zz = 0;
+        while (yy >= ey) { yy -= ey; ++zz; }
+        for (; zz < ez;) {
+            const int gy = wrapi(oy + yy, g.n2), gz = wrapi(oz + zz, g.n3);
+            const int64_t rowbase = ((int64_t)gz * g.n2 + gy) * g.n1;
+            for (int ch = lane; ch < nch; ch += 32) {
+                const int gx = wrapi(ox + ch * VEC, g.n1);
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    cp_async16(box + c * sc + zz * sz + yy * sy + ch * VEC, src.p[c] + rowbase + gx);
+            }
+            yy += SL_THREADS / 32;
+            while (yy >= ey) { yy -= ey; ++zz; }
+        }
+    }
+
+    // (B) displacements and epilogue operands of this thread's points
     T dd[SL_TZ][3];
+    typename Epi::Pre pre[SL_TZ];
 #pragma unroll
     for (int k = 0; k < SL_TZ; ++k) {
         const int z = z0 + k;
@@ -238,24 +281,15 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_gather(Grid g, Src<T, NC> src
         const bool ok = xyok && z < g.n3;
 #pragma unroll
         for (int a = 0; a < 3; ++a) dd[k][a] = ok ? __ldg(d + a * g.M + id) : T(0);
+        if (ok) pre[k] = epi.load(id);
     }
 
-    const int sy = capx, sz = capx * capy, sc = capx * capy * capz;
-    if (fits) {
-        const int rows = ey * ez;
-        for (int r = wy; r < rows; r += SL_THREADS / 32) {
-            const int yy = r % ey, zz = r / ey;
-            const int gy = wrapi(oy + yy, g.n2), gz = wrapi(oz + zz, g.n3);
-            const int64_t rowbase = ((int64_t)gz * g.n2 + gy) * g.n1;
-            for (int xx = lane; xx < ex; xx += 32) {
-                const int gx = wrapi(ox + xx, g.n1);
-#pragma unroll
-                for (int c = 0; c < NC; ++c) box[c * sc + zz * sz + yy * sy + xx] = __ldg(src.p[c] + rowbase + gx);
-            }
-        }
-    }
+    // (C)
+    if (fits) cp_async_wait_all();
     __syncthreads();
     if (!xyok) return;
+
+    // (D)
 #pragma unroll
     for (int k = 0; k < SL_TZ; ++k) {
         const int z = z0 + k;
@@ -279,7 +313,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_gather(Grid g, Src<T, NC> src
 #pragma unroll
             for (int c = 0; c < NC; ++c) val[c] = interp_global(src.p[c], g, q1, q2, q3, w1, w2, w3);
         }
-        epi(id, val);
+        epi.store(id, val, pre[k]);
     }
 }
 

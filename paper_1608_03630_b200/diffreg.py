@@ -29,7 +29,7 @@ DR_OP_GRAD, DR_OP_DIV, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY = range(5)
 EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr_set_velocity",
            "dr_forward_solve", "dr_adjoint_solve", "dr_hessian_matvec", "dr_precond_apply", "dr_sync",
            "dr_last_error", "dr_status_string", "dr_op_spectral", "dr_op_interp", "dr_get_departure",
-           "dr_get_field"]
+           "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry"]
 
 
 class dr_config(ctypes.Structure):
@@ -62,7 +62,11 @@ def lib():
                            ("dr_hessian_matvec", [vp, vp, vp]), ("dr_precond_apply", [vp, vp, vp]),
                            ("dr_sync", [vp]), ("dr_op_spectral", [vp, i32, vp, vp]),
                            ("dr_op_interp", [vp, vp, i64, vp, vp]), ("dr_get_departure", [vp, i32, vp]),
-                           ("dr_get_field", [vp, i32, i32, vp])]:
+                           ("dr_get_field", [vp, i32, i32, vp]), ("dr_profile_enable", [vp, i32]),
+                           ("dr_profile_reset", [vp]),
+                           ("dr_profile_count", [vp, ctypes.POINTER(i32), ctypes.POINTER(i64)]),
+                           ("dr_profile_entry", [vp, i32, ctypes.c_char_p, i32, ctypes.POINTER(i64),
+                                                 ctypes.POINTER(ctypes.c_double)])]:
             getattr(L, name).argtypes = args
             getattr(L, name).restype = ctypes.c_int
         L.dr_create.restype = ctypes.c_int
@@ -184,6 +188,27 @@ class Context:
 
     def sync(self):
         self._check(lib().dr_sync(self.h))
+
+    # ---- tracing ----
+    def profile_enable(self, on: bool = True):
+        self._check(lib().dr_profile_enable(self.h, int(bool(on))))
+
+    def profile_reset(self):
+        self._check(lib().dr_profile_reset(self.h))
+
+    def profile(self):
+        """({tag: (launches, total_ms)}, total kernel launches since the last reset)."""
+        n = ctypes.c_int()
+        tot = ctypes.c_int64()
+        self._check(lib().dr_profile_count(self.h, ctypes.byref(n), ctypes.byref(tot)))
+        out = {}
+        for i in range(n.value):
+            name = ctypes.create_string_buffer(64)
+            k = ctypes.c_int64()
+            ms = ctypes.c_double()
+            self._check(lib().dr_profile_entry(self.h, i, name, 64, ctypes.byref(k), ctypes.byref(ms)))
+            out[name.value.decode()] = (k.value, ms.value)
+        return out, tot.value
 
     # ---- test hooks ----
     def op_spectral(self, op: int, x, out=None):

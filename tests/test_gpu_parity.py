@@ -98,7 +98,7 @@ def test_interp_points(dr, fp64):
     assert rel(out, ref) < tols(fp64)[0]
     # node exactness: t = 0 reproduces the node value exactly
     fv = np64(f)
-    assert out[-3] == fv[0, 0, 0] and out[-2] == fv[3, 15, 31] and out[-1] == fv[7, 3, 5]
+    assert out[-3] == fv[0, 0, 0] and out[-2] == fv[63, 15, 31] and out[-1] == fv[7, 3, 5]
     # empty input is a no-op
     ctx.op_interp(f.cuda(), torch.zeros((3, 0), dtype=f.dtype, device="cuda"))
 
@@ -280,6 +280,9 @@ def test_call_order_and_argument_errors(dr):
 
 
 def test_matvec_linearity_and_determinism(dr):
+    """H is linear in vt.  The data term (b~) is checked tightly; the full H vt only to 1e-4 because the
+    fp32 rounding of the input 2x - 3y itself is amplified by the H2 symbol |k|^4 (DESIGN.md,
+    "fp32 conditioning of the regulariser")."""
     n, nt = 32, 4
     ctx = dr.Context(dr.Config(n=n, nt=nt))
     rT = synth.round32(synth.blobs(1, n, kcut=8)).cuda()
@@ -288,7 +291,12 @@ def test_matvec_linearity_and_determinism(dr):
     ctx.forward_solve()
     x = synth.round32(synth.smooth_vec(3, n, kmax=4)).cuda()
     y = synth.round32(synth.smooth_vec(4, n, kmax=4)).cuda()
-    hx, hy = ctx.hessian_matvec(x), ctx.hessian_matvec(y)
+    hx = ctx.hessian_matvec(x)
+    bx = ctx.get_field(dr.DR_FIELD_BTILDE)
+    hy = ctx.hessian_matvec(y)
+    by = ctx.get_field(dr.DR_FIELD_BTILDE)
     h = ctx.hessian_matvec((2 * x - 3 * y).contiguous())
-    assert rel(np64(h), np64(2 * hx - 3 * hy)) < 1e-6
+    b = ctx.get_field(dr.DR_FIELD_BTILDE)
+    assert rel(np64(b), np64(2 * bx - 3 * by)) < 1e-5
+    assert rel(np64(h), np64(2 * hx - 3 * hy)) < 1e-4
     assert torch.equal(ctx.hessian_matvec(x), hx)  # bitwise deterministic
