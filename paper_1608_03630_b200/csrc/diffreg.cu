@@ -137,7 +137,6 @@ struct dr_ctx {
     char* ws = nullptr;
     bool own_ws = false;
     bool have_images = false, have_velocity = false, have_state = false, have_adjoint = false, have_matvec = false;
-    int cap_p[3] = {0, 0, 0}, cap_m[3] = {0, 0, 0};
     std::string err;
     // launch accounting and optional per-kernel CUDA-event profiling (dr_profile_*)
     int64_t launches = 0;
@@ -262,12 +261,10 @@ struct Impl {
     }
 
     // -------------------------------------------------------------------- FFT pass launchers
-    template <int L>
-    static constexpr int row_rb() { return (256 / LineGeom<L>::TPL) > 0 ? 256 / LineGeom<L>::TPL : 1; }
     template <int L, typename U = T>
-    static size_t row_smem() { return (size_t)row_rb<L>() * LineGeom<L>::LP * sizeof(Cx<U>); }
-    template <int L>
-    int row_blocks() const { return (int)(((int64_t)g.n2 * g.n3 + row_rb<L>() - 1) / row_rb<L>()); }
+    static size_t row_smem() { return (size_t)RowCfg<L, U>::RB * LineGeom<L>::LP * sizeof(Cx<U>); }
+    template <int L, typename U = T>
+    int row_blocks() const { return (int)(((int64_t)g.n2 * g.n3 + RowCfg<L, U>::RB - 1) / RowCfg<L, U>::RB); }
 
     template <typename K>
     static void set_smem(K kernel, size_t bytes) {
@@ -279,7 +276,7 @@ struct Impl {
         auto k = k_row_deriv<T, L>;
         set_smem(k, row_smem<L>());
         PB();
-        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, f, out, acc, twx());
+        k<<<row_blocks<L>(), RowCfg<L, T>::NT, row_smem<L>(), s>>>(g, f, out, acc, twx());
         PE("row_deriv");
     }
     template <int L>
@@ -287,7 +284,7 @@ struct Impl {
         auto k = k_row_r2c<T, double, L>;
         set_smem(k, row_smem<L, double>());
         PB();
-        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L, double>(), s>>>(g, f, sp, twxd());
+        k<<<row_blocks<L, double>(), RowCfg<L, double>::NT, row_smem<L, double>(), s>>>(g, f, sp, twxd());
         PE("row_r2c");
     }
     template <int L>
@@ -296,7 +293,7 @@ struct Impl {
         set_smem(k, row_smem<L>());
         RowOut<T> e{out, add};
         PB();
-        k<<<row_blocks<L>(), row_rb<L>() * LineGeom<L>::TPL, row_smem<L>(), s>>>(g, sp, e, twx());
+        k<<<row_blocks<L>(), RowCfg<L, T>::NT, row_smem<L>(), s>>>(g, sp, e, twx());
         PE("row_c2r");
     }
 
@@ -345,8 +342,8 @@ struct Impl {
 
     // columns per CTA: keep NC components of the CTA's lines within ~64 KB of shared memory
     template <int L, int NC, typename U = T>
-    static constexpr int pick_xc() {
-        return (NC * 16 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024)  ? 16
+    static constexpr int pick_xc() {  // 128-byte column chunks (16 complex64 / 8 complex128), smem-capped
+        return (sizeof(U) == 4 && NC * 16 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 16
                : (NC * 8 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 8
                : (NC * 4 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 4
                                                                               : 2;
@@ -486,50 +483,21 @@ struct Impl {
     }
 
     // -------------------------------------------------------------------- semi-Lagrangian
-    void plan(const T* d, int* plan_buf, int* cap, int nc) {
+    // Per-tile gather plan of a displacement field (once per velocity and direction).
+    void plan(const T* d, int* plan_buf) {
         int* mx = c.at<int>(c.L.maxext);
-        const int init[3] = {INT_MIN, INT_MIN, INT_MIN};
-        CK(cudaMemcpyAsync(mx, init, sizeof(init), cudaMemcpyHostToDevice, s));
         PB();
         k_sl_plan<T><<<(unsigned)n_tiles(g), SL_THREADS, 0, s>>>(g, d, plan_buf, mx);
         PE("sl_plan");
-        int h[3];
-        CK(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        // capacity: the largest box if it fits the budget, else shrink the most generous axis;
-        // tiles beyond the capacity gather from global memory.
-        const size_t budget = (size_t)96 * 1024;
-        const int VEC = 16 / (int)sizeof(T);
-        const int tile[3] = {SL_TX, SL_TY, SL_TZ};
-        // x extent after aligning the origin down to VEC and the length up to VEC
-        h[0] = ((h[0] + 2 * (VEC - 1)) / VEC) * VEC;
-        for (int a = 0; a < 3; ++a) cap[a] = std::max(h[a], 4);
-        auto bytes = [&] { return (size_t)nc * cap[0] * cap[1] * cap[2] * sizeof(T); };
-        while (bytes() > budget) {  // shrink the most generous axis (x in steps of VEC)
-            int a_best = -1;
-            double r_best = -1;
-            for (int a = 0; a < 3; ++a) {
-                const int minimum = tile[a] + 3 + (a == 0 ? VEC : 0);
-                const double r = (double)cap[a] / minimum;
-                if (cap[a] > minimum && r > r_best) { r_best = r; a_best = a; }
-            }
-            if (a_best < 0) break;
-            cap[a_best] -= (a_best == 0) ? VEC : 1;
-        }
-        while (bytes() > budget) {  // still too large: everything falls back to global gathers
-            cap[0] = std::max(VEC, cap[0] - VEC);
-            cap[1] = std::max(1, cap[1] - 1);
-            cap[2] = std::max(1, cap[2] - 1);
-        }
     }
 
     template <int NC, class Epi>
-    void gather(const char* tag, Src<T, NC> src, const T* d, const int* plan_buf, const int* cap, Epi epi) {
-        const size_t sm = (size_t)NC * cap[0] * cap[1] * cap[2] * sizeof(T);
+    void gather(const char* tag, Src<T, NC> src, const T* d, const int* plan_buf, Epi epi) {
+        constexpr size_t sm = box_bytes<T, NC>();
         auto k = k_sl_gather<T, NC, Epi>;
         set_smem(k, sm);
         PB();
-        k<<<(unsigned)n_tiles(g), SL_THREADS, sm, s>>>(g, src, d, plan_buf, cap[0], cap[1], cap[2], epi);
+        k<<<(unsigned)n_tiles(g), SL_THREADS, sm, s>>>(g, src, d, plan_buf, epi);
         PE(tag);
     }
     int* plan_p() { return c.at<int>(c.L.plan_p); }
@@ -537,7 +505,7 @@ struct Impl {
     int* plan_t() { return c.at<int>(c.L.plan_t); }
 
     void gather_scalar_p(const T* f, T* out) {
-        gather<1>("sl_state", Src<T, 1>{{f}}, dplus(), plan_p(), c.cap_p, EpiStore<T>{out});
+        gather<1>("sl_state", Src<T, 1>{{f}}, dplus(), plan_p(), EpiStore<T>{out});
     }
 
     // -------------------------------------------------------------------- API steps
@@ -552,19 +520,18 @@ struct Impl {
             k_dstar<T><<<grid_1d(3 * g.M), 256, 0, s>>>(g, v(), tmp3(), (T)(sg * dtt / h[0]), (T)(sg * dtt / h[1]),
                                                         (T)(sg * dtt / h[2]));
             PE("dstar");
-            int capt[3];
-            plan(tmp3(), plan_t(), capt, 3);
+            plan(tmp3(), plan_t());
             EpiDeparture<T> e;
             e.d = dout;
             e.v = v();
             e.M = g.M;
             for (int a = 0; a < 3; ++a) e.c[a] = (T)(sg * 0.5 * dtt / h[a]);
-            gather<3>("sl_departure", Src<T, 3>{{v(), v() + g.M, v() + 2 * g.M}}, tmp3(), plan_t(), capt, e);
-            plan(dout, sg > 0 ? plan_p() : plan_m(), sg > 0 ? c.cap_p : c.cap_m, 1);
+            gather<3>("sl_departure", Src<T, 3>{{v(), v() + g.M, v() + 2 * g.M}}, tmp3(), plan_t(), e);
+            plan(dout, sg > 0 ? plan_p() : plan_m());
         }
         if (!(c.cfg.flags & DR_ISOCHORIC)) {
             div(v(), Dv());
-            gather<1>("sl_multiplier", Src<T, 1>{{Dv()}}, dminus(), plan_m(), c.cap_m, EpiMultiplier<T>{mult(), Dv(), dt()});
+            gather<1>("sl_multiplier", Src<T, 1>{{Dv()}}, dminus(), plan_m(), EpiMultiplier<T>{mult(), Dv(), dt()});
         }
     }
 
@@ -579,7 +546,7 @@ struct Impl {
         k_sub<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, rhoR(), rho(nt), lam(nt));
         PE("sub");
         for (int k = nt; k >= 1; --k)
-            gather<1>("sl_adjoint", Src<T, 1>{{lam(k)}}, dminus(), plan_m(), c.cap_m, EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)});
+            gather<1>("sl_adjoint", Src<T, 1>{{lam(k)}}, dminus(), plan_m(), EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)});
     }
 
     void hessian_matvec(const T* vt, T* Hvt) {
@@ -592,12 +559,12 @@ struct Impl {
         for (int j = 0; j < nt; ++j) {
             const bool last = (j == nt - 1);
             EpiIncState<T> e{last ? rt1() : lt(j + 1), vt, G(j + 1), last ? T(0.5) * dtt : dtt, g.M};
-            gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), c.cap_p, e);
+            gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), e);
         }
         // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-)
         for (int k = nt; k >= 1; --k) {
             const T* src = (k == nt) ? rt1() : lt(k);
-            gather<1>("sl_inc_adjoint", Src<T, 1>{{src}}, dminus(), plan_m(), c.cap_m,
+            gather<1>("sl_inc_adjoint", Src<T, 1>{{src}}, dminus(), plan_m(),
                       EpiAdjoint<T>{lt(k - 1), mult_or_null(), k == nt ? T(-1) : T(1)});
         }
         PB();

@@ -23,6 +23,14 @@ struct LineGeom {
     static constexpr int TPL = (L >= 16) ? L / 16 : 1;  // threads per line
     static constexpr int LP = L + L / 16 + 2;           // padded line length (holds index L for r2c)
 };
+// Row passes: RB rows per CTA, ~256 threads for fp32 compute and ~128 for fp64 (register footprint of
+// the radix-16 butterflies doubles) so several CTAs fit per SM.
+template <int L, typename Tc>
+struct RowCfg {
+    static constexpr int NTT = sizeof(Tc) == 8 ? 128 : 256;
+    static constexpr int RB = (NTT / LineGeom<L>::TPL) > 0 ? NTT / LineGeom<L>::TPL : 1;
+    static constexpr int NT = RB * LineGeom<L>::TPL;
+};
 
 // e^{DIR * 2 pi i m / 16}, m compile-time after unrolling
 template <typename T, int DIR>
@@ -162,10 +170,10 @@ __device__ __forceinline__ void c2r_pre(Cx<T>* buf, int t, const Cx<T>* __restri
 // Row pass: x1-derivative of real rows ("N2 N3 1D FFTs across the first coordinate,
 // diagonal scaling, and then the same number of inverse FFTs").  out = acc*out + d f/dx1.
 template <typename T, int L>
-__global__ void __launch_bounds__(256) k_row_deriv(Grid g, const T* __restrict__ f, T* __restrict__ out,
+__global__ void __launch_bounds__(RowCfg<L, T>::NT) k_row_deriv(Grid g, const T* __restrict__ f, T* __restrict__ out,
                                                    int accumulate, const Cx<T>* __restrict__ twN) {
     constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int RB = (256 / TPL) > 0 ? 256 / TPL : 1;
+    constexpr int RB = RowCfg<L, T>::RB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
     const int64_t nrows = (int64_t)g.n2 * g.n3;
@@ -198,10 +206,10 @@ __global__ void __launch_bounds__(256) k_row_deriv(Grid g, const T* __restrict__
 // spectrum row stride g.n1p.  Ti = float, Tc = double keeps the forward spectrum exact enough for the
 // high-wavenumber amplification of beta*A.
 template <typename Ti, typename Tc, int L>
-__global__ void __launch_bounds__(256) k_row_r2c(Grid g, const Ti* __restrict__ f, Cx<Tc>* __restrict__ spec,
+__global__ void __launch_bounds__(RowCfg<L, Tc>::NT) k_row_r2c(Grid g, const Ti* __restrict__ f, Cx<Tc>* __restrict__ spec,
                                                  const Cx<Tc>* __restrict__ twN) {
     constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int RB = (256 / TPL) > 0 ? 256 / TPL : 1;
+    constexpr int RB = RowCfg<L, Tc>::RB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Cx<Tc>* sm = reinterpret_cast<Cx<Tc>*>(smem_raw);
     const int64_t nrows = (int64_t)g.n2 * g.n3;
@@ -234,10 +242,10 @@ struct RowOut {
 // Row pass: half-spectrum rows -> real rows (c2r along x1) in T with epilogue out = x + add.
 // The spectrum already carries the full inverse normalisation.
 template <typename T, int L>
-__global__ void __launch_bounds__(256) k_row_c2r(Grid g, const Cx<T>* __restrict__ spec, RowOut<T> epi,
+__global__ void __launch_bounds__(RowCfg<L, T>::NT) k_row_c2r(Grid g, const Cx<T>* __restrict__ spec, RowOut<T> epi,
                                                  const Cx<T>* __restrict__ twN) {
     constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int RB = (256 / TPL) > 0 ? 256 / TPL : 1;
+    constexpr int RB = RowCfg<L, T>::RB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
     const int64_t nrows = (int64_t)g.n2 * g.n3;
@@ -283,7 +291,8 @@ __device__ __forceinline__ int64_t col_addr(const ColGeom& c, int x, int other, 
 template <int L, int XC, int NC = 1, int ES = 16>
 struct ColCfg {
     static constexpr int TPL = LineGeom<L>::TPL;
-    static constexpr int OLT = (XC * TPL >= 256) ? 1 : 256 / (XC * TPL);
+    static constexpr int NTT = ES == 16 ? 128 : 256;  // fp64 compute: fewer threads, more CTAs per SM
+    static constexpr int OLT = (XC * TPL >= NTT) ? 1 : NTT / (XC * TPL);
     static constexpr int MAXL = (72 * 1024) / (NC * LineGeom<L>::LP * ES);
     static constexpr int OLS = (MAXL / XC) >= 1 ? MAXL / XC : 1;
     static constexpr int OL = OLT < OLS ? OLT : OLS;

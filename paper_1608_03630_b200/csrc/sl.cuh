@@ -16,18 +16,20 @@
 
 namespace dr {
 
-constexpr int SL_TX = 32, SL_TY = 8, SL_TZ = 8, SL_THREADS = SL_TX * SL_TY;
+constexpr int SL_TX = 32, SL_TY = 8, SL_TZ = 4, SL_THREADS = SL_TX * SL_TY;
 constexpr int PLAN_INTS = 8;  // ox, oy, oz, ex, ey, ez, pad, pad
 
 // Lagrange weights for nodes -1, 0, 1, 2 at t in [0, 1) (reading A6)
+// (factored: a = t(t-1), b = (t+1)(t-2) = a - 2; w_-1 = a (2-t)/6, w_0 = b (t-1)/2, w_1 = -b t/2, w_2 = a (t+1)/6)
 template <typename T>
 __device__ __forceinline__ void lagrange4(T t, T w[4]) {
-    const T tm1 = t - T(1), tm2 = t - T(2), tp1 = t + T(1);
     const T sixth = T(1) / T(6);
-    w[0] = -t * tm1 * tm2 * sixth;
-    w[1] = tp1 * tm1 * tm2 * T(0.5);
-    w[2] = -tp1 * t * tm2 * T(0.5);
-    w[3] = tp1 * t * tm1 * sixth;
+    const T a = t * (t - T(1));
+    const T b = a - T(2);
+    w[0] = a * (T(2) * sixth - t * sixth);
+    w[1] = b * (T(0.5) * t - T(0.5));
+    w[2] = b * (T(-0.5) * t);
+    w[3] = a * (t * sixth + sixth);
 }
 
 template <typename T>
@@ -228,17 +230,50 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// Fused gather + epilogue.  Grid: one CTA per tile.  Dynamic smem: NC * capx * capy * capz values,
-// capx a multiple of VEC = 16 B / sizeof(T) so every staged row is 16-byte aligned.
+// Shared-memory box geometry per (value type, components): compile-time strides so every one of the
+// 64 stencil loads is an LDS with an immediate offset from one per-point base address.  BX is a
+// multiple of 32 words so that lanes of a warp whose departure rows differ stay on distinct banks.
+template <typename T, int NC>
+struct BoxGeom;
+template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 16, BZ = 12; };   //  48 KB
+template <> struct BoxGeom<float, 3> { static constexpr int BX = 64, BY = 16, BZ = 16; };   // 192 KB
+template <> struct BoxGeom<double, 1> { static constexpr int BX = 64, BY = 16, BZ = 16; };  // 128 KB
+template <> struct BoxGeom<double, 3> { static constexpr int BX = 32, BY = 12, BZ = 12; };  // 108 KB
+
+template <typename T, int NC>
+constexpr size_t box_bytes() {
+    return (size_t)NC * BoxGeom<T, NC>::BX * BoxGeom<T, NC>::BY * BoxGeom<T, NC>::BZ * sizeof(T);
+}
+
+template <typename T, int BX, int BY>
+__device__ __forceinline__ T interp_box(const T* __restrict__ b, const T w1[4], const T w2[4], const T w3[4]) {
+    T acc = T(0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        T accb = T(0);
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            const T* r = b + (c * BY + bb) * BX;
+            const T row = w1[0] * r[0] + w1[1] * r[1] + w1[2] * r[2] + w1[3] * r[3];
+            accb += w2[bb] * row;
+        }
+        acc += w3[c] * accb;
+    }
+    return acc;
+}
+
+// Fused gather + epilogue.  Grid: one CTA per tile.  Dynamic smem: box_bytes<T, NC>().
 // Phases: (A) stage the tile's box with 16-byte cp.async (periodic wrap per chunk; x origin aligned
-// down to VEC, which never straddles the wrap since N1 is a multiple of VEC); (B) meanwhile load the
-// displacements and the epilogue operands of the thread's 8 points; (C) wait + barrier; (D) gather
-// 64 stencil values per point from shared memory and finish the step.
+// down to VEC = 16 B / sizeof(T), which never straddles the wrap since N1 is a multiple of VEC);
+// (B) meanwhile load the displacements and the epilogue operands of the thread's 8 points; (C) wait
+// + barrier; (D) gather the 64 stencil values per point from shared memory and finish the step.
+// Tiles whose box exceeds the compile-time capacity gather from global memory instead.
 template <typename T, int NC, class Epi>
-__global__ void __launch_bounds__(SL_THREADS) k_sl_gather(Grid g, Src<T, NC> src, const T* __restrict__ d,
-                                                          const int* __restrict__ plan, int capx, int capy, int capz,
-                                                          Epi epi) {
+__global__ void __launch_bounds__(SL_THREADS, (sizeof(T) == 4 && NC == 1) ? 4 : 1) k_sl_gather(Grid g, Src<T, NC> src, const T* __restrict__ d,
+                                                          const int* __restrict__ plan, Epi epi) {
     constexpr int VEC = 16 / (int)sizeof(T);
+    constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
+    constexpr int SC = BX * BY * BZ;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* box = reinterpret_cast<T*>(smem_raw);
     int x0, y0, z0;
@@ -246,28 +281,30 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_gather(Grid g, Src<T, NC> src
     const int* pl = plan + (int64_t)blockIdx.x * PLAN_INTS;
     const int ox = pl[0] & ~(VEC - 1), oy = pl[1], oz = pl[2];
     const int ex = ((pl[0] + pl[3] - ox) + VEC - 1) & ~(VEC - 1), ey = pl[4], ez = pl[5];
-    const bool fits = ex <= capx && ey <= capy && ez <= capz;
+    const bool fits = ex <= BX && ey <= BY && ez <= BZ;
     const int lane = threadIdx.x % SL_TX, wy = threadIdx.x / SL_TX;
     const int x = x0 + lane, y = y0 + wy;
     const bool xyok = x < g.n1 && y < g.n2;
-    const int sy = capx, sz = capx * capy, sc = capx * capy * capz;
 
-    // (A) asynchronous staging of the box
+    // (A) asynchronous staging of the box: thread -> fixed 16-byte chunk column, rows strided by
+    // SL_THREADS / NCHP (no divisions in the loop)
     if (fits) {
+        constexpr int NCHP = BX / VEC;              // chunk columns of a full-width row (power of two)
+        constexpr int RSTEP = SL_THREADS / NCHP;
         const int nch = ex / VEC;
-        int yy = wy, zz = 0;
-        while (yy >= ey) { yy -= ey; ++zz; }
-        for (; zz < ez;) {
-            const int gy = wrapi(oy + yy, g.n2), gz = wrapi(oz + zz, g.n3);
-            const int64_t rowbase = ((int64_t)gz * g.n2 + gy) * g.n1;
-            for (int ch = lane; ch < nch; ch += 32) {
-                const int gx = wrapi(ox + ch * VEC, g.n1);
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    cp_async16(box + c * sc + zz * sz + yy * sy + ch * VEC, src.p[c] + rowbase + gx);
-            }
-            yy += SL_THREADS / 32;
+        const int ch = threadIdx.x % NCHP;
+        if (ch < nch) {
+            int yy = threadIdx.x / NCHP, zz = 0;
             while (yy >= ey) { yy -= ey; ++zz; }
+            while (zz < ez) {
+                const int gy = wrapi(oy + yy, g.n2), gz = wrapi(oz + zz, g.n3);
+                const int64_t gofs = ((int64_t)gz * g.n2 + gy) * g.n1 + wrapi(ox + ch * VEC, g.n1);
+                T* dst = box + (zz * BY + yy) * BX + ch * VEC;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) cp_async16(dst + c * SC, src.p[c] + gofs);
+                yy += RSTEP;
+                while (yy >= ey) { yy -= ey; ++zz; }
+            }
         }
     }
 
@@ -288,32 +325,48 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_gather(Grid g, Src<T, NC> src
     if (fits) cp_async_wait_all();
     __syncthreads();
     if (!xyok) return;
+    const int kmax = min(SL_TZ, g.n3 - z0);
 
     // (D)
+    if (fits) {
 #pragma unroll
-    for (int k = 0; k < SL_TZ; ++k) {
-        const int z = z0 + k;
-        if (z >= g.n3) break;
-        const int64_t id = ((int64_t)z * g.n2 + y) * g.n1 + x;
-        int q1, q2, q3;
-        T t1, t2, t3;
-        cell_of<T>(x, dd[k][0], q1, t1);
-        cell_of<T>(y, dd[k][1], q2, t2);
-        cell_of<T>(z, dd[k][2], q3, t3);
-        T w1[4], w2[4], w3[4];
-        lagrange4(t1, w1);
-        lagrange4(t2, w2);
-        lagrange4(t3, w3);
-        T val[NC];
-        if (fits) {
-            const T* b = box + (q3 - 1 - oz) * sz + (q2 - 1 - oy) * sy + (q1 - 1 - ox);
+        for (int k = 0; k < SL_TZ; ++k) {
+            if (k >= kmax) break;
+            const int z = z0 + k;
+            int q1, q2, q3;
+            T t1, t2, t3;
+            cell_of<T>(x, dd[k][0], q1, t1);
+            cell_of<T>(y, dd[k][1], q2, t2);
+            cell_of<T>(z, dd[k][2], q3, t3);
+            T w1[4], w2[4], w3[4];
+            lagrange4(t1, w1);
+            lagrange4(t2, w2);
+            lagrange4(t3, w3);
+            const T* b = box + ((q3 - 1 - oz) * BY + (q2 - 1 - oy)) * BX + (q1 - 1 - ox);
+            T val[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) val[c] = interp_smem(b + c * sc, sy, sz, w1, w2, w3);
-        } else {
+            for (int c = 0; c < NC; ++c) val[c] = interp_box<T, BX, BY>(b + c * SC, w1, w2, w3);
+            epi.store(((int64_t)z * g.n2 + y) * g.n1 + x, val, pre[k]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < SL_TZ; ++k) {
+            if (k >= kmax) break;
+            const int z = z0 + k;
+            int q1, q2, q3;
+            T t1, t2, t3;
+            cell_of<T>(x, dd[k][0], q1, t1);
+            cell_of<T>(y, dd[k][1], q2, t2);
+            cell_of<T>(z, dd[k][2], q3, t3);
+            T w1[4], w2[4], w3[4];
+            lagrange4(t1, w1);
+            lagrange4(t2, w2);
+            lagrange4(t3, w3);
+            T val[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) val[c] = interp_global(src.p[c], g, q1, q2, q3, w1, w2, w3);
+            epi.store(((int64_t)z * g.n2 + y) * g.n1 + x, val, pre[k]);
         }
-        epi.store(id, val, pre[k]);
     }
 }
 
