@@ -54,6 +54,7 @@ def test_workspace_scales_with_config(L):
     a = dr.dr_workspace_bytes(dr.Config(n=64, nt=4))
     b = dr.dr_workspace_bytes(dr.Config(n=64, nt=8))
     c = dr.dr_workspace_bytes(dr.Config(n=64, nt=4, fp64=True))
-    assert a < b and 1.9 * a < c < 2.1 * a
+    # forward half spectra are complex128 in both precisions (DESIGN reading A20), so fp64 is < 2x
+    assert a < b and 1.5 * a < c < 2.1 * a
     # 256^3, nt=4 fp32 fits comfortably in one B200 (180 GB)
     assert dr.dr_workspace_bytes(dr.Config(n=256, nt=4)) < 8e9
