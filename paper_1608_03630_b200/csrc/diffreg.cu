@@ -134,6 +134,7 @@ struct dr_ctx {
     Grid g;
     Layout L;
     cudaStream_t stream = nullptr;
+    int num_sms = 148;
     char* ws = nullptr;
     bool own_ws = false;
     bool have_images = false, have_velocity = false, have_state = false, have_adjoint = false, have_matvec = false;
@@ -261,40 +262,46 @@ struct Impl {
     }
 
     // -------------------------------------------------------------------- FFT pass launchers
-    template <int L, typename U = T>
-    static size_t row_smem() { return (size_t)RowCfg<L, U>::RB * LineGeom<L>::LP * sizeof(Cx<U>); }
-    template <int L, typename U = T>
-    int row_blocks() const { return (int)(((int64_t)g.n2 * g.n3 + RowCfg<L, U>::RB - 1) / RowCfg<L, U>::RB); }
-
     template <typename K>
     static void set_smem(K kernel, size_t bytes) {
         if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     }
 
+    // Launch of an FFT pass: DB = persistent double-buffered (as many CTAs as fit on the GPU at once),
+    // else one tile per CTA.
+    template <class PassT, bool DB = false>
+    void stream(const char* tag, const PassT& pass, int64_t ntiles) {
+        auto k = k_stream<PassT, DB>;
+        const size_t sm = (DB ? 2 : 1) * PassT::BUF;
+        static int occ = 0;  // per pass instantiation
+        if (occ == 0) {
+            set_smem(k, sm);
+            int o = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, PassT::NT, sm));
+            occ = o > 0 ? o : 1;
+        }
+        const int grid = DB ? (int)std::min<int64_t>(ntiles, (int64_t)occ * c.num_sms) : (int)ntiles;
+        PB();
+        k<<<grid, PassT::NT, sm, s>>>(pass);
+        PE(tag);
+    }
+    template <int RB>
+    int64_t row_tiles() const { return ((int64_t)g.n2 * g.n3 + RB - 1) / RB; }
+
     template <int L>
     void row_deriv_L(const T* f, T* out, int acc) {
-        auto k = k_row_deriv<T, L>;
-        set_smem(k, row_smem<L>());
-        PB();
-        k<<<row_blocks<L>(), RowCfg<L, T>::NT, row_smem<L>(), s>>>(g, f, out, acc, twx());
-        PE("row_deriv");
+        using PT = RowDerivPass<T, L>;
+        stream("row_deriv", PT{g, f, out, acc, twx()}, row_tiles<PT::RB>());
     }
     template <int L>
     void row_r2c_L(const T* f, Cx<double>* sp) {
-        auto k = k_row_r2c<T, double, L>;
-        set_smem(k, row_smem<L, double>());
-        PB();
-        k<<<row_blocks<L, double>(), RowCfg<L, double>::NT, row_smem<L, double>(), s>>>(g, f, sp, twxd());
-        PE("row_r2c");
+        using PT = RowR2cPass<T, double, L>;
+        stream("row_r2c", PT{g, f, sp, twxd()}, row_tiles<PT::RB>());
     }
     template <int L>
     void row_c2r_L(const Cx<T>* sp, T* out, const T* add) {
-        auto k = k_row_c2r<T, L>;
-        set_smem(k, row_smem<L>());
-        RowOut<T> e{out, add};
-        PB();
-        k<<<row_blocks<L>(), RowCfg<L, T>::NT, row_smem<L>(), s>>>(g, sp, e, twx());
-        PE("row_c2r");
+        using PT = RowC2rPass<T, L>;
+        stream("row_c2r", PT{g, sp, RowOut<T>{out, add}, twx()}, row_tiles<PT::RB>());
     }
 
 #define DR_SWITCH_ROW(Lval, call)                          \
@@ -340,25 +347,9 @@ struct Impl {
 #undef CALL
     }
 
-    // columns per CTA: keep NC components of the CTA's lines within ~64 KB of shared memory
-    template <int L, int NC, typename U = T>
-    static constexpr int pick_xc() {  // 128-byte column chunks (16 complex64 / 8 complex128), smem-capped
-        return (sizeof(U) == 4 && NC * 16 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 16
-               : (NC * 8 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 8
-               : (NC * 4 * LineGeom<L>::LP * (int)sizeof(Cx<U>) <= 72 * 1024) ? 4
-                                                                              : 2;
-    }
-    template <int L, int XC, int NC, typename U>
-    using CCfg = ColCfg<L, XC, NC, (int)sizeof(Cx<U>)>;
-    template <int L, int XC, int NC, typename U>
-    static size_t col_smem() {
-        return (size_t)NC * CCfg<L, XC, NC, U>::LINES * LineGeom<L>::LP * sizeof(Cx<U>);
-    }
-    template <int L, int XC, int NC, typename U>
-    int col_blocks(const ColGeom& cg, int nother) const {
-        const int nxb = (cg.nx + XC - 1) / XC;
-        constexpr int OL = CCfg<L, XC, NC, U>::OL;
-        return nxb * ((nother + OL - 1) / OL);
+    template <class PT>
+    static int64_t col_tiles(const ColGeom& cg, int nother) {
+        return (int64_t)((cg.nx + PT::XC - 1) / PT::XC) * ((nother + PT::OL - 1) / PT::OL);
     }
 
     ColGeom spec_geom() const { return ColGeom{g.n1p, g.n1c, g.n2, g.n3}; }
@@ -366,15 +357,10 @@ struct Impl {
 
     template <int L, int AX>
     void col_deriv_L(const T* f, T* out, int acc) {
-        constexpr int XC = pick_xc<L, 1>();
+        using PT = ColDerivPass<T, L, AX>;
         const ColGeom cg = pair_geom();
-        auto k = k_col_deriv<T, L, XC, AX>;
-        const size_t sm = col_smem<L, XC, 1, T>();
-        set_smem(k, sm);
-        PB();
-        k<<<col_blocks<L, XC, 1, T>(cg, AX == 2 ? g.n3 : g.n2), CCfg<L, XC, 1, T>::NT, sm, s>>>(
-            cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, AX == 2 ? twy() : twz());
-        PE("col_deriv");
+        stream("col_deriv", PT{cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, AX == 2 ? twy() : twz()},
+               col_tiles<PT>(cg, AX == 2 ? g.n3 : g.n2));
     }
     void col_deriv(int ax, const T* f, T* out, int acc) {
         if (ax == 2) {
@@ -390,15 +376,9 @@ struct Impl {
 
     template <typename U, int L, int DIR>
     void col_fft_L(Cx<U>* sp, const Cx<U>* tw) {
-        const char* tag = DIR < 0 ? "col_fft_fwd" : "col_fft_inv";
-        constexpr int XC = pick_xc<L, 1, U>();
+        using PT = ColFftPass<U, L, DIR>;
         const ColGeom cg = spec_geom();
-        auto k = k_col_fft<U, L, XC, DIR>;
-        const size_t sm = col_smem<L, XC, 1, U>();
-        set_smem(k, sm);
-        PB();
-        k<<<col_blocks<L, XC, 1, U>(cg, g.n3), CCfg<L, XC, 1, U>::NT, sm, s>>>(cg, sp, tw);
-        PE(tag);
+        stream(DIR < 0 ? "col_fft_fwd" : "col_fft_inv", PT{cg, sp, tw}, col_tiles<PT>(cg, g.n3));
     }
     void col_fft_fwd(Cx<double>* sp) {  // forward along x2, in double
 #define CALL(LL) col_fft_L<double, LL, -1>(sp, twyd())
@@ -413,20 +393,16 @@ struct Impl {
 
     template <int L, int KIND>
     void middle_L(Cx<double>* const* in, Cx<T>* const* out) {
-        constexpr int NCI = Sym<double, KIND>::NCI, NCO = Sym<double, KIND>::NCO;
-        constexpr int XC = pick_xc<L, NCI, double>();
+        using PT = MiddlePass<double, T, L, KIND>;
         const ColGeom cg = spec_geom();
-        SpecPtrs<double, NCI> pi;
-        SpecPtrs<T, NCO> po;
-        for (int i = 0; i < NCI; ++i) pi.p[i] = in[i];
-        for (int i = 0; i < NCO; ++i) po.p[i] = out[i];
-        SymInfo si{c.cfg.reg, c.cfg.beta, 2.0 / (double)g.M};
-        auto k = k_col_middle<double, T, L, XC, KIND>;
-        const size_t sm = col_smem<L, XC, NCI, double>();
-        set_smem(k, sm);
-        PB();
-        k<<<col_blocks<L, XC, NCI, double>(cg, g.n2), CCfg<L, XC, NCI, double>::NT, sm, s>>>(cg, pi, po, si, twzd());
-        PE("col_middle");
+        PT pt;
+        pt.c = cg;
+        for (int i = 0; i < PT::NCI; ++i) pt.in.p[i] = in[i];
+        for (int i = 0; i < PT::NCO; ++i) pt.out.p[i] = out[i];
+        pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / (double)g.M};
+        pt.tw = twzd();
+        pt.two = twz();
+        stream("col_middle", pt, col_tiles<PT>(cg, g.n2));
     }
     template <int KIND>
     void middle(Cx<double>* const* in, Cx<T>* const* out) {
@@ -496,8 +472,12 @@ struct Impl {
         constexpr size_t sm = box_bytes<T, NC>();
         auto k = k_sl_gather<T, NC, Epi>;
         set_smem(k, sm);
+        const Disp<T> dp{{d, d + g.M, d + 2 * g.M}};
+        const int nt = (int)n_tiles(g);
+        // double-buffered geometries run persistent (a few CTAs per SM); single-stage ones one tile per CTA
+        const int grid = BoxGeom<T, NC>::STAGES == 2 ? std::min(nt, c.num_sms * BoxGeom<T, NC>::MINB) : nt;
         PB();
-        k<<<(unsigned)n_tiles(g), SL_THREADS, sm, s>>>(g, src, d, plan_buf, epi);
+        k<<<(unsigned)grid, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
         PE(tag);
     }
     int* plan_p() { return c.at<int>(c.L.plan_p); }
@@ -522,9 +502,12 @@ struct Impl {
             PE("dstar");
             plan(tmp3(), plan_t());
             EpiDeparture<T> e;
-            e.d = dout;
-            e.v = v();
-            e.M = g.M;
+            e.d0 = dout;
+            e.d1 = dout + g.M;
+            e.d2 = dout + 2 * g.M;
+            e.v0 = v();
+            e.v1 = v() + g.M;
+            e.v2 = v() + 2 * g.M;
             for (int a = 0; a < 3; ++a) e.c[a] = (T)(sg * 0.5 * dtt / h[a]);
             gather<3>("sl_departure", Src<T, 3>{{v(), v() + g.M, v() + 2 * g.M}}, tmp3(), plan_t(), e);
             plan(dout, sg > 0 ? plan_p() : plan_m());
@@ -558,18 +541,41 @@ struct Impl {
         PE("inc_init");
         for (int j = 0; j < nt; ++j) {
             const bool last = (j == nt - 1);
-            EpiIncState<T> e{last ? rt1() : lt(j + 1), vt, G(j + 1), last ? T(0.5) * dtt : dtt, g.M};
+            const T* Gj = G(j + 1);
+            EpiIncState<T> e{last ? rt1() : lt(j + 1), vt, vt + g.M, vt + 2 * g.M, Gj, Gj + g.M, Gj + 2 * g.M,
+                             last ? T(0.5) * dtt : dtt};
             gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), e);
         }
-        // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-)
+        // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-); every step
+        // also accumulates its term of the b~ trapezoid quadrature in its epilogue
         for (int k = nt; k >= 1; --k) {
             const T* src = (k == nt) ? rt1() : lt(k);
-            gather<1>("sl_inc_adjoint", Src<T, 1>{{src}}, dminus(), plan_m(),
-                      EpiAdjoint<T>{lt(k - 1), mult_or_null(), k == nt ? T(-1) : T(1)});
+            const T* Gk = G(k - 1);
+            const T wk = (k - 1 == 0) ? T(0.5) * dtt : dtt;
+            if (k == nt) {
+                EpiAdjoint<T, 1> e{};
+                e.out = lt(k - 1);
+                e.m = mult_or_null();
+                e.scale = T(-1);
+                e.b0 = bt(); e.b1 = bt() + g.M; e.b2 = bt() + 2 * g.M;
+                e.G0 = Gk; e.G1 = Gk + g.M; e.G2 = Gk + 2 * g.M;
+                e.w = wk;
+                e.nu = rt1(); e.snu = T(-1);
+                const T* Gn = G(nt);
+                e.H0 = Gn; e.H1 = Gn + g.M; e.H2 = Gn + 2 * g.M;
+                e.wn = T(0.5) * dtt;
+                gather<1>("sl_inc_adjoint_q1", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+            } else {
+                EpiAdjoint<T, 2> e{};
+                e.out = lt(k - 1);
+                e.m = mult_or_null();
+                e.scale = T(1);
+                e.b0 = bt(); e.b1 = bt() + g.M; e.b2 = bt() + 2 * g.M;
+                e.G0 = Gk; e.G1 = Gk + g.M; e.G2 = Gk + 2 * g.M;
+                e.w = wk;
+                gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+            }
         }
-        PB();
-        k_quadrature<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, nt, lt(0), rt1(), T(-1), G(0), bt(), dtt);
-        PE("quadrature");
         // spectral tail: H vt = beta A vt + P b~
         if (c.cfg.flags & DR_ISOCHORIC) {
             Cx<double>* sd[6] = {specD(0), specD(1), specD(2), specD(3), specD(4), specD(5)};
@@ -671,6 +677,12 @@ dr_status dr_create(const dr_config* cfg, void* workspace, size_t workspace_byte
     c->g = make_grid(cfg);
     c->L = layout(cfg);
     c->stream = reinterpret_cast<cudaStream_t>(stream);
+    {
+        int dev = 0, nsm = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+            c->num_sms = nsm;
+        cudaGetLastError();
+    }
     if (workspace) {
         if (workspace_bytes < c->L.total) {
             delete c;

@@ -1,7 +1,8 @@
 // fft.cuh -- shared-memory Stockham FFT passes for the spectral operators (§III-B1,
-// L303 §III-C1).  Every pass streams a field once from HBM into shared memory, transforms whole
-// lines there (radix-16 register butterflies, padded smem to avoid bank conflicts, fp32/fp64
-// twiddles from a table built in double precision on the host) and streams it back.
+// L303 §III-C1).  Every pass streams a field once from HBM into shared memory (16/8-byte cp.async,
+// all of a CTA's loads in flight at once), transforms whole lines there (register butterflies of
+// radix 16 in fp32 / radix 8 in fp64, padded smem against bank conflicts, twiddles from tables built
+// in double precision on the host) and streams it back.
 //
 // Pass kinds
 //   row_deriv      real rows (x1) -> d/dx1 (r2c, i k'_1, c2r), one HBM read + one write
@@ -20,17 +21,45 @@ namespace dr {
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }
 template <int L>
 struct LineGeom {
-    static constexpr int TPL = (L >= 16) ? L / 16 : 1;  // threads per line
-    static constexpr int LP = L + L / 16 + 2;           // padded line length (holds index L for r2c)
+    static constexpr int LP = L + L / 16 + 2;  // padded line length (holds index L for r2c)
 };
-// Row passes: RB rows per CTA, ~256 threads for fp32 compute and ~128 for fp64 (register footprint of
-// the radix-16 butterflies doubles) so several CTAs fit per SM.
-template <int L, typename Tc>
+// Threads per line: each owns the 16 values of one radix-16 butterfly per stage.
+template <int L, typename T>
+struct Tpl {
+    static constexpr int R = 16;
+    static constexpr int V = (L >= R) ? L / R : 1;
+};
+template <typename T>
+struct CtaThreads {  // fp64 passes: fewer threads per CTA (large register footprint), more CTAs per SM
+    static constexpr int V = sizeof(T) == 8 ? 128 : 256;
+};
+// Minimum resident CTAs of a pass for __launch_bounds__: 3 x 256 threads for fp32 compute (<= 80
+// registers); 3 x 128 for fp64 (<= 170 registers for the radix-16 fp64 butterflies).
+template <typename T, int NT>
+struct MinB {
+    static constexpr int V = sizeof(T) == 8 ? ((384 / NT) > 0 ? 384 / NT : 1) : ((768 / NT) > 0 ? 768 / NT : 1);
+};
+// Row passes: RB rows per CTA of ~256 threads.  Ti = type of the staged input when it differs from
+// the compute type Tc (fp32 rows converted to fp64 in shared memory), else Ti = Tc.
+template <int L, typename Tc, typename Ti = Tc>
 struct RowCfg {
-    static constexpr int NTT = sizeof(Tc) == 8 ? 128 : 256;
-    static constexpr int RB = (NTT / LineGeom<L>::TPL) > 0 ? NTT / LineGeom<L>::TPL : 1;
-    static constexpr int NT = RB * LineGeom<L>::TPL;
+    static constexpr int TPL = Tpl<L, Tc>::V;
+    static constexpr int RB = (CtaThreads<Tc>::V / TPL) > 0 ? CtaThreads<Tc>::V / TPL : 1;
+    static constexpr int NT = RB * TPL;
+    static constexpr size_t SMEM = (size_t)RB * LineGeom<L>::LP *
+                                   (sizeof(Cx<Tc>) + (sizeof(Ti) != sizeof(Tc) ? sizeof(Cx<Ti>) : 0));
 };
+
+template <typename C>
+__device__ __forceinline__ void cp_async_elem(C* smem, const C* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (sizeof(C) == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_join() {
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+}
 
 // e^{DIR * 2 pi i m / 16}, m compile-time after unrolling
 template <typename T, int DIR>
@@ -74,11 +103,10 @@ struct DFT<T, 1, DIR> {
 };
 
 // One Stockham autosort stage of radix R (Ns = product of the previous radices) on a line of
-// length L held in padded shared memory.  Each of the TPL threads of the line owns 16 values
-// (L/R/TPL butterflies).  tw: table of e^{-2 pi i m / (L*tws)}, m < L*tws.
-template <typename T, int L, int R, int Ns, int DIR>
+// length L held in padded shared memory.  Each of the TPL threads of the line owns NB = L/R/TPL
+// butterflies.  tw: table of e^{-2 pi i m / (L*tws)}, m < L*tws.
+template <typename T, int L, int R, int Ns, int DIR, int TPL>
 __device__ __forceinline__ void stockham_stage(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws) {
-    constexpr int TPL = LineGeom<L>::TPL;
     constexpr int NB = (L / R) / TPL;
     Cx<T> x[NB][R];
 #pragma unroll
@@ -109,20 +137,21 @@ __device__ __forceinline__ void stockham_stage(Cx<T>* buf, int t, const Cx<T>* _
     __syncthreads();
 }
 
-// Whole-line FFT (in place, padded layout).  Radix plan: 16 x 16 x ... x r.
+template <typename T, int L, int DIR, int TPL, int R, int Ns>
+__device__ __forceinline__ void fft_stages(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws) {
+    if constexpr (Ns * R >= L) {
+        stockham_stage<T, L, L / Ns, Ns, DIR, TPL>(buf, t, tw, tws);
+    } else {
+        stockham_stage<T, L, R, Ns, DIR, TPL>(buf, t, tw, tws);
+        fft_stages<T, L, DIR, TPL, R, Ns * R>(buf, t, tw, tws);
+    }
+}
+
+// Whole-line FFT (in place, padded layout), radix plan R x R x ... x r with R = 16 (fp32) / 8 (fp64).
 // Every thread of the CTA must call this (it contains __syncthreads).
 template <typename T, int L, int DIR>
 __device__ __forceinline__ void fft_line(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws) {
-    if constexpr (L <= 16) {
-        stockham_stage<T, L, L, 1, DIR>(buf, t, tw, tws);
-    } else if constexpr (L <= 256) {
-        stockham_stage<T, L, 16, 1, DIR>(buf, t, tw, tws);
-        stockham_stage<T, L, L / 16, 16, DIR>(buf, t, tw, tws);
-    } else {
-        stockham_stage<T, L, 16, 1, DIR>(buf, t, tw, tws);
-        stockham_stage<T, L, 16, 16, DIR>(buf, t, tw, tws);
-        stockham_stage<T, L, L / 256, 256, DIR>(buf, t, tw, tws);
-    }
+    fft_stages<T, L, DIR, Tpl<L, T>::V, Tpl<L, T>::R, 1>(buf, t, tw, tws);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -130,9 +159,8 @@ __device__ __forceinline__ void fft_line(Cx<T>* buf, int t, const Cx<T>* __restr
 // z_n = x_{2n} + i x_{2n+1}.  After the forward L-point FFT Z, X_k (k = 0..L) of the N-point DFT:
 //   E = (Z_k + conj Z_{L-k})/2, O = (Z_k - conj Z_{L-k})/(2i), X_k = E + W^k O, X_{L-k} = conj(E - W^k O),
 // W = e^{-2 pi i/N}.  Pairs (k, L-k) are handled by one thread, so the update is in place.
-template <typename T, int L>
+template <typename T, int L, int TPL>
 __device__ __forceinline__ void r2c_post(Cx<T>* buf, int t, const Cx<T>* __restrict__ twN) {
-    constexpr int TPL = LineGeom<L>::TPL;
     for (int k = t; k <= L / 2; k += TPL) {
         const Cx<T> zk = buf[P(k)];
         const Cx<T> zl = buf[P(k == 0 ? 0 : L - k)];
@@ -151,9 +179,8 @@ __device__ __forceinline__ void r2c_post(Cx<T>* buf, int t, const Cx<T>* __restr
 
 // inverse: given X_0..X_L, Z_k = E + i O with E = (X_k + conj X_{L-k})/2,
 // O = (X_k - conj X_{L-k}) conj(W^k)/2, and Z_{L-k} = conj(E) + i conj(O).
-template <typename T, int L>
+template <typename T, int L, int TPL>
 __device__ __forceinline__ void c2r_pre(Cx<T>* buf, int t, const Cx<T>* __restrict__ twN) {
-    constexpr int TPL = LineGeom<L>::TPL;
     for (int k = t; k <= L / 2; k += TPL) {
         const Cx<T> xk = buf[P(k)];
         const Cx<T> xl = buf[P(L - k)];
@@ -166,71 +193,146 @@ __device__ __forceinline__ void c2r_pre(Cx<T>* buf, int t, const Cx<T>* __restri
     __syncthreads();
 }
 
-// ---------------------------------------------------------------------------------------------
+// Stage RB contiguous rows of L complex values (row r of the CTA at src + r L) into padded lines
+// sm + r LP, asynchronously, one complex value (8 or 16 bytes) per cp.async.
+template <typename C, int L, int NT>
+__device__ __forceinline__ void row_stage(C* sm, const C* __restrict__ src, int nvalid) {
+    constexpr int LP = LineGeom<L>::LP;
+    for (int e = threadIdx.x; e < nvalid * L; e += NT) cp_async_elem(sm + (e / L) * LP + P(e % L), src + e);
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// Driver shared by every FFT pass.  DB = true: persistent, a CTA walks tiles blockIdx.x, + gridDim.x,
+// ... with two shared-memory buffers (the next tile's cp.async loads fly while the current tile is
+// transformed and stored); DB = false: one tile per CTA, the hardware overlaps resident CTAs.
+// PassT supplies NT, MINB, BUF (bytes per buffer), ntiles(), load(tile, smem), run(tile, smem).
+template <class PassT, bool DB>
+__global__ void __launch_bounds__(PassT::NT, PassT::MINB) k_stream(PassT pass) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int tile = blockIdx.x;
+    const int ntiles = pass.ntiles();
+    if (tile >= ntiles) return;
+    if constexpr (!DB) {  // one tile per CTA: load, transform, store
+        pass.load(tile, smem_raw);
+        cp_async_join();
+        pass.run(tile, smem_raw);
+        return;
+    }
+    pass.load(tile, smem_raw);
+    cp_async_commit();
+    int cur = 0;
+    for (;;) {
+        const int next = tile + gridDim.x;
+        const bool more = next < ntiles;
+        if (more) pass.load(next, smem_raw + (cur ^ 1) * PassT::BUF);
+        cp_async_commit();
+        cp_async_wait1();  // everything but the newest group has landed: the current tile is in smem
+        __syncthreads();
+        pass.run(tile, smem_raw + cur * PassT::BUF);
+        if (!more) break;
+        __syncthreads();  // the current buffer is refilled by the next iteration's prefetch
+        tile = next;
+        cur ^= 1;
+    }
+}
+
 // Row pass: x1-derivative of real rows ("N2 N3 1D FFTs across the first coordinate,
 // diagonal scaling, and then the same number of inverse FFTs").  out = acc*out + d f/dx1.
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L, T>::NT) k_row_deriv(Grid g, const T* __restrict__ f, T* __restrict__ out,
-                                                   int accumulate, const Cx<T>* __restrict__ twN) {
-    constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int RB = RowCfg<L, T>::RB;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
-    const int64_t nrows = (int64_t)g.n2 * g.n3;
-    const int64_t row0 = (int64_t)blockIdx.x * RB;
-    const Cx<T>* src = reinterpret_cast<const Cx<T>*>(f) + row0 * L;
-    const int nvalid = (int)((nrows - row0) < RB ? (nrows - row0) : RB);
-    for (int e = threadIdx.x; e < nvalid * L; e += blockDim.x) sm[(e / L) * LP + P(e % L)] = src[e];
-    __syncthreads();
-    const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    Cx<T>* buf = sm + line * LP;
-    fft_line<T, L, -1>(buf, t, twN, 2);
-    r2c_post<T, L>(buf, t, twN);
-    // X_k *= i k'_1 / L  (k = 0..L; Nyquist k = L is zeroed, reading A2; 1/L normalises the c2r)
-    for (int k = t; k <= L; k += TPL) {
-        const T kk = (k == L) ? T(0) : T(k);
-        buf[P(k)] = mul_i(buf[P(k)], kk / T(L));
+struct RowDerivPass {
+    using RC = RowCfg<L, T>;
+    static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr size_t BUF = (size_t)RB * LP * sizeof(Cx<T>);
+    Grid g;
+    const T* f;
+    T* out;
+    int accumulate;
+    const Cx<T>* twN;
+    __device__ __forceinline__ int ntiles() const { return (int)(((int64_t)g.n2 * g.n3 + RB - 1) / RB); }
+    __device__ __forceinline__ int nvalid(int tile) const {
+        const int64_t rem = (int64_t)g.n2 * g.n3 - (int64_t)tile * RB;
+        return (int)(rem < RB ? rem : RB);
     }
-    __syncthreads();
-    c2r_pre<T, L>(buf, t, twN);
-    fft_line<T, L, +1>(buf, t, twN, 2);
-    Cx<T>* dst = reinterpret_cast<Cx<T>*>(out) + row0 * L;
-    for (int e = threadIdx.x; e < nvalid * L; e += blockDim.x) {
-        Cx<T> v = sm[(e / L) * LP + P(e % L)];
-        if (accumulate) { const Cx<T> o = dst[e]; v = v + o; }
-        dst[e] = v;
+    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
+        row_stage<Cx<T>, L, NT>(reinterpret_cast<Cx<T>*>(smem), reinterpret_cast<const Cx<T>*>(f) + (int64_t)tile * RB * L,
+                                nvalid(tile));
     }
-}
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        const int nv = nvalid(tile);
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        Cx<T>* buf = sm + line * LP;
+        fft_line<T, L, -1>(buf, t, twN, 2);
+        r2c_post<T, L, TPL>(buf, t, twN);
+        // X_k *= i k'_1 / L  (k = 0..L; Nyquist k = L is zeroed, reading A2; 1/L normalises the c2r)
+        for (int k = t; k <= L; k += TPL) {
+            const T kk = (k == L) ? T(0) : T(k);
+            buf[P(k)] = mul_i(buf[P(k)], kk / T(L));
+        }
+        __syncthreads();
+        c2r_pre<T, L, TPL>(buf, t, twN);
+        fft_line<T, L, +1>(buf, t, twN, 2);
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(out) + (int64_t)tile * RB * L;
+        for (int e = threadIdx.x; e < nv * L; e += NT) {
+            Cx<T> v = sm[(e / L) * LP + P(e % L)];
+            if (accumulate) { const Cx<T> o = dst[e]; v = v + o; }
+            dst[e] = v;
+        }
+    }
+};
 
 // Row pass: real rows (type Ti) -> half-spectrum rows (r2c along x1) computed and stored in Tc,
 // spectrum row stride g.n1p.  Ti = float, Tc = double keeps the forward spectrum exact enough for the
 // high-wavenumber amplification of beta*A.
+// The fp32 rows are staged asynchronously into their own buffer and widened in shared memory.
 template <typename Ti, typename Tc, int L>
-__global__ void __launch_bounds__(RowCfg<L, Tc>::NT) k_row_r2c(Grid g, const Ti* __restrict__ f, Cx<Tc>* __restrict__ spec,
-                                                 const Cx<Tc>* __restrict__ twN) {
-    constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int RB = RowCfg<L, Tc>::RB;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Cx<Tc>* sm = reinterpret_cast<Cx<Tc>*>(smem_raw);
-    const int64_t nrows = (int64_t)g.n2 * g.n3;
-    const int64_t row0 = (int64_t)blockIdx.x * RB;
-    const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f) + row0 * L;
-    const int nvalid = (int)((nrows - row0) < RB ? (nrows - row0) : RB);
-    for (int e = threadIdx.x; e < nvalid * L; e += blockDim.x) {
-        const Cx<Ti> v = src[e];
-        sm[(e / L) * LP + P(e % L)] = cx<Tc>((Tc)v.re, (Tc)v.im);
+struct RowR2cPass {
+    using RC = RowCfg<L, Tc, Ti>;
+    static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = MinB<Tc, NT>::V;
+    static constexpr size_t BUF = RC::SMEM;
+    static constexpr size_t STG = (size_t)RB * LP * sizeof(Cx<Tc>);  // offset of the Ti staging lines
+    Grid g;
+    const Ti* f;
+    Cx<Tc>* spec;
+    const Cx<Tc>* twN;
+    __device__ __forceinline__ int ntiles() const { return (int)(((int64_t)g.n2 * g.n3 + RB - 1) / RB); }
+    __device__ __forceinline__ int nvalid(int tile) const {
+        const int64_t rem = (int64_t)g.n2 * g.n3 - (int64_t)tile * RB;
+        return (int)(rem < RB ? rem : RB);
     }
-    __syncthreads();
-    const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    Cx<Tc>* buf = sm + line * LP;
-    fft_line<Tc, L, -1>(buf, t, twN, 2);
-    r2c_post<Tc, L>(buf, t, twN);
-    constexpr int NC = L + 1;
-    for (int e = threadIdx.x; e < nvalid * NC; e += blockDim.x) {
-        const int r = e / NC, k = e % NC;
-        spec[(row0 + r) * g.n1p + k] = sm[r * LP + P(k)];
+    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
+        const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f) + (int64_t)tile * RB * L;
+        if constexpr (sizeof(Ti) == sizeof(Tc)) row_stage<Cx<Tc>, L, NT>(reinterpret_cast<Cx<Tc>*>(smem), reinterpret_cast<const Cx<Tc>*>(src), nvalid(tile));
+        else row_stage<Cx<Ti>, L, NT>(reinterpret_cast<Cx<Ti>*>(smem + STG), src, nvalid(tile));
     }
-}
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        Cx<Tc>* sm = reinterpret_cast<Cx<Tc>*>(smem);
+        const int nv = nvalid(tile);
+        if constexpr (sizeof(Ti) != sizeof(Tc)) {
+            const Cx<Ti>* st = reinterpret_cast<const Cx<Ti>*>(smem + STG);
+            for (int e = threadIdx.x; e < nv * L; e += NT) {
+                const int o = (e / L) * LP + P(e % L);
+                const Cx<Ti> v = st[o];
+                sm[o] = cx<Tc>((Tc)v.re, (Tc)v.im);
+            }
+            __syncthreads();
+        }
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        Cx<Tc>* buf = sm + line * LP;
+        fft_line<Tc, L, -1>(buf, t, twN, 2);
+        r2c_post<Tc, L, TPL>(buf, t, twN);
+        constexpr int NC = L + 1;
+        const int64_t row0 = (int64_t)tile * RB;
+        for (int e = threadIdx.x; e < nv * NC; e += NT) {
+            const int r = e / NC, k = e % NC;
+            spec[(row0 + r) * g.n1p + k] = sm[r * LP + P(k)];
+        }
+    }
+};
 
 // Row pass epilogue for the c2r inverse: out = x (+ add)
 template <typename T>
@@ -242,33 +344,47 @@ struct RowOut {
 // Row pass: half-spectrum rows -> real rows (c2r along x1) in T with epilogue out = x + add.
 // The spectrum already carries the full inverse normalisation.
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L, T>::NT) k_row_c2r(Grid g, const Cx<T>* __restrict__ spec, RowOut<T> epi,
-                                                 const Cx<T>* __restrict__ twN) {
-    constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int RB = RowCfg<L, T>::RB;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
-    const int64_t nrows = (int64_t)g.n2 * g.n3;
-    const int64_t row0 = (int64_t)blockIdx.x * RB;
-    const int nvalid = (int)((nrows - row0) < RB ? (nrows - row0) : RB);
-    constexpr int NC = L + 1;
-    for (int e = threadIdx.x; e < nvalid * NC; e += blockDim.x) {
-        const int r = e / NC, k = e % NC;
-        sm[r * LP + P(k)] = spec[(row0 + r) * g.n1p + k];
+struct RowC2rPass {
+    using RC = RowCfg<L, T>;
+    static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr size_t BUF = (size_t)RB * LP * sizeof(Cx<T>);
+    Grid g;
+    const Cx<T>* spec;
+    RowOut<T> epi;
+    const Cx<T>* twN;
+    __device__ __forceinline__ int ntiles() const { return (int)(((int64_t)g.n2 * g.n3 + RB - 1) / RB); }
+    __device__ __forceinline__ int nvalid(int tile) const {
+        const int64_t rem = (int64_t)g.n2 * g.n3 - (int64_t)tile * RB;
+        return (int)(rem < RB ? rem : RB);
     }
-    __syncthreads();
-    const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    Cx<T>* buf = sm + line * LP;
-    c2r_pre<T, L>(buf, t, twN);
-    fft_line<T, L, +1>(buf, t, twN, 2);
-    Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out) + row0 * L;
-    const Cx<T>* add = epi.add ? reinterpret_cast<const Cx<T>*>(epi.add) + row0 * L : nullptr;
-    for (int e = threadIdx.x; e < nvalid * L; e += blockDim.x) {
-        Cx<T> v = sm[(e / L) * LP + P(e % L)];
-        if (add) v = v + add[e];
-        dst[e] = v;
+    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        constexpr int NC = L + 1;
+        const int64_t row0 = (int64_t)tile * RB;
+        const int nv = nvalid(tile);
+        for (int e = threadIdx.x; e < nv * NC; e += NT) {
+            const int r = e / NC, k = e % NC;
+            cp_async_elem(sm + r * LP + P(k), spec + (row0 + r) * g.n1p + k);
+        }
     }
-}
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        const int nv = nvalid(tile);
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        Cx<T>* buf = sm + line * LP;
+        c2r_pre<T, L, TPL>(buf, t, twN);
+        fft_line<T, L, +1>(buf, t, twN, 2);
+        const int64_t row0 = (int64_t)tile * RB;
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out) + row0 * L;
+        const Cx<T>* add = epi.add ? reinterpret_cast<const Cx<T>*>(epi.add) + row0 * L : nullptr;
+        for (int e = threadIdx.x; e < nv * L; e += NT) {
+            Cx<T> v = sm[(e / L) * LP + P(e % L)];
+            if (add) v = v + add[e];
+            dst[e] = v;
+        }
+    }
+};
 
 // ---------------------------------------------------------------------------------------------
 // Column passes along x2 (AX = 2) or x3 (AX = 3) of a complex array with W complex columns per row
@@ -286,38 +402,43 @@ __device__ __forceinline__ int64_t col_addr(const ColGeom& c, int x, int other, 
     return ((int64_t)p * c.n2 + other) * c.W + x;               // other = i2, p = i3
 }
 
-// CTA shape of a column pass: XC columns x OL transverse lines, TPL threads per line.  OL is chosen for
-// ~256 threads but capped so that NC components of ES-byte complex values fit in ~72 KB of smem.
-template <int L, int XC, int NC = 1, int ES = 16>
+// CTA shape of a column pass: XC columns (one 128-byte segment: 16 complex64 / 8 complex128) x OL
+// transverse lines, TPL threads per line, ~256 threads, capped so NC components of the CTA's lines
+// fit in ~96 KB of shared memory.
+template <int L, typename T, int NC = 1>
 struct ColCfg {
-    static constexpr int TPL = LineGeom<L>::TPL;
-    static constexpr int NTT = ES == 16 ? 128 : 256;  // fp64 compute: fewer threads, more CTAs per SM
-    static constexpr int OLT = (XC * TPL >= NTT) ? 1 : NTT / (XC * TPL);
-    static constexpr int MAXL = (72 * 1024) / (NC * LineGeom<L>::LP * ES);
+    static constexpr int ES = (int)sizeof(Cx<T>);
+    static constexpr int TPL = Tpl<L, T>::V;
+    static constexpr int LPB = LineGeom<L>::LP * ES;  // bytes per line
+    static constexpr int XC0 = 128 / ES;
+    static constexpr int XC = (NC * XC0 * LPB <= 96 * 1024) ? XC0 : (NC * (XC0 / 2) * LPB <= 96 * 1024) ? XC0 / 2 : XC0 / 4;
+    static constexpr int OLT = (XC * TPL >= CtaThreads<T>::V) ? 1 : CtaThreads<T>::V / (XC * TPL);
+    static constexpr int MAXL = (96 * 1024) / (NC * LPB);
     static constexpr int OLS = (MAXL / XC) >= 1 ? MAXL / XC : 1;
     static constexpr int OL = OLT < OLS ? OLT : OLS;
     static constexpr int NT = XC * OL * TPL;
     static constexpr int LINES = XC * OL;
+    static constexpr size_t SMEM = (size_t)NC * LINES * LineGeom<L>::LP * ES;
 };
 
-template <typename T, int L, int XC, int OL, int AX>
+template <typename T, int L, int XC, int OL, int AX, int NT>
 __device__ __forceinline__ void col_load(Cx<T>* sm, const Cx<T>* __restrict__ src, const ColGeom& c, int x0, int o0,
                                          int nother) {
     constexpr int LP = LineGeom<L>::LP;
-    for (int e = threadIdx.x; e < XC * L * OL; e += blockDim.x) {
+    for (int e = threadIdx.x; e < XC * L * OL; e += NT) {
         const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
         const int x = x0 + xi, o = o0 + oi;
-        Cx<T> v = cx(T(0), T(0));
-        if (x < c.nx && o < nother) v = src[col_addr<AX>(c, x, o, p)];
-        sm[(oi * XC + xi) * LP + P(p)] = v;
+        Cx<T>* d = sm + (oi * XC + xi) * LP + P(p);
+        if (x < c.nx && o < nother) cp_async_elem(d, src + col_addr<AX>(c, x, o, p));
+        else *d = cx(T(0), T(0));
     }
 }
 
-template <typename T, int L, int XC, int OL, int AX, bool ACC, typename To = T>
+template <typename T, int L, int XC, int OL, int AX, bool ACC, int NT, typename To = T>
 __device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<To>* __restrict__ dst, const ColGeom& c, int x0, int o0,
                                           int nother) {
     constexpr int LP = LineGeom<L>::LP;
-    for (int e = threadIdx.x; e < XC * L * OL; e += blockDim.x) {
+    for (int e = threadIdx.x; e < XC * L * OL; e += NT) {
         const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
         const int x = x0 + xi, o = o0 + oi;
         if (x < c.nx && o < nother) {
@@ -331,50 +452,77 @@ __device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<To>* __restrict__ 
 }
 
 // Derivative along x2 / x3 of a real field (viewed as complex pairs): out (+)= d f / dx_AX.
-template <typename T, int L, int XC, int AX>
-__global__ void __launch_bounds__(ColCfg<L, XC, 1, sizeof(Cx<T>)>::NT) k_col_deriv(ColGeom c, const Cx<T>* __restrict__ src,
-                                                                 Cx<T>* __restrict__ dst, int accumulate,
-                                                                 const Cx<T>* __restrict__ tw) {
-    constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int OL = ColCfg<L, XC, 1, sizeof(Cx<T>)>::OL;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
-    const int nxb = (c.nx + XC - 1) / XC;
-    const int x0 = (blockIdx.x % nxb) * XC;
-    const int o0 = (blockIdx.x / nxb) * OL;
-    const int nother = (AX == 2) ? c.n3 : c.n2;
-    col_load<T, L, XC, OL, AX>(sm, src, c, x0, o0, nother);
-    __syncthreads();
-    const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    Cx<T>* buf = sm + line * LP;
-    fft_line<T, L, -1>(buf, t, tw, 1);
-    for (int k = t; k < L; k += TPL) {
-        const T kp = (T)wavenum_odd(k, L);
-        buf[P(k)] = mul_i(buf[P(k)], kp / T(L));
+template <typename T, int L, int AX>
+struct ColDerivPass {
+    using CC = ColCfg<L, T>;
+    static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
+    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr size_t BUF = CC::SMEM;
+    ColGeom c;
+    const Cx<T>* src;
+    Cx<T>* dst;
+    int accumulate;
+    const Cx<T>* tw;
+    __device__ __forceinline__ int nother() const { return (AX == 2) ? c.n3 : c.n2; }
+    __device__ __forceinline__ int ntiles() const { return ((c.nx + XC - 1) / XC) * ((nother() + OL - 1) / OL); }
+    __device__ __forceinline__ void origin(int tile, int& x0, int& o0) const {
+        const int nxb = (c.nx + XC - 1) / XC;
+        x0 = (tile % nxb) * XC;
+        o0 = (tile / nxb) * OL;
     }
-    __syncthreads();
-    fft_line<T, L, +1>(buf, t, tw, 1);
-    if (accumulate) col_store<T, L, XC, OL, AX, true>(sm, dst, c, x0, o0, nother);
-    else col_store<T, L, XC, OL, AX, false>(sm, dst, c, x0, o0, nother);
-}
+    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
+        int x0, o0;
+        origin(tile, x0, o0);
+        col_load<T, L, XC, OL, AX, NT>(reinterpret_cast<Cx<T>*>(smem), src, c, x0, o0, nother());
+    }
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        int x0, o0;
+        origin(tile, x0, o0);
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        Cx<T>* buf = sm + line * LP;
+        fft_line<T, L, -1>(buf, t, tw, 1);
+        for (int k = t; k < L; k += TPL) {
+            const T kp = (T)wavenum_odd(k, L);
+            buf[P(k)] = mul_i(buf[P(k)], kp / T(L));
+        }
+        __syncthreads();
+        fft_line<T, L, +1>(buf, t, tw, 1);
+        if (accumulate) col_store<T, L, XC, OL, AX, true, NT>(sm, dst, c, x0, o0, nother());
+        else col_store<T, L, XC, OL, AX, false, NT>(sm, dst, c, x0, o0, nother());
+    }
+};
 
 // Plain complex FFT of spectrum columns along x2 (forward DIR=-1 or inverse DIR=+1), in place.
-template <typename T, int L, int XC, int DIR>
-__global__ void __launch_bounds__(ColCfg<L, XC, 1, sizeof(Cx<T>)>::NT) k_col_fft(ColGeom c, Cx<T>* __restrict__ spec,
-                                                               const Cx<T>* __restrict__ tw) {
-    constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int OL = ColCfg<L, XC, 1, sizeof(Cx<T>)>::OL;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
-    const int nxb = (c.nx + XC - 1) / XC;
-    const int x0 = (blockIdx.x % nxb) * XC;
-    const int o0 = (blockIdx.x / nxb) * OL;
-    col_load<T, L, XC, OL, 2>(sm, spec, c, x0, o0, c.n3);
-    __syncthreads();
-    const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    fft_line<T, L, DIR>(sm + line * LP, t, tw, 1);
-    col_store<T, L, XC, OL, 2, false>(sm, spec, c, x0, o0, c.n3);
-}
+template <typename T, int L, int DIR>
+struct ColFftPass {
+    using CC = ColCfg<L, T>;
+    static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
+    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr size_t BUF = CC::SMEM;
+    ColGeom c;
+    Cx<T>* spec;
+    const Cx<T>* tw;
+    __device__ __forceinline__ int ntiles() const { return ((c.nx + XC - 1) / XC) * ((c.n3 + OL - 1) / OL); }
+    __device__ __forceinline__ void origin(int tile, int& x0, int& o0) const {
+        const int nxb = (c.nx + XC - 1) / XC;
+        x0 = (tile % nxb) * XC;
+        o0 = (tile / nxb) * OL;
+    }
+    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
+        int x0, o0;
+        origin(tile, x0, o0);
+        col_load<T, L, XC, OL, 2, NT>(reinterpret_cast<Cx<T>*>(smem), spec, c, x0, o0, c.n3);
+    }
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        int x0, o0;
+        origin(tile, x0, o0);
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        fft_line<T, L, DIR>(sm + line * LP, t, tw, 1);
+        col_store<T, L, XC, OL, 2, false, NT>(sm, spec, c, x0, o0, c.n3);
+    }
+};
 
 // ---------------------------------------------------------------------------------------------
 // Spectral symbols applied in the x3 middle pass.  k = (k1, k2, k3) signed wavenumbers,
@@ -439,51 +587,70 @@ struct SpecPtrs {
     Cx<T>* p[NC];
 };
 
-// x3 middle pass: forward FFT of NCI spectra along x3, symbol, inverse FFT of NCO spectra, all in Ti;
-// results are stored in To (the inverse passes after the symbol may run in the I/O precision: their
-// rounding is relative to the already-amplified signal).
-template <typename Ti, typename To, int L, int XC, int KIND>
-__global__ void __launch_bounds__(ColCfg<L, XC, Sym<Ti, KIND>::NCI, sizeof(Cx<Ti>)>::NT) k_col_middle(ColGeom c, SpecPtrs<Ti, Sym<Ti, KIND>::NCI> in,
-                                                                  SpecPtrs<To, Sym<Ti, KIND>::NCO> out, SymInfo s,
-                                                                  const Cx<Ti>* __restrict__ tw) {
+// x3 middle pass: forward FFT of NCI spectra along x3 in Ti, symbol in Ti, then the NCO results are
+// narrowed to To in a second shared-memory region and transformed back in To (the inverse passes after
+// the symbol may run in the I/O precision: their rounding is relative to the already-amplified signal).
+template <typename Ti, typename To, int L, int KIND>
+struct MiddlePass {
     using T = Ti;
-    constexpr int TPL = LineGeom<L>::TPL, LP = LineGeom<L>::LP;
-    constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
-    using CC = ColCfg<L, XC, NCI, sizeof(Cx<T>)>;
-    constexpr int OL = CC::OL, LINES = CC::LINES;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem_raw);
-    const int nxb = (c.nx + XC - 1) / XC;
-    const int x0 = (blockIdx.x % nxb) * XC;
-    const int o0 = (blockIdx.x / nxb) * OL;
-#pragma unroll
-    for (int ci = 0; ci < NCI; ++ci) col_load<T, L, XC, OL, 3>(sm + ci * LINES * LP, in.p[ci], c, x0, o0, c.n2);
-    __syncthreads();
-    const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-#pragma unroll
-    for (int ci = 0; ci < NCI; ++ci) fft_line<T, L, -1>(sm + ci * LINES * LP + line * LP, t, tw, 1);
-    // symbol: element (line, p): k1 = column index x (0..N1/2), k2 from the transverse index, k3 from p
-    const int n1 = 2 * (c.nx - 1);
-    for (int e = threadIdx.x; e < LINES * L; e += blockDim.x) {
-        const int ln = e / L, p = e % L;
-        const int xi = ln % XC, oi = ln / XC;
-        const int x = x0 + xi, o = o0 + oi;
-        if (x >= c.nx || o >= c.n2) continue;
-        Cx<T> v[NCI];
-#pragma unroll
-        for (int ci = 0; ci < NCI; ++ci) v[ci] = sm[ci * LINES * LP + ln * LP + P(p)];
-        const int k1 = x, k2 = wavenum(o, c.n2), k3 = wavenum(p, L);
-        const int kp1 = (x == n1 / 2) ? 0 : x, kp2 = wavenum_odd(o, c.n2), kp3 = wavenum_odd(p, L);
-        Sym<T, KIND>::apply(s, v, k1, k2, k3, kp1, kp2, kp3);
-#pragma unroll
-        for (int co = 0; co < NCO; ++co) sm[co * LINES * LP + ln * LP + P(p)] = v[co];
+    static constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
+    using CC = ColCfg<L, T, NCI>;
+    static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
+    static_assert(Tpl<L, To>::V == TPL, "inverse lines use the same threads");
+    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr size_t BUFI = CC::SMEM;
+    static constexpr size_t BUF = BUFI + (size_t)NCO * LINES * LP * sizeof(Cx<To>);
+    ColGeom c;
+    SpecPtrs<Ti, NCI> in;
+    SpecPtrs<To, NCO> out;
+    SymInfo s;
+    const Cx<Ti>* tw;
+    const Cx<To>* two;  // inverse twiddles in To
+    __device__ __forceinline__ int ntiles() const { return ((c.nx + XC - 1) / XC) * ((c.n2 + OL - 1) / OL); }
+    __device__ __forceinline__ void origin(int tile, int& x0, int& o0) const {
+        const int nxb = (c.nx + XC - 1) / XC;
+        x0 = (tile % nxb) * XC;
+        o0 = (tile / nxb) * OL;
     }
-    __syncthreads();
+    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        int x0, o0;
+        origin(tile, x0, o0);
 #pragma unroll
-    for (int co = 0; co < NCO; ++co) fft_line<T, L, +1>(sm + co * LINES * LP + line * LP, t, tw, 1);
+        for (int ci = 0; ci < NCI; ++ci) col_load<T, L, XC, OL, 3, NT>(sm + ci * LINES * LP, in.p[ci], c, x0, o0, c.n2);
+    }
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        Cx<To>* so = reinterpret_cast<Cx<To>*>(smem + BUFI);
+        int x0, o0;
+        origin(tile, x0, o0);
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
 #pragma unroll
-    for (int co = 0; co < NCO; ++co)
-        col_store<T, L, XC, OL, 3, false, To>(sm + co * LINES * LP, out.p[co], c, x0, o0, c.n2);
-}
+        for (int ci = 0; ci < NCI; ++ci) fft_line<T, L, -1>(sm + ci * LINES * LP + line * LP, t, tw, 1);
+        // symbol: element (line, p): k1 = column index x (0..N1/2), k2 from the transverse index, k3 from p
+        const int n1 = 2 * (c.nx - 1);
+        for (int e = threadIdx.x; e < LINES * L; e += NT) {
+            const int ln = e / L, p = e % L;
+            const int xi = ln % XC, oi = ln / XC;
+            const int x = x0 + xi, o = o0 + oi;
+            Cx<T> v[NCI];
+#pragma unroll
+            for (int ci = 0; ci < NCI; ++ci) v[ci] = sm[ci * LINES * LP + ln * LP + P(p)];
+            if (x < c.nx && o < c.n2) {
+                const int k1 = x, k2 = wavenum(o, c.n2), k3 = wavenum(p, L);
+                const int kp1 = (x == n1 / 2) ? 0 : x, kp2 = wavenum_odd(o, c.n2), kp3 = wavenum_odd(p, L);
+                Sym<T, KIND>::apply(s, v, k1, k2, k3, kp1, kp2, kp3);
+            }
+#pragma unroll
+            for (int co = 0; co < NCO; ++co) so[co * LINES * LP + ln * LP + P(p)] = cx<To>((To)v[co].re, (To)v[co].im);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int co = 0; co < NCO; ++co) fft_line<To, L, +1>(so + co * LINES * LP + line * LP, t, two, 1);
+#pragma unroll
+        for (int co = 0; co < NCO; ++co)
+            col_store<To, L, XC, OL, 3, false, NT, To>(so + co * LINES * LP, out.p[co], c, x0, o0, c.n2);
+    }
+};
 
 }  // namespace dr

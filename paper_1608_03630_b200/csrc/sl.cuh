@@ -16,7 +16,7 @@
 
 namespace dr {
 
-constexpr int SL_TX = 32, SL_TY = 8, SL_TZ = 4, SL_THREADS = SL_TX * SL_TY;
+constexpr int SL_TX = 32, SL_TY = 8, SL_TZ = 8, SL_THREADS = SL_TX * SL_TY;
 constexpr int PLAN_INTS = 8;  // ox, oy, oz, ex, ey, ez, pad, pad
 
 // Lagrange weights for nodes -1, 0, 1, 2 at t in [0, 1) (reading A6)
@@ -153,41 +153,91 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restr
 }
 
 // ---------------------------------------------------------------------------------------------
-// Epilogues of the fused gather kernel.  `load(id)` fetches (and pre-reduces) the voxel's pointwise
-// operands before the box wait, so their latency overlaps the shared-memory staging; `store(id, val,
-// pre)` finishes the step with the NC interpolated components `val` at the departure point.
+// Epilogues of the fused gather kernel.  `late(id)` issues the voxel's pointwise operand loads just
+// before its interpolation (they fly while the 64 stencil reads run); `store(id, val, late)` finishes
+// the step with the NC interpolated components `val` at the departure point.  Indices are 32-bit
+// (M <= 2^30); vector fields are passed as one pointer per component.
+struct NoLate {};
+struct NoPre {};
+
 template <typename T>
 struct EpiStore {  // state solve: rho_{j+1} = I[rho_j](X+)   (Eq. 7 with f = 0)
     T* out;
-    struct Pre {};
-    __device__ __forceinline__ Pre load(int64_t) const { return Pre{}; }
-    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre&) const { out[id] = val[0]; }
+    using Pre = NoPre;
+    using Late = NoLate;
+    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
+    __device__ __forceinline__ Late late(uint32_t) const { return Late{}; }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late&) const { out[id] = val[0]; }
 };
 
-template <typename T>
-struct EpiAdjoint {  // adjoint-like step: nu_{k-1} = scale * m * I[nu_k](X-)  (Eq. 7, f = nu div v; D7)
-    T* out;
-    const T* m;  // nullable (isochoric: m == 1)
+// Adjoint-like step: nu_{k-1} = scale * m * I[nu_k](X-)  (Eq. 7 with f = nu div v; D7).
+// QUAD != 0 also accumulates the trapezoid quadrature b~ = dt sum_j w_j lambda~_j G_j (P:L196-198,
+// reading A12) step by step, so the streaming sum rides on the gather's shared-memory-bound time:
+// QUAD = 1 (first step, k = nt): b~ = w_nt nu_nt G_nt + w_{nt-1} nu_{nt-1} G_{nt-1}, nu_nt read at x;
+// QUAD = 2 (k < nt): b~ += w_{k-1} nu_{k-1} G_{k-1}.
+template <typename T, int QUAD = 0>
+struct EpiAdjoint {
+    T* out;        // nu_{k-1}
+    const T* m;    // nullable (isochoric: m == 1)
     T scale;
-    struct Pre { T m; };
-    __device__ __forceinline__ Pre load(int64_t id) const { return Pre{m ? scale * __ldg(m + id) : scale}; }
-    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const { out[id] = p.m * val[0]; }
+    // quadrature operands (QUAD != 0)
+    T* b0; T* b1; T* b2;                     // b~ components (read-modify-write when QUAD == 2)
+    const T* G0; const T* G1; const T* G2;   // G_{k-1}
+    T w;                                     // dt w_{k-1}
+    const T* nu; T snu;                      // QUAD == 1: nu_nt = snu * nu[x]
+    const T* H0; const T* H1; const T* H2;   // QUAD == 1: G_nt
+    T wn;                                    // QUAD == 1: dt w_nt
+    using Pre = NoPre;
+    struct Late { T m; T g[3]; T b[3]; };
+    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
+    __device__ __forceinline__ Late late(uint32_t id) const {
+        Late l;
+        l.m = m ? scale * __ldg(m + id) : scale;
+        if constexpr (QUAD != 0) {
+            l.g[0] = __ldg(G0 + id);
+            l.g[1] = __ldg(G1 + id);
+            l.g[2] = __ldg(G2 + id);
+            if constexpr (QUAD == 2) {
+                l.b[0] = b0[id];
+                l.b[1] = b1[id];
+                l.b[2] = b2[id];
+            } else {
+                const T ln = wn * snu * __ldg(nu + id);
+                l.b[0] = ln * __ldg(H0 + id);
+                l.b[1] = ln * __ldg(H1 + id);
+                l.b[2] = ln * __ldg(H2 + id);
+            }
+        }
+        return l;
+    }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
+        const T r = l.m * val[0];
+        out[id] = r;
+        if constexpr (QUAD != 0) {
+            const T wr = w * r;
+            b0[id] = l.b[0] + wr * l.g[0];
+            b1[id] = l.b[1] + wr * l.g[1];
+            b2[id] = l.b[2] + wr * l.g[2];
+        }
+    }
 };
 
 template <typename T>
 struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+) + c f_{j+1}, f = -vt.G_{j+1}
     T* out;
-    const T* vt;  // vector field
-    const T* G;   // vector field grad rho_{j+1}
+    const T* vt0; const T* vt1; const T* vt2;  // vt components
+    const T* G0; const T* G1; const T* G2;     // grad rho_{j+1} components
     T c;
-    int64_t M;
-    struct Pre { T cf; };
-    __device__ __forceinline__ Pre load(int64_t id) const {
-        const T f = -(__ldg(vt + id) * __ldg(G + id) + __ldg(vt + M + id) * __ldg(G + M + id) +
-                      __ldg(vt + 2 * M + id) * __ldg(G + 2 * M + id));
-        return Pre{c * f};
+    using Pre = NoPre;
+    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
+    struct Late { T v[3], g[3]; };
+    __device__ __forceinline__ Late late(uint32_t id) const {
+        return Late{{__ldg(vt0 + id), __ldg(vt1 + id), __ldg(vt2 + id)}, {__ldg(G0 + id), __ldg(G1 + id), __ldg(G2 + id)}};
     }
-    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const { out[id] = val[0] + p.cf; }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
+        const T f = l.v[0] * l.g[0] + l.v[1] * l.g[1] + l.v[2] * l.g[2];
+        out[id] = val[0] - c * f;
+    }
 };
 
 template <typename T>
@@ -195,33 +245,39 @@ struct EpiMultiplier {  // m = 1 + dt/2 (Dbar + D + dt Dbar D), Dbar = I[div v](
     T* m;
     const T* D;
     T dt;
-    struct Pre { T D; };
-    __device__ __forceinline__ Pre load(int64_t id) const { return Pre{__ldg(D + id)}; }
-    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const {
+    using Pre = NoPre;
+    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
+    struct Late { T D; };
+    __device__ __forceinline__ Late late(uint32_t id) const { return Late{__ldg(D + id)}; }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
         const T Db = val[0];
-        m[id] = T(1) + T(0.5) * dt * (Db + p.D + dt * Db * p.D);
+        m[id] = T(1) + T(0.5) * dt * (Db + l.D + dt * Db * l.D);
     }
 };
 
 template <typename T>
 struct EpiDeparture {  // d = sigma dt/2 (v(x) + I[v](X*)) / h  (Eq. 6, cell units)
-    T* d;
-    const T* v;
+    T* d0; T* d1; T* d2;
+    const T* v0; const T* v1; const T* v2;
     T c[3];  // sigma * dt / (2 h_a)
-    int64_t M;
-    struct Pre { T v[3]; };
-    __device__ __forceinline__ Pre load(int64_t id) const {
-        return Pre{{__ldg(v + id), __ldg(v + M + id), __ldg(v + 2 * M + id)}};
-    }
-    __device__ __forceinline__ void store(int64_t id, const T* val, const Pre& p) const {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) d[a * M + id] = c[a] * (p.v[a] + val[a]);
+    using Pre = NoPre;
+    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
+    struct Late { T v[3]; };
+    __device__ __forceinline__ Late late(uint32_t id) const { return Late{{__ldg(v0 + id), __ldg(v1 + id), __ldg(v2 + id)}}; }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
+        d0[id] = c[0] * (l.v[0] + val[0]);
+        d1[id] = c[1] * (l.v[1] + val[1]);
+        d2[id] = c[2] * (l.v[2] + val[2]);
     }
 };
 
 template <typename T, int NC>
 struct Src {
     const T* p[NC];
+};
+template <typename T>
+struct Disp {  // displacement field components (cell units)
+    const T* p[3];
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -231,18 +287,22 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // Shared-memory box geometry per (value type, components): compile-time strides so every one of the
-// 64 stencil loads is an LDS with an immediate offset from one per-point base address.  BX is a
-// multiple of 32 words so that lanes of a warp whose departure rows differ stay on distinct banks.
+// 64 stencil loads is an LDS with an immediate offset from one per-point base address.  The row and
+// plane strides are multiples of 32 words: the 32 lanes of a warp read consecutive columns, so when
+// their departure rows or planes differ (the displacement crosses a cell boundary along x) they still
+// hit 32 distinct banks.  BX holds a 32-wide tile's x-extent (32 + 3 + deformation spread + 16-B
+// alignment), BY/BZ an 8-deep tile's.
 template <typename T, int NC>
 struct BoxGeom;
-template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 16, BZ = 12; };   //  48 KB
-template <> struct BoxGeom<float, 3> { static constexpr int BX = 64, BY = 16, BZ = 16; };   // 192 KB
-template <> struct BoxGeom<double, 1> { static constexpr int BX = 64, BY = 16, BZ = 16; };  // 128 KB
-template <> struct BoxGeom<double, 3> { static constexpr int BX = 32, BY = 12, BZ = 12; };  // 108 KB
+// STAGES = 2: double-buffered boxes (next tile staged during the current one); MINB CTAs per SM.
+template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 3, STAGES = 1; };   // 58 KB
+template <> struct BoxGeom<float, 3> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1, STAGES = 1; };   // 173 KB
+template <> struct BoxGeom<double, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1, STAGES = 1; };  // 115 KB
+template <> struct BoxGeom<double, 3> { static constexpr int BX = 48, BY = 14, BZ = 14, MINB = 1, STAGES = 1; };  // 221 KB
 
 template <typename T, int NC>
 constexpr size_t box_bytes() {
-    return (size_t)NC * BoxGeom<T, NC>::BX * BoxGeom<T, NC>::BY * BoxGeom<T, NC>::BZ * sizeof(T);
+    return (size_t)BoxGeom<T, NC>::STAGES * NC * BoxGeom<T, NC>::BX * BoxGeom<T, NC>::BY * BoxGeom<T, NC>::BZ * sizeof(T);
 }
 
 template <typename T, int BX, int BY>
@@ -262,110 +322,257 @@ __device__ __forceinline__ T interp_box(const T* __restrict__ b, const T w1[4], 
     return acc;
 }
 
-// Fused gather + epilogue.  Grid: one CTA per tile.  Dynamic smem: box_bytes<T, NC>().
-// Phases: (A) stage the tile's box with 16-byte cp.async (periodic wrap per chunk; x origin aligned
-// down to VEC = 16 B / sizeof(T), which never straddles the wrap since N1 is a multiple of VEC);
-// (B) meanwhile load the displacements and the epilogue operands of the thread's 8 points; (C) wait
-// + barrier; (D) gather the 64 stencil values per point from shared memory and finish the step.
-// Tiles whose box exceeds the compile-time capacity gather from global memory instead.
-template <typename T, int NC, class Epi>
-__global__ void __launch_bounds__(SL_THREADS, (sizeof(T) == 4 && NC == 1) ? 4 : 1) k_sl_gather(Grid g, Src<T, NC> src, const T* __restrict__ d,
-                                                          const int* __restrict__ plan, Epi epi) {
+// Two points at once with packed fp32x2 arithmetic (sm_100 FFMA2): lane .x = point A, .y = point B.
+__device__ __forceinline__ void lagrange4x2(float2 t, float2 w[4]) {
+    const float2 a = __fmul2_rn(t, __fadd2_rn(t, make_float2(-1.f, -1.f)));   // t (t - 1)
+    const float2 b = __fadd2_rn(a, make_float2(-2.f, -2.f));                    // (t + 1)(t - 2)
+    const float s = 1.f / 6.f;
+    w[0] = __fmul2_rn(a, __ffma2_rn(t, make_float2(-s, -s), make_float2(2.f * s, 2.f * s)));
+    w[1] = __fmul2_rn(b, __ffma2_rn(t, make_float2(0.5f, 0.5f), make_float2(-0.5f, -0.5f)));
+    w[2] = __fmul2_rn(b, __fmul2_rn(t, make_float2(-0.5f, -0.5f)));
+    w[3] = __fmul2_rn(a, __ffma2_rn(t, make_float2(s, s), make_float2(s, s)));
+}
+
+template <int BX, int BY>
+__device__ __forceinline__ float2 interp_box2(const float* __restrict__ bA, const float* __restrict__ bB,
+                                              const float2 w1[4], const float2 w2[4], const float2 w3[4]) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        float2 accb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            const float* rA = bA + (c * BY + bb) * BX;
+            const float* rB = bB + (c * BY + bb) * BX;
+            float2 row = __fmul2_rn(w1[0], make_float2(rA[0], rB[0]));
+            row = __ffma2_rn(w1[1], make_float2(rA[1], rB[1]), row);
+            row = __ffma2_rn(w1[2], make_float2(rA[2], rB[2]), row);
+            row = __ffma2_rn(w1[3], make_float2(rA[3], rB[3]), row);
+            accb = (bb == 0) ? __fmul2_rn(w2[0], row) : __ffma2_rn(w2[bb], row, accb);
+        }
+        acc = (c == 0) ? __fmul2_rn(w3[0], accb) : __ffma2_rn(w3[c], accb, acc);
+    }
+    return acc;
+}
+
+// Fused gather + epilogue, persistent.  Grid: a few CTAs per SM; each CTA walks tiles
+// t = blockIdx.x, blockIdx.x + gridDim.x, ... (32 x 8 x 8 voxels; thread = (x, y) column of 8 points).
+// Dynamic smem: STAGES boxes of box_bytes<T, NC>().  With STAGES = 2 the next tile's box is staged
+// (16-byte cp.async, periodic wrap per chunk; x origin aligned down to VEC = 16 B / sizeof(T), which
+// never straddles the wrap since N1 is a multiple of VEC) and its displacements are loaded into
+// registers while the current tile is interpolated, so HBM/L2 latency hides behind the
+// shared-memory-bound gather.  Per point: 64 stencil values from shared memory, points k and k + 4
+// as one packed fp32x2 pair (FFMA2); the epilogue operands are issued before the pair's
+// interpolation and consumed after it.  Tiles whose box exceeds the compile-time capacity gather
+// from global memory instead (same arithmetic, one point at a time).
+template <typename T, int NC>
+struct TileCtx {
+    int x0, y0, z0, ox, oy, oz, ex, ey, ez;
+    bool fits;
+};
+
+template <typename T, int NC>
+__device__ __forceinline__ TileCtx<T, NC> tile_ctx(const Grid& g, const int* __restrict__ plan, int tile) {
+    constexpr int VEC = 16 / (int)sizeof(T);
+    constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
+    TileCtx<T, NC> c;
+    tile_coords(g, tile, c.x0, c.y0, c.z0);
+    const int4 p = __ldg(reinterpret_cast<const int4*>(plan + (size_t)tile * PLAN_INTS));
+    const int4 q = __ldg(reinterpret_cast<const int4*>(plan + (size_t)tile * PLAN_INTS + 4));
+    c.ox = p.x & ~(VEC - 1);
+    c.oy = p.y;
+    c.oz = p.z;
+    c.ex = ((p.x + p.w - c.ox) + VEC - 1) & ~(VEC - 1);
+    c.ey = q.x;
+    c.ez = q.y;
+    c.fits = c.ex <= BX && c.ey <= BY && c.ez <= BZ;
+    return c;
+}
+
+template <typename T, int NC>
+__device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, const TileCtx<T, NC>& c, T* box) {
     constexpr int VEC = 16 / (int)sizeof(T);
     constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
     constexpr int SC = BX * BY * BZ;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* box = reinterpret_cast<T*>(smem_raw);
-    int x0, y0, z0;
-    tile_coords(g, blockIdx.x, x0, y0, z0);
-    const int* pl = plan + (int64_t)blockIdx.x * PLAN_INTS;
-    const int ox = pl[0] & ~(VEC - 1), oy = pl[1], oz = pl[2];
-    const int ex = ((pl[0] + pl[3] - ox) + VEC - 1) & ~(VEC - 1), ey = pl[4], ez = pl[5];
-    const bool fits = ex <= BX && ey <= BY && ez <= BZ;
-    const int lane = threadIdx.x % SL_TX, wy = threadIdx.x / SL_TX;
-    const int x = x0 + lane, y = y0 + wy;
-    const bool xyok = x < g.n1 && y < g.n2;
-
-    // (A) asynchronous staging of the box: thread -> fixed 16-byte chunk column, rows strided by
-    // SL_THREADS / NCHP (no divisions in the loop)
-    if (fits) {
-        constexpr int NCHP = BX / VEC;              // chunk columns of a full-width row (power of two)
-        constexpr int RSTEP = SL_THREADS / NCHP;
-        const int nch = ex / VEC;
-        const int ch = threadIdx.x % NCHP;
-        if (ch < nch) {
-            int yy = threadIdx.x / NCHP, zz = 0;
-            while (yy >= ey) { yy -= ey; ++zz; }
-            while (zz < ez) {
-                const int gy = wrapi(oy + yy, g.n2), gz = wrapi(oz + zz, g.n3);
-                const int64_t gofs = ((int64_t)gz * g.n2 + gy) * g.n1 + wrapi(ox + ch * VEC, g.n1);
-                T* dst = box + (zz * BY + yy) * BX + ch * VEC;
+    constexpr int NCHP = BX / VEC;
+    constexpr int RSTEP = SL_THREADS / NCHP;
+    if (!c.fits) return;
+    const int nch = c.ex / VEC;
+    const int ch = threadIdx.x % NCHP;
+    const int r0 = threadIdx.x / NCHP;
+    if (ch >= nch || r0 >= RSTEP) return;
+    int yy = r0, zz = 0;
+    while (yy >= c.ey) { yy -= c.ey; ++zz; }
+    const int gx = wrapi(c.ox + ch * VEC, g.n1);
+    while (zz < c.ez) {
+        const int gy = wrapi(c.oy + yy, g.n2), gz = wrapi(c.oz + zz, g.n3);
+        const uint32_t gofs = ((uint32_t)gz * g.n2 + gy) * g.n1 + gx;
+        T* dst = box + (zz * BY + yy) * BX + ch * VEC;
 #pragma unroll
-                for (int c = 0; c < NC; ++c) cp_async16(dst + c * SC, src.p[c] + gofs);
-                yy += RSTEP;
-                while (yy >= ey) { yy -= ey; ++zz; }
-            }
-        }
+        for (int cc = 0; cc < NC; ++cc) cp_async16(dst + cc * SC, src.p[cc] + gofs);
+        yy += RSTEP;
+        while (yy >= c.ey) { yy -= c.ey; ++zz; }
     }
+}
 
-    // (B) displacements and epilogue operands of this thread's points
-    T dd[SL_TZ][3];
-    typename Epi::Pre pre[SL_TZ];
+template <typename T, class Epi>
+__device__ __forceinline__ void load_disp(const Grid& g, const Disp<T>& d, int x0, int y0, int z0, T (&dd)[SL_TZ][3],
+                                          typename Epi::Pre (&pre)[SL_TZ], const Epi& epi) {
+    const int x = x0 + (threadIdx.x % SL_TX), y = y0 + threadIdx.x / SL_TX;
+    const bool xyok = x < g.n1 && y < g.n2;
+    const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
+    const uint32_t id0 = ((uint32_t)z0 * g.n2 + y) * g.n1 + x;
 #pragma unroll
     for (int k = 0; k < SL_TZ; ++k) {
-        const int z = z0 + k;
-        const int64_t id = ((int64_t)z * g.n2 + y) * g.n1 + x;
-        const bool ok = xyok && z < g.n3;
+        const bool ok = xyok && z0 + k < g.n3;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) dd[k][a] = ok ? __ldg(d + a * g.M + id) : T(0);
-        if (ok) pre[k] = epi.load(id);
+        for (int a = 0; a < 3; ++a) dd[k][a] = ok ? __ldg(d.p[a] + id0 + k * plane) : T(0);
+        if (ok) pre[k] = epi.early(id0 + k * plane);
     }
+}
 
-    // (C)
-    if (fits) cp_async_wait_all();
-    __syncthreads();
-    if (!xyok) return;
-    const int kmax = min(SL_TZ, g.n3 - z0);
-
-    // (D)
-    if (fits) {
+template <typename T, int NC, class Epi>
+__device__ __forceinline__ void compute_tile(const Grid& g, const Src<T, NC>& src, const Disp<T>& d,
+                                             const TileCtx<T, NC>& c, const T* __restrict__ box,
+                                             const T (&dd)[SL_TZ][3], const typename Epi::Pre (&pre)[SL_TZ],
+                                             const Epi& epi) {
+    constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
+    constexpr int SC = BX * BY * BZ;
+    constexpr int H = SL_TZ / 2;
+    const int x = c.x0 + (threadIdx.x % SL_TX), y = c.y0 + threadIdx.x / SL_TX;
+    if (x >= g.n1 || y >= g.n2) return;
+    const int kmax = min(SL_TZ, g.n3 - c.z0);
+    const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
+    const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
+    if (c.fits) {
+        if constexpr (sizeof(T) == 4) {
 #pragma unroll
-        for (int k = 0; k < SL_TZ; ++k) {
-            if (k >= kmax) break;
-            const int z = z0 + k;
+            for (int p = 0; p < H; ++p) {
+                if (p >= kmax) break;
+                const bool okB = p + H < kmax;
+                const uint32_t idA = id0 + p * plane, idB = id0 + (p + H) * plane;
+                int qA[3], qB[3];
+                float tA[3], tB[3];
+                const int ii[3] = {x, y, c.z0 + p};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    cell_of<float>(ii[a], dd[p][a], qA[a], tA[a]);
+                    cell_of<float>(ii[a] + (a == 2 ? H : 0), dd[p + H][a], qB[a], tB[a]);
+                    if (!okB) { qB[a] = qA[a]; tB[a] = tA[a]; }
+                }
+                const typename Epi::Late lA = epi.late(idA);
+                typename Epi::Late lB;
+                if (okB) lB = epi.late(idB);
+                float2 w[3][4];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) lagrange4x2(make_float2(tA[a], tB[a]), w[a]);
+                const float* bA = box + ((qA[2] - 1 - c.oz) * BY + (qA[1] - 1 - c.oy)) * BX + (qA[0] - 1 - c.ox);
+                const float* bB = box + ((qB[2] - 1 - c.oz) * BY + (qB[1] - 1 - c.oy)) * BX + (qB[0] - 1 - c.ox);
+                float vA[NC], vB[NC];
+#pragma unroll
+                for (int cc = 0; cc < NC; ++cc) {
+                    const float2 r = interp_box2<BX, BY>(bA + cc * SC, bB + cc * SC, w[0], w[1], w[2]);
+                    vA[cc] = r.x;
+                    vB[cc] = r.y;
+                }
+                epi.store(idA, vA, pre[p], lA);
+                if (okB) epi.store(idB, vB, pre[p + H], lB);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < SL_TZ; ++k) {
+                if (k >= kmax) break;
+                const uint32_t id = id0 + k * plane;
+                const typename Epi::Late lt = epi.late(id);
+                int q1, q2, q3;
+                T t1, t2, t3;
+                cell_of<T>(x, dd[k][0], q1, t1);
+                cell_of<T>(y, dd[k][1], q2, t2);
+                cell_of<T>(c.z0 + k, dd[k][2], q3, t3);
+                T w1[4], w2[4], w3[4];
+                lagrange4(t1, w1);
+                lagrange4(t2, w2);
+                lagrange4(t3, w3);
+                const T* b = box + ((q3 - 1 - c.oz) * BY + (q2 - 1 - c.oy)) * BX + (q1 - 1 - c.ox);
+                T val[NC];
+#pragma unroll
+                for (int cc = 0; cc < NC; ++cc) val[cc] = interp_box<T, BX, BY>(b + cc * SC, w1, w2, w3);
+                epi.store(id, val, pre[k], lt);
+            }
+        }
+    } else {  // re-reads its operands so that the register arrays stay statically indexed
+#pragma unroll 1
+        for (int k = 0; k < kmax; ++k) {
+            const uint32_t id = id0 + k * plane;
+            const typename Epi::Late lt = epi.late(id);
             int q1, q2, q3;
             T t1, t2, t3;
-            cell_of<T>(x, dd[k][0], q1, t1);
-            cell_of<T>(y, dd[k][1], q2, t2);
-            cell_of<T>(z, dd[k][2], q3, t3);
+            cell_of<T>(x, __ldg(d.p[0] + id), q1, t1);
+            cell_of<T>(y, __ldg(d.p[1] + id), q2, t2);
+            cell_of<T>(c.z0 + k, __ldg(d.p[2] + id), q3, t3);
             T w1[4], w2[4], w3[4];
             lagrange4(t1, w1);
             lagrange4(t2, w2);
             lagrange4(t3, w3);
-            const T* b = box + ((q3 - 1 - oz) * BY + (q2 - 1 - oy)) * BX + (q1 - 1 - ox);
             T val[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) val[c] = interp_box<T, BX, BY>(b + c * SC, w1, w2, w3);
-            epi.store(((int64_t)z * g.n2 + y) * g.n1 + x, val, pre[k]);
+            for (int cc = 0; cc < NC; ++cc) val[cc] = interp_global(src.p[cc], g, q1, q2, q3, w1, w2, w3);
+            epi.store(id, val, epi.early(id), lt);
+        }
+    }
+}
+
+template <typename T, int NC, class Epi>
+__global__ void __launch_bounds__(SL_THREADS, BoxGeom<T, NC>::MINB)
+    k_sl_gather(Grid g, Src<T, NC> src, Disp<T> d, const int* __restrict__ plan, int ntiles, Epi epi) {
+    constexpr int STAGES = BoxGeom<T, NC>::STAGES;
+    constexpr int SB = BoxGeom<T, NC>::BX * BoxGeom<T, NC>::BY * BoxGeom<T, NC>::BZ * NC;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* boxes = reinterpret_cast<T*>(smem_raw);
+    int tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    T dd[SL_TZ][3];
+    typename Epi::Pre pre[SL_TZ];
+    TileCtx<T, NC> cur = tile_ctx<T, NC>(g, plan, tile);
+    if constexpr (STAGES == 2) {
+        stage_box<T, NC>(g, src, cur, boxes);
+        load_disp<T, Epi>(g, d, cur.x0, cur.y0, cur.z0, dd, pre, epi);
+        int buf = 0;
+        for (;;) {
+            const int next = tile + gridDim.x;
+            cp_async_wait_all();
+            __syncthreads();  // box[buf] complete; every thread is done with box[buf ^ 1]
+            T dn[SL_TZ][3];
+            typename Epi::Pre pn[SL_TZ];
+            TileCtx<T, NC> nc;
+            if (next < ntiles) {
+                nc = tile_ctx<T, NC>(g, plan, next);
+                stage_box<T, NC>(g, src, nc, boxes + (buf ^ 1) * SB);
+                load_disp<T, Epi>(g, d, nc.x0, nc.y0, nc.z0, dn, pn, epi);
+            }
+            compute_tile<T, NC, Epi>(g, src, d, cur, boxes + buf * SB, dd, pre, epi);
+            if (next >= ntiles) break;
+            tile = next;
+            cur = nc;
+            buf ^= 1;
+#pragma unroll
+            for (int k = 0; k < SL_TZ; ++k) {
+                pre[k] = pn[k];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) dd[k][a] = dn[k][a];
+            }
         }
     } else {
-#pragma unroll
-        for (int k = 0; k < SL_TZ; ++k) {
-            if (k >= kmax) break;
-            const int z = z0 + k;
-            int q1, q2, q3;
-            T t1, t2, t3;
-            cell_of<T>(x, dd[k][0], q1, t1);
-            cell_of<T>(y, dd[k][1], q2, t2);
-            cell_of<T>(z, dd[k][2], q3, t3);
-            T w1[4], w2[4], w3[4];
-            lagrange4(t1, w1);
-            lagrange4(t2, w2);
-            lagrange4(t3, w3);
-            T val[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) val[c] = interp_global(src.p[c], g, q1, q2, q3, w1, w2, w3);
-            epi.store(((int64_t)z * g.n2 + y) * g.n1 + x, val, pre[k]);
+        for (;;) {
+            stage_box<T, NC>(g, src, cur, boxes);
+            load_disp<T, Epi>(g, d, cur.x0, cur.y0, cur.z0, dd, pre, epi);
+            cp_async_wait_all();
+            __syncthreads();
+            compute_tile<T, NC, Epi>(g, src, d, cur, boxes, dd, pre, epi);
+            tile += gridDim.x;
+            if (tile >= ntiles) break;
+            __syncthreads();  // everyone is done with the box before it is restaged
+            cur = tile_ctx<T, NC>(g, plan, tile);
         }
     }
 }

@@ -20,7 +20,7 @@ if [ "${SKIPBENCH:-0}" != "1" ]; then
 fi
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 600 $CMD > gpurun_out/plain_${TAG}.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain_${TAG}.log; exit 1; }
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:dr:: -c 800 --csv \
   --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch_${TAG}.log 2>&1
 echo "ncu launch rc=$?"
 i=0
@@ -28,5 +28,12 @@ for K in "${KRES[@]}"; do
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:${K}" -s ${KSKIP:-4} -c 1 -o gpurun_out/prof_${TAG}_$i $CMD > gpurun_out/ncu_full_${TAG}_$i.log 2>&1
   echo "ncu full $K rc=$?"
+  R=gpurun_out/prof_${TAG}_$i.ncu-rep
+  if [ -f $R ]; then
+    ncu -i $R --page details --csv > gpurun_out/details_${TAG}_$i.csv 2>/dev/null
+    ncu -i $R --page raw --csv > gpurun_out/raw_${TAG}_$i.csv 2>/dev/null
+    python tools/ncu_summary.py $R > gpurun_out/summary_${TAG}_$i.txt 2>&1
+    [ "${KEEPREP:-0}" = "1" ] || rm -f $R
+  fi
   i=$((i+1))
 done
