@@ -91,6 +91,45 @@ dr_status dr_create(const dr_config* cfg, void* workspace, size_t workspace_byte
                     dr_ctx** out);
 dr_status dr_destroy(dr_ctx* ctx);
 
+/* ---------------------------------------------------------------------------------------------
+ * Slab decomposition over P GPUs (the B200 replacement of the paper's pencil
+ * decomposition, and of its ghost-layer interpolation, Algorithm 1).
+ * Rank r owns the x3 planes [r N3/P, (r+1) N3/P) of every field; all field arguments of a
+ * distributed context are that rank's slab: scalar [N3/P][N2][N1], vector [3][N3/P][N2][N1].
+ * Requirements: P | N3, P | N2, N3/P >= 5 (ghost planes (4, 5) cover x3 displacements of up to
+ * 3 cells; larger ones return DR_ERR_PLAN from dr_set_velocity -- the off-rank departure-point
+ * scatter is not implemented).  Exchanges: ghost planes before every semi-Lagrangian gather and
+ * all-to-all transposes around the x3 FFT pass, stream-ordered on the context stream.  Every rank
+ * must make the same sequence of calls (collective semantics).
+ *
+ * Communicators (owned by the caller, must outlive the contexts that use them):
+ *   NCCL     -- one process per GPU: rank 0 calls dr_nccl_get_unique_id, the id is broadcast by the
+ *               caller (e.g. torch.distributed), every rank calls dr_comm_create_nccl.
+ *   loopback -- P virtual ranks inside one process on one GPU (testing): dr_hub_create(P), then one
+ *               dr_comm_create_loopback(hub, r) per rank; each rank's calls must run on its own host
+ *               thread and its own stream (ranks rendezvous on host barriers inside every exchange).
+ * Errors: DR_ERR_NCCL (NCCL failure, or libnccl.so.2 not loadable), DR_ERR_ARG (bad rank/size). */
+typedef struct dr_comm dr_comm;
+typedef struct dr_hub dr_hub;
+dr_status dr_nccl_get_unique_id(uint8_t out[128]);
+dr_status dr_comm_create_nccl(const uint8_t uid[128], int rank, int nranks, dr_comm** out);
+dr_status dr_hub_create(int nranks, dr_hub** out);
+dr_status dr_hub_destroy(dr_hub* hub);
+dr_status dr_comm_create_loopback(dr_hub* hub, int rank, dr_comm** out);
+dr_status dr_comm_destroy(dr_comm* comm);
+
+/* Host-only partition query: the slab [z0, z0 + nz) of `rank` (no GPU needed). */
+dr_status dr_slab(const dr_config* cfg, int nranks, int rank, int* z0, int* nz);
+
+/* Workspace of one rank's context (0 if the configuration is invalid for nranks). */
+size_t dr_workspace_bytes_dist(const dr_config* cfg, int nranks);
+
+/* Create a rank's context; comm = NULL is exactly dr_create (one rank).  Same workspace / stream
+ * rules as dr_create. */
+dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, size_t workspace_bytes,
+                         void* stream, dr_ctx** out);
+
+
 /* Template rho_T and reference rho_R images (scalar fields).  Copied.  Invalidates the
  * adjoint solve (and the forward solve, whose initial condition is rho_T). */
 dr_status dr_set_images(dr_ctx* ctx, const void* rho_T, const void* rho_R);

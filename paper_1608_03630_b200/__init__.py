@@ -5,3 +5,4 @@ thin ctypes binding.  Nothing here falls back to a CPU implementation.
 """
 from .diffreg import *  # noqa: F401,F403
 from .diffreg import Config, Context, DiffRegError, lib  # noqa: F401
+from . import dist  # noqa: F401,E402

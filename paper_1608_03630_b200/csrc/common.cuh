@@ -28,14 +28,20 @@ __device__ __forceinline__ Cx<T> scale(Cx<T> a, T s) { return cx(a.re * s, a.im 
 template <typename T>
 __device__ __forceinline__ Cx<T> mul_i(Cx<T> a, T s) { return cx(-a.im * s, a.re * s); }
 
-// Grid geometry: power-of-two extents, x1 fastest.
+// Grid geometry of one rank's slab: power-of-two extents, x1 fastest.  With one rank the slab is the
+// whole grid.  With P ranks rank r owns the x3 planes [z0, z0 + n3) of the global
+// n3g, and the scalar fields that semi-Lagrangian gathers read carry zg ghost planes below and zgh
+// above (ghost = 1: x3 indices of gathers are slab-local with ghosts instead of periodic wraps).
 struct Grid {
-    int n1, n2, n3;        // extents
+    int n1, n2, n3;        // local extents (n3 = slab thickness)
     int l1, l2, l3;        // log2 extents
-    int64_t M;             // n1*n2*n3
+    int64_t M;             // n1*n2*n3 local voxels
     int n1c;               // n1/2 + 1: half-spectrum row length
     int n1p;               // padded spectrum row stride (>= n1c, multiple of 16)
-    int64_t S;             // n3*n2*n1p complex entries of one spectrum
+    int64_t S;             // n3*n2*n1p complex entries of one local spectrum
+    int z0, n3g;           // global x3 offset of the slab, global x3 extent
+    int zg, zgh;           // ghost planes below / above the slab (0 with one rank)
+    int ghost;             // 1: slab mode (gathers index x3 through the ghosts, no wrap)
 };
 
 __device__ __forceinline__ int wrapi(int i, int n) { return i & (n - 1); }  // n is a power of two

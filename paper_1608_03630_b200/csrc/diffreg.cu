@@ -1,7 +1,8 @@
 // diffreg.cu -- C-ABI implementation (include/diffreg.h) of the B200 Gauss-Newton Hessian matvec of
-// arXiv 1608.03630.  Host orchestration of the CUDA kernels in fft.cuh / sl.cuh / pointwise.cuh:
-// every step of the hot path runs in those kernels; this file only sizes the workspace, validates
-// arguments and call order, and launches.  See DESIGN.md for the data layout and the dataflow.
+// arXiv 1608.03630.  Host orchestration of the CUDA kernels in fft.cuh / sl.cuh / pointwise.cuh and
+// of the slab exchanges in comm.cuh: every step of the hot path runs in those kernels; this file
+// sizes the workspace, validates arguments and call order, and launches.  See DESIGN.md for the data
+// layout and the dataflow.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -9,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -17,6 +19,7 @@
 #include "fft.cuh"
 #include "pointwise.cuh"
 #include "sl.cuh"
+#include "comm.cuh"
 
 using namespace dr;
 
@@ -46,7 +49,11 @@ int ilog2(int n) {
 }
 bool pow2_in_range(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
 
-dr_status validate(const dr_config* c) {
+// Ghost planes of a slab: the stencil of a departure point s3 spans floor(s3)-1 ..
+// floor(s3)+2, so (4, 5) planes cover x3 displacements |d3| <= 3 cells.
+constexpr int GHOST_LO = 4, GHOST_HI = 5;
+
+dr_status validate(const dr_config* c, int nranks = 1) {
     if (!c) return DR_ERR_ARG;
     for (int a = 0; a < 3; ++a)
         if (!pow2_in_range(c->n[a])) return DR_ERR_GRID;
@@ -54,14 +61,19 @@ dr_status validate(const dr_config* c) {
     if (c->reg != DR_REG_H1 && c->reg != DR_REG_H2) return DR_ERR_PARAM;
     if (!(c->beta > 0.0) || !std::isfinite(c->beta)) return DR_ERR_PARAM;
     if (c->flags & ~(uint32_t)(DR_ISOCHORIC | DR_FP64)) return DR_ERR_PARAM;
+    if (nranks < 1) return DR_ERR_ARG;
+    if (nranks > 1) {  // slabs: P | N3 and P | N2 (x2 blocks of the transposes), slab >= ghost width
+        if (c->n[2] % nranks || c->n[1] % nranks) return DR_ERR_GRID;
+        if (c->n[2] / nranks < GHOST_HI) return DR_ERR_GRID;
+    }
     return DR_OK;
 }
 
-Grid make_grid(const dr_config* c) {
-    Grid g;
+Grid make_grid(const dr_config* c, int rank = 0, int nranks = 1) {
+    Grid g{};
     g.n1 = c->n[0];
     g.n2 = c->n[1];
-    g.n3 = c->n[2];
+    g.n3 = c->n[2] / nranks;
     g.l1 = ilog2(g.n1);
     g.l2 = ilog2(g.n2);
     g.l3 = ilog2(g.n3);
@@ -69,6 +81,11 @@ Grid make_grid(const dr_config* c) {
     g.n1c = g.n1 / 2 + 1;
     g.n1p = ((g.n1c + 15) / 16) * 16;
     g.S = (int64_t)g.n3 * g.n2 * g.n1p;
+    g.z0 = rank * g.n3;
+    g.n3g = c->n[2];
+    g.ghost = nranks > 1;
+    g.zg = g.ghost ? GHOST_LO : 0;
+    g.zgh = g.ghost ? GHOST_HI : 0;
     return g;
 }
 
@@ -76,42 +93,53 @@ int64_t n_tiles(const Grid& g) {
     return (int64_t)((g.n1 + SL_TX - 1) / SL_TX) * ((g.n2 + SL_TY - 1) / SL_TY) * ((g.n3 + SL_TZ - 1) / SL_TZ);
 }
 
-// Workspace layout (byte offsets, 256-aligned).  Field counts in units of M values of type T.
+// Workspace layout (byte offsets, 256-aligned).  "Ghosted" slots (the fields semi-Lagrangian gathers
+// read: rho_j, lambda_j, lambda~_j / g_j, rho~(1), div v, and each velocity component) hold
+// zg + n3 + zgh planes; every other slot holds the slab's n3 planes.
 struct Layout {
-    size_t rhoT, rhoR, v, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, plan_p, plan_m,
-        plan_t, maxext, twx, twy, twz, twxd, twyd, twzd, total;
+    size_t F, GF, vstride;
+    size_t rhoT, rhoR, v, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
+        plan_m, plan_t, maxext, twx, twy, twz, twxd, twyd, twzd, total;
 };
 
-Layout layout(const dr_config* c) {
-    const Grid g = make_grid(c);
+Layout layout(const dr_config* c, int nranks = 1) {
+    const Grid g = make_grid(c, 0, nranks);
     const size_t es = (c->flags & DR_FP64) ? 8 : 4;
-    const size_t F = (size_t)g.M * es;
+    const size_t plane = (size_t)g.n1 * g.n2;
     const int nt = c->nt;
+    const bool dist = nranks > 1;
     Layout L{};
+    L.F = (size_t)g.M * es;
+    L.GF = ((size_t)(g.n3 + g.zg + g.zgh) * plane * es + 255) & ~(size_t)255;
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
         off += (bytes + 255) & ~(size_t)255;
         return o;
     };
-    L.rhoT = take(F);
-    L.rhoR = take(F);
-    L.v = take(3 * F);
-    L.dp = take(3 * F);
-    L.dm = take(3 * F);
-    L.m = take(F);
-    L.D = take(F);
-    L.rho = take((size_t)nt * F);             // rho_1..rho_nt (rho_0 is rhoT)
-    L.G = take((size_t)(nt + 1) * 3 * F);     // grad rho_j
-    L.lam = take((size_t)(nt + 1) * F);       // lambda_j
-    L.lt = take((size_t)nt * F);              // lambda~_0..lambda~_{nt-1} (also g_j scratch)
-    L.rt1 = take(F);                          // rho~(1)
-    L.bt = take(3 * F);                       // b~
-    L.tmp3 = take(3 * F);                     // d* and scratch
-    L.stin = take(3 * F);                     // host staging in
-    L.stout = take(3 * F);                    // host staging out
-    L.specD = take(6 * (size_t)g.S * 16);     // six forward half spectra, complex<double>
-    L.specF = take(3 * (size_t)g.S * 2 * es); // three inverse-direction half spectra, complex<T>
+    L.rhoT = take(L.GF);                      // rho_0 = rho_T (ghosted)
+    L.rhoR = take(L.F);
+    L.v = take(3 * L.GF);                     // velocity components (ghosted)
+    L.vstride = L.GF / es;
+    L.dp = take(3 * L.F);
+    L.dm = take(3 * L.F);
+    L.m = take(L.F);
+    L.D = take(L.GF);
+    L.rho = take((size_t)nt * L.GF);          // rho_1..rho_nt
+    L.G = take((size_t)(nt + 1) * 3 * L.F);   // grad rho_j
+    L.lam = take((size_t)(nt + 1) * L.GF);    // lambda_j
+    L.lt = take((size_t)nt * L.GF);           // lambda~_0..lambda~_{nt-1} (also the g_j of the inc-state sweep)
+    L.rt1 = take(L.GF);                       // rho~(1)
+    L.bt = take(3 * L.F);                     // b~
+    L.tmp3 = take(3 * L.F);                   // d* and scratch
+    L.stin = take(3 * L.F);                   // host staging in
+    L.stout = take(3 * L.F);                  // host staging out
+    // forward half spectra (complex<double>): 6 (+2 transpose buffers with slabs); inverse-direction
+    // (complex<T>): 3 (+2)
+    L.specD = take((size_t)(dist ? 8 : 6) * g.S * 16);
+    L.specF = take((size_t)(dist ? 5 : 3) * g.S * 2 * es);
+    L.xs = dist ? take(L.F) : 0;              // real-field transpose buffers (x3 derivatives)
+    L.xr = dist ? take(L.F) : 0;
     const size_t pb = (size_t)n_tiles(g) * PLAN_INTS * sizeof(int);
     L.plan_p = take(pb);
     L.plan_m = take(pb);
@@ -119,15 +147,22 @@ Layout layout(const dr_config* c) {
     L.maxext = take(16 * sizeof(int));
     L.twx = take((size_t)g.n1 * 2 * es);
     L.twy = take((size_t)g.n2 * 2 * es);
-    L.twz = take((size_t)g.n3 * 2 * es);
+    L.twz = take((size_t)g.n3g * 2 * es);
     L.twxd = take((size_t)g.n1 * 16);
     L.twyd = take((size_t)g.n2 * 16);
-    L.twzd = take((size_t)g.n3 * 16);
+    L.twzd = take((size_t)g.n3g * 16);
     L.total = off;
     return L;
 }
 
 }  // namespace
+
+struct dr_comm {
+    std::unique_ptr<dr::Comm> impl;
+};
+struct dr_hub {
+    std::unique_ptr<dr::Hub> impl;
+};
 
 struct dr_ctx {
     dr_config cfg;
@@ -135,6 +170,8 @@ struct dr_ctx {
     Layout L;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
+    int rank = 0, nranks = 1;
+    dr::Comm* comm = nullptr;  // not owned; NULL with one rank
     char* ws = nullptr;
     bool own_ws = false;
     bool have_images = false, have_velocity = false, have_state = false, have_adjoint = false, have_matvec = false;
@@ -149,6 +186,7 @@ struct dr_ctx {
     struct Acc { std::string tag; int64_t n = 0; double ms = 0; };
     std::vector<Acc> acc;
     cudaEvent_t cur_start = nullptr;
+    bool dist() const { return nranks > 1; }
     cudaEvent_t take_event() {
         if (ev_used == ev_pool.size()) {
             cudaEvent_t e;
@@ -200,6 +238,36 @@ void dr_ctx::prof_flush() {
 namespace {
 
 template <typename T>
+struct V3 {  // a vector field as three component pointers
+    T* c[3];
+};
+template <typename T>
+V3<T> vec(T* base, size_t stride) { return V3<T>{{base, base + stride, base + 2 * stride}}; }
+template <typename T>
+V3<const T> cvec(const V3<T>& v) { return V3<const T>{{v.c[0], v.c[1], v.c[2]}}; }
+
+template <typename T>
+__global__ void k_pack_split(Grid g, const T* __restrict__ f, T* __restrict__ out, int nb) {
+    // [i3][i2][i1] -> [i2 / nb][i3][i2 % nb][i1]
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.M; e += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(e % g.n1);
+        const int64_t r = e / g.n1;
+        const int y = (int)(r % g.n2), z = (int)(r / g.n2);
+        out[((((int64_t)(y / nb) * g.n3 + z) * nb) + (y % nb)) * g.n1 + x] = f[e];
+    }
+}
+template <typename T>
+__global__ void k_unpack_split(Grid g, const T* __restrict__ in, T* __restrict__ f, int nb, int accumulate) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.M; e += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(e % g.n1);
+        const int64_t r = e / g.n1;
+        const int y = (int)(r % g.n2), z = (int)(r / g.n2);
+        const T v = in[((((int64_t)(y / nb) * g.n3 + z) * nb) + (y % nb)) * g.n1 + x];
+        f[e] = accumulate ? f[e] + v : v;
+    }
+}
+
+template <typename T>
 struct Impl {
     dr_ctx& c;
     const Grid& g;
@@ -208,23 +276,30 @@ struct Impl {
     void PB() { c.prof_begin(); }
     void PE(const char* tag) { c.prof_end(tag); }
 
+    size_t plane() const { return (size_t)g.n1 * g.n2; }
+    T* gf(size_t off) { return c.at<T>(off) + (size_t)g.zg * plane(); }  // interior of a ghosted slot
+    size_t gstride() const { return c.L.GF / sizeof(T); }
     T dt() const { return T(1) / T(c.cfg.nt); }
-    T* rhoT() { return c.at<T>(c.L.rhoT); }
+    T* rhoT() { return gf(c.L.rhoT); }
     T* rhoR() { return c.at<T>(c.L.rhoR); }
-    T* v() { return c.at<T>(c.L.v); }
+    T* vc(int a) { return gf(c.L.v) + (size_t)a * gstride(); }
+    V3<T> v3() { return V3<T>{{vc(0), vc(1), vc(2)}}; }
     T* dplus() { return c.at<T>(c.L.dp); }
     T* dminus() { return c.at<T>(c.L.dm); }
     T* mult() { return c.at<T>(c.L.m); }
-    T* Dv() { return c.at<T>(c.L.D); }
-    T* rho(int j) { return j == 0 ? rhoT() : c.at<T>(c.L.rho) + (size_t)(j - 1) * g.M; }
+    T* Dv() { return gf(c.L.D); }
+    T* rho(int j) { return j == 0 ? rhoT() : gf(c.L.rho) + (size_t)(j - 1) * gstride(); }
     T* G(int j) { return c.at<T>(c.L.G) + (size_t)j * 3 * g.M; }
-    T* lam(int j) { return c.at<T>(c.L.lam) + (size_t)j * g.M; }
-    T* lt(int j) { return c.at<T>(c.L.lt) + (size_t)j * g.M; }
-    T* rt1() { return c.at<T>(c.L.rt1); }
+    V3<T> G3(int j) { return vec(G(j), (size_t)g.M); }
+    T* lam(int j) { return gf(c.L.lam) + (size_t)j * gstride(); }
+    T* lt(int j) { return gf(c.L.lt) + (size_t)j * gstride(); }
+    T* rt1() { return gf(c.L.rt1); }
     T* bt() { return c.at<T>(c.L.bt); }
     T* tmp3() { return c.at<T>(c.L.tmp3); }
     T* stin() { return c.at<T>(c.L.stin); }
     T* stout() { return c.at<T>(c.L.stout); }
+    T* xs() { return c.at<T>(c.L.xs); }
+    T* xr() { return c.at<T>(c.L.xr); }
     Cx<double>* specD(int i) { return c.at<Cx<double>>(c.L.specD) + (size_t)i * g.S; }
     Cx<T>* specF(int i) { return c.at<Cx<T>>(c.L.specF) + (size_t)i * g.S; }
     const Cx<T>* twx() { return c.at<Cx<T>>(c.L.twx); }
@@ -238,6 +313,44 @@ struct Impl {
     int grid_1d(int64_t n, int block = 256) const {
         int64_t b = (n + block - 1) / block;
         return (int)std::min<int64_t>(b, 148 * 16);
+    }
+
+    // -------------------------------------------------------------------- slab exchanges
+    int nb() const { return g.n2 / c.nranks; }  // x2 block of one rank in the transposed layout
+    void exchange(const std::vector<P2P>& ops) {
+        PB();
+        try {
+            c.comm->group(ops, s);
+        } catch (const NcclError& e) {
+            fail(DR_ERR_NCCL, e.what());
+        } catch (const std::exception& e) {
+            fail(DR_ERR_NCCL, e.what());
+        }
+        PE("exchange");
+    }
+    // ghost planes of a ghosted scalar field (interior pointer f): my top zg planes go to rank + 1 (its
+    // lower ghosts), my bottom zgh planes to rank - 1 (its upper ghosts); periodic in rank.
+    void ghosts(T* f) {
+        if (!c.dist()) return;
+        const int P = c.nranks, up = (c.rank + 1) % P, dn = (c.rank + P - 1) % P;
+        const size_t pl = plane() * sizeof(T);
+        std::vector<P2P> ops = {
+            P2P{true, up, f + (size_t)(g.n3 - g.zg) * plane(), nullptr, g.zg * pl},
+            P2P{false, dn, nullptr, f - (size_t)g.zg * plane(), g.zg * pl},
+            P2P{true, dn, f, nullptr, g.zgh * pl},
+            P2P{false, up, nullptr, f + (size_t)g.n3 * plane(), g.zgh * pl},
+        };
+        exchange(ops);
+    }
+    // all-to-all of P equal contiguous chunks: chunk q of send goes to rank q, chunk q of recv comes
+    // from rank q
+    void alltoall(const void* send, void* recv, size_t chunk_bytes) {
+        std::vector<P2P> ops;
+        for (int q = 0; q < c.nranks; ++q) {
+            ops.push_back(P2P{true, q, static_cast<const char*>(send) + q * chunk_bytes, nullptr, chunk_bytes});
+            ops.push_back(P2P{false, q, nullptr, static_cast<char*>(recv) + q * chunk_bytes, chunk_bytes});
+        }
+        exchange(ops);
     }
 
     // -------------------------------------------------------------------- twiddle tables
@@ -255,10 +368,10 @@ struct Impl {
     void init_twiddles() {
         fill_twiddles<T>(g.n1, c.L.twx);
         fill_twiddles<T>(g.n2, c.L.twy);
-        fill_twiddles<T>(g.n3, c.L.twz);
+        fill_twiddles<T>(g.n3g, c.L.twz);
         fill_twiddles<double>(g.n1, c.L.twxd);
         fill_twiddles<double>(g.n2, c.L.twyd);
-        fill_twiddles<double>(g.n3, c.L.twzd);
+        fill_twiddles<double>(g.n3g, c.L.twzd);
     }
 
     // -------------------------------------------------------------------- FFT pass launchers
@@ -351,111 +464,144 @@ struct Impl {
     static int64_t col_tiles(const ColGeom& cg, int nother) {
         return (int64_t)((cg.nx + PT::XC - 1) / PT::XC) * ((nother + PT::OL - 1) / PT::OL);
     }
-
     ColGeom spec_geom() const { return ColGeom{g.n1p, g.n1c, g.n2, g.n3}; }
     ColGeom pair_geom() const { return ColGeom{g.n1 / 2, g.n1 / 2, g.n2, g.n3}; }
+    // the transposed slab: all N3 planes of this rank's x2 block
+    ColGeom spec_geom_t() const { return ColGeom{g.n1p, g.n1c, nb(), g.n3g, c.rank * nb(), g.n2}; }
+    ColGeom pair_geom_t() const { return ColGeom{g.n1 / 2, g.n1 / 2, nb(), g.n3g, c.rank * nb(), g.n2}; }
 
     template <int L, int AX>
-    void col_deriv_L(const T* f, T* out, int acc) {
+    void col_deriv_L(const ColGeom& cg, const T* f, T* out, int acc) {
         using PT = ColDerivPass<T, L, AX>;
-        const ColGeom cg = pair_geom();
         stream("col_deriv", PT{cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, AX == 2 ? twy() : twz()},
-               col_tiles<PT>(cg, AX == 2 ? g.n3 : g.n2));
+               col_tiles<PT>(cg, AX == 2 ? cg.n3 : cg.n2));
     }
+    // out (+)= d f / dx_ax (1-D transforms along the axis only); x3 on slabs transposes first
     void col_deriv(int ax, const T* f, T* out, int acc) {
         if (ax == 2) {
-#define CALL(LL) col_deriv_L<LL, 2>(f, out, acc)
+#define CALL(LL) col_deriv_L<LL, 2>(pair_geom(), f, out, acc)
             DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
-        } else {
-#define CALL(LL) col_deriv_L<LL, 3>(f, out, acc)
+            return;
+        }
+        if (!c.dist()) {
+#define CALL(LL) col_deriv_L<LL, 3>(pair_geom(), f, out, acc)
             DR_SWITCH_COL(g.n3, CALL)
 #undef CALL
+            return;
         }
+        const size_t chunk = (size_t)g.n3 * nb() * g.n1 * sizeof(T);
+        PB();
+        k_pack_split<T><<<grid_1d(g.M), 256, 0, s>>>(g, f, xs(), nb());
+        PE("pack");
+        alltoall(xs(), xr(), chunk);
+#define CALL(LL) col_deriv_L<LL, 3>(pair_geom_t(), xr(), xr(), 0)
+        DR_SWITCH_COL(g.n3g, CALL)
+#undef CALL
+        alltoall(xr(), xs(), chunk);
+        PB();
+        k_unpack_split<T><<<grid_1d(g.M), 256, 0, s>>>(g, xs(), out, nb(), acc);
+        PE("unpack");
     }
 
     template <typename U, int L, int DIR>
-    void col_fft_L(Cx<U>* sp, const Cx<U>* tw) {
+    void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out) {
         using PT = ColFftPass<U, L, DIR>;
         const ColGeom cg = spec_geom();
-        stream(DIR < 0 ? "col_fft_fwd" : "col_fft_inv", PT{cg, sp, tw}, col_tiles<PT>(cg, g.n3));
+        stream(DIR < 0 ? "col_fft_fwd" : "col_fft_inv", PT{cg, src, dst, tw, nb_in, nb_out}, col_tiles<PT>(cg, g.n3));
     }
-    void col_fft_fwd(Cx<double>* sp) {  // forward along x2, in double
-#define CALL(LL) col_fft_L<double, LL, -1>(sp, twyd())
+    void col_fft_fwd(const Cx<double>* src, Cx<double>* dst, int nb_out) {  // forward along x2, in double
+#define CALL(LL) col_fft_L<double, LL, -1>(src, dst, twyd(), 0, nb_out)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
-    void col_fft_inv(Cx<T>* sp) {  // inverse along x2, in T
-#define CALL(LL) col_fft_L<T, LL, +1>(sp, twy())
+    void col_fft_inv(const Cx<T>* src, Cx<T>* dst, int nb_in) {  // inverse along x2, in T
+#define CALL(LL) col_fft_L<T, LL, +1>(src, dst, twy(), nb_in, 0)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
 
     template <int L, int KIND>
-    void middle_L(Cx<double>* const* in, Cx<T>* const* out) {
+    void middle_L(const ColGeom& cg, Cx<double>* const* in, Cx<T>* const* out) {
         using PT = MiddlePass<double, T, L, KIND>;
-        const ColGeom cg = spec_geom();
         PT pt;
         pt.c = cg;
         for (int i = 0; i < PT::NCI; ++i) pt.in.p[i] = in[i];
         for (int i = 0; i < PT::NCO; ++i) pt.out.p[i] = out[i];
-        pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / (double)g.M};
+        pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g)};
         pt.tw = twzd();
         pt.two = twz();
-        stream("col_middle", pt, col_tiles<PT>(cg, g.n2));
+        stream("col_middle", pt, col_tiles<PT>(cg, cg.n2));
     }
     template <int KIND>
     void middle(Cx<double>* const* in, Cx<T>* const* out) {
-#define CALL(LL) middle_L<LL, KIND>(in, out)
-        DR_SWITCH_COL(g.n3, CALL)
+        const ColGeom cg = c.dist() ? spec_geom_t() : spec_geom();
+#define CALL(LL) middle_L<LL, KIND>(cg, in, out)
+        DR_SWITCH_COL(g.n3g, CALL)
 #undef CALL
     }
 
     // -------------------------------------------------------------------- spectral operators
-    void grad(const T* f, T* out3) {
-        row_deriv(f, out3, 0);
-        col_deriv(2, f, out3 + g.M, 0);
-        col_deriv(3, f, out3 + 2 * g.M, 0);
+    // Forward half spectrum of a real slab field into spectrum slot `slot`: x1 r2c, x2 forward FFT and,
+    // with slabs, the all-to-all into the transposed layout the x3 middle pass reads.
+    void spec_forward(const T* f, int slot) {
+        if (!c.dist()) {
+            row_r2c(f, specD(slot));
+            col_fft_fwd(specD(slot), specD(slot), 0);
+            return;
+        }
+        row_r2c(f, specD(6));
+        col_fft_fwd(specD(6), specD(7), nb());  // writes the split layout: one contiguous chunk per rank
+        alltoall(specD(7), specD(slot), (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<double>));
     }
-    void div(const T* u3, T* out) {
-        row_deriv(u3, out, 0);
-        col_deriv(2, u3 + g.M, out, 1);
-        col_deriv(3, u3 + 2 * g.M, out, 1);
+    // Back from the middle pass's output slot to a real slab field (+ add).
+    void spec_inverse(int slot, T* out, const T* add) {
+        if (!c.dist()) {
+            col_fft_inv(specF(slot), specF(slot), 0);
+            row_c2r(specF(slot), out, add);
+            return;
+        }
+        alltoall(specF(slot), specF(3), (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<T>));
+        col_fft_inv(specF(3), specF(4), nb());
+        row_c2r(specF(4), out, add);
+    }
+
+    void grad(const T* f, V3<T> out) {
+        row_deriv(f, out.c[0], 0);
+        col_deriv(2, f, out.c[1], 0);
+        col_deriv(3, f, out.c[2], 0);
+    }
+    void div(V3<const T> u, T* out) {
+        row_deriv(u.c[0], out, 0);
+        col_deriv(2, u.c[1], out, 1);
+        col_deriv(3, u.c[2], out, 1);
     }
     // out_c = F^-1[sym F in_c] (+ add_c), componentwise symbol KIND 0/1.  Forward passes (x1 r2c, x2)
-    // and the x3 middle pass run in double; the inverse x2 / x1 passes in T.
+    // and the x3 forward transform run in double; the inverse x3 / x2 / x1 passes in T.
     template <int KIND>
-    void scalar_symbol3(const T* in3, T* out3, const T* add3) {
+    void scalar_symbol3(V3<const T> in, V3<T> out, const V3<const T>* add) {
         for (int cc = 0; cc < 3; ++cc) {
+            spec_forward(in.c[cc], 0);
             Cx<double>* sd = specD(0);
             Cx<T>* sf = specF(0);
-            row_r2c(in3 + cc * g.M, sd);
-            col_fft_fwd(sd);
             middle<KIND>(&sd, &sf);
-            col_fft_inv(sf);
-            row_c2r(sf, out3 + cc * g.M, add3 ? add3 + cc * g.M : nullptr);
+            spec_inverse(0, out.c[cc], add ? add->c[cc] : nullptr);
         }
     }
     // coupled 3-component symbol (KIND 2, 3): out = F^-1[sym F in]
     template <int KIND>
-    void vector_symbol3(const T* in3, T* out3) {
+    void vector_symbol3(V3<const T> in, V3<T> out) {
         Cx<double>* sd[3] = {specD(0), specD(1), specD(2)};
         Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
-        for (int cc = 0; cc < 3; ++cc) {
-            row_r2c(in3 + cc * g.M, sd[cc]);
-            col_fft_fwd(sd[cc]);
-        }
+        for (int cc = 0; cc < 3; ++cc) spec_forward(in.c[cc], cc);
         middle<KIND>(sd, sf);
-        for (int cc = 0; cc < 3; ++cc) {
-            col_fft_inv(sf[cc]);
-            row_c2r(sf[cc], out3 + cc * g.M, nullptr);
-        }
+        for (int cc = 0; cc < 3; ++cc) spec_inverse(cc, out.c[cc], nullptr);
     }
-    void reg_apply(const T* in3, T* out3) { scalar_symbol3<0>(in3, out3, nullptr); }
-    void leray(const T* in3, T* out3) { vector_symbol3<2>(in3, out3); }
-    void precond(const T* r3, T* z3) {
-        if (c.cfg.flags & DR_ISOCHORIC) vector_symbol3<3>(r3, z3);
-        else scalar_symbol3<1>(r3, z3, nullptr);
+    void reg_apply(V3<const T> in, V3<T> out) { scalar_symbol3<0>(in, out, nullptr); }
+    void leray(V3<const T> in, V3<T> out) { vector_symbol3<2>(in, out); }
+    void precond(V3<const T> r, V3<T> z) {
+        if (c.cfg.flags & DR_ISOCHORIC) vector_symbol3<3>(r, z);
+        else scalar_symbol3<1>(r, z, nullptr);
     }
 
     // -------------------------------------------------------------------- semi-Lagrangian
@@ -467,8 +613,13 @@ struct Impl {
         PE("sl_plan");
     }
 
+    // gather sources are ghosted fields: the kernel indexes x3 from the slot base (zg planes below)
     template <int NC, class Epi>
     void gather(const char* tag, Src<T, NC> src, const T* d, const int* plan_buf, Epi epi) {
+        for (int cc = 0; cc < NC; ++cc) {
+            ghosts(const_cast<T*>(src.p[cc]));
+            src.p[cc] -= (size_t)g.zg * plane();
+        }
         constexpr size_t sm = box_bytes<T, NC>();
         auto k = k_sl_gather<T, NC, Epi>;
         set_smem(k, sm);
@@ -484,43 +635,57 @@ struct Impl {
     int* plan_m() { return c.at<int>(c.L.plan_m); }
     int* plan_t() { return c.at<int>(c.L.plan_t); }
 
-    void gather_scalar_p(const T* f, T* out) {
+    void gather_scalar_p(T* f, T* out) {
         gather<1>("sl_state", Src<T, 1>{{f}}, dplus(), plan_p(), EpiStore<T>{out});
     }
 
     // -------------------------------------------------------------------- API steps
     void set_velocity(const T* vin) {
-        CK(cudaMemcpyAsync(v(), vin, 3 * g.M * sizeof(T), cudaMemcpyDefault, s));
-        if (c.cfg.flags & DR_ISOCHORIC) leray(v(), v());
-        const double h[3] = {2.0 * M_PI / g.n1, 2.0 * M_PI / g.n2, 2.0 * M_PI / g.n3};
+        for (int a = 0; a < 3; ++a)
+            CK(cudaMemcpyAsync(vc(a), vin + (size_t)a * g.M, g.M * sizeof(T), cudaMemcpyDefault, s));
+        if (c.cfg.flags & DR_ISOCHORIC) leray(cvec(v3()), v3());
+        CK(cudaMemsetAsync(c.at<int>(c.L.maxext), 0, 16 * sizeof(int), s));
+        const double h[3] = {2.0 * M_PI / g.n1, 2.0 * M_PI / g.n2, 2.0 * M_PI / g.n3g};
         const double dtt = 1.0 / c.cfg.nt;
         for (int sg = 1; sg >= -1; sg -= 2) {
             T* dout = sg > 0 ? dplus() : dminus();
             PB();
-            k_dstar<T><<<grid_1d(3 * g.M), 256, 0, s>>>(g, v(), tmp3(), (T)(sg * dtt / h[0]), (T)(sg * dtt / h[1]),
-                                                        (T)(sg * dtt / h[2]));
+            k_dstar<T><<<grid_1d(g.M), 256, 0, s>>>(g, vc(0), vc(1), vc(2), tmp3(), (T)(sg * dtt / h[0]),
+                                                    (T)(sg * dtt / h[1]), (T)(sg * dtt / h[2]));
             PE("dstar");
             plan(tmp3(), plan_t());
             EpiDeparture<T> e;
             e.d0 = dout;
             e.d1 = dout + g.M;
             e.d2 = dout + 2 * g.M;
-            e.v0 = v();
-            e.v1 = v() + g.M;
-            e.v2 = v() + 2 * g.M;
+            e.v0 = vc(0);
+            e.v1 = vc(1);
+            e.v2 = vc(2);
             for (int a = 0; a < 3; ++a) e.c[a] = (T)(sg * 0.5 * dtt / h[a]);
-            gather<3>("sl_departure", Src<T, 3>{{v(), v() + g.M, v() + 2 * g.M}}, tmp3(), plan_t(), e);
+            check_plan();
+            gather<3>("sl_departure", Src<T, 3>{{vc(0), vc(1), vc(2)}}, tmp3(), plan_t(), e);
             plan(dout, sg > 0 ? plan_p() : plan_m());
         }
+        check_plan();
         if (!(c.cfg.flags & DR_ISOCHORIC)) {
-            div(v(), Dv());
+            div(cvec(v3()), Dv());
             gather<1>("sl_multiplier", Src<T, 1>{{Dv()}}, dminus(), plan_m(), EpiMultiplier<T>{mult(), Dv(), dt()});
         }
+    }
+    // slabs: every departure stencil must lie in the rank's planes plus ghosts (no off-rank scatter yet)
+    void check_plan() {
+        if (!c.dist()) return;
+        int flag = 0;
+        CK(cudaMemcpyAsync(&flag, c.at<int>(c.L.maxext) + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (flag)
+            fail(DR_ERR_PLAN, "x3 displacement exceeds the slab ghost planes (|d3| <= 3 cells supported; "
+                              "off-rank departure-point scatter is not implemented)");
     }
 
     void forward_solve() {
         for (int j = 0; j < c.cfg.nt; ++j) gather_scalar_p(rho(j), rho(j + 1));
-        for (int j = 0; j <= c.cfg.nt; ++j) grad(rho(j), G(j));
+        for (int j = 0; j <= c.cfg.nt; ++j) grad(rho(j), G3(j));
     }
 
     void adjoint_solve() {
@@ -549,7 +714,7 @@ struct Impl {
         // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-); every step
         // also accumulates its term of the b~ trapezoid quadrature in its epilogue
         for (int k = nt; k >= 1; --k) {
-            const T* src = (k == nt) ? rt1() : lt(k);
+            T* src = (k == nt) ? rt1() : lt(k);
             const T* Gk = G(k - 1);
             const T wk = (k - 1 == 0) ? T(0.5) * dtt : dtt;
             if (k == nt) {
@@ -577,30 +742,23 @@ struct Impl {
             }
         }
         // spectral tail: H vt = beta A vt + P b~
+        const V3<const T> vt3 = cvec(vec(const_cast<T*>(vt), (size_t)g.M));
+        const V3<const T> bt3 = cvec(vec(bt(), (size_t)g.M));
+        V3<T> out3 = vec(Hvt, (size_t)g.M);
         if (c.cfg.flags & DR_ISOCHORIC) {
             Cx<double>* sd[6] = {specD(0), specD(1), specD(2), specD(3), specD(4), specD(5)};
             Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
             for (int cc = 0; cc < 3; ++cc) {
-                row_r2c(vt + cc * g.M, sd[cc]);
-                col_fft_fwd(sd[cc]);
-                row_r2c(bt() + cc * g.M, sd[3 + cc]);
-                col_fft_fwd(sd[3 + cc]);
+                spec_forward(vt3.c[cc], cc);
+                spec_forward(bt3.c[cc], 3 + cc);
             }
             middle<4>(sd, sf);
-            for (int cc = 0; cc < 3; ++cc) {
-                col_fft_inv(sf[cc]);
-                row_c2r(sf[cc], Hvt + cc * g.M, nullptr);
-            }
+            for (int cc = 0; cc < 3; ++cc) spec_inverse(cc, out3.c[cc], nullptr);
         } else {
-            scalar_symbol3<0>(vt, Hvt, bt());
+            scalar_symbol3<0>(vt3, out3, &bt3);
         }
     }
 };
-
-dr_status guard(dr_ctx* c, dr_status st, const std::string& m) {
-    if (c) c->err = m;
-    return st;
-}
 
 template <typename F>
 dr_status run(dr_ctx* c, F&& f) {
@@ -612,6 +770,9 @@ dr_status run(dr_ctx* c, F&& f) {
     } catch (const DrError& e) {
         c->err = e.msg;
         return e.s;
+    } catch (const NcclError& e) {
+        c->err = e.what();
+        return DR_ERR_NCCL;
     } catch (const std::exception& e) {
         c->err = e.what();
         return DR_ERR_CUDA;
@@ -658,24 +819,110 @@ void dispatch(dr_ctx* c, F&& f) {
     }
 }
 
+template <typename F>
+dr_status comm_run(F&& f) {
+    try {
+        f();
+        return DR_OK;
+    } catch (const NcclError&) {
+        return DR_ERR_NCCL;
+    } catch (const std::exception&) {
+        return DR_ERR_NCCL;
+    }
+}
+
 }  // namespace
 
 extern "C" {
 
-size_t dr_workspace_bytes(const dr_config* cfg) {
-    if (validate(cfg) != DR_OK) return 0;
-    return layout(cfg).total;
+size_t dr_workspace_bytes(const dr_config* cfg) { return dr_workspace_bytes_dist(cfg, 1); }
+
+size_t dr_workspace_bytes_dist(const dr_config* cfg, int nranks) {
+    if (validate(cfg, nranks) != DR_OK) return 0;
+    return layout(cfg, nranks).total;
+}
+
+dr_status dr_slab(const dr_config* cfg, int nranks, int rank, int* z0, int* nz) {
+    const dr_status v = validate(cfg, nranks);
+    if (v != DR_OK) return v;
+    if (rank < 0 || rank >= nranks || !z0 || !nz) return DR_ERR_ARG;
+    const Grid g = make_grid(cfg, rank, nranks);
+    *z0 = g.z0;
+    *nz = g.n3;
+    return DR_OK;
+}
+
+dr_status dr_nccl_get_unique_id(uint8_t out[128]) {
+    if (!out) return DR_ERR_ARG;
+    return comm_run([&] {
+        ncclUniqueId id;
+        nccl_ck(NcclApi::get().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, id.internal, 128);
+    });
+}
+
+dr_status dr_comm_create_nccl(const uint8_t uid[128], int rank, int nranks, dr_comm** out) {
+    if (!uid || !out || nranks < 1 || rank < 0 || rank >= nranks) return DR_ERR_ARG;
+    *out = nullptr;
+    return comm_run([&] {
+        auto* c = new dr_comm();
+        try {
+            c->impl.reset(new NcclComm(uid, rank, nranks));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+dr_status dr_hub_create(int nranks, dr_hub** out) {
+    if (!out || nranks < 1) return DR_ERR_ARG;
+    auto* h = new dr_hub();
+    h->impl.reset(new Hub(nranks));
+    *out = h;
+    return DR_OK;
+}
+
+dr_status dr_hub_destroy(dr_hub* h) {
+    if (!h) return DR_ERR_ARG;
+    delete h;
+    return DR_OK;
+}
+
+dr_status dr_comm_create_loopback(dr_hub* hub, int rank, dr_comm** out) {
+    if (!hub || !out || rank < 0 || rank >= hub->impl->size) return DR_ERR_ARG;
+    auto* c = new dr_comm();
+    c->impl.reset(new LoopbackComm(hub->impl.get(), rank));
+    *out = c;
+    return DR_OK;
+}
+
+dr_status dr_comm_destroy(dr_comm* c) {
+    if (!c) return DR_ERR_ARG;
+    delete c;
+    return DR_OK;
 }
 
 dr_status dr_create(const dr_config* cfg, void* workspace, size_t workspace_bytes, void* stream, dr_ctx** out) {
+    return dr_create_dist(cfg, nullptr, workspace, workspace_bytes, stream, out);
+}
+
+dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, size_t workspace_bytes, void* stream,
+                         dr_ctx** out) {
     if (!out) return DR_ERR_ARG;
     *out = nullptr;
-    const dr_status v = validate(cfg);
+    const int nranks = comm ? comm->impl->size : 1;
+    const int rank = comm ? comm->impl->rank : 0;
+    const dr_status v = validate(cfg, nranks);
     if (v != DR_OK) return v;
     dr_ctx* c = new dr_ctx();
     c->cfg = *cfg;
-    c->g = make_grid(cfg);
-    c->L = layout(cfg);
+    c->rank = rank;
+    c->nranks = nranks;
+    c->comm = comm ? comm->impl.get() : nullptr;
+    c->g = make_grid(cfg, rank, nranks);
+    c->L = layout(cfg, nranks);
     c->stream = reinterpret_cast<cudaStream_t>(stream);
     {
         int dev = 0, nsm = 0;
@@ -722,9 +969,11 @@ dr_status dr_destroy(dr_ctx* c) {
 dr_status dr_set_images(dr_ctx* c, const void* rho_T, const void* rho_R) {
     return run(c, [&] {
         if (!rho_T || !rho_R) fail(DR_ERR_ARG, "rho_T and rho_R must be non-NULL");
-        const size_t F = c->g.M * elem_size(c);
-        CK(cudaMemcpyAsync(c->ws + c->L.rhoT, rho_T, F, cudaMemcpyDefault, c->stream));
-        CK(cudaMemcpyAsync(c->ws + c->L.rhoR, rho_R, F, cudaMemcpyDefault, c->stream));
+        dispatch(c, [&](auto& im) {
+            const size_t F = c->g.M * elem_size(c);
+            CK(cudaMemcpyAsync(im.rhoT(), rho_T, F, cudaMemcpyDefault, c->stream));
+            CK(cudaMemcpyAsync(im.rhoR(), rho_R, F, cudaMemcpyDefault, c->stream));
+        });
         c->have_images = true;
         c->have_state = c->have_adjoint = c->have_matvec = false;
     });
@@ -736,7 +985,7 @@ dr_status dr_set_velocity(dr_ctx* c, const void* v) {
         c->have_velocity = false;
         c->have_state = c->have_adjoint = c->have_matvec = false;
         dispatch(c, [&](auto& im) {
-            using T = std::remove_pointer_t<decltype(im.v())>;
+            using T = std::remove_pointer_t<decltype(im.rhoR())>;
             im.set_velocity(static_cast<const T*>(v));
         });
         c->have_velocity = true;
@@ -746,28 +995,29 @@ dr_status dr_set_velocity(dr_ctx* c, const void* v) {
 dr_status dr_forward_solve(dr_ctx* c, void* rho1_out) {
     return run(c, [&] {
         if (!c->have_images || !c->have_velocity) fail(DR_ERR_ORDER, "forward_solve needs set_images and set_velocity");
-        dispatch(c, [&](auto& im) { im.forward_solve(); });
-        c->have_state = true;
-        c->have_adjoint = c->have_matvec = false;
-        if (rho1_out) {
-            const size_t F = c->g.M * elem_size(c);
-            CK(cudaMemcpyAsync(rho1_out, c->ws + c->L.rho + (size_t)(c->cfg.nt - 1) * F, F,
-                               cudaMemcpyDefault, c->stream));
-            if (!is_device_ptr(rho1_out)) CK(cudaStreamSynchronize(c->stream));
-        }
+        dispatch(c, [&](auto& im) {
+            im.forward_solve();
+            c->have_state = true;
+            c->have_adjoint = c->have_matvec = false;
+            if (rho1_out) {
+                CK(cudaMemcpyAsync(rho1_out, im.rho(c->cfg.nt), c->g.M * elem_size(c), cudaMemcpyDefault, c->stream));
+                if (!is_device_ptr(rho1_out)) CK(cudaStreamSynchronize(c->stream));
+            }
+        });
     });
 }
 
 dr_status dr_adjoint_solve(dr_ctx* c, void* lambda0_out) {
     return run(c, [&] {
         if (!c->have_state) fail(DR_ERR_ORDER, "adjoint_solve needs forward_solve");
-        dispatch(c, [&](auto& im) { im.adjoint_solve(); });
-        c->have_adjoint = true;
-        if (lambda0_out) {
-            const size_t F = c->g.M * elem_size(c);
-            CK(cudaMemcpyAsync(lambda0_out, c->ws + c->L.lam, F, cudaMemcpyDefault, c->stream));
-            if (!is_device_ptr(lambda0_out)) CK(cudaStreamSynchronize(c->stream));
-        }
+        dispatch(c, [&](auto& im) {
+            im.adjoint_solve();
+            c->have_adjoint = true;
+            if (lambda0_out) {
+                CK(cudaMemcpyAsync(lambda0_out, im.lam(0), c->g.M * elem_size(c), cudaMemcpyDefault, c->stream));
+                if (!is_device_ptr(lambda0_out)) CK(cudaStreamSynchronize(c->stream));
+            }
+        });
     });
 }
 
@@ -780,7 +1030,7 @@ dr_status dr_hessian_matvec(dr_ctx* c, const void* vt, void* Hvt) {
         const void* in = stage_in(c, vt, V, c->ws + c->L.stin);
         with_output(c, Hvt, V, c->ws + c->L.stout, [&](void* out) {
             dispatch(c, [&](auto& im) {
-                using T = std::remove_pointer_t<decltype(im.v())>;
+                using T = std::remove_pointer_t<decltype(im.rhoR())>;
                 im.hessian_matvec(static_cast<const T*>(in), static_cast<T*>(out));
             });
         });
@@ -795,13 +1045,13 @@ dr_status dr_precond_apply(dr_ctx* c, const void* r, void* z) {
         const void* in = stage_in(c, r, V, c->ws + c->L.stin);
         with_output(c, z, V, c->ws + c->L.stout, [&](void* out) {
             dispatch(c, [&](auto& im) {
-                using T = std::remove_pointer_t<decltype(im.v())>;
-                im.precond(static_cast<const T*>(in), static_cast<T*>(out));
+                using T = std::remove_pointer_t<decltype(im.rhoR())>;
+                const T* i = static_cast<const T*>(in);
+                im.precond(cvec(vec(const_cast<T*>(i), (size_t)c->g.M)), vec(static_cast<T*>(out), (size_t)c->g.M));
             });
         });
     });
 }
-
 dr_status dr_profile_enable(dr_ctx* c, int enable) {
     return run(c, [&] {
         c->prof_flush();
@@ -840,7 +1090,13 @@ dr_status dr_profile_entry(dr_ctx* c, int i, char* name, int name_len, int64_t* 
 }
 
 dr_status dr_sync(dr_ctx* c) {
-    return run(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+    return run(c, [&] {
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->comm) {
+            const std::string e = c->comm->check();
+            if (!e.empty()) fail(DR_ERR_NCCL, e);
+        }
+    });
 }
 
 const char* dr_last_error(const dr_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -865,15 +1121,18 @@ dr_status dr_op_spectral(dr_ctx* c, int op, const void* in, void* out) {
     return run(c, [&] {
         if (!in || !out) fail(DR_ERR_ARG, "in/out must be non-NULL");
         dispatch(c, [&](auto& im) {
-            using T = std::remove_pointer_t<decltype(im.v())>;
+            using T = std::remove_pointer_t<decltype(im.rhoR())>;
             const T* i = static_cast<const T*>(in);
             T* o = static_cast<T*>(out);
+            const size_t M = c->g.M;
+            const V3<const T> i3 = cvec(vec(const_cast<T*>(i), M));
+            const V3<T> o3 = vec(o, M);
             switch (op) {
-                case DR_OP_GRAD: im.grad(i, o); break;
-                case DR_OP_DIV: im.div(i, o); break;
-                case DR_OP_REG: im.reg_apply(i, o); break;
-                case DR_OP_PRECOND: im.precond(i, o); break;
-                case DR_OP_LERAY: im.leray(i, o); break;
+                case DR_OP_GRAD: im.grad(i, o3); break;
+                case DR_OP_DIV: im.div(i3, o); break;
+                case DR_OP_REG: im.reg_apply(i3, o3); break;
+                case DR_OP_PRECOND: im.precond(i3, o3); break;
+                case DR_OP_LERAY: im.leray(i3, o3); break;
                 default: fail(DR_ERR_ARG, "unknown spectral op");
             }
         });
@@ -883,10 +1142,11 @@ dr_status dr_op_spectral(dr_ctx* c, int op, const void* in, void* out) {
 dr_status dr_op_interp(dr_ctx* c, const void* f, int64_t npts, const void* s, void* out) {
     return run(c, [&] {
         if (npts < 0) fail(DR_ERR_ARG, "bad interp arguments");
+        if (c->dist()) fail(DR_ERR_ARG, "dr_op_interp is a single-rank test hook");
         if (npts == 0) return;
         if (!f || !s || !out) fail(DR_ERR_ARG, "bad interp arguments");
         dispatch(c, [&](auto& im) {
-            using T = std::remove_pointer_t<decltype(im.v())>;
+            using T = std::remove_pointer_t<decltype(im.rhoR())>;
             im.PB();
             k_interp_points<T><<<im.grid_1d(npts), 256, 0, c->stream>>>(c->g, static_cast<const T*>(f), npts,
                                                                           static_cast<const T*>(s), static_cast<T*>(out));
@@ -907,69 +1167,68 @@ dr_status dr_get_departure(dr_ctx* c, int sigma, void* d_out) {
 dr_status dr_get_field(dr_ctx* c, int which, int j, void* out) {
     return run(c, [&] {
         if (!out) fail(DR_ERR_ARG, "out must be non-NULL");
-        const size_t F = c->g.M * elem_size(c);
         const int nt = c->cfg.nt;
-        size_t off = 0, bytes = F;
         auto need = [&](bool ok, const char* m) {
             if (!ok) fail(DR_ERR_ORDER, m);
         };
         auto jrange = [&]() {
             if (j < 0 || j > nt) fail(DR_ERR_ARG, "slice index out of range");
         };
-        switch (which) {
-            case DR_FIELD_STATE:
-                need(c->have_state, "needs forward_solve");
-                jrange();
-                off = (j == 0) ? c->L.rhoT : c->L.rho + (size_t)(j - 1) * F;
-                break;
-            case DR_FIELD_STATE_GRAD:
-                need(c->have_state, "needs forward_solve");
-                jrange();
-                off = c->L.G + (size_t)j * 3 * F;
-                bytes = 3 * F;
-                break;
-            case DR_FIELD_ADJOINT:
-                need(c->have_adjoint, "needs adjoint_solve");
-                jrange();
-                off = c->L.lam + (size_t)j * F;
-                break;
-            case DR_FIELD_INC_STATE:
-                need(c->have_matvec, "needs hessian_matvec");
-                off = c->L.rt1;
-                break;
-            case DR_FIELD_INC_ADJOINT:
-                need(c->have_matvec, "needs hessian_matvec");
-                jrange();
-                if (j == nt) {  // lambda~(1) = -rho~(1) (Eq. 5d); materialise it
-                    dispatch(c, [&](auto& im) {
-                        using T = std::remove_pointer_t<decltype(im.v())>;
+        dispatch(c, [&](auto& im) {
+            using T = std::remove_pointer_t<decltype(im.rhoR())>;
+            const size_t F = c->g.M * sizeof(T);
+            T* o = static_cast<T*>(out);
+            auto copy = [&](const T* src, size_t bytes, T* dst) {
+                CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+            };
+            switch (which) {
+                case DR_FIELD_STATE:
+                    need(c->have_state, "needs forward_solve");
+                    jrange();
+                    copy(im.rho(j), F, o);
+                    break;
+                case DR_FIELD_STATE_GRAD:
+                    need(c->have_state, "needs forward_solve");
+                    jrange();
+                    copy(im.G(j), 3 * F, o);
+                    break;
+                case DR_FIELD_ADJOINT:
+                    need(c->have_adjoint, "needs adjoint_solve");
+                    jrange();
+                    copy(im.lam(j), F, o);
+                    break;
+                case DR_FIELD_INC_STATE:
+                    need(c->have_matvec, "needs hessian_matvec");
+                    copy(im.rt1(), F, o);
+                    break;
+                case DR_FIELD_INC_ADJOINT:
+                    need(c->have_matvec, "needs hessian_matvec");
+                    jrange();
+                    if (j == nt) {  // lambda~(1) = -rho~(1) (Eq. 5d); materialise it
                         im.PB();
-                        k_scale<T><<<im.grid_1d(c->g.M), 256, 0, c->stream>>>(c->g.M, im.rt1(), static_cast<T*>(out), T(-1));
+                        k_scale<T><<<im.grid_1d(c->g.M), 256, 0, c->stream>>>(c->g.M, im.rt1(), o, T(-1));
                         im.PE("scale");
-                    });
-                    return;
-                }
-                off = c->L.lt + (size_t)j * F;
-                break;
-            case DR_FIELD_BTILDE:
-                need(c->have_matvec, "needs hessian_matvec");
-                off = c->L.bt;
-                bytes = 3 * F;
-                break;
-            case DR_FIELD_MULTIPLIER:
-                need(c->have_velocity, "needs set_velocity");
-                if (c->cfg.flags & DR_ISOCHORIC) fail(DR_ERR_ARG, "isochoric contexts have m == 1");
-                off = c->L.m;
-                break;
-            case DR_FIELD_VELOCITY:
-                need(c->have_velocity, "needs set_velocity");
-                off = c->L.v;
-                bytes = 3 * F;
-                break;
-            default:
-                fail(DR_ERR_ARG, "unknown field");
-        }
-        CK(cudaMemcpyAsync(out, c->ws + off, bytes, cudaMemcpyDeviceToDevice, c->stream));
+                    } else {
+                        copy(im.lt(j), F, o);
+                    }
+                    break;
+                case DR_FIELD_BTILDE:
+                    need(c->have_matvec, "needs hessian_matvec");
+                    copy(im.bt(), 3 * F, o);
+                    break;
+                case DR_FIELD_MULTIPLIER:
+                    need(c->have_velocity, "needs set_velocity");
+                    if (c->cfg.flags & DR_ISOCHORIC) fail(DR_ERR_ARG, "isochoric contexts have m == 1");
+                    copy(im.mult(), F, o);
+                    break;
+                case DR_FIELD_VELOCITY:
+                    need(c->have_velocity, "needs set_velocity");
+                    for (int a = 0; a < 3; ++a) copy(im.vc(a), F, o + (size_t)a * c->g.M);
+                    break;
+                default:
+                    fail(DR_ERR_ARG, "unknown field");
+            }
+        });
     });
 }
 

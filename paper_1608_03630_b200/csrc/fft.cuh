@@ -394,12 +394,19 @@ struct ColGeom {
     int W;      // row stride in complex elements
     int nx;     // valid columns (x < nx)
     int n2, n3;
+    int k2off = 0, n2g = 0;  // slab transposes: global x2 index = local + k2off, global extent n2g
 };
 
+// "Split" layout of a slab's spectrum (multi-GPU x2 passes): the x2 extent is cut into blocks of nb
+// lines, block q destined to / received from rank q, stored as [q][i3][i2 % nb][x] so every rank's
+// chunk of an all-to-all transpose is contiguous.  nb = 0: the plain [i3][i2][x] layout.
 template <int AX>
-__device__ __forceinline__ int64_t col_addr(const ColGeom& c, int x, int other, int p) {
-    if (AX == 2) return ((int64_t)other * c.n2 + p) * c.W + x;  // other = i3, p = i2
-    return ((int64_t)p * c.n2 + other) * c.W + x;               // other = i2, p = i3
+__device__ __forceinline__ int64_t col_addr(const ColGeom& c, int x, int other, int p, int nb = 0) {
+    if (AX == 2) {
+        if (nb) return ((((int64_t)(p / nb) * c.n3 + other) * nb) + (p % nb)) * c.W + x;
+        return ((int64_t)other * c.n2 + p) * c.W + x;  // other = i3, p = i2
+    }
+    return ((int64_t)p * c.n2 + other) * c.W + x;      // other = i2, p = i3
 }
 
 // CTA shape of a column pass: XC columns (one 128-byte segment: 16 complex64 / 8 complex128) x OL
@@ -423,20 +430,20 @@ struct ColCfg {
 
 template <typename T, int L, int XC, int OL, int AX, int NT>
 __device__ __forceinline__ void col_load(Cx<T>* sm, const Cx<T>* __restrict__ src, const ColGeom& c, int x0, int o0,
-                                         int nother) {
+                                         int nother, int nb = 0) {
     constexpr int LP = LineGeom<L>::LP;
     for (int e = threadIdx.x; e < XC * L * OL; e += NT) {
         const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
         const int x = x0 + xi, o = o0 + oi;
         Cx<T>* d = sm + (oi * XC + xi) * LP + P(p);
-        if (x < c.nx && o < nother) cp_async_elem(d, src + col_addr<AX>(c, x, o, p));
+        if (x < c.nx && o < nother) cp_async_elem(d, src + col_addr<AX>(c, x, o, p, nb));
         else *d = cx(T(0), T(0));
     }
 }
 
 template <typename T, int L, int XC, int OL, int AX, bool ACC, int NT, typename To = T>
 __device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<To>* __restrict__ dst, const ColGeom& c, int x0, int o0,
-                                          int nother) {
+                                          int nother, int nb = 0) {
     constexpr int LP = LineGeom<L>::LP;
     for (int e = threadIdx.x; e < XC * L * OL; e += NT) {
         const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
@@ -444,7 +451,7 @@ __device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<To>* __restrict__ 
         if (x < c.nx && o < nother) {
             const Cx<T> w = sm[(oi * XC + xi) * LP + P(p)];
             Cx<To> v = cx<To>((To)w.re, (To)w.im);
-            const int64_t a = col_addr<AX>(c, x, o, p);
+            const int64_t a = col_addr<AX>(c, x, o, p, nb);
             if (ACC) v = v + dst[a];
             dst[a] = v;
         }
@@ -493,7 +500,9 @@ struct ColDerivPass {
     }
 };
 
-// Plain complex FFT of spectrum columns along x2 (forward DIR=-1 or inverse DIR=+1), in place.
+// Complex FFT of spectrum columns along x2 (forward DIR=-1 or inverse DIR=+1), src -> dst (may alias
+// when both layouts are plain).  nb_in / nb_out != 0 select the split layout on that side (the
+// all-to-all chunks of the multi-GPU transposes), fusing the pack / unpack into this pass.
 template <typename T, int L, int DIR>
 struct ColFftPass {
     using CC = ColCfg<L, T>;
@@ -501,8 +510,10 @@ struct ColFftPass {
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr size_t BUF = CC::SMEM;
     ColGeom c;
-    Cx<T>* spec;
+    const Cx<T>* src;
+    Cx<T>* dst;
     const Cx<T>* tw;
+    int nb_in, nb_out;
     __device__ __forceinline__ int ntiles() const { return ((c.nx + XC - 1) / XC) * ((c.n3 + OL - 1) / OL); }
     __device__ __forceinline__ void origin(int tile, int& x0, int& o0) const {
         const int nxb = (c.nx + XC - 1) / XC;
@@ -512,7 +523,7 @@ struct ColFftPass {
     __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
         int x0, o0;
         origin(tile, x0, o0);
-        col_load<T, L, XC, OL, 2, NT>(reinterpret_cast<Cx<T>*>(smem), spec, c, x0, o0, c.n3);
+        col_load<T, L, XC, OL, 2, NT>(reinterpret_cast<Cx<T>*>(smem), src, c, x0, o0, c.n3, nb_in);
     }
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
@@ -520,7 +531,7 @@ struct ColFftPass {
         origin(tile, x0, o0);
         const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
         fft_line<T, L, DIR>(sm + line * LP, t, tw, 1);
-        col_store<T, L, XC, OL, 2, false, NT>(sm, spec, c, x0, o0, c.n3);
+        col_store<T, L, XC, OL, 2, false, NT>(sm, dst, c, x0, o0, c.n3, nb_out);
     }
 };
 
@@ -637,8 +648,9 @@ struct MiddlePass {
 #pragma unroll
             for (int ci = 0; ci < NCI; ++ci) v[ci] = sm[ci * LINES * LP + ln * LP + P(p)];
             if (x < c.nx && o < c.n2) {
-                const int k1 = x, k2 = wavenum(o, c.n2), k3 = wavenum(p, L);
-                const int kp1 = (x == n1 / 2) ? 0 : x, kp2 = wavenum_odd(o, c.n2), kp3 = wavenum_odd(p, L);
+                const int og = o + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
+                const int k1 = x, k2 = wavenum(og, n2g), k3 = wavenum(p, L);
+                const int kp1 = (x == n1 / 2) ? 0 : x, kp2 = wavenum_odd(og, n2g), kp3 = wavenum_odd(p, L);
                 Sym<T, KIND>::apply(s, v, k1, k2, k3, kp1, kp2, kp3);
             }
 #pragma unroll

@@ -73,7 +73,7 @@ __device__ __forceinline__ T interp_global(const T* __restrict__ f, const Grid& 
     T acc = T(0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        const int j3 = wrapi(q3 + c - 1, g.n3);
+        const int j3 = g.ghost ? q3 + c - 1 - g.z0 + g.zg : wrapi(q3 + c - 1, g.n3);
         T accb = T(0);
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
@@ -99,6 +99,8 @@ __device__ __forceinline__ void tile_coords(const Grid& g, int tile, int& x0, in
 // ---------------------------------------------------------------------------------------------
 // Plan: per tile, the unwrapped box [min q - 1, max q + 2] of the stencil nodes of its departure
 // points, and the running maximum extents over all tiles (for sizing shared memory).
+// maxext[0..2]: running maximum box extents; maxext[3] is set to 1 when, in slab mode, a tile's box
+// leaves the rank's planes plus ghosts (the displacement exceeds the ghost width: DR_ERR_PLAN).
 template <typename T>
 __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restrict__ d, int* __restrict__ plan,
                                                         int* __restrict__ maxext) {
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restr
             const int z = z0 + k;
             if (z >= g.n3) break;
             const int64_t id = ((int64_t)z * g.n2 + y) * g.n1 + x;
-            const int ii[3] = {x, y, z};
+            const int ii[3] = {x, y, z + g.z0};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 int q;
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restr
             atomicMax(&maxext[a], p[3 + a]);
         }
         p[6] = p[7] = 0;
+        if (g.ghost && (p[2] - g.z0 + g.zg < 0 || p[2] + p[5] - g.z0 > g.n3 + g.zgh)) atomicOr(&maxext[3], 1);
     }
 }
 
@@ -405,7 +408,8 @@ __device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, 
     while (yy >= c.ey) { yy -= c.ey; ++zz; }
     const int gx = wrapi(c.ox + ch * VEC, g.n1);
     while (zz < c.ez) {
-        const int gy = wrapi(c.oy + yy, g.n2), gz = wrapi(c.oz + zz, g.n3);
+        const int gy = wrapi(c.oy + yy, g.n2);
+        const int gz = g.ghost ? c.oz + zz - g.z0 + g.zg : wrapi(c.oz + zz, g.n3);
         const uint32_t gofs = ((uint32_t)gz * g.n2 + gy) * g.n1 + gx;
         T* dst = box + (zz * BY + yy) * BX + ch * VEC;
 #pragma unroll
@@ -453,7 +457,7 @@ __device__ __forceinline__ void compute_tile(const Grid& g, const Src<T, NC>& sr
                 const uint32_t idA = id0 + p * plane, idB = id0 + (p + H) * plane;
                 int qA[3], qB[3];
                 float tA[3], tB[3];
-                const int ii[3] = {x, y, c.z0 + p};
+                const int ii[3] = {x, y, c.z0 + p + g.z0};
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     cell_of<float>(ii[a], dd[p][a], qA[a], tA[a]);
@@ -488,7 +492,7 @@ __device__ __forceinline__ void compute_tile(const Grid& g, const Src<T, NC>& sr
                 T t1, t2, t3;
                 cell_of<T>(x, dd[k][0], q1, t1);
                 cell_of<T>(y, dd[k][1], q2, t2);
-                cell_of<T>(c.z0 + k, dd[k][2], q3, t3);
+                cell_of<T>(c.z0 + k + g.z0, dd[k][2], q3, t3);
                 T w1[4], w2[4], w3[4];
                 lagrange4(t1, w1);
                 lagrange4(t2, w2);
@@ -509,7 +513,7 @@ __device__ __forceinline__ void compute_tile(const Grid& g, const Src<T, NC>& sr
             T t1, t2, t3;
             cell_of<T>(x, __ldg(d.p[0] + id), q1, t1);
             cell_of<T>(y, __ldg(d.p[1] + id), q2, t2);
-            cell_of<T>(c.z0 + k, __ldg(d.p[2] + id), q3, t3);
+            cell_of<T>(c.z0 + k + g.z0, __ldg(d.p[2] + id), q3, t3);
             T w1[4], w2[4], w3[4];
             lagrange4(t1, w1);
             lagrange4(t2, w2);
@@ -577,14 +581,15 @@ __global__ void __launch_bounds__(SL_THREADS, BoxGeom<T, NC>::MINB)
     }
 }
 
-// First-stage displacement of Eq. 6: d* = sigma dt v / h (cells), X* = x - h d*.
+// First-stage displacement of Eq. 6: d* = sigma dt v / h (cells), X* = x - h d*.  v: component pointers
+// (slab interiors), dstar: [3][M].
 template <typename T>
-__global__ void k_dstar(Grid g, const T* __restrict__ v, T* __restrict__ dstar, T c0, T c1, T c2) {
-    const int64_t n = 3 * g.M;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int a = (int)(e / g.M);
-        const T c = a == 0 ? c0 : (a == 1 ? c1 : c2);
-        dstar[e] = c * v[e];
+__global__ void k_dstar(Grid g, const T* __restrict__ v0, const T* __restrict__ v1, const T* __restrict__ v2,
+                        T* __restrict__ dstar, T c0, T c1, T c2) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.M; e += (int64_t)gridDim.x * blockDim.x) {
+        dstar[e] = c0 * v0[e];
+        dstar[g.M + e] = c1 * v1[e];
+        dstar[2 * g.M + e] = c2 * v2[e];
     }
 }
 

@@ -29,7 +29,9 @@ DR_OP_GRAD, DR_OP_DIV, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY = range(5)
 EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr_set_velocity",
            "dr_forward_solve", "dr_adjoint_solve", "dr_hessian_matvec", "dr_precond_apply", "dr_sync",
            "dr_last_error", "dr_status_string", "dr_op_spectral", "dr_op_interp", "dr_get_departure",
-           "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry"]
+           "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry",
+           "dr_nccl_get_unique_id", "dr_comm_create_nccl", "dr_hub_create", "dr_hub_destroy",
+           "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist"]
 
 
 class dr_config(ctypes.Structure):
@@ -70,6 +72,18 @@ def lib():
             getattr(L, name).argtypes = args
             getattr(L, name).restype = ctypes.c_int
         L.dr_create.restype = ctypes.c_int
+        L.dr_workspace_bytes_dist.argtypes = [ctypes.POINTER(dr_config), i32]
+        L.dr_workspace_bytes_dist.restype = ctypes.c_size_t
+        L.dr_create_dist.argtypes = [ctypes.POINTER(dr_config), vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
+        L.dr_create_dist.restype = ctypes.c_int
+        for name, args in [("dr_nccl_get_unique_id", [ctypes.c_char_p]),
+                           ("dr_comm_create_nccl", [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]),
+                           ("dr_hub_create", [i32, ctypes.POINTER(vp)]), ("dr_hub_destroy", [vp]),
+                           ("dr_comm_create_loopback", [vp, i32, ctypes.POINTER(vp)]), ("dr_comm_destroy", [vp]),
+                           ("dr_slab", [ctypes.POINTER(dr_config), i32, i32, ctypes.POINTER(i32),
+                                        ctypes.POINTER(i32)])]:
+            getattr(L, name).argtypes = args
+            getattr(L, name).restype = ctypes.c_int
         L.dr_last_error.argtypes = [vp]
         L.dr_last_error.restype = ctypes.c_char_p
         L.dr_status_string.argtypes = [ctypes.c_int]
@@ -114,21 +128,100 @@ def dr_workspace_bytes(cfg: Config) -> int:
     return int(lib().dr_workspace_bytes(ctypes.byref(c)))
 
 
-class Context:
-    """One dr_ctx: owns its workspace tensor (torch device memory) and uses the given CUDA stream."""
+def dr_workspace_bytes_dist(cfg: Config, nranks: int) -> int:
+    c = cfg.c()
+    return int(lib().dr_workspace_bytes_dist(ctypes.byref(c), nranks))
 
-    def __init__(self, cfg: Config, device="cuda", stream: torch.cuda.Stream | None = None):
+
+def dr_slab(cfg: Config, nranks: int, rank: int) -> tuple[int, int]:
+    """(z0, nz): the x3 planes [z0, z0 + nz) rank `rank` of `nranks` owns (host-only, no GPU)."""
+    c = cfg.c()
+    z0, nz = ctypes.c_int(), ctypes.c_int()
+    st = lib().dr_slab(ctypes.byref(c), nranks, rank, ctypes.byref(z0), ctypes.byref(nz))
+    if st != DR_OK:
+        raise DiffRegError(st, lib().dr_status_string(st).decode())
+    return z0.value, nz.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = lib().dr_nccl_get_unique_id(buf)
+    if st != DR_OK:
+        raise DiffRegError(st, lib().dr_status_string(st).decode())
+    return buf.raw
+
+
+class Comm:
+    """A communicator of the slab path: NCCL (one process per GPU) or loopback (virtual ranks of one
+    process, see Hub).  Must outlive the contexts that use it."""
+
+    def __init__(self, handle, rank: int, size: int, keep=None):
+        self.h, self.rank, self.size, self._keep = handle, rank, size, keep
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, size: int) -> "Comm":
+        h = ctypes.c_void_p()
+        st = lib().dr_comm_create_nccl(uid, rank, size, ctypes.byref(h))
+        if st != DR_OK:
+            raise DiffRegError(st, lib().dr_status_string(st).decode())
+        return cls(h, rank, size)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().dr_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Hub:
+    """P virtual ranks in one process on one GPU (testing the slab path without P GPUs): each rank's
+    context must be driven from its own host thread on its own stream."""
+
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        st = lib().dr_hub_create(nranks, ctypes.byref(h))
+        if st != DR_OK:
+            raise DiffRegError(st, "dr_hub_create")
+        self.h, self.size = h, nranks
+
+    def comm(self, rank: int) -> Comm:
+        h = ctypes.c_void_p()
+        st = lib().dr_comm_create_loopback(self.h, rank, ctypes.byref(h))
+        if st != DR_OK:
+            raise DiffRegError(st, "dr_comm_create_loopback")
+        return Comm(h, rank, self.size, keep=self)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().dr_hub_destroy(self.h)
+            self.h = None
+
+
+class Context:
+    """One dr_ctx: owns its workspace tensor (torch device memory) and uses the given CUDA stream.
+    With `comm` the context is one rank of the slab decomposition and every field is its x3 slab."""
+
+    def __init__(self, cfg: Config, device="cuda", stream: torch.cuda.Stream | None = None, comm: Comm | None = None):
         self.cfg = cfg
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        nbytes = dr_workspace_bytes(cfg)
+        self.comm = comm
+        self.nranks = comm.size if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
+        self.z0, self.nz = dr_slab(cfg, self.nranks, self.rank)
+        nbytes = dr_workspace_bytes_dist(cfg, self.nranks)
         if nbytes == 0:
-            raise DiffRegError(DR_ERR_PARAM, f"invalid config {cfg}")
+            raise DiffRegError(DR_ERR_PARAM, f"invalid config {cfg} for {self.nranks} ranks")
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         c = cfg.c()
         h = ctypes.c_void_p()
-        st = lib().dr_create(ctypes.byref(c), _ptr(self.workspace), nbytes,
-                             ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        st = lib().dr_create_dist(ctypes.byref(c), comm.h if comm is not None else None, _ptr(self.workspace), nbytes,
+                                  ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
         if st != DR_OK:
             raise DiffRegError(st, lib().dr_status_string(st).decode())
         self.h = h
@@ -148,12 +241,17 @@ class Context:
         except Exception:
             pass
 
-    # allocation helpers (on the context device)
+    # allocation helpers (on the context device; the rank's slab)
+    @property
+    def shape(self):
+        n3, n2, n1 = self.cfg.shape
+        return (self.nz, n2, n1)
+
     def scalar(self, device=None):
-        return torch.empty(self.cfg.shape, dtype=self.cfg.dtype, device=device or self.device)
+        return torch.empty(self.shape, dtype=self.cfg.dtype, device=device or self.device)
 
     def vector(self, device=None):
-        return torch.empty((3,) + self.cfg.shape, dtype=self.cfg.dtype, device=device or self.device)
+        return torch.empty((3,) + self.shape, dtype=self.cfg.dtype, device=device or self.device)
 
     def _in(self, t):
         assert t.dtype == self.cfg.dtype and t.is_contiguous(), (t.dtype, self.cfg.dtype)

@@ -1,0 +1,151 @@
+"""Slab decomposition on one GPU: P virtual ranks in one process (loopback communicator,
+one host thread + one stream per rank) against the single-rank library on the same inputs.
+
+Pins: the per-point arithmetic of every gather, FFT line, symbol and quadrature is the
+same on slabs as on the whole grid, so departure points, states, adjoints, gradients, the Hessian
+matvec and the preconditioner must agree bit for bit; a loose 1e-6 relative bound is asserted as well
+in case a future pass reorders a sum.  The single-rank path itself is held to the oracle by
+test_gpu_parity.py."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dr():
+    from paper_1608_03630_b200 import build
+    build.build()
+    import paper_1608_03630_b200 as m
+    m.lib()
+    return m
+
+
+def rel(a, b):
+    a = a.double().cpu().numpy().ravel()
+    b = b.double().cpu().numpy().ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def run_ranks(P, fn):
+    """fn(rank) on P threads; re-raises the first failure."""
+    out, err = [None] * P, []
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if err:
+        raise err[0]
+    return out
+
+
+def pipeline(ctx, rT, rR, v, vt):
+    """The library's full hot path on one context; returns every observable it exposes."""
+    dr = pytest.importorskip("paper_1608_03630_b200")
+    F = dr.diffreg
+    ctx.set_images(rT, rR)
+    ctx.set_velocity(v)
+    res = {"d+": ctx.get_departure(+1), "d-": ctx.get_departure(-1), "vel": ctx.get_field(F.DR_FIELD_VELOCITY)}
+    if not ctx.cfg.isochoric:
+        res["m"] = ctx.get_field(F.DR_FIELD_MULTIPLIER)
+    ctx.forward_solve()
+    nt = ctx.cfg.nt
+    for j in range(nt + 1):
+        res[f"rho{j}"] = ctx.get_field(F.DR_FIELD_STATE, j)
+        res[f"G{j}"] = ctx.get_field(F.DR_FIELD_STATE_GRAD, j)
+    ctx.adjoint_solve()
+    res["lam0"] = ctx.get_field(F.DR_FIELD_ADJOINT, 0)
+    res["Hv"] = ctx.hessian_matvec(vt)
+    res["bt"] = ctx.get_field(F.DR_FIELD_BTILDE)
+    res["z"] = ctx.precond_apply(vt)
+    res["reg"] = ctx.op_spectral(F.DR_OP_REG, vt)
+    res["leray"] = ctx.op_spectral(F.DR_OP_LERAY, vt)
+    res["div"] = ctx.op_spectral(F.DR_OP_DIV, vt)
+    ctx.sync()
+    return {k: t.clone() for k, t in res.items()}
+
+
+CASES = [
+    # n, nt, iso, velocity (max displacement must stay within the 4/5 ghost planes along x3)
+    ((32, 32, 32), 4, False, lambda n: synth.smooth_vec(9, n, kmax=4, cells_per_step=2.0, nt=4)),
+    ((64, 32, 16), 2, True, lambda n: synth.smooth_vec(5, n, kmax=3, cells_per_step=1.5, nt=2, divfree=True)),
+    ((16, 64, 32), 4, False, lambda n: synth.v_star(n)),
+]
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_slabs_match_single_rank(dr, P, case):
+    n, nt, iso, vgen = CASES[case]
+    D = dr.dist
+    cfg = dr.Config(n=n, nt=nt, reg=dr.DR_REG_H2, beta=1e-2, isochoric=iso)
+    if dr.diffreg.dr_workspace_bytes_dist(cfg, P) == 0:
+        pytest.skip("grid not divisible into P slabs")
+    rT = synth.round32(synth.blobs(11, n, kcut=6)).cuda()
+    rR = synth.round32(synth.blobs(12, n, kcut=6)).cuda()
+    v = synth.round32(vgen(n)).cuda()
+    vt = synth.round32(synth.smooth_vec(13, n, kmax=4)).cuda()
+    ref = pipeline(dr.Context(cfg), rT, rR, v, vt)
+
+    hub = dr.diffreg.Hub(P)
+    comms = [hub.comm(r) for r in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ctxs = [dr.Context(cfg, stream=streams[r], comm=comms[r]) for r in range(P)]
+    torch.cuda.synchronize()
+    sl = lambda x, r: D.slab_of(x, cfg, P, r)  # noqa: E731
+    ins = [(sl(rT, r), sl(rR, r), sl(v, r), sl(vt, r)) for r in range(P)]
+    torch.cuda.synchronize()
+
+    def rank(r):
+        with torch.cuda.stream(streams[r]):
+            out = pipeline(ctxs[r], *ins[r])
+        streams[r].synchronize()
+        return out
+
+    outs = run_ranks(P, rank)
+    for k, full in ref.items():
+        got = D.assemble([o[k] for o in outs])
+        assert got.shape == full.shape, k
+        assert rel(got, full) < 1e-6, (k, rel(got, full))
+        assert torch.equal(got, full), (k, rel(got, full))
+    for c in ctxs:
+        c.close()
+    for c in comms:
+        c.close()
+    hub.close()
+
+
+def test_slab_rejects_displacement_beyond_ghosts(dr):
+    """|d3| > 3 cells leaves the ghost planes: set_velocity reports DR_ERR_PLAN on every rank."""
+    P, n = 2, (16, 16, 32)
+    cfg = dr.Config(n=n, nt=2)
+    v = synth.round32(synth.smooth_vec(4, n, kmax=2, cells_per_step=6.0, nt=2)).cuda()
+    hub = dr.diffreg.Hub(P)
+    comms = [hub.comm(r) for r in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ctxs = [dr.Context(cfg, stream=streams[r], comm=comms[r]) for r in range(P)]
+    vs = [dr.dist.slab_of(v, cfg, P, r) for r in range(P)]
+    torch.cuda.synchronize()
+
+    def rank(r):
+        with torch.cuda.stream(streams[r]):
+            try:
+                ctxs[r].set_velocity(vs[r])
+            except dr.DiffRegError as e:
+                return e.status
+        return 0
+
+    assert run_ranks(P, rank) == [dr.DR_ERR_PLAN] * P
