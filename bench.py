@@ -225,7 +225,7 @@ def run_reference(args, ws, rank):
               f"(departure points, state solve, gradients: {setup_s:.1f} s) is untimed")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"cfg3 {n}^3 nt={NT} H2 beta=1e-2 GN non-isochoric (oracle sample)",
                       "grid": [n] * 3, "nt": NT},
            "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": sample},
@@ -241,8 +241,15 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     M = n ** 3
     cfg = dr.Config(n=n, nt=NT, reg=dr.DR_REG_H2, beta=1e-2)
-    ctx = dr.Context(cfg, device=dev)
+    # N > 1: the same 256^3 problem split into x3 slabs, one per GPU (strong scaling);
+    # the library's NCCL communicator is bootstrapped from a unique id broadcast over torch.distributed
+    comm = dr.dist.make_comm(rank, ws) if ws > 1 else None
+    ctx = dr.Context(cfg, device=dev, comm=comm)
     rT, rR, v, vts = make_inputs(n, dev)
+    if ws > 1:
+        sl = lambda x: dr.dist.slab_of(x, cfg, ws, rank)  # noqa: E731
+        rT, rR, v, vts = sl(rT), sl(rR), sl(v), [sl(x) for x in vts]
+        torch.cuda.synchronize()
     ctx.set_images(rT, rR)
     Hv = [torch.empty_like(vts[0]) for _ in range(NMV)]
     Z = [torch.empty_like(vts[0]) for _ in range(NMV)]
@@ -280,8 +287,9 @@ def run_ours(args, ws, rank, local):
     ctx.profile_enable(False)
     ms_max = max_over_ranks(ms, ws)
     T = ms_max / 1e3
-    value = ws * args.steps * NMV / T
-    vox_steps = ws * args.steps * (NT * M + NT * M + NMV * 2 * NT * M) / T
+    # every matvec is one collective over all ranks of the whole 256^3 problem (strong scaling)
+    value = args.steps * NMV / T
+    vox_steps = args.steps * (NT * M + NT * M + NMV * 2 * NT * M) / T
 
     # ---- matvec-only throughput (secondary)
     torch.cuda.synchronize()
@@ -291,13 +299,15 @@ def run_ours(args, ws, rank, local):
         ctx.hessian_matvec(vts[i], Hv[i])
     m1.record(stream)
     torch.cuda.synchronize()
-    mv_ms = m0.elapsed_time(m1) / NMV
+    mv_ms = max_over_ranks(m0.elapsed_time(m1) / NMV, ws)
 
     # ---- dominant kernel roofline (algorithmic bytes / live CUDA-event duration)
     peak, peak_kind = peaks()
     table = []
     for tag, (k, tms) in prof.items():
         b = algo_bytes(tag, n, NT)
+        if b is not None:
+            b = b // ws  # per-rank share of the slab-decomposed launch
         avg = tms / k
         table.append({"tag": tag, "launches": k, "total_ms": tms, "avg_ms": avg, "share": tms / ms,
                       "algo_bytes": b, "gbs": (b / (avg / 1e3) / 1e9) if b else None})
@@ -342,8 +352,8 @@ def run_ours(args, ws, rank, local):
         torch.cuda.synchronize()
         barrier(ws)
         hms = max_over_ranks(h0.elapsed_time(h1), ws)
-        fb = 4 * M
-        e2e = {"value": ws * ksteps * NMV / (hms / 1e3), "unit": "matvec/s",
+        fb = 4 * M // ws
+        e2e = {"value": ksteps * NMV / (hms / 1e3), "unit": "matvec/s",
                "h2d_bytes_per_step": 2 * fb + 3 * fb + NMV * (3 * fb + 3 * fb),
                "d2h_bytes_per_step": NMV * (3 * fb + 3 * fb), "steps": ksteps}
 
@@ -363,14 +373,14 @@ def run_ours(args, ws, rank, local):
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": ws, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                "config": {"workload": f"cfg3: {n}^3 nt={NT} H2 beta=1e-2 GN non-isochoric; step = set_velocity + "
                                       f"forward_solve + adjoint_solve + {NMV} x (hessian_matvec + precond_apply)",
                           "grid": [n] * 3, "nt": NT, "reg": "H2", "beta": 1e-2, "isochoric": False,
                           "matvecs_per_step": NMV,
-                          "l2": "inputs larger than L2 (working set ~%.1f GB >> 126 MB)" % (
-                              dr.dr_workspace_bytes(cfg) / 1e9),
-                          "parallelism": "single" if ws == 1 else f"replicas x{ws}"},
+                          "l2": "inputs larger than L2 (working set ~%.1f GB per GPU >> 126 MB)" % (
+                              dr.diffreg.dr_workspace_bytes_dist(cfg, ws) / 1e9),
+                          "parallelism": "single" if ws == 1 else f"x3 slabs x{ws} (NCCL ghost planes + all-to-all)"},
                "voxel_steps_per_s": vox_steps, "matvec_only_ms": mv_ms,
                "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu}
         print(json.dumps(out), flush=True)
