@@ -624,11 +624,9 @@ struct Impl {
         auto k = k_sl_gather<T, NC, Epi>;
         set_smem(k, sm);
         const Disp<T> dp{{d, d + g.M, d + 2 * g.M}};
-        const int nt = (int)n_tiles(g);
-        // double-buffered geometries run persistent (a few CTAs per SM); single-stage ones one tile per CTA
-        const int grid = BoxGeom<T, NC>::STAGES == 2 ? std::min(nt, c.num_sms * BoxGeom<T, NC>::MINB) : nt;
+        const int nt = (int)n_tiles(g);  // one CTA per tile
         PB();
-        k<<<(unsigned)grid, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
+        k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
         PE(tag);
     }
     int* plan_p() { return c.at<int>(c.L.plan_p); }

@@ -161,16 +161,13 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restr
 // the step with the NC interpolated components `val` at the departure point.  Indices are 32-bit
 // (M <= 2^30); vector fields are passed as one pointer per component.
 struct NoLate {};
-struct NoPre {};
 
 template <typename T>
 struct EpiStore {  // state solve: rho_{j+1} = I[rho_j](X+)   (Eq. 7 with f = 0)
     T* out;
-    using Pre = NoPre;
     using Late = NoLate;
-    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
     __device__ __forceinline__ Late late(uint32_t) const { return Late{}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late&) const { out[id] = val[0]; }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late&) const { out[id] = val[0]; }
 };
 
 // Adjoint-like step: nu_{k-1} = scale * m * I[nu_k](X-)  (Eq. 7 with f = nu div v; D7).
@@ -190,9 +187,7 @@ struct EpiAdjoint {
     const T* nu; T snu;                      // QUAD == 1: nu_nt = snu * nu[x]
     const T* H0; const T* H1; const T* H2;   // QUAD == 1: G_nt
     T wn;                                    // QUAD == 1: dt w_nt
-    using Pre = NoPre;
     struct Late { T m; T g[3]; T b[3]; };
-    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
     __device__ __forceinline__ Late late(uint32_t id) const {
         Late l;
         l.m = m ? scale * __ldg(m + id) : scale;
@@ -213,7 +208,7 @@ struct EpiAdjoint {
         }
         return l;
     }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
         const T r = l.m * val[0];
         out[id] = r;
         if constexpr (QUAD != 0) {
@@ -231,13 +226,11 @@ struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+
     const T* vt0; const T* vt1; const T* vt2;  // vt components
     const T* G0; const T* G1; const T* G2;     // grad rho_{j+1} components
     T c;
-    using Pre = NoPre;
-    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
     struct Late { T v[3], g[3]; };
     __device__ __forceinline__ Late late(uint32_t id) const {
         return Late{{__ldg(vt0 + id), __ldg(vt1 + id), __ldg(vt2 + id)}, {__ldg(G0 + id), __ldg(G1 + id), __ldg(G2 + id)}};
     }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
         const T f = l.v[0] * l.g[0] + l.v[1] * l.g[1] + l.v[2] * l.g[2];
         out[id] = val[0] - c * f;
     }
@@ -248,11 +241,9 @@ struct EpiMultiplier {  // m = 1 + dt/2 (Dbar + D + dt Dbar D), Dbar = I[div v](
     T* m;
     const T* D;
     T dt;
-    using Pre = NoPre;
-    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
     struct Late { T D; };
     __device__ __forceinline__ Late late(uint32_t id) const { return Late{__ldg(D + id)}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
         const T Db = val[0];
         m[id] = T(1) + T(0.5) * dt * (Db + l.D + dt * Db * l.D);
     }
@@ -263,11 +254,9 @@ struct EpiDeparture {  // d = sigma dt/2 (v(x) + I[v](X*)) / h  (Eq. 6, cell uni
     T* d0; T* d1; T* d2;
     const T* v0; const T* v1; const T* v2;
     T c[3];  // sigma * dt / (2 h_a)
-    using Pre = NoPre;
-    __device__ __forceinline__ Pre early(uint32_t) const { return Pre{}; }
     struct Late { T v[3]; };
     __device__ __forceinline__ Late late(uint32_t id) const { return Late{{__ldg(v0 + id), __ldg(v1 + id), __ldg(v2 + id)}}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Pre&, const Late& l) const {
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
         d0[id] = c[0] * (l.v[0] + val[0]);
         d1[id] = c[1] * (l.v[1] + val[1]);
         d2[id] = c[2] * (l.v[2] + val[2]);
@@ -297,15 +286,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // alignment), BY/BZ an 8-deep tile's.
 template <typename T, int NC>
 struct BoxGeom;
-// STAGES = 2: double-buffered boxes (next tile staged during the current one); MINB CTAs per SM.
-template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 3, STAGES = 1; };   // 58 KB
-template <> struct BoxGeom<float, 3> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1, STAGES = 1; };   // 173 KB
-template <> struct BoxGeom<double, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1, STAGES = 1; };  // 115 KB
-template <> struct BoxGeom<double, 3> { static constexpr int BX = 48, BY = 14, BZ = 14, MINB = 1, STAGES = 1; };  // 221 KB
+// MINB: CTAs per SM the register budget must allow.
+template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 3; };   // 58 KB
+template <> struct BoxGeom<float, 3> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };   // 173 KB
+template <> struct BoxGeom<double, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };  // 115 KB
+template <> struct BoxGeom<double, 3> { static constexpr int BX = 48, BY = 14, BZ = 14, MINB = 1; };  // 221 KB
 
 template <typename T, int NC>
 constexpr size_t box_bytes() {
-    return (size_t)BoxGeom<T, NC>::STAGES * NC * BoxGeom<T, NC>::BX * BoxGeom<T, NC>::BY * BoxGeom<T, NC>::BZ * sizeof(T);
+    return (size_t)NC * BoxGeom<T, NC>::BX * BoxGeom<T, NC>::BY * BoxGeom<T, NC>::BZ * sizeof(T);
 }
 
 template <typename T, int BX, int BY>
@@ -358,16 +347,9 @@ __device__ __forceinline__ float2 interp_box2(const float* __restrict__ bA, cons
     return acc;
 }
 
-// Fused gather + epilogue, persistent.  Grid: a few CTAs per SM; each CTA walks tiles
-// t = blockIdx.x, blockIdx.x + gridDim.x, ... (32 x 8 x 8 voxels; thread = (x, y) column of 8 points).
-// Dynamic smem: STAGES boxes of box_bytes<T, NC>().  With STAGES = 2 the next tile's box is staged
-// (16-byte cp.async, periodic wrap per chunk; x origin aligned down to VEC = 16 B / sizeof(T), which
-// never straddles the wrap since N1 is a multiple of VEC) and its displacements are loaded into
-// registers while the current tile is interpolated, so HBM/L2 latency hides behind the
-// shared-memory-bound gather.  Per point: 64 stencil values from shared memory, points k and k + 4
-// as one packed fp32x2 pair (FFMA2); the epilogue operands are issued before the pair's
-// interpolation and consumed after it.  Tiles whose box exceeds the compile-time capacity gather
-// from global memory instead (same arithmetic, one point at a time).
+// Tile context: origin of the tile and the planned box (x origin aligned down to VEC = 16 B /
+// sizeof(T) so rows stage as 16-byte cp.async chunks; N1 is a multiple of VEC, so a chunk never
+// straddles the periodic wrap).
 template <typename T, int NC>
 struct TileCtx {
     int x0, y0, z0, ox, oy, oz, ex, ey, ez;
@@ -419,92 +401,100 @@ __device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, 
     }
 }
 
+// Operands of one pair of points (k, k + 4) of a thread: displacements and the epilogue's pointwise
+// operands.  They are loaded one pair ahead (pair 0 together with the box staging), so every global
+// load has a whole pair's interpolation (~300 instructions per warp) to land.
 template <typename T, class Epi>
-__device__ __forceinline__ void load_disp(const Grid& g, const Disp<T>& d, int x0, int y0, int z0, T (&dd)[SL_TZ][3],
-                                          typename Epi::Pre (&pre)[SL_TZ], const Epi& epi) {
-    const int x = x0 + (threadIdx.x % SL_TX), y = y0 + threadIdx.x / SL_TX;
-    const bool xyok = x < g.n1 && y < g.n2;
-    const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
-    const uint32_t id0 = ((uint32_t)z0 * g.n2 + y) * g.n1 + x;
+struct PairIn {
+    T dA[3], dB[3];
+    typename Epi::Late lA, lB;
+};
+
+template <typename T, class Epi>
+__device__ __forceinline__ void load_pair(const Disp<T>& d, const Epi& epi, uint32_t idA, uint32_t idB, bool okA,
+                                          bool okB, PairIn<T, Epi>& in) {
 #pragma unroll
-    for (int k = 0; k < SL_TZ; ++k) {
-        const bool ok = xyok && z0 + k < g.n3;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) dd[k][a] = ok ? __ldg(d.p[a] + id0 + k * plane) : T(0);
-        if (ok) pre[k] = epi.early(id0 + k * plane);
+    for (int a = 0; a < 3; ++a) {
+        in.dA[a] = okA ? __ldg(d.p[a] + idA) : T(0);
+        in.dB[a] = okB ? __ldg(d.p[a] + idB) : T(0);
     }
+    if (okA) in.lA = epi.late(idA);
+    if (okB) in.lB = epi.late(idB);
 }
 
+// Interpolate a pair from the staged box and finish both points.
 template <typename T, int NC, class Epi>
-__device__ __forceinline__ void compute_tile(const Grid& g, const Src<T, NC>& src, const Disp<T>& d,
-                                             const TileCtx<T, NC>& c, const T* __restrict__ box,
-                                             const T (&dd)[SL_TZ][3], const typename Epi::Pre (&pre)[SL_TZ],
-                                             const Epi& epi) {
+__device__ __forceinline__ void pair_from_box(const Grid& g, const TileCtx<T, NC>& c, const T* __restrict__ box,
+                                              int x, int y, int zA, uint32_t idA, uint32_t idB, bool okB,
+                                              const PairIn<T, Epi>& in, const Epi& epi) {
     constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
     constexpr int SC = BX * BY * BZ;
     constexpr int H = SL_TZ / 2;
+    int qA[3], qB[3];
+    T tA[3], tB[3];
+    const int ii[3] = {x, y, zA + g.z0};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        cell_of<T>(ii[a], in.dA[a], qA[a], tA[a]);
+        cell_of<T>(ii[a] + (a == 2 ? H : 0), in.dB[a], qB[a], tB[a]);
+        if (!okB) { qB[a] = qA[a]; tB[a] = tA[a]; }
+    }
+    const T* bA = box + ((qA[2] - 1 - c.oz) * BY + (qA[1] - 1 - c.oy)) * BX + (qA[0] - 1 - c.ox);
+    const T* bB = box + ((qB[2] - 1 - c.oz) * BY + (qB[1] - 1 - c.oy)) * BX + (qB[0] - 1 - c.ox);
+    T vA[NC], vB[NC];
+    if constexpr (sizeof(T) == 4) {
+        float2 w[3][4];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) lagrange4x2(make_float2(tA[a], tB[a]), w[a]);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+            const float2 r = interp_box2<BX, BY>(bA + cc * SC, bB + cc * SC, w[0], w[1], w[2]);
+            vA[cc] = r.x;
+            vB[cc] = r.y;
+        }
+    } else {
+        T w1[4], w2[4], w3[4];
+        lagrange4(tA[0], w1);
+        lagrange4(tA[1], w2);
+        lagrange4(tA[2], w3);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) vA[cc] = interp_box<T, BX, BY>(bA + cc * SC, w1, w2, w3);
+        if (okB) {
+            lagrange4(tB[0], w1);
+            lagrange4(tB[1], w2);
+            lagrange4(tB[2], w3);
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc) vB[cc] = interp_box<T, BX, BY>(bB + cc * SC, w1, w2, w3);
+        }
+    }
+    epi.store(idA, vA, in.lA);
+    if (okB) epi.store(idB, vB, in.lB);
+}
+
+// Fused gather + epilogue.  Grid: one CTA per 32 x 8 x 8 tile; thread = (x, y) column of 8 points,
+// processed as 4 pairs (k, k + 4).  Dynamic smem: box_bytes<T, NC>().
+// (A) stage the tile's box with 16-byte cp.async (periodic wrap per chunk in x1/x2; x3 wraps, or with
+// slabs indexes through the ghost planes); load pair 0's operands meanwhile; (B) wait + barrier;
+// (C) per pair: issue the next pair's loads, gather the 64 stencil values per point from shared memory
+// -- the two points as one packed fp32x2 pair (FFMA2) -- and finish the step.  Tiles whose box exceeds
+// the compile-time capacity gather from global memory instead (same arithmetic, one point at a time).
+template <typename T, int NC, class Epi>
+__global__ void __launch_bounds__(SL_THREADS, BoxGeom<T, NC>::MINB)
+    k_sl_gather(Grid g, Src<T, NC> src, Disp<T> d, const int* __restrict__ plan, int ntiles, Epi epi) {
+    constexpr int H = SL_TZ / 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* box = reinterpret_cast<T*>(smem_raw);
+    const int tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    const TileCtx<T, NC> c = tile_ctx<T, NC>(g, plan, tile);
+    stage_box<T, NC>(g, src, c, box);
     const int x = c.x0 + (threadIdx.x % SL_TX), y = c.y0 + threadIdx.x / SL_TX;
-    if (x >= g.n1 || y >= g.n2) return;
+    const bool xyok = x < g.n1 && y < g.n2;
     const int kmax = min(SL_TZ, g.n3 - c.z0);
     const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
     const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
-    if (c.fits) {
-        if constexpr (sizeof(T) == 4) {
-#pragma unroll
-            for (int p = 0; p < H; ++p) {
-                if (p >= kmax) break;
-                const bool okB = p + H < kmax;
-                const uint32_t idA = id0 + p * plane, idB = id0 + (p + H) * plane;
-                int qA[3], qB[3];
-                float tA[3], tB[3];
-                const int ii[3] = {x, y, c.z0 + p + g.z0};
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    cell_of<float>(ii[a], dd[p][a], qA[a], tA[a]);
-                    cell_of<float>(ii[a] + (a == 2 ? H : 0), dd[p + H][a], qB[a], tB[a]);
-                    if (!okB) { qB[a] = qA[a]; tB[a] = tA[a]; }
-                }
-                const typename Epi::Late lA = epi.late(idA);
-                typename Epi::Late lB;
-                if (okB) lB = epi.late(idB);
-                float2 w[3][4];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) lagrange4x2(make_float2(tA[a], tB[a]), w[a]);
-                const float* bA = box + ((qA[2] - 1 - c.oz) * BY + (qA[1] - 1 - c.oy)) * BX + (qA[0] - 1 - c.ox);
-                const float* bB = box + ((qB[2] - 1 - c.oz) * BY + (qB[1] - 1 - c.oy)) * BX + (qB[0] - 1 - c.ox);
-                float vA[NC], vB[NC];
-#pragma unroll
-                for (int cc = 0; cc < NC; ++cc) {
-                    const float2 r = interp_box2<BX, BY>(bA + cc * SC, bB + cc * SC, w[0], w[1], w[2]);
-                    vA[cc] = r.x;
-                    vB[cc] = r.y;
-                }
-                epi.store(idA, vA, pre[p], lA);
-                if (okB) epi.store(idB, vB, pre[p + H], lB);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < SL_TZ; ++k) {
-                if (k >= kmax) break;
-                const uint32_t id = id0 + k * plane;
-                const typename Epi::Late lt = epi.late(id);
-                int q1, q2, q3;
-                T t1, t2, t3;
-                cell_of<T>(x, dd[k][0], q1, t1);
-                cell_of<T>(y, dd[k][1], q2, t2);
-                cell_of<T>(c.z0 + k + g.z0, dd[k][2], q3, t3);
-                T w1[4], w2[4], w3[4];
-                lagrange4(t1, w1);
-                lagrange4(t2, w2);
-                lagrange4(t3, w3);
-                const T* b = box + ((q3 - 1 - c.oz) * BY + (q2 - 1 - c.oy)) * BX + (q1 - 1 - c.ox);
-                T val[NC];
-#pragma unroll
-                for (int cc = 0; cc < NC; ++cc) val[cc] = interp_box<T, BX, BY>(b + cc * SC, w1, w2, w3);
-                epi.store(id, val, pre[k], lt);
-            }
-        }
-    } else {  // re-reads its operands so that the register arrays stay statically indexed
+    if (!c.fits) {  // global-memory fallback (no barrier needed: nothing was staged)
+        if (!xyok) return;
 #pragma unroll 1
         for (int k = 0; k < kmax; ++k) {
             const uint32_t id = id0 + k * plane;
@@ -521,63 +511,24 @@ __device__ __forceinline__ void compute_tile(const Grid& g, const Src<T, NC>& sr
             T val[NC];
 #pragma unroll
             for (int cc = 0; cc < NC; ++cc) val[cc] = interp_global(src.p[cc], g, q1, q2, q3, w1, w2, w3);
-            epi.store(id, val, epi.early(id), lt);
+            epi.store(id, val, lt);
         }
+        return;
     }
-}
-
-template <typename T, int NC, class Epi>
-__global__ void __launch_bounds__(SL_THREADS, BoxGeom<T, NC>::MINB)
-    k_sl_gather(Grid g, Src<T, NC> src, Disp<T> d, const int* __restrict__ plan, int ntiles, Epi epi) {
-    constexpr int STAGES = BoxGeom<T, NC>::STAGES;
-    constexpr int SB = BoxGeom<T, NC>::BX * BoxGeom<T, NC>::BY * BoxGeom<T, NC>::BZ * NC;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* boxes = reinterpret_cast<T*>(smem_raw);
-    int tile = blockIdx.x;
-    if (tile >= ntiles) return;
-    T dd[SL_TZ][3];
-    typename Epi::Pre pre[SL_TZ];
-    TileCtx<T, NC> cur = tile_ctx<T, NC>(g, plan, tile);
-    if constexpr (STAGES == 2) {
-        stage_box<T, NC>(g, src, cur, boxes);
-        load_disp<T, Epi>(g, d, cur.x0, cur.y0, cur.z0, dd, pre, epi);
-        int buf = 0;
-        for (;;) {
-            const int next = tile + gridDim.x;
-            cp_async_wait_all();
-            __syncthreads();  // box[buf] complete; every thread is done with box[buf ^ 1]
-            T dn[SL_TZ][3];
-            typename Epi::Pre pn[SL_TZ];
-            TileCtx<T, NC> nc;
-            if (next < ntiles) {
-                nc = tile_ctx<T, NC>(g, plan, next);
-                stage_box<T, NC>(g, src, nc, boxes + (buf ^ 1) * SB);
-                load_disp<T, Epi>(g, d, nc.x0, nc.y0, nc.z0, dn, pn, epi);
-            }
-            compute_tile<T, NC, Epi>(g, src, d, cur, boxes + buf * SB, dd, pre, epi);
-            if (next >= ntiles) break;
-            tile = next;
-            cur = nc;
-            buf ^= 1;
+    PairIn<T, Epi> cur;
+    if (xyok) load_pair<T, Epi>(d, epi, id0, id0 + H * plane, 0 < kmax, H < kmax, cur);
+    cp_async_wait_all();
+    __syncthreads();
+    if (!xyok) return;
 #pragma unroll
-            for (int k = 0; k < SL_TZ; ++k) {
-                pre[k] = pn[k];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) dd[k][a] = dn[k][a];
-            }
-        }
-    } else {
-        for (;;) {
-            stage_box<T, NC>(g, src, cur, boxes);
-            load_disp<T, Epi>(g, d, cur.x0, cur.y0, cur.z0, dd, pre, epi);
-            cp_async_wait_all();
-            __syncthreads();
-            compute_tile<T, NC, Epi>(g, src, d, cur, boxes, dd, pre, epi);
-            tile += gridDim.x;
-            if (tile >= ntiles) break;
-            __syncthreads();  // everyone is done with the box before it is restaged
-            cur = tile_ctx<T, NC>(g, plan, tile);
-        }
+    for (int p = 0; p < H; ++p) {
+        if (p >= kmax) break;
+        PairIn<T, Epi> nxt;
+        if (p + 1 < H && p + 1 < kmax)
+            load_pair<T, Epi>(d, epi, id0 + (p + 1) * plane, id0 + (p + 1 + H) * plane, true, p + 1 + H < kmax, nxt);
+        pair_from_box<T, NC, Epi>(g, c, box, x, y, c.z0 + p, id0 + p * plane, id0 + (p + H) * plane, p + H < kmax,
+                                  cur, epi);
+        cur = nxt;
     }
 }
 
