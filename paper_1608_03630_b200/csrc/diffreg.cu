@@ -380,22 +380,17 @@ struct Impl {
         if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     }
 
-    // Launch of an FFT pass: DB = persistent double-buffered (as many CTAs as fit on the GPU at once),
-    // else one tile per CTA.
-    template <class PassT, bool DB = false>
+    // Launch of an FFT pass: one CTA per tile.
+    template <class PassT>
     void stream(const char* tag, const PassT& pass, int64_t ntiles) {
-        auto k = k_stream<PassT, DB>;
-        const size_t sm = (DB ? 2 : 1) * PassT::BUF;
-        static int occ = 0;  // per pass instantiation
-        if (occ == 0) {
-            set_smem(k, sm);
-            int o = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, PassT::NT, sm));
-            occ = o > 0 ? o : 1;
+        auto k = k_stream<PassT>;
+        static bool attr = false;  // per pass instantiation
+        if (!attr) {
+            set_smem(k, PassT::BUF);
+            attr = true;
         }
-        const int grid = DB ? (int)std::min<int64_t>(ntiles, (int64_t)occ * c.num_sms) : (int)ntiles;
         PB();
-        k<<<grid, PassT::NT, sm, s>>>(pass);
+        k<<<(unsigned)ntiles, PassT::NT, PassT::BUF, s>>>(pass);
         PE(tag);
     }
     template <int RB>

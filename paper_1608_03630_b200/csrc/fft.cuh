@@ -1,8 +1,10 @@
-// fft.cuh -- shared-memory Stockham FFT passes for the spectral operators (§III-B1,
-// L303 §III-C1).  Every pass streams a field once from HBM into shared memory (16/8-byte cp.async,
-// all of a CTA's loads in flight at once), transforms whole lines there (register butterflies of
-// radix 16 in fp32 / radix 8 in fp64, padded smem against bank conflicts, twiddles from tables built
-// in double precision on the host) and streams it back.
+// fft.cuh -- Stockham FFT passes for the spectral operators (§III-B1, L303 §III-C1).
+// Every pass streams a field once through the SM: the first radix-16 stage of a line reads its 16
+// operands straight from global memory into registers (coalesced: consecutive lanes read consecutive
+// addresses), the stages in between exchange through padded shared memory, and the last stage writes
+// its results straight to global memory in natural order -- one shared-memory round trip per stage
+// boundary instead of staging whole lines in and out.  Register butterflies of radix 16 with
+// constant-folded inner twiddles; stage twiddles from tables built in double precision on the host.
 //
 // Pass kinds
 //   row_deriv      real rows (x1) -> d/dx1 (r2c, i k'_1, c2r), one HBM read + one write
@@ -39,27 +41,14 @@ template <typename T, int NT>
 struct MinB {
     static constexpr int V = sizeof(T) == 8 ? ((384 / NT) > 0 ? 384 / NT : 1) : ((768 / NT) > 0 ? 768 / NT : 1);
 };
-// Row passes: RB rows per CTA of ~256 threads.  Ti = type of the staged input when it differs from
-// the compute type Tc (fp32 rows converted to fp64 in shared memory), else Ti = Tc.
-template <int L, typename Tc, typename Ti = Tc>
+// Row passes: RB rows per CTA.
+template <int L, typename Tc>
 struct RowCfg {
     static constexpr int TPL = Tpl<L, Tc>::V;
     static constexpr int RB = (CtaThreads<Tc>::V / TPL) > 0 ? CtaThreads<Tc>::V / TPL : 1;
     static constexpr int NT = RB * TPL;
-    static constexpr size_t SMEM = (size_t)RB * LineGeom<L>::LP *
-                                   (sizeof(Cx<Tc>) + (sizeof(Ti) != sizeof(Tc) ? sizeof(Cx<Ti>) : 0));
+    static constexpr size_t SMEM = (size_t)RB * LineGeom<L>::LP * sizeof(Cx<Tc>);
 };
-
-template <typename C>
-__device__ __forceinline__ void cp_async_elem(C* smem, const C* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    if constexpr (sizeof(C) == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_join() {
-    asm volatile("cp.async.wait_all;\n" ::);
-    __syncthreads();
-}
 
 // e^{DIR * 2 pi i m / 16}, m compile-time after unrolling
 template <typename T, int DIR>
@@ -102,20 +91,30 @@ struct DFT<T, 1, DIR> {
     static __device__ __forceinline__ void run(Cx<T>*) {}
 };
 
-// One Stockham autosort stage of radix R (Ns = product of the previous radices) on a line of
-// length L held in padded shared memory.  Each of the TPL threads of the line owns NB = L/R/TPL
-// butterflies.  tw: table of e^{-2 pi i m / (L*tws)}, m < L*tws.
-template <typename T, int L, int R, int Ns, int DIR, int TPL>
-__device__ __forceinline__ void stockham_stage(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws) {
+// ---------------------------------------------------------------------------------------------
+// Line accessors: element i (0 <= i < L) of the line a thread works on.
+template <typename T>
+struct SmemLine {
+    Cx<T>* b;
+    __device__ __forceinline__ Cx<T> ld(int i) const { return b[P(i)]; }
+    __device__ __forceinline__ void st(int i, const Cx<T>& v) const { b[P(i)] = v; }
+};
+
+// One Stockham autosort stage of radix R (Ns = product of the previous radices) on a line of length L.
+// Each of the TPL threads of the line owns NB = L/R/TPL butterflies; operands come from src.ld, results
+// go to dst.st (shared memory or global).  SYNC: the stage is in place in shared memory, so all reads
+// must finish (barrier) before the writes.  tw: table of e^{-2 pi i m / (L*tws)}, m < L*tws.
+template <typename T, int L, int R, int Ns, int DIR, int TPL, bool SYNC, class Src, class Dst>
+__device__ __forceinline__ void stage_io(int t, const Cx<T>* __restrict__ tw, int tws, const Src& src, const Dst& dst) {
     constexpr int NB = (L / R) / TPL;
     Cx<T> x[NB][R];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         const int j = t + b * TPL;
 #pragma unroll
-        for (int r = 0; r < R; ++r) x[b][r] = buf[P(j + r * (L / R))];
+        for (int r = 0; r < R; ++r) x[b][r] = src.ld(j + r * (L / R));
     }
-    __syncthreads();
+    if (SYNC) __syncthreads();
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         const int j = t + b * TPL;
@@ -132,111 +131,93 @@ __device__ __forceinline__ void stockham_stage(Cx<T>* buf, int t, const Cx<T>* _
         DFT<T, R, DIR>::run(x[b]);
         const int base = (j - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[P(base + r * Ns)] = x[b][r];
+        for (int r = 0; r < R; ++r) dst.st(base + r * Ns, x[b][r]);
     }
-    __syncthreads();
 }
 
-template <typename T, int L, int DIR, int TPL, int R, int Ns>
-__device__ __forceinline__ void fft_stages(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws) {
-    if constexpr (Ns * R >= L) {
-        stockham_stage<T, L, L / Ns, Ns, DIR, TPL>(buf, t, tw, tws);
+// stages Ns, Ns*16, ... of a line whose data sit in shared memory `buf`; the last stage writes to dst
+template <typename T, int L, int DIR, int TPL, int Ns, bool DST_SMEM, class Dst>
+__device__ __forceinline__ void stages_rest(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws, const Dst& dst) {
+    if constexpr (Ns * 16 >= L) {
+        stage_io<T, L, L / Ns, Ns, DIR, TPL, DST_SMEM>(t, tw, tws, SmemLine<T>{buf}, dst);
+        if (DST_SMEM) __syncthreads();
     } else {
-        stockham_stage<T, L, R, Ns, DIR, TPL>(buf, t, tw, tws);
-        fft_stages<T, L, DIR, TPL, R, Ns * R>(buf, t, tw, tws);
+        stage_io<T, L, 16, Ns, DIR, TPL, true>(t, tw, tws, SmemLine<T>{buf}, SmemLine<T>{buf});
+        __syncthreads();
+        stages_rest<T, L, DIR, TPL, Ns * 16, DST_SMEM>(buf, t, tw, tws, dst);
     }
 }
 
-// Whole-line FFT (in place, padded layout), radix plan R x R x ... x r with R = 16 (fp32) / 8 (fp64).
-// Every thread of the CTA must call this (it contains __syncthreads).
+// Whole-line FFT, radix plan 16 x 16 x ... x r: src -> [shared line buf] -> dst.  SRC_SMEM / DST_SMEM:
+// the source / destination is `buf` itself (in place).  Every thread of the CTA must call this (it
+// contains __syncthreads); on return with DST_SMEM the results are visible to the whole CTA.
+template <typename T, int L, int DIR, bool SRC_SMEM, bool DST_SMEM, class Src, class Dst>
+__device__ __forceinline__ void fft_line_io(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws, const Src& src,
+                                            const Dst& dst) {
+    constexpr int TPL = Tpl<L, T>::V;
+    if constexpr (L <= 16) {
+        stage_io<T, L, L, 1, DIR, TPL, SRC_SMEM && DST_SMEM>(t, tw, tws, src, dst);
+        if (DST_SMEM) __syncthreads();
+    } else {
+        stage_io<T, L, 16, 1, DIR, TPL, SRC_SMEM>(t, tw, tws, src, SmemLine<T>{buf});
+        __syncthreads();
+        stages_rest<T, L, DIR, TPL, 16, DST_SMEM>(buf, t, tw, tws, dst);
+    }
+}
+
+// in-place line FFT in shared memory
 template <typename T, int L, int DIR>
 __device__ __forceinline__ void fft_line(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws) {
-    fft_stages<T, L, DIR, Tpl<L, T>::V, Tpl<L, T>::R, 1>(buf, t, tw, tws);
+    fft_line_io<T, L, DIR, true, true>(buf, t, tw, tws, SmemLine<T>{buf}, SmemLine<T>{buf});
 }
 
 // ---------------------------------------------------------------------------------------------
 // real <-> half-complex post/pre-processing of a row of N = 2L reals packed as L complex
 // z_n = x_{2n} + i x_{2n+1}.  After the forward L-point FFT Z, X_k (k = 0..L) of the N-point DFT:
 //   E = (Z_k + conj Z_{L-k})/2, O = (Z_k - conj Z_{L-k})/(2i), X_k = E + W^k O, X_{L-k} = conj(E - W^k O),
-// W = e^{-2 pi i/N}.  Pairs (k, L-k) are handled by one thread, so the update is in place.
-template <typename T, int L, int TPL>
-__device__ __forceinline__ void r2c_post(Cx<T>* buf, int t, const Cx<T>* __restrict__ twN) {
-    for (int k = t; k <= L / 2; k += TPL) {
-        const Cx<T> zk = buf[P(k)];
-        const Cx<T> zl = buf[P(k == 0 ? 0 : L - k)];
-        const Cx<T> E = cx((zk.re + zl.re) * T(0.5), (zk.im - zl.im) * T(0.5));
-        // (Z_k - conj Z_{L-k}) / (2i) = (a + ib)/(2i) = (b - ia)/2 with a + ib = Z_k - conj Z_{L-k}
-        const T a = zk.re - zl.re, b = zk.im + zl.im;
-        const Cx<T> O = cx(b * T(0.5), -a * T(0.5));
-        const Cx<T> WO = cmul(twN[k], O);
-        const Cx<T> Xk = E + WO;
-        const Cx<T> Xl = conj(E - WO);
-        buf[P(k)] = Xk;
-        buf[P(L - k)] = Xl;  // k = 0 writes X_L into slot L; k = L/2 writes the same slot twice
-    }
-    __syncthreads();
-}
-
-// inverse: given X_0..X_L, Z_k = E + i O with E = (X_k + conj X_{L-k})/2,
+// W = e^{-2 pi i/N}.  Inverse: Z_k = E + i O with E = (X_k + conj X_{L-k})/2,
 // O = (X_k - conj X_{L-k}) conj(W^k)/2, and Z_{L-k} = conj(E) + i conj(O).
-template <typename T, int L, int TPL>
-__device__ __forceinline__ void c2r_pre(Cx<T>* buf, int t, const Cx<T>* __restrict__ twN) {
-    for (int k = t; k <= L / 2; k += TPL) {
-        const Cx<T> xk = buf[P(k)];
-        const Cx<T> xl = buf[P(L - k)];
-        const Cx<T> E = cx((xk.re + xl.re) * T(0.5), (xk.im - xl.im) * T(0.5));
-        const Cx<T> D = cx((xk.re - xl.re) * T(0.5), (xk.im + xl.im) * T(0.5));
-        const Cx<T> O = cmul(D, conj(twN[k]));
-        buf[P(k)] = cx(E.re - O.im, E.im + O.re);            // E + iO
-        if (k != 0 && 2 * k != L) buf[P(L - k)] = cx(E.re + O.im, -E.im + O.re);  // conj(E) + i conj(O)
-    }
-    __syncthreads();
+template <typename T>
+__device__ __forceinline__ void r2c_pair(Cx<T> zk, Cx<T> zl, Cx<T> w, Cx<T>& Xk, Cx<T>& Xl) {
+    const Cx<T> E = cx((zk.re + zl.re) * T(0.5), (zk.im - zl.im) * T(0.5));
+    const T a = zk.re - zl.re, b = zk.im + zl.im;  // (Z_k - conj Z_{L-k}) / (2i) = (b - ia)/2
+    const Cx<T> O = cx(b * T(0.5), -a * T(0.5));
+    const Cx<T> WO = cmul(w, O);
+    Xk = E + WO;
+    Xl = conj(E - WO);
+}
+template <typename T>
+__device__ __forceinline__ void c2r_pair(Cx<T> xk, Cx<T> xl, Cx<T> w, Cx<T>& Zk, Cx<T>& Zl) {
+    const Cx<T> E = cx((xk.re + xl.re) * T(0.5), (xk.im - xl.im) * T(0.5));
+    const Cx<T> D = cx((xk.re - xl.re) * T(0.5), (xk.im + xl.im) * T(0.5));
+    const Cx<T> O = cmul(D, conj(w));
+    Zk = cx(E.re - O.im, E.im + O.re);   // E + iO
+    Zl = cx(E.re + O.im, -E.im + O.re);  // conj(E) + i conj(O)
 }
 
-// Stage RB contiguous rows of L complex values (row r of the CTA at src + r L) into padded lines
-// sm + r LP, asynchronously, one complex value (8 or 16 bytes) per cp.async.
-template <typename C, int L, int NT>
-__device__ __forceinline__ void row_stage(C* sm, const C* __restrict__ src, int nvalid) {
-    constexpr int LP = LineGeom<L>::LP;
-    for (int e = threadIdx.x; e < nvalid * L; e += NT) cp_async_elem(sm + (e / L) * LP + P(e % L), src + e);
-}
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-
-// Driver shared by every FFT pass.  DB = true: persistent, a CTA walks tiles blockIdx.x, + gridDim.x,
-// ... with two shared-memory buffers (the next tile's cp.async loads fly while the current tile is
-// transformed and stored); DB = false: one tile per CTA, the hardware overlaps resident CTAs.
-// PassT supplies NT, MINB, BUF (bytes per buffer), ntiles(), load(tile, smem), run(tile, smem).
-template <class PassT, bool DB>
-__global__ void __launch_bounds__(PassT::NT, PassT::MINB) k_stream(PassT pass) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    int tile = blockIdx.x;
-    const int ntiles = pass.ntiles();
-    if (tile >= ntiles) return;
-    if constexpr (!DB) {  // one tile per CTA: load, transform, store
-        pass.load(tile, smem_raw);
-        cp_async_join();
-        pass.run(tile, smem_raw);
-        return;
+// Row accessors (row = contiguous line of L complex values)
+template <typename Ti, typename Tc>
+struct RowLd {  // reads type Ti, widens to Tc
+    const Cx<Ti>* p;
+    __device__ __forceinline__ Cx<Tc> ld(int i) const {
+        const Cx<Ti> v = p[i];
+        return cx<Tc>((Tc)v.re, (Tc)v.im);
     }
-    pass.load(tile, smem_raw);
-    cp_async_commit();
-    int cur = 0;
-    for (;;) {
-        const int next = tile + gridDim.x;
-        const bool more = next < ntiles;
-        if (more) pass.load(next, smem_raw + (cur ^ 1) * PassT::BUF);
-        cp_async_commit();
-        cp_async_wait1();  // everything but the newest group has landed: the current tile is in smem
-        __syncthreads();
-        pass.run(tile, smem_raw + cur * PassT::BUF);
-        if (!more) break;
-        __syncthreads();  // the current buffer is refilled by the next iteration's prefetch
-        tile = next;
-        cur ^= 1;
+};
+template <typename T>
+struct RowSt {  // out = v (+ add) (+ out when acc); nothing when !on
+    Cx<T>* p;
+    const Cx<T>* add;
+    int acc;
+    bool on;
+    __device__ __forceinline__ void st(int i, const Cx<T>& v) const {
+        if (!on) return;
+        Cx<T> r = v;
+        if (add) r = r + add[i];
+        if (acc) r = r + p[i];
+        p[i] = r;
     }
-}
+};
 
 // Row pass: x1-derivative of real rows ("N2 N3 1D FFTs across the first coordinate,
 // diagonal scaling, and then the same number of inverse FFTs").  out = acc*out + d f/dx1.
@@ -245,151 +226,122 @@ struct RowDerivPass {
     using RC = RowCfg<L, T>;
     static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
-    static constexpr size_t BUF = (size_t)RB * LP * sizeof(Cx<T>);
+    static constexpr size_t BUF = RC::SMEM;
     Grid g;
     const T* f;
     T* out;
     int accumulate;
     const Cx<T>* twN;
-    __device__ __forceinline__ int ntiles() const { return (int)(((int64_t)g.n2 * g.n3 + RB - 1) / RB); }
-    __device__ __forceinline__ int nvalid(int tile) const {
-        const int64_t rem = (int64_t)g.n2 * g.n3 - (int64_t)tile * RB;
-        return (int)(rem < RB ? rem : RB);
-    }
-    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
-        row_stage<Cx<T>, L, NT>(reinterpret_cast<Cx<T>*>(smem), reinterpret_cast<const Cx<T>*>(f) + (int64_t)tile * RB * L,
-                                nvalid(tile));
-    }
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
-        const int nv = nvalid(tile);
+        const int64_t nrows = (int64_t)g.n2 * g.n3;
         const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows;
+        if (!ok) row = nrows - 1;  // duplicate work on the last row, never stored
         Cx<T>* buf = sm + line * LP;
-        fft_line<T, L, -1>(buf, t, twN, 2);
-        r2c_post<T, L, TPL>(buf, t, twN);
-        // X_k *= i k'_1 / L  (k = 0..L; Nyquist k = L is zeroed, reading A2; 1/L normalises the c2r)
-        for (int k = t; k <= L; k += TPL) {
-            const T kk = (k == L) ? T(0) : T(k);
-            buf[P(k)] = mul_i(buf[P(k)], kk / T(L));
+        const Cx<T>* src = reinterpret_cast<const Cx<T>*>(f) + row * L;
+        fft_line_io<T, L, -1, false, true>(buf, t, twN, 2, RowLd<T, T>{src}, SmemLine<T>{buf});
+        // post-process pairs (k, L-k), multiply by i k'_1 / L (Nyquist k = L zeroed, reading A2; 1/L
+        // normalises the c2r), pre-process back -- all on the same pair, in place
+        for (int k = t; k <= L / 2; k += TPL) {
+            const int l = (k == 0) ? 0 : L - k;
+            Cx<T> Xk, Xl;
+            r2c_pair(buf[P(k)], buf[P(l)], twN[k], Xk, Xl);
+            // k = 0: Xl is X_L (Nyquist, zeroed); X_0 gets k' = 0
+            Xk = mul_i(Xk, T(k) / T(L));
+            Xl = (k == 0) ? cx(T(0), T(0)) : mul_i(Xl, T(L - k) / T(L));
+            if (k == L / 2 && L > 1) Xl = Xk;  // the same slot (L - k = k)
+            Cx<T> Zk, Zl;
+            c2r_pair(Xk, (k == 0) ? cx(T(0), T(0)) : Xl, twN[k], Zk, Zl);
+            buf[P(k)] = Zk;
+            if (k != 0 && 2 * k != L) buf[P(L - k)] = Zl;
         }
         __syncthreads();
-        c2r_pre<T, L, TPL>(buf, t, twN);
-        fft_line<T, L, +1>(buf, t, twN, 2);
-        Cx<T>* dst = reinterpret_cast<Cx<T>*>(out) + (int64_t)tile * RB * L;
-        for (int e = threadIdx.x; e < nv * L; e += NT) {
-            Cx<T> v = sm[(e / L) * LP + P(e % L)];
-            if (accumulate) { const Cx<T> o = dst[e]; v = v + o; }
-            dst[e] = v;
-        }
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(out) + row * L;
+        fft_line_io<T, L, +1, true, false>(buf, t, twN, 2, SmemLine<T>{buf}, RowSt<T>{dst, nullptr, accumulate, ok});
     }
 };
 
 // Row pass: real rows (type Ti) -> half-spectrum rows (r2c along x1) computed and stored in Tc,
 // spectrum row stride g.n1p.  Ti = float, Tc = double keeps the forward spectrum exact enough for the
 // high-wavenumber amplification of beta*A.
-// The fp32 rows are staged asynchronously into their own buffer and widened in shared memory.
 template <typename Ti, typename Tc, int L>
 struct RowR2cPass {
-    using RC = RowCfg<L, Tc, Ti>;
+    using RC = RowCfg<L, Tc>;
     static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
     static constexpr int MINB = MinB<Tc, NT>::V;
     static constexpr size_t BUF = RC::SMEM;
-    static constexpr size_t STG = (size_t)RB * LP * sizeof(Cx<Tc>);  // offset of the Ti staging lines
     Grid g;
     const Ti* f;
     Cx<Tc>* spec;
     const Cx<Tc>* twN;
-    __device__ __forceinline__ int ntiles() const { return (int)(((int64_t)g.n2 * g.n3 + RB - 1) / RB); }
-    __device__ __forceinline__ int nvalid(int tile) const {
-        const int64_t rem = (int64_t)g.n2 * g.n3 - (int64_t)tile * RB;
-        return (int)(rem < RB ? rem : RB);
-    }
-    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
-        const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f) + (int64_t)tile * RB * L;
-        if constexpr (sizeof(Ti) == sizeof(Tc)) row_stage<Cx<Tc>, L, NT>(reinterpret_cast<Cx<Tc>*>(smem), reinterpret_cast<const Cx<Tc>*>(src), nvalid(tile));
-        else row_stage<Cx<Ti>, L, NT>(reinterpret_cast<Cx<Ti>*>(smem + STG), src, nvalid(tile));
-    }
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<Tc>* sm = reinterpret_cast<Cx<Tc>*>(smem);
-        const int nv = nvalid(tile);
-        if constexpr (sizeof(Ti) != sizeof(Tc)) {
-            const Cx<Ti>* st = reinterpret_cast<const Cx<Ti>*>(smem + STG);
-            for (int e = threadIdx.x; e < nv * L; e += NT) {
-                const int o = (e / L) * LP + P(e % L);
-                const Cx<Ti> v = st[o];
-                sm[o] = cx<Tc>((Tc)v.re, (Tc)v.im);
-            }
-            __syncthreads();
-        }
+        const int64_t nrows = (int64_t)g.n2 * g.n3;
         const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows;
+        if (!ok) row = nrows - 1;
         Cx<Tc>* buf = sm + line * LP;
-        fft_line<Tc, L, -1>(buf, t, twN, 2);
-        r2c_post<Tc, L, TPL>(buf, t, twN);
-        constexpr int NC = L + 1;
-        const int64_t row0 = (int64_t)tile * RB;
-        for (int e = threadIdx.x; e < nv * NC; e += NT) {
-            const int r = e / NC, k = e % NC;
-            spec[(row0 + r) * g.n1p + k] = sm[r * LP + P(k)];
+        const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f) + row * L;
+        fft_line_io<Tc, L, -1, false, true>(buf, t, twN, 2, RowLd<Ti, Tc>{src}, SmemLine<Tc>{buf});
+        if (!ok) return;
+        Cx<Tc>* out = spec + row * g.n1p;
+        for (int k = t; k <= L / 2; k += TPL) {
+            Cx<Tc> Xk, Xl;
+            r2c_pair(buf[P(k)], buf[P(k == 0 ? 0 : L - k)], twN[k], Xk, Xl);
+            out[k] = Xk;
+            out[L - k] = Xl;  // k = 0 writes X_L; k = L/2 writes the same value twice
         }
     }
 };
 
-// Row pass epilogue for the c2r inverse: out = x (+ add)
+// Row pass: half-spectrum rows -> real rows (c2r along x1) in T with epilogue out = x + add.
+// The spectrum already carries the full inverse normalisation.
 template <typename T>
 struct RowOut {
     T* out;
     const T* add;  // nullable: field added after the inverse (b~ in the non-isochoric matvec)
 };
 
-// Row pass: half-spectrum rows -> real rows (c2r along x1) in T with epilogue out = x + add.
-// The spectrum already carries the full inverse normalisation.
 template <typename T, int L>
 struct RowC2rPass {
     using RC = RowCfg<L, T>;
     static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
-    static constexpr size_t BUF = (size_t)RB * LP * sizeof(Cx<T>);
+    static constexpr size_t BUF = RC::SMEM;
     Grid g;
     const Cx<T>* spec;
     RowOut<T> epi;
     const Cx<T>* twN;
-    __device__ __forceinline__ int ntiles() const { return (int)(((int64_t)g.n2 * g.n3 + RB - 1) / RB); }
-    __device__ __forceinline__ int nvalid(int tile) const {
-        const int64_t rem = (int64_t)g.n2 * g.n3 - (int64_t)tile * RB;
-        return (int)(rem < RB ? rem : RB);
-    }
-    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
-        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
-        constexpr int NC = L + 1;
-        const int64_t row0 = (int64_t)tile * RB;
-        const int nv = nvalid(tile);
-        for (int e = threadIdx.x; e < nv * NC; e += NT) {
-            const int r = e / NC, k = e % NC;
-            cp_async_elem(sm + r * LP + P(k), spec + (row0 + r) * g.n1p + k);
-        }
-    }
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
-        const int nv = nvalid(tile);
+        const int64_t nrows = (int64_t)g.n2 * g.n3;
         const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows;
+        if (!ok) row = nrows - 1;
         Cx<T>* buf = sm + line * LP;
-        c2r_pre<T, L, TPL>(buf, t, twN);
-        fft_line<T, L, +1>(buf, t, twN, 2);
-        const int64_t row0 = (int64_t)tile * RB;
-        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out) + row0 * L;
-        const Cx<T>* add = epi.add ? reinterpret_cast<const Cx<T>*>(epi.add) + row0 * L : nullptr;
-        for (int e = threadIdx.x; e < nv * L; e += NT) {
-            Cx<T> v = sm[(e / L) * LP + P(e % L)];
-            if (add) v = v + add[e];
-            dst[e] = v;
+        const Cx<T>* in = spec + row * g.n1p;
+        for (int k = t; k <= L / 2; k += TPL) {
+            Cx<T> Zk, Zl;
+            c2r_pair(in[k], in[L - k], twN[k], Zk, Zl);
+            buf[P(k)] = Zk;
+            if (k != 0 && 2 * k != L) buf[P(L - k)] = Zl;
         }
+        __syncthreads();
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out) + row * L;
+        const Cx<T>* add = epi.add ? reinterpret_cast<const Cx<T>*>(epi.add) + row * L : nullptr;
+        fft_line_io<T, L, +1, true, false>(buf, t, twN, 2, SmemLine<T>{buf}, RowSt<T>{dst, add, 0, ok});
     }
 };
 
 // ---------------------------------------------------------------------------------------------
 // Column passes along x2 (AX = 2) or x3 (AX = 3) of a complex array with W complex columns per row
 // (W = n1p for spectra, N1/2 for a real field read as pairs) and extents (W, n2, n3).
-// A CTA owns XC consecutive columns x OL lines of the other transverse axis.
+// A CTA owns XC consecutive columns x OL lines of the other transverse axis; consecutive lanes own
+// consecutive columns, so every global access of a stage is a full 128-byte segment.
 struct ColGeom {
     int W;      // row stride in complex elements
     int nx;     // valid columns (x < nx)
@@ -409,9 +361,58 @@ __device__ __forceinline__ int64_t col_addr(const ColGeom& c, int x, int other, 
     return ((int64_t)p * c.n2 + other) * c.W + x;      // other = i2, p = i3
 }
 
+// Element p of one line of a column array: address base + (p >> sh) * hi + (p & mk) * lo, which covers
+// the plain layouts (sh = 30: one block) and the split layout (blocks of nb = 2^sh lines).
+// Out-of-range lines (on = false) read 0 and store nothing.
+template <typename T>
+struct ColAcc {
+    Cx<T>* b;
+    int64_t hi;
+    int lo, sh, mk;
+    bool on;
+    int acc;
+    __device__ __forceinline__ int64_t at(int p) const { return (int64_t)(p >> sh) * hi + (int64_t)(p & mk) * lo; }
+    __device__ __forceinline__ Cx<T> ld(int p) const { return on ? b[at(p)] : cx(T(0), T(0)); }
+    __device__ __forceinline__ void st(int p, const Cx<T>& v) const {
+        if (!on) return;
+        Cx<T>* q = b + at(p);
+        *q = acc ? v + *q : v;
+    }
+};
+
+template <int AX, typename T>
+__device__ __forceinline__ ColAcc<T> col_acc(Cx<T>* a, const ColGeom& c, int x, int o, int nb, bool on, int acc) {
+    ColAcc<T> r;
+    r.on = on;
+    r.acc = acc;
+    r.sh = 30;
+    r.mk = 0x3fffffff;
+    r.hi = 0;
+    if (!on) {
+        x = 0;
+        o = 0;
+    }
+    if (AX == 2) {
+        r.lo = c.W;
+        if (nb) {
+            int l = 0;
+            while ((1 << l) < nb) ++l;
+            r.sh = l;
+            r.mk = nb - 1;
+            r.hi = (int64_t)c.n3 * nb * c.W;
+            r.b = a + ((int64_t)o * nb) * c.W + x;
+        } else {
+            r.b = a + ((int64_t)o * c.n2) * c.W + x;
+        }
+    } else {
+        r.lo = c.n2 * c.W;
+        r.b = a + (int64_t)o * c.W + x;
+    }
+    return r;
+}
+
 // CTA shape of a column pass: XC columns (one 128-byte segment: 16 complex64 / 8 complex128) x OL
-// transverse lines, TPL threads per line, ~256 threads, capped so NC components of the CTA's lines
-// fit in ~96 KB of shared memory.
+// transverse lines, TPL threads per line, capped so NC components of the CTA's lines fit in ~96 KB.
 template <int L, typename T, int NC = 1>
 struct ColCfg {
     static constexpr int ES = (int)sizeof(Cx<T>);
@@ -428,34 +429,20 @@ struct ColCfg {
     static constexpr size_t SMEM = (size_t)NC * LINES * LineGeom<L>::LP * ES;
 };
 
-template <typename T, int L, int XC, int OL, int AX, int NT>
-__device__ __forceinline__ void col_load(Cx<T>* sm, const Cx<T>* __restrict__ src, const ColGeom& c, int x0, int o0,
-                                         int nother, int nb = 0) {
-    constexpr int LP = LineGeom<L>::LP;
-    for (int e = threadIdx.x; e < XC * L * OL; e += NT) {
-        const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
-        const int x = x0 + xi, o = o0 + oi;
-        Cx<T>* d = sm + (oi * XC + xi) * LP + P(p);
-        if (x < c.nx && o < nother) cp_async_elem(d, src + col_addr<AX>(c, x, o, p, nb));
-        else *d = cx(T(0), T(0));
-    }
+// thread -> (column xi, thread-in-line t, transverse line oi); line index oi * XC + xi
+template <int XC, int TPL>
+__device__ __forceinline__ void col_thread(int& xi, int& t, int& oi) {
+    xi = threadIdx.x % XC;
+    const int r = threadIdx.x / XC;
+    t = r % TPL;
+    oi = r / TPL;
 }
 
-template <typename T, int L, int XC, int OL, int AX, bool ACC, int NT, typename To = T>
-__device__ __forceinline__ void col_store(const Cx<T>* sm, Cx<To>* __restrict__ dst, const ColGeom& c, int x0, int o0,
-                                          int nother, int nb = 0) {
-    constexpr int LP = LineGeom<L>::LP;
-    for (int e = threadIdx.x; e < XC * L * OL; e += NT) {
-        const int xi = e % XC, p = (e / XC) % L, oi = e / (XC * L);
-        const int x = x0 + xi, o = o0 + oi;
-        if (x < c.nx && o < nother) {
-            const Cx<T> w = sm[(oi * XC + xi) * LP + P(p)];
-            Cx<To> v = cx<To>((To)w.re, (To)w.im);
-            const int64_t a = col_addr<AX>(c, x, o, p, nb);
-            if (ACC) v = v + dst[a];
-            dst[a] = v;
-        }
-    }
+template <int XC, int OL>
+__device__ __forceinline__ void col_origin(const ColGeom& c, int tile, int& x0, int& o0) {
+    const int nxb = (c.nx + XC - 1) / XC;
+    x0 = (tile % nxb) * XC;
+    o0 = (tile / nxb) * OL;
 }
 
 // Derivative along x2 / x3 of a real field (viewed as complex pairs): out (+)= d f / dx_AX.
@@ -470,39 +457,29 @@ struct ColDerivPass {
     Cx<T>* dst;
     int accumulate;
     const Cx<T>* tw;
-    __device__ __forceinline__ int nother() const { return (AX == 2) ? c.n3 : c.n2; }
-    __device__ __forceinline__ int ntiles() const { return ((c.nx + XC - 1) / XC) * ((nother() + OL - 1) / OL); }
-    __device__ __forceinline__ void origin(int tile, int& x0, int& o0) const {
-        const int nxb = (c.nx + XC - 1) / XC;
-        x0 = (tile % nxb) * XC;
-        o0 = (tile / nxb) * OL;
-    }
-    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
-        int x0, o0;
-        origin(tile, x0, o0);
-        col_load<T, L, XC, OL, AX, NT>(reinterpret_cast<Cx<T>*>(smem), src, c, x0, o0, nother());
-    }
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
-        int x0, o0;
-        origin(tile, x0, o0);
-        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-        Cx<T>* buf = sm + line * LP;
-        fft_line<T, L, -1>(buf, t, tw, 1);
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int x = x0 + xi, o = o0 + oi, nother = (AX == 2) ? c.n3 : c.n2;
+        const bool on = x < c.nx && o < nother;
+        Cx<T>* buf = sm + (oi * XC + xi) * LP;
+        fft_line_io<T, L, -1, false, true>(buf, t, tw, 1, col_acc<AX>(const_cast<Cx<T>*>(src), c, x, o, 0, on, 0),
+                                           SmemLine<T>{buf});
         for (int k = t; k < L; k += TPL) {
             const T kp = (T)wavenum_odd(k, L);
             buf[P(k)] = mul_i(buf[P(k)], kp / T(L));
         }
         __syncthreads();
-        fft_line<T, L, +1>(buf, t, tw, 1);
-        if (accumulate) col_store<T, L, XC, OL, AX, true, NT>(sm, dst, c, x0, o0, nother());
-        else col_store<T, L, XC, OL, AX, false, NT>(sm, dst, c, x0, o0, nother());
+        fft_line_io<T, L, +1, true, false>(buf, t, tw, 1, SmemLine<T>{buf}, col_acc<AX>(dst, c, x, o, 0, on, accumulate));
     }
 };
 
 // Complex FFT of spectrum columns along x2 (forward DIR=-1 or inverse DIR=+1), src -> dst (may alias
-// when both layouts are plain).  nb_in / nb_out != 0 select the split layout on that side (the
-// all-to-all chunks of the multi-GPU transposes), fusing the pack / unpack into this pass.
+// when both layouts are plain: every element is read by its own CTA before that CTA writes it).
+// nb_in / nb_out != 0 select the split layout on that side (the all-to-all chunks of the multi-GPU
+// transposes), fusing the pack / unpack into this pass.
 template <typename T, int L, int DIR>
 struct ColFftPass {
     using CC = ColCfg<L, T>;
@@ -514,24 +491,16 @@ struct ColFftPass {
     Cx<T>* dst;
     const Cx<T>* tw;
     int nb_in, nb_out;
-    __device__ __forceinline__ int ntiles() const { return ((c.nx + XC - 1) / XC) * ((c.n3 + OL - 1) / OL); }
-    __device__ __forceinline__ void origin(int tile, int& x0, int& o0) const {
-        const int nxb = (c.nx + XC - 1) / XC;
-        x0 = (tile % nxb) * XC;
-        o0 = (tile / nxb) * OL;
-    }
-    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
-        int x0, o0;
-        origin(tile, x0, o0);
-        col_load<T, L, XC, OL, 2, NT>(reinterpret_cast<Cx<T>*>(smem), src, c, x0, o0, c.n3, nb_in);
-    }
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
-        int x0, o0;
-        origin(tile, x0, o0);
-        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
-        fft_line<T, L, DIR>(sm + line * LP, t, tw, 1);
-        col_store<T, L, XC, OL, 2, false, NT>(sm, dst, c, x0, o0, c.n3, nb_out);
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int x = x0 + xi, o = o0 + oi;
+        const bool on = x < c.nx && o < c.n3;
+        Cx<T>* buf = sm + (oi * XC + xi) * LP;
+        fft_line_io<T, L, DIR, false, false>(buf, t, tw, 1, col_acc<2>(const_cast<Cx<T>*>(src), c, x, o, nb_in, on, 0),
+                                             col_acc<2>(dst, c, x, o, nb_out, on, 0));
     }
 };
 
@@ -617,33 +586,26 @@ struct MiddlePass {
     SymInfo s;
     const Cx<Ti>* tw;
     const Cx<To>* two;  // inverse twiddles in To
-    __device__ __forceinline__ int ntiles() const { return ((c.nx + XC - 1) / XC) * ((c.n2 + OL - 1) / OL); }
-    __device__ __forceinline__ void origin(int tile, int& x0, int& o0) const {
-        const int nxb = (c.nx + XC - 1) / XC;
-        x0 = (tile % nxb) * XC;
-        o0 = (tile / nxb) * OL;
-    }
-    __device__ __forceinline__ void load(int tile, unsigned char* smem) const {
-        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
-        int x0, o0;
-        origin(tile, x0, o0);
-#pragma unroll
-        for (int ci = 0; ci < NCI; ++ci) col_load<T, L, XC, OL, 3, NT>(sm + ci * LINES * LP, in.p[ci], c, x0, o0, c.n2);
-    }
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
         Cx<To>* so = reinterpret_cast<Cx<To>*>(smem + BUFI);
-        int x0, o0;
-        origin(tile, x0, o0);
-        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int line = oi * XC + xi;
+        const bool on = x0 + xi < c.nx && o0 + oi < c.n2;
 #pragma unroll
-        for (int ci = 0; ci < NCI; ++ci) fft_line<T, L, -1>(sm + ci * LINES * LP + line * LP, t, tw, 1);
+        for (int ci = 0; ci < NCI; ++ci) {
+            Cx<T>* buf = sm + ci * LINES * LP + line * LP;
+            fft_line_io<T, L, -1, false, true>(buf, t, tw, 1, col_acc<3>(in.p[ci], c, x0 + xi, o0 + oi, 0, on, 0),
+                                               SmemLine<T>{buf});
+        }
         // symbol: element (line, p): k1 = column index x (0..N1/2), k2 from the transverse index, k3 from p
         const int n1 = 2 * (c.nx - 1);
         for (int e = threadIdx.x; e < LINES * L; e += NT) {
             const int ln = e / L, p = e % L;
-            const int xi = ln % XC, oi = ln / XC;
-            const int x = x0 + xi, o = o0 + oi;
+            const int lxi = ln % XC, loi = ln / XC;
+            const int x = x0 + lxi, o = o0 + loi;
             Cx<T> v[NCI];
 #pragma unroll
             for (int ci = 0; ci < NCI; ++ci) v[ci] = sm[ci * LINES * LP + ln * LP + P(p)];
@@ -658,11 +620,19 @@ struct MiddlePass {
         }
         __syncthreads();
 #pragma unroll
-        for (int co = 0; co < NCO; ++co) fft_line<To, L, +1>(so + co * LINES * LP + line * LP, t, two, 1);
-#pragma unroll
-        for (int co = 0; co < NCO; ++co)
-            col_store<To, L, XC, OL, 3, false, NT, To>(so + co * LINES * LP, out.p[co], c, x0, o0, c.n2);
+        for (int co = 0; co < NCO; ++co) {
+            Cx<To>* buf = so + co * LINES * LP + line * LP;
+            fft_line_io<To, L, +1, true, false>(buf, t, two, 1, SmemLine<To>{buf},
+                                                col_acc<3>(out.p[co], c, x0 + xi, o0 + oi, 0, on, 0));
+        }
     }
 };
+
+// One CTA per tile of a pass.
+template <class PassT>
+__global__ void __launch_bounds__(PassT::NT, PassT::MINB) k_stream(PassT pass) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pass.run(blockIdx.x, smem_raw);
+}
 
 }  // namespace dr
