@@ -77,6 +77,9 @@ typedef struct dr_config {
     int32_t reg;    /* DR_REG_H1 or DR_REG_H2                                                     */
     uint32_t flags; /* DR_ISOCHORIC | DR_FP64                                                     */
     double beta;    /* regularisation parameter beta > 0 (Eq. 2a)                      */
+    int32_t ghost_lo, ghost_hi; /* slab ghost planes below / above (multi-GPU only; 0 -> 4 / 5).  A
+                                   gather stencil spans floor(s3)-1 .. floor(s3)+2, so (g, g+1) planes
+                                   cover x3 displacements |d3| <= g - 1 cells; 1 <= g <= N3/P.         */
 } dr_config;
 
 typedef struct dr_ctx dr_ctx;
@@ -96,9 +99,10 @@ dr_status dr_destroy(dr_ctx* ctx);
  * decomposition, and of its ghost-layer interpolation, Algorithm 1).
  * Rank r owns the x3 planes [r N3/P, (r+1) N3/P) of every field; all field arguments of a
  * distributed context are that rank's slab: scalar [N3/P][N2][N1], vector [3][N3/P][N2][N1].
- * Requirements: P | N3, P | N2, N3/P >= 5 (ghost planes (4, 5) cover x3 displacements of up to
- * 3 cells; larger ones return DR_ERR_PLAN from dr_set_velocity -- the off-rank departure-point
- * scatter is not implemented).  Exchanges: ghost planes before every semi-Lagrangian gather and
+ * Requirements: P | N3, P | N2, N3/P >= ghost_hi (default ghost planes (4, 5) cover x3 displacements
+ * of up to 3 cells; dr_config.ghost_lo/hi widen them up to a whole slab; a displacement beyond the
+ * ghosts returns DR_ERR_PLAN from dr_set_velocity -- the off-rank departure-point scatter of the
+ * paper's Algorithm 1 is not implemented, widened ghosts replace it).  Exchanges: ghost planes before every semi-Lagrangian gather and
  * all-to-all transposes around the x3 FFT pass, stream-ordered on the context stream.  Every rank
  * must make the same sequence of calls (collective semantics).
  *

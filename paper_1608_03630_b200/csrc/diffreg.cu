@@ -50,8 +50,10 @@ int ilog2(int n) {
 bool pow2_in_range(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
 
 // Ghost planes of a slab: the stencil of a departure point s3 spans floor(s3)-1 ..
-// floor(s3)+2, so (4, 5) planes cover x3 displacements |d3| <= 3 cells.
+// floor(s3)+2, so (g, g + 1) planes cover x3 displacements |d3| <= g - 1 cells.  Default (4, 5).
 constexpr int GHOST_LO = 4, GHOST_HI = 5;
+int ghost_lo(const dr_config* c) { return c->ghost_lo > 0 ? c->ghost_lo : GHOST_LO; }
+int ghost_hi(const dr_config* c) { return c->ghost_hi > 0 ? c->ghost_hi : GHOST_HI; }
 
 dr_status validate(const dr_config* c, int nranks = 1) {
     if (!c) return DR_ERR_ARG;
@@ -64,7 +66,8 @@ dr_status validate(const dr_config* c, int nranks = 1) {
     if (nranks < 1) return DR_ERR_ARG;
     if (nranks > 1) {  // slabs: P | N3 and P | N2 (x2 blocks of the transposes), slab >= ghost width
         if (c->n[2] % nranks || c->n[1] % nranks) return DR_ERR_GRID;
-        if (c->n[2] / nranks < GHOST_HI) return DR_ERR_GRID;
+        if (c->ghost_lo < 0 || c->ghost_hi < 0) return DR_ERR_PARAM;
+        if (c->n[2] / nranks < ghost_lo(c) || c->n[2] / nranks < ghost_hi(c)) return DR_ERR_GRID;
     }
     return DR_OK;
 }
@@ -84,8 +87,8 @@ Grid make_grid(const dr_config* c, int rank = 0, int nranks = 1) {
     g.z0 = rank * g.n3;
     g.n3g = c->n[2];
     g.ghost = nranks > 1;
-    g.zg = g.ghost ? GHOST_LO : 0;
-    g.zgh = g.ghost ? GHOST_HI : 0;
+    g.zg = g.ghost ? ghost_lo(c) : 0;
+    g.zgh = g.ghost ? ghost_hi(c) : 0;
     return g;
 }
 
@@ -672,7 +675,7 @@ struct Impl {
         CK(cudaMemcpyAsync(&flag, c.at<int>(c.L.maxext) + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (flag)
-            fail(DR_ERR_PLAN, "x3 displacement exceeds the slab ghost planes (|d3| <= 3 cells supported; "
+            fail(DR_ERR_PLAN, "x3 displacement exceeds the slab ghost planes (widen dr_config.ghost_lo/hi; "
                               "off-rank departure-point scatter is not implemented)");
     }
 

@@ -28,7 +28,7 @@ struct LineGeom {
 // Threads per line: each owns the 16 values of one radix-16 butterfly per stage.
 template <int L, typename T>
 struct Tpl {
-    static constexpr int R = 16;
+    static constexpr int R = 16;  // (radix 8 for fp64 halves the registers but adds a shared-memory exchange: slower)
     static constexpr int V = (L >= R) ? L / R : 1;
 };
 template <typename T>
@@ -135,33 +135,33 @@ __device__ __forceinline__ void stage_io(int t, const Cx<T>* __restrict__ tw, in
     }
 }
 
-// stages Ns, Ns*16, ... of a line whose data sit in shared memory `buf`; the last stage writes to dst
-template <typename T, int L, int DIR, int TPL, int Ns, bool DST_SMEM, class Dst>
+// stages Ns, Ns*R, ... of a line whose data sit in shared memory `buf`; the last stage writes to dst
+template <typename T, int L, int DIR, int TPL, int R, int Ns, bool DST_SMEM, class Dst>
 __device__ __forceinline__ void stages_rest(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws, const Dst& dst) {
-    if constexpr (Ns * 16 >= L) {
+    if constexpr (Ns * R >= L) {
         stage_io<T, L, L / Ns, Ns, DIR, TPL, DST_SMEM>(t, tw, tws, SmemLine<T>{buf}, dst);
         if (DST_SMEM) __syncthreads();
     } else {
-        stage_io<T, L, 16, Ns, DIR, TPL, true>(t, tw, tws, SmemLine<T>{buf}, SmemLine<T>{buf});
+        stage_io<T, L, R, Ns, DIR, TPL, true>(t, tw, tws, SmemLine<T>{buf}, SmemLine<T>{buf});
         __syncthreads();
-        stages_rest<T, L, DIR, TPL, Ns * 16, DST_SMEM>(buf, t, tw, tws, dst);
+        stages_rest<T, L, DIR, TPL, R, Ns * R, DST_SMEM>(buf, t, tw, tws, dst);
     }
 }
 
-// Whole-line FFT, radix plan 16 x 16 x ... x r: src -> [shared line buf] -> dst.  SRC_SMEM / DST_SMEM:
+// Whole-line FFT, radix plan R x R x ... x r (R = 16 fp32, 8 fp64): src -> [shared line buf] -> dst.  SRC_SMEM / DST_SMEM:
 // the source / destination is `buf` itself (in place).  Every thread of the CTA must call this (it
 // contains __syncthreads); on return with DST_SMEM the results are visible to the whole CTA.
 template <typename T, int L, int DIR, bool SRC_SMEM, bool DST_SMEM, class Src, class Dst>
 __device__ __forceinline__ void fft_line_io(Cx<T>* buf, int t, const Cx<T>* __restrict__ tw, int tws, const Src& src,
                                             const Dst& dst) {
-    constexpr int TPL = Tpl<L, T>::V;
-    if constexpr (L <= 16) {
+    constexpr int TPL = Tpl<L, T>::V, R = Tpl<L, T>::R;
+    if constexpr (L <= R) {
         stage_io<T, L, L, 1, DIR, TPL, SRC_SMEM && DST_SMEM>(t, tw, tws, src, dst);
         if (DST_SMEM) __syncthreads();
     } else {
-        stage_io<T, L, 16, 1, DIR, TPL, SRC_SMEM>(t, tw, tws, src, SmemLine<T>{buf});
+        stage_io<T, L, R, 1, DIR, TPL, SRC_SMEM>(t, tw, tws, src, SmemLine<T>{buf});
         __syncthreads();
-        stages_rest<T, L, DIR, TPL, 16, DST_SMEM>(buf, t, tw, tws, dst);
+        stages_rest<T, L, DIR, TPL, R, R, DST_SMEM>(buf, t, tw, tws, dst);
     }
 }
 
@@ -576,7 +576,7 @@ struct MiddlePass {
     static constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
     using CC = ColCfg<L, T, NCI>;
     static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
-    static_assert(Tpl<L, To>::V == TPL, "inverse lines use the same threads");
+    static constexpr int TPLO = Tpl<L, To>::V;  // threads per inverse line (fp32: fewer than fp64)
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr size_t BUFI = CC::SMEM;
     static constexpr size_t BUF = BUFI + (size_t)NCO * LINES * LP * sizeof(Cx<To>);
@@ -619,11 +619,24 @@ struct MiddlePass {
             for (int co = 0; co < NCO; ++co) so[co * LINES * LP + ln * LP + P(p)] = cx<To>((To)v[co].re, (To)v[co].im);
         }
         __syncthreads();
+        // inverse lines: the CTA's NT threads cover LINES lines of TPLO threads in NT / (LINES * TPLO) rounds
+        static_assert(NT % TPLO == 0, "inverse thread mapping");
+        constexpr int PER = NT / TPLO;  // lines per round
 #pragma unroll
         for (int co = 0; co < NCO; ++co) {
-            Cx<To>* buf = so + co * LINES * LP + line * LP;
-            fft_line_io<To, L, +1, true, false>(buf, t, two, 1, SmemLine<To>{buf},
-                                                col_acc<3>(out.p[co], c, x0 + xi, o0 + oi, 0, on, 0));
+#pragma unroll
+            for (int l0 = 0; l0 < LINES; l0 += PER) {
+                // thread -> (column, t, line) with columns fastest, as in col_thread
+                const int lxi = threadIdx.x % XC;
+                const int rr = threadIdx.x / XC;
+                const int lt = rr % TPLO, loi = l0 / XC + rr / TPLO;
+                const int ln = loi * XC + lxi;
+                const bool act = ln < LINES;
+                const bool lon = act && x0 + lxi < c.nx && o0 + loi < c.n2;
+                Cx<To>* buf = so + co * LINES * LP + (act ? ln : 0) * LP;
+                fft_line_io<To, L, +1, true, false>(buf, lt, two, 1, SmemLine<To>{buf},
+                                                    col_acc<3>(out.p[co], c, x0 + lxi, o0 + loi, 0, lon, 0));
+            }
         }
     }
 };

@@ -36,7 +36,8 @@ EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr
 
 class dr_config(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32 * 3), ("nt", ctypes.c_int32), ("reg", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("beta", ctypes.c_double)]
+                ("flags", ctypes.c_uint32), ("beta", ctypes.c_double), ("ghost_lo", ctypes.c_int32),
+                ("ghost_hi", ctypes.c_int32)]
 
 
 class DiffRegError(RuntimeError):
@@ -104,6 +105,8 @@ class Config:
     beta: float = 1e-2
     isochoric: bool = False
     fp64: bool = False
+    ghost_lo: int = 0  # slab ghost planes (multi-GPU; 0 -> library default 4 / 5)
+    ghost_hi: int = 0
 
     def c(self) -> dr_config:
         n = (self.n,) * 3 if isinstance(self.n, int) else tuple(self.n)
@@ -111,6 +114,7 @@ class Config:
         cfg = dr_config()
         cfg.n[:] = list(n)
         cfg.nt, cfg.reg, cfg.flags, cfg.beta = self.nt, self.reg, flags, self.beta
+        cfg.ghost_lo, cfg.ghost_hi = self.ghost_lo, self.ghost_hi
         return cfg
 
     @property

@@ -89,3 +89,6 @@ def test_slab_partition_and_limits():
     assert dr_workspace_bytes_dist(Config(n=(32, 64, 16)), 4) == 0  # N3/P = 4 < 5 ghost planes
     with pytest.raises(DiffRegError):
         dr_slab(cfg, 2, 2)
+    # widened ghosts must fit in a slab
+    assert dr_workspace_bytes_dist(Config(n=(32, 16, 64), ghost_lo=7, ghost_hi=8), 8) > 0
+    assert dr_workspace_bytes_dist(Config(n=(32, 16, 64), ghost_lo=8, ghost_hi=9), 8) == 0

@@ -128,6 +128,33 @@ def test_slabs_match_single_rank(dr, P, case):
     hub.close()
 
 
+def test_widened_ghosts_carry_large_displacement(dr):
+    """~6 cells/step (BASELINE config 5's displacement) with ghost planes (7, 8): bit-identical to one rank."""
+    P, n = 2, (32, 16, 32)
+    cfg = dr.Config(n=n, nt=2, ghost_lo=7, ghost_hi=8)
+    rT = synth.round32(synth.blobs(21, n, kcut=5)).cuda()
+    v = synth.round32(synth.smooth_vec(22, n, kmax=2, cells_per_step=6.0, nt=2)).cuda()
+    vt = synth.round32(synth.smooth_vec(23, n, kmax=3)).cuda()
+    ref = pipeline(dr.Context(cfg), rT, rT, v, vt)
+    hub = dr.diffreg.Hub(P)
+    comms = [hub.comm(r) for r in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ctxs = [dr.Context(cfg, stream=streams[r], comm=comms[r]) for r in range(P)]
+    sl = lambda x, r: dr.dist.slab_of(x, cfg, P, r)  # noqa: E731
+    ins = [(sl(rT, r), sl(rT, r), sl(v, r), sl(vt, r)) for r in range(P)]
+    torch.cuda.synchronize()
+
+    def rank(r):
+        with torch.cuda.stream(streams[r]):
+            out = pipeline(ctxs[r], *ins[r])
+        streams[r].synchronize()
+        return out
+
+    outs = run_ranks(P, rank)
+    for k, full in ref.items():
+        assert torch.equal(dr.dist.assemble([o[k] for o in outs]), full), k
+
+
 def test_slab_rejects_displacement_beyond_ghosts(dr):
     """|d3| > 3 cells leaves the ghost planes: set_velocity reports DR_ERR_PLAN on every rank."""
     P, n = 2, (16, 16, 32)
