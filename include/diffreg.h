@@ -163,6 +163,18 @@ dr_status dr_hessian_matvec(dr_ctx* ctx, const void* vt, void* Hvt);
  * projection in isochoric contexts.  r, z: vector fields, may alias.  Requires only the context. */
 dr_status dr_precond_apply(dr_ctx* ctx, const void* r, void* z);
 
+/* NEXT-1: reduced gradient g = beta A v + P b, b = int_0^1 lambda grad rho dt
+ * (Eq. 4; trapezoid in time, reading A12; P = Leray when isochoric).  Requires
+ * dr_forward_solve; runs dr_adjoint_solve first if it has not run since.  g: vector field, device or
+ * host pointer (host: the call synchronises). */
+dr_status dr_gradient(dr_ctx* ctx, void* g);
+
+/* Objective J = 1/2 <rho(1) - rho_R, rho(1) - rho_R> + beta/2 <v, A v> (Eq. 2a) with the
+ * inner product h1 h2 h3 sum, accumulated in fp64 deterministically; with slabs the sum runs
+ * over all ranks (collective) and every rank gets the same value.  Requires dr_forward_solve.  J and
+ * misfit (the first term) are host pointers, either may be NULL.  Synchronises the stream. */
+dr_status dr_objective(dr_ctx* ctx, double* J, double* misfit);
+
 /* Wait for all work of the context; surfaces asynchronous CUDA errors. */
 dr_status dr_sync(dr_ctx* ctx);
 

@@ -101,8 +101,8 @@ int64_t n_tiles(const Grid& g) {
 // zg + n3 + zgh planes; every other slot holds the slab's n3 planes.
 struct Layout {
     size_t F, GF, vstride;
-    size_t rhoT, rhoR, v, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
-        plan_m, plan_t, maxext, twx, twy, twz, twxd, twyd, twzd, total;
+    size_t rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
+        plan_m, plan_t, maxext, red, twx, twy, twz, twxd, twyd, twzd, total;
 };
 
 Layout layout(const dr_config* c, int nranks = 1) {
@@ -123,6 +123,7 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.rhoT = take(L.GF);                      // rho_0 = rho_T (ghosted)
     L.rhoR = take(L.F);
     L.v = take(3 * L.GF);                     // velocity components (ghosted)
+    L.vin = (c->flags & DR_ISOCHORIC) ? take(3 * L.F) : 0;  // the caller's v before projection
     L.vstride = L.GF / es;
     L.dp = take(3 * L.F);
     L.dm = take(3 * L.F);
@@ -148,6 +149,7 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.plan_m = take(pb);
     L.plan_t = take(pb);
     L.maxext = take(16 * sizeof(int));
+    L.red = take(4096 * sizeof(double));  // reduction partials + per-rank gather slots
     L.twx = take((size_t)g.n1 * 2 * es);
     L.twy = take((size_t)g.n2 * 2 * es);
     L.twz = take((size_t)g.n3g * 2 * es);
@@ -287,6 +289,7 @@ struct Impl {
     T* rhoR() { return c.at<T>(c.L.rhoR); }
     T* vc(int a) { return gf(c.L.v) + (size_t)a * gstride(); }
     V3<T> v3() { return V3<T>{{vc(0), vc(1), vc(2)}}; }
+    T* vraw() { return c.at<T>(c.L.vin); }
     T* dplus() { return c.at<T>(c.L.dp); }
     T* dminus() { return c.at<T>(c.L.dm); }
     T* mult() { return c.at<T>(c.L.m); }
@@ -637,9 +640,13 @@ struct Impl {
 
     // -------------------------------------------------------------------- API steps
     void set_velocity(const T* vin) {
-        for (int a = 0; a < 3; ++a)
-            CK(cudaMemcpyAsync(vc(a), vin + (size_t)a * g.M, g.M * sizeof(T), cudaMemcpyDefault, s));
-        if (c.cfg.flags & DR_ISOCHORIC) leray(cvec(v3()), v3());
+        if (c.cfg.flags & DR_ISOCHORIC) {  // keep the caller's v: the gradient projects beta A v + b at once
+            CK(cudaMemcpyAsync(vraw(), vin, 3 * g.M * sizeof(T), cudaMemcpyDefault, s));
+            leray(cvec(vec(vraw(), (size_t)g.M)), v3());
+        } else {
+            for (int a = 0; a < 3; ++a)
+                CK(cudaMemcpyAsync(vc(a), vin + (size_t)a * g.M, g.M * sizeof(T), cudaMemcpyDefault, s));
+        }
         CK(cudaMemsetAsync(c.at<int>(c.L.maxext), 0, 16 * sizeof(int), s));
         const double h[3] = {2.0 * M_PI / g.n1, 2.0 * M_PI / g.n2, 2.0 * M_PI / g.n3g};
         const double dtt = 1.0 / c.cfg.nt;
@@ -693,6 +700,86 @@ struct Impl {
             gather<1>("sl_adjoint", Src<T, 1>{{lam(k)}}, dminus(), plan_m(), EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)});
     }
 
+    // out = beta A u + P b (P = Leray when isochoric, else I): the tail of Eq. 5e and of Eq. 4
+    void reg_plus_data(V3<const T> u, V3<const T> b, V3<T> out) {
+        if (c.cfg.flags & DR_ISOCHORIC) {
+            Cx<double>* sd[6] = {specD(0), specD(1), specD(2), specD(3), specD(4), specD(5)};
+            Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
+            for (int cc = 0; cc < 3; ++cc) {
+                spec_forward(u.c[cc], cc);
+                spec_forward(b.c[cc], 3 + cc);
+            }
+            middle<4>(sd, sf);
+            for (int cc = 0; cc < 3; ++cc) spec_inverse(cc, out.c[cc], nullptr);
+        } else {
+            scalar_symbol3<0>(u, out, &b);
+        }
+    }
+
+    // NEXT-1: reduced gradient g = beta A v + P b, b = dt sum_j w_j lambda_j G_j (Eq. 4)
+    void gradient(V3<T> gout) {
+        PB();
+        k_quadrature<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, c.cfg.nt, lam(0), gstride(), G(0), tmp3(), dt());
+        PE("quadrature");
+        if (c.cfg.flags & DR_ISOCHORIC) {
+            // g = L(beta A v_in + b): beta A L v_in = L beta A v_in, so the fp32 rounding of the stored
+            // projected v never meets the |k|^4 amplification (reading A20)
+            Cx<double>* sd[6] = {specD(0), specD(1), specD(2), specD(3), specD(4), specD(5)};
+            Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
+            for (int cc = 0; cc < 3; ++cc) {
+                spec_forward(vraw() + (size_t)cc * g.M, cc);
+                spec_forward(tmp3() + (size_t)cc * g.M, 3 + cc);
+            }
+            middle<5>(sd, sf);
+            for (int cc = 0; cc < 3; ++cc) spec_inverse(cc, gout.c[cc], nullptr);
+        } else {
+            reg_plus_data(cvec(v3()), cvec(vec(tmp3(), (size_t)g.M)), gout);
+        }
+    }
+
+    // sum over all ranks of one double per rank (device scalar at `val`), identical on every rank
+    double allsum(double* val) {
+        double* slots = c.at<double>(c.L.red) + 3072;
+        const int P = c.nranks;
+        CK(cudaMemcpyAsync(slots + c.rank, val, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (c.dist()) {
+            std::vector<P2P> ops;
+            for (int q = 0; q < P; ++q) {
+                if (q == c.rank) continue;
+                ops.push_back(P2P{true, q, val, nullptr, sizeof(double)});
+                ops.push_back(P2P{false, q, nullptr, slots + q, sizeof(double)});
+            }
+            exchange(ops);
+        }
+        std::vector<double> h(P);
+        CK(cudaMemcpyAsync(h.data(), slots, P * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double t = 0;
+        for (int q = 0; q < P; ++q) t += h[q];  // rank order: the same on every rank
+        return t;
+    }
+    double reduce(const T* a, const T* b, const T* a2, int mode, int64_t n) {
+        double* part = c.at<double>(c.L.red);
+        const int nb = (int)std::min<int64_t>(2048, (n + 255) / 256);
+        PB();
+        k_dot_parts<T><<<nb, 256, 0, s>>>(n, a, b, a2, nullptr, part, mode);
+        PE("reduce");
+        PB();
+        k_sum_parts<<<1, 256, 0, s>>>(part, nb, part + 2048);
+        PE("reduce");
+        return allsum(part + 2048);
+    }
+    // J = 1/2 <rho(1) - rho_R, rho(1) - rho_R> + beta/2 <v, A v>  (Eq. 2a; S:L53 inner product)
+    void objective(double* J, double* misfit) {
+        const double hv = (2.0 * M_PI / g.n1) * (2.0 * M_PI / g.n2) * (2.0 * M_PI / g.n3g);
+        const double mis = 0.5 * hv * reduce(rho(c.cfg.nt), nullptr, rhoR(), 1, g.M);
+        reg_apply(cvec(v3()), vec(tmp3(), (size_t)g.M));  // beta A v
+        double vav = 0;
+        for (int a = 0; a < 3; ++a) vav += reduce(vc(a), tmp3() + (size_t)a * g.M, nullptr, 0, g.M);
+        if (misfit) *misfit = mis;
+        if (J) *J = mis + 0.5 * hv * vav;
+    }
+
     void hessian_matvec(const T* vt, T* Hvt) {
         const int nt = c.cfg.nt;
         const T dtt = dt();
@@ -738,21 +825,8 @@ struct Impl {
             }
         }
         // spectral tail: H vt = beta A vt + P b~
-        const V3<const T> vt3 = cvec(vec(const_cast<T*>(vt), (size_t)g.M));
-        const V3<const T> bt3 = cvec(vec(bt(), (size_t)g.M));
-        V3<T> out3 = vec(Hvt, (size_t)g.M);
-        if (c.cfg.flags & DR_ISOCHORIC) {
-            Cx<double>* sd[6] = {specD(0), specD(1), specD(2), specD(3), specD(4), specD(5)};
-            Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
-            for (int cc = 0; cc < 3; ++cc) {
-                spec_forward(vt3.c[cc], cc);
-                spec_forward(bt3.c[cc], 3 + cc);
-            }
-            middle<4>(sd, sf);
-            for (int cc = 0; cc < 3; ++cc) spec_inverse(cc, out3.c[cc], nullptr);
-        } else {
-            scalar_symbol3<0>(vt3, out3, &bt3);
-        }
+        reg_plus_data(cvec(vec(const_cast<T*>(vt), (size_t)g.M)), cvec(vec(bt(), (size_t)g.M)),
+                      vec(Hvt, (size_t)g.M));
     }
 };
 
@@ -1048,6 +1122,31 @@ dr_status dr_precond_apply(dr_ctx* c, const void* r, void* z) {
         });
     });
 }
+dr_status dr_gradient(dr_ctx* c, void* gout) {
+    return run(c, [&] {
+        if (!gout) fail(DR_ERR_ARG, "g must be non-NULL");
+        if (!c->have_state) fail(DR_ERR_ORDER, "gradient needs forward_solve");
+        const size_t V = 3 * c->g.M * elem_size(c);
+        with_output(c, gout, V, c->ws + c->L.stout, [&](void* out) {
+            dispatch(c, [&](auto& im) {
+                using T = std::remove_pointer_t<decltype(im.rhoR())>;
+                if (!c->have_adjoint) {
+                    im.adjoint_solve();
+                    c->have_adjoint = true;
+                }
+                im.gradient(vec(static_cast<T*>(out), (size_t)c->g.M));
+            });
+        });
+    });
+}
+
+dr_status dr_objective(dr_ctx* c, double* J, double* misfit) {
+    return run(c, [&] {
+        if (!c->have_state) fail(DR_ERR_ORDER, "objective needs forward_solve");
+        dispatch(c, [&](auto& im) { im.objective(J, misfit); });
+    });
+}
+
 dr_status dr_profile_enable(dr_ctx* c, int enable) {
     return run(c, [&] {
         c->prof_flush();

@@ -521,9 +521,10 @@ __device__ __forceinline__ T sym_a(const SymInfo& s, T kk) { return s.reg == 1 ?
 // kind 2: Y = norm * L_hat X                      (Leray, 3 -> 3)
 // kind 3: Y = norm * L_hat X / (beta a_hat(k))    (isochoric preconditioner)
 // kind 4: Y = norm * (beta a(k) V + L_hat B)      (isochoric matvec tail, 6 -> 3)
+// kind 5: Y = norm * L_hat (beta a(k) V + B)      (isochoric gradient from the unprojected v, 6 -> 3)
 template <typename T, int KIND>
 struct Sym {
-    static constexpr int NCI = (KIND <= 1) ? 1 : (KIND == 4 ? 6 : 3);
+    static constexpr int NCI = (KIND <= 1) ? 1 : (KIND >= 4 ? 6 : 3);
     static constexpr int NCO = (KIND <= 1) ? 1 : 3;
     static __device__ __forceinline__ void apply(const SymInfo& s, Cx<T>* x, int k1, int k2, int k3, int kp1, int kp2,
                                                  int kp3) {
@@ -537,8 +538,18 @@ struct Sym {
         } else {
             const T q1 = T(kp1), q2 = T(kp2), q3 = T(kp3);
             const T qq = q1 * q1 + q2 * q2 + q3 * q3;
-            Cx<T>* B = (KIND == 4) ? x + 3 : x;
-            Cx<T> b0 = B[0], b1 = B[1], b2 = B[2];
+            Cx<T> b0, b1, b2;
+            if (KIND == 5) {  // project beta a V + B
+                const T ra = (T)s.beta * sym_a<T>(s, kk);
+                b0 = scale(x[0], ra) + x[3];
+                b1 = scale(x[1], ra) + x[4];
+                b2 = scale(x[2], ra) + x[5];
+            } else {
+                Cx<T>* B = (KIND == 4) ? x + 3 : x;
+                b0 = B[0];
+                b1 = B[1];
+                b2 = B[2];
+            }
             if (qq != T(0)) {
                 const T inv = T(1) / qq;
                 const Cx<T> kd = cx((q1 * b0.re + q2 * b1.re + q3 * b2.re) * inv, (q1 * b0.im + q2 * b1.im + q3 * b2.im) * inv);

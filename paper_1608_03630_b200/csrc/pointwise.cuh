@@ -27,17 +27,16 @@ __global__ void k_scale(int64_t M, const T* __restrict__ a, T* __restrict__ out,
         out[i] = s * a[i];
 }
 
-// b~ = dt sum_j w_j lambda~_j G_j, w_0 = w_nt = 1/2 (trapezoid, reading A12).
-// lambda~_j (j < nt) are consecutive scalar slices at lt; lambda~_nt = sgn_last * last.
-// G_j: consecutive vector slices at G (stride 3M).
+// b = dt sum_j w_j lambda_j G_j, w_0 = w_nt = 1/2 (trapezoid, reading A12; Eq. 4 with the
+// time integral of P:L157).  lambda_j: slices lam + j * lstride; G_j: consecutive vector slices (3M).
 template <typename T>
-__global__ void k_quadrature(int64_t M, int nt, const T* __restrict__ lt, const T* __restrict__ last, T sgn_last,
-                             const T* __restrict__ G, T* __restrict__ b, T dt) {
+__global__ void k_quadrature(int64_t M, int nt, const T* __restrict__ lam, size_t lstride, const T* __restrict__ G,
+                             T* __restrict__ b, T dt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
         T b0 = T(0), b1 = T(0), b2 = T(0);
         for (int j = 0; j <= nt; ++j) {
             const T w = (j == 0 || j == nt) ? T(0.5) * dt : dt;
-            const T l = w * ((j < nt) ? lt[(int64_t)j * M + i] : sgn_last * last[i]);
+            const T l = w * lam[(size_t)j * lstride + i];
             const T* Gj = G + (int64_t)j * 3 * M;
             b0 += l * Gj[i];
             b1 += l * Gj[M + i];
@@ -47,6 +46,46 @@ __global__ void k_quadrature(int64_t M, int nt, const T* __restrict__ lt, const 
         b[M + i] = b1;
         b[2 * M + i] = b2;
     }
+}
+
+// Deterministic fp64 dot product, pass 1: block b writes sum_{i in its grid-stride set} a_i c_i (and, with
+// a2/c2, + the same for a second pair) to part[b].  Pass 2 (k_sum_parts, one block) adds the parts in
+// block order.  Used by the objective (Eq. 2a) -- the inner product of S:L53, h^3 sum.
+template <typename T>
+__global__ void __launch_bounds__(256) k_dot_parts(int64_t M, const T* __restrict__ a, const T* __restrict__ c,
+                                                   const T* __restrict__ a2, T* dummy, double* __restrict__ part,
+                                                   int mode) {
+    // mode 0: sum a*c; mode 1: sum (a - a2)^2
+    __shared__ double red[256];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        if (mode == 0) acc += (double)a[i] * (double)c[i];
+        else {
+            const double d = (double)a[i] - (double)a2[i];
+            acc += d * d;
+        }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+    (void)dummy;
+}
+
+__global__ void __launch_bounds__(256) k_sum_parts(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double red[256];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) acc += part[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
 }
 
 }  // namespace dr

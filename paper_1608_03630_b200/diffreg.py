@@ -31,7 +31,8 @@ EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr
            "dr_last_error", "dr_status_string", "dr_op_spectral", "dr_op_interp", "dr_get_departure",
            "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry",
            "dr_nccl_get_unique_id", "dr_comm_create_nccl", "dr_hub_create", "dr_hub_destroy",
-           "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist"]
+           "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist",
+           "dr_gradient", "dr_objective"]
 
 
 class dr_config(ctypes.Structure):
@@ -77,7 +78,9 @@ def lib():
         L.dr_workspace_bytes_dist.restype = ctypes.c_size_t
         L.dr_create_dist.argtypes = [ctypes.POINTER(dr_config), vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
         L.dr_create_dist.restype = ctypes.c_int
-        for name, args in [("dr_nccl_get_unique_id", [ctypes.c_char_p]),
+        for name, args in [("dr_gradient", [vp, vp]),
+                           ("dr_objective", [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+                           ("dr_nccl_get_unique_id", [ctypes.c_char_p]),
                            ("dr_comm_create_nccl", [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]),
                            ("dr_hub_create", [i32, ctypes.POINTER(vp)]), ("dr_hub_destroy", [vp]),
                            ("dr_comm_create_loopback", [vp, i32, ctypes.POINTER(vp)]), ("dr_comm_destroy", [vp]),
@@ -290,6 +293,19 @@ class Context:
 
     def sync(self):
         self._check(lib().dr_sync(self.h))
+
+    # ---- NEXT-1: gradient and objective ----
+    def gradient(self, g=None):
+        if g is None:
+            g = self.vector()
+        self._check(lib().dr_gradient(self.h, _ptr(g)))
+        return g
+
+    def objective(self):
+        """(J, misfit) as Python floats (collective with slabs)."""
+        J, m = ctypes.c_double(), ctypes.c_double()
+        self._check(lib().dr_objective(self.h, ctypes.byref(J), ctypes.byref(m)))
+        return J.value, m.value
 
     # ---- tracing ----
     def profile_enable(self, on: bool = True):

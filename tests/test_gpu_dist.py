@@ -74,8 +74,12 @@ def pipeline(ctx, rT, rR, v, vt):
     res["reg"] = ctx.op_spectral(F.DR_OP_REG, vt)
     res["leray"] = ctx.op_spectral(F.DR_OP_LERAY, vt)
     res["div"] = ctx.op_spectral(F.DR_OP_DIV, vt)
+    res["grad"] = ctx.gradient()
+    J, mis = ctx.objective()
     ctx.sync()
-    return {k: t.clone() for k, t in res.items()}
+    out = {k: t.clone() for k, t in res.items()}
+    out["_J"] = (J, mis)
+    return out
 
 
 CASES = [
@@ -116,7 +120,13 @@ def test_slabs_match_single_rank(dr, P, case):
         return out
 
     outs = run_ranks(P, rank)
+    for o in outs:  # the objective is a collective: every rank holds the same sum (rank-order partials)
+        assert o["_J"] == outs[0]["_J"]
+        assert abs(o["_J"][0] - ref["_J"][0]) <= 1e-12 * abs(ref["_J"][0])
+        assert abs(o["_J"][1] - ref["_J"][1]) <= 1e-12 * abs(ref["_J"][1]) + 1e-300
     for k, full in ref.items():
+        if k == "_J":
+            continue
         got = D.assemble([o[k] for o in outs])
         assert got.shape == full.shape, k
         assert rel(got, full) < 1e-6, (k, rel(got, full))
@@ -152,6 +162,8 @@ def test_widened_ghosts_carry_large_displacement(dr):
 
     outs = run_ranks(P, rank)
     for k, full in ref.items():
+        if k == "_J":
+            continue
         assert torch.equal(dr.dist.assemble([o[k] for o in outs]), full), k
 
 

@@ -300,3 +300,26 @@ def test_matvec_linearity_and_determinism(dr):
     assert rel(np64(b), np64(2 * bx - 3 * by)) < 1e-5
     assert rel(np64(h), np64(2 * hx - 3 * hy)) < 1e-4
     assert torch.equal(ctx.hessian_matvec(x), hx)  # bitwise deterministic
+
+
+# ------------------------------------------------------------------ NEXT-1: gradient and objective
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("case", CASES[:3], ids=[c[0] for c in CASES[:3]])
+def test_gradient_objective(dr, case, fp64):
+    """g = beta A v + P b, b = int lambda grad rho (Eq. 4) and J (Eq. 2a) against the oracle's D14."""
+    name, n, nt, vgen, iso = case
+    top, tmv = tols(fp64)
+    ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, fp64)
+    st = O.set_velocity(prob, v64)
+    ctx.forward_solve()
+    g = np64(ctx.gradient())
+    gref = O.gradient(prob, st)
+    # fp64: beta A v amplifies FFT rounding (~1e-16) by |k|^4 up to (32 sqrt 3)^4 ~ 1e7 against the
+    # |k|^4 ~ 4 of v*'s own modes (reading A20's conditioning, in fp64), so 1e-10 rather than 1e-11
+    assert rel(g, gref) < (1e-10 if fp64 else tmv)
+    J, mis = ctx.objective()
+    Jref = O.objective(prob, st)
+    r = st.rho[-1] - prob.rho_R
+    assert abs(mis - 0.5 * O.inner(r, r)) <= (1e-12 if fp64 else 1e-5) * abs(0.5 * O.inner(r, r))
+    assert abs(J - Jref) <= (1e-12 if fp64 else 1e-5) * abs(Jref)
