@@ -175,6 +175,15 @@ dr_status dr_gradient(dr_ctx* ctx, void* g);
  * misfit (the first term) are host pointers, either may be NULL.  Synchronises the stream. */
 dr_status dr_objective(dr_ctx* ctx, double* J, double* misfit);
 
+/* NEXT-2: inexact preconditioned CG for the Newton step H dv = -g (PCG with
+ * the inverse-regulariser preconditioner, Leray-projected when isochoric; relative tolerance from the
+ * gradient norm, e.g. the quadratic forcing eta = min(0.5, |g| / |g_0|) of P:L433).  Starts from
+ * dv = 0; stops when |r| <= eta |g| (discrete L2 norms, fp64 accumulation, summed over all ranks) or
+ * after maxit Hessian matvecs.  g, dv: vector fields (device or host), must not alias.  iters /
+ * relres (nullable, host): matvecs used and |r| / |g|.  Requires dr_forward_solve.  Synchronises
+ * the stream once per inner product. */
+dr_status dr_pcg(dr_ctx* ctx, const void* g, void* dv, double eta, int maxit, int* iters, double* relres);
+
 /* Wait for all work of the context; surfaces asynchronous CUDA errors. */
 dr_status dr_sync(dr_ctx* ctx);
 

@@ -331,3 +331,40 @@ def objective(prob: Problem, st: VelocityState) -> float:
     """J = 1/2 <rho(1) - rho_R, rho(1) - rho_R> + beta/2 <v, A v> (Eq. 2a; D14)."""
     r = st.rho[-1] - prob.rho_R
     return 0.5 * inner(r, r) + 0.5 * inner(st.v, reg_apply(st.v, prob.reg, prob.beta))
+
+
+# ------------------------------------------------------------------ NEXT-2: inexact PCG (P:L234)
+
+def forcing(gnorm: float, g0norm: float) -> float:
+    """Quadratic forcing (Eisenstat-Walker): eta = min(0.5, |g| / |g_0|), so the
+    Newton-system residual is <= eta |g| ~ |g|^2 / |g_0| (reading A22 in DESIGN.md)."""
+    return min(0.5, gnorm / g0norm)
+
+
+def pcg(prob: Problem, st: VelocityState, g: np.ndarray, eta: float, maxit: int):
+    """Preconditioned CG on H dv = -g from dv = 0 (PCG, preconditioner (beta A)^-1, inexact
+    with relative tolerance eta on the residual |r| <= eta |g|).  Norms and inner products are the
+    discrete L2 ones (D1).  Returns (dv, iterations, |r| / |g|)."""
+    g = _c(g)
+    dv = np.zeros_like(g)
+    r = -g
+    gnorm = math.sqrt(inner(g, g))
+    z = precond(r, prob.reg, prob.beta, prob.iso)
+    p = z.copy()
+    rz = inner(r, z)
+    it = 0
+    rnorm = gnorm
+    while it < maxit and rnorm > eta * gnorm:
+        q = hessian_matvec(prob, st, p)
+        alpha = rz / inner(p, q)
+        dv = dv + alpha * p
+        r = r - alpha * q
+        it += 1
+        rnorm = math.sqrt(inner(r, r))
+        if rnorm <= eta * gnorm:
+            break
+        z = precond(r, prob.reg, prob.beta, prob.iso)
+        rz_new = inner(r, z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return dv, it, rnorm / gnorm

@@ -21,6 +21,14 @@ __global__ void k_sub(int64_t M, const T* __restrict__ a, const T* __restrict__ 
         out[i] = a[i] - b[i];
 }
 
+// y = a x + b y (vector updates of the PCG iteration; coefficients in fp64, fields in T).  b == 0
+// overwrites y without reading it (it may hold anything, NaN included).
+template <typename T>
+__global__ void k_axpby(int64_t n, double a, const T* __restrict__ x, double b, T* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = (b == 0.0) ? (T)(a * (double)x[i]) : (T)(a * (double)x[i] + b * (double)y[i]);
+}
+
 template <typename T>
 __global__ void k_scale(int64_t M, const T* __restrict__ a, T* __restrict__ out, T s) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)

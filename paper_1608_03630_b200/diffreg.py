@@ -32,7 +32,7 @@ EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr
            "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry",
            "dr_nccl_get_unique_id", "dr_comm_create_nccl", "dr_hub_create", "dr_hub_destroy",
            "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist",
-           "dr_gradient", "dr_objective"]
+           "dr_gradient", "dr_objective", "dr_pcg"]
 
 
 class dr_config(ctypes.Structure):
@@ -78,7 +78,9 @@ def lib():
         L.dr_workspace_bytes_dist.restype = ctypes.c_size_t
         L.dr_create_dist.argtypes = [ctypes.POINTER(dr_config), vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
         L.dr_create_dist.restype = ctypes.c_int
-        for name, args in [("dr_gradient", [vp, vp]),
+        for name, args in [("dr_pcg", [vp, vp, vp, ctypes.c_double, i32, ctypes.POINTER(i32),
+                                       ctypes.POINTER(ctypes.c_double)]),
+                           ("dr_gradient", [vp, vp]),
                            ("dr_objective", [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
                            ("dr_nccl_get_unique_id", [ctypes.c_char_p]),
                            ("dr_comm_create_nccl", [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]),
@@ -300,6 +302,14 @@ class Context:
             g = self.vector()
         self._check(lib().dr_gradient(self.h, _ptr(g)))
         return g
+
+    def pcg(self, g, eta: float, maxit: int, dv=None):
+        """Newton step dv with H dv ~ -g (|r| <= eta |g|); returns (dv, iterations, |r| / |g|)."""
+        if dv is None:
+            dv = self.vector(g.device)
+        it, rr = ctypes.c_int(), ctypes.c_double()
+        self._check(lib().dr_pcg(self.h, self._in(g), _ptr(dv), eta, maxit, ctypes.byref(it), ctypes.byref(rr)))
+        return dv, it.value, rr.value
 
     def objective(self):
         """(J, misfit) as Python floats (collective with slabs)."""

@@ -76,6 +76,8 @@ def pipeline(ctx, rT, rR, v, vt):
     res["div"] = ctx.op_spectral(F.DR_OP_DIV, vt)
     res["grad"] = ctx.gradient()
     J, mis = ctx.objective()
+    dv, it, rr = ctx.pcg(vt, 0.0, 2)
+    res["pcg"] = dv
     ctx.sync()
     out = {k: t.clone() for k, t in res.items()}
     out["_J"] = (J, mis)
@@ -130,7 +132,8 @@ def test_slabs_match_single_rank(dr, P, case):
         got = D.assemble([o[k] for o in outs])
         assert got.shape == full.shape, k
         assert rel(got, full) < 1e-6, (k, rel(got, full))
-        assert torch.equal(got, full), (k, rel(got, full))
+        if k != "pcg":  # PCG's inner products sum per-rank partials: equal to rounding, not bitwise
+            assert torch.equal(got, full), (k, rel(got, full))
     for c in ctxs:
         c.close()
     for c in comms:

@@ -323,3 +323,28 @@ def test_gradient_objective(dr, case, fp64):
     r = st.rho[-1] - prob.rho_R
     assert abs(mis - 0.5 * O.inner(r, r)) <= (1e-12 if fp64 else 1e-5) * abs(0.5 * O.inner(r, r))
     assert abs(J - Jref) <= (1e-12 if fp64 else 1e-5) * abs(Jref)
+
+
+# ------------------------------------------------------------------ NEXT-2: PCG
+
+@pytest.mark.parametrize("case", [CASES[1], CASES[0]], ids=["vstar64", "cfg1"])
+def test_pcg_against_oracle(dr, case):
+    """Fixed iteration count (eta = 0): the GPU's fp32 PCG iterate follows the fp64 oracle's PCG; the
+    inexact solve's residual, re-evaluated with the ORACLE's matvec, is below eta |g| (+ fp32 slack)."""
+    name, n, nt, vgen, iso = case
+    ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+    st = O.set_velocity(prob, v64)
+    ctx.forward_solve()
+    # isochoric problems live in the divergence-free subspace (the preconditioner projects), so their
+    # right-hand sides -- gradients -- are divergence-free
+    g, g64 = prep(synth.smooth_vec(41, n, kmax=6, divfree=iso), False)
+    dv, it, rr = ctx.pcg(g.cuda(), 0.0, 3)
+    ref, it_ref, rr_ref = O.pcg(prob, st, g64, 0.0, 3)
+    assert it == it_ref == 3
+    assert rel(np64(dv), ref) < 1e-4
+    assert abs(rr - rr_ref) < 1e-3 * rr_ref
+    eta = 0.05
+    dv, it, rr = ctx.pcg(g.cuda(), eta, 50)
+    res = O.hessian_matvec(prob, st, np64(dv)) + g64
+    assert rr <= eta and 0 < it < 50
+    assert np.sqrt(O.inner(res, res) / O.inner(g64, g64)) < eta + 1e-4

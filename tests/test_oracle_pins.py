@@ -516,3 +516,32 @@ def test_gradient_matches_fd_of_objective():
               O.objective(prob, O.set_velocity(prob, v - eps * vt))) / (2 * eps)
         defects.append(abs(O.inner(g, vt) - fd) / abs(fd))
     assert defects[1] < defects[0] and defects[1] < 4e-3, defects
+
+
+# ------------------------------------------------------------------ NEXT-2: PCG against a dense solve
+
+def test_pcg_matches_dense_solve_at_constant_velocity():
+    """At constant v the discrete GN Hessian is exactly symmetric (P12) and positive definite, so PCG
+    run to a tight tolerance must reproduce numpy.linalg.solve of the dense matrix H, assembled column
+    by column from the oracle matvec on a 4^3 grid (192 unknowns); the forcing rule is checked too."""
+    n, nt = 4, 2
+    prob, st = _const_v_problem(n, nt, (0.37, -0.81, 0.55))
+    N = 3 * n ** 3
+    H = np.empty((N, N))
+    for j in range(N):
+        e = np.zeros(N)
+        e[j] = 1.0
+        H[:, j] = O.hessian_matvec(prob, st, e.reshape(3, n, n, n)).ravel()
+    assert np.abs(H - H.T).max() < 1e-12 * np.abs(H).max()
+    assert np.linalg.eigvalsh(0.5 * (H + H.T)).min() > 0
+    g = synth.smooth_vec(40, n, kmax=1).numpy()
+    dv_ref = np.linalg.solve(H, -g.ravel()).reshape(g.shape)
+    dv, it, rr = O.pcg(prob, st, g, 1e-12, 500)
+    assert rr <= 1e-12 and it <= N
+    assert rel(dv, dv_ref) < 1e-9
+    # inexact solve: the returned residual really is below eta |g|
+    dv2, it2, rr2 = O.pcg(prob, st, g, 0.1, 500)
+    res = O.hessian_matvec(prob, st, dv2) + g
+    assert math.sqrt(O.inner(res, res)) <= 0.1 * math.sqrt(O.inner(g, g)) * (1 + 1e-9) and it2 < it
+    assert abs(rr2 - math.sqrt(O.inner(res, res) / O.inner(g, g))) < 1e-9
+    assert O.forcing(1.0, 1.0) == 0.5 and O.forcing(0.01, 1.0) == 0.01
