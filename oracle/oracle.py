@@ -250,6 +250,32 @@ def inc_state_solve(vt: np.ndarray, G: list[np.ndarray], d_plus: np.ndarray, nt:
     return rt
 
 
+def inc_adjoint_newton_solve(rt1: np.ndarray, lam: list[np.ndarray], vt: np.ndarray, d_minus: np.ndarray, Dv,
+                             nt: int) -> list[np.ndarray]:
+    """Full-Newton incremental adjoint, Eq. 5c with the lambda term kept (NEXT-3):
+      -d_t lt - div(lt v + lam vt) = 0,  lt(1) = -rt(1)  (Eq. 5d).
+    In tau = 1 - t with -v: d_tau lt + (-v).grad lt = lt div v + s, s(t) = div(lam(t) vt)
+    (spectral div, D3).  Eq. 7 with the f terms that depend on X interpolated (reading A11):
+      f0(X) = nu0(X) I[div v](X) + I[s(t_k)](X)     (old level t_k, at the departure point)
+      f*(x) = nu*(x) div v(x) + s(x, t_{k-1})       (new level, at the grid point)
+    Dv = None: div v == 0 (isochoric), the first terms vanish."""
+    dt = 1.0 / nt
+    s = [div(lam[k] * vt) for k in range(nt + 1)]
+    out = [None] * (nt + 1)
+    out[nt] = -_c(rt1)
+    Dbar = None if Dv is None else sl_gather(Dv, d_minus)
+    for k in range(nt, 0, -1):
+        sX = sl_gather(s[k], d_minus)
+        if Dv is None:
+            fX = (lambda nu0X, sX=sX: sX)
+            fx = (lambda nus, k=k: s[k - 1])
+        else:
+            fX = (lambda nu0X, sX=sX: nu0X * Dbar + sX)
+            fx = (lambda nus, k=k: nus * Dv + s[k - 1])
+        out[k - 1] = sl_step(out[k], d_minus, dt, f_at_X=fX, f_at_x=fx)
+    return out
+
+
 def quadrature(lam: list[np.ndarray], G: list[np.ndarray], nt: int) -> np.ndarray:
     """b = int_0^1 lam grad rho dt by the trapezoidal rule on t_j = j dt (reading A12)."""
     dt = 1.0 / nt
@@ -302,15 +328,25 @@ def adjoint_solve(prob: Problem, st: VelocityState) -> list[np.ndarray]:
     return adjoint_like_solve(prob.rho_R - st.rho[-1], st.d_minus, st.Dv, prob.nt)
 
 
-def hessian_matvec(prob: Problem, st: VelocityState, vt: np.ndarray, parts: bool = False):
-    """Gauss-Newton Hessian matvec (Eqs. 5a-5e, GN: the two lambda terms dropped):
-      rho-tilde by Algorithm 2, lam-tilde(1) = -rho-tilde(1) (Eq. 5d), backward GN incremental adjoint,
-      b-tilde = int lam-tilde grad rho dt, H vt = beta A vt + P b-tilde (P = Leray if isochoric, else I)."""
+def hessian_matvec(prob: Problem, st: VelocityState, vt: np.ndarray, parts: bool = False, newton: bool = False,
+                   lam=None):
+    """Hessian matvec (Eqs. 5a-5e):
+      rho-tilde by Algorithm 2, lam-tilde(1) = -rho-tilde(1) (Eq. 5d), backward incremental adjoint,
+      b-tilde = int lam-tilde grad rho dt [+ int lam grad rho-tilde dt], H vt = beta A vt + P b-tilde
+      (P = Leray if isochoric, else I).  Gauss-Newton (default): the two lambda terms dropped.
+      newton=True (NEXT-3): both kept -- div(lam vt) in Eq. 5c and lam grad rho-tilde in b-tilde; needs
+      the adjoint slices `lam` (computed by adjoint_solve when not given)."""
     vt = _c(vt)
     nt = prob.nt
     rt = inc_state_solve(vt, st.G, st.d_plus, nt)
-    lt = adjoint_like_solve(-rt[nt], st.d_minus, st.Dv, nt)
-    bt = quadrature(lt, st.G, nt)
+    if newton:
+        if lam is None:
+            lam = adjoint_solve(prob, st)
+        lt = inc_adjoint_newton_solve(rt[nt], lam, vt, st.d_minus, st.Dv, nt)
+        bt = quadrature(lt, st.G, nt) + quadrature(lam, [grad(r) for r in rt], nt)
+    else:
+        lt = adjoint_like_solve(-rt[nt], st.d_minus, st.Dv, nt)
+        bt = quadrature(lt, st.G, nt)
     reg_term = reg_apply(vt, prob.reg, prob.beta)
     data_term = leray(bt) if prob.iso else bt
     Hv = reg_term + data_term
