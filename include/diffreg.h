@@ -69,13 +69,15 @@ enum { DR_REG_H1 = 1,      /* A = -Laplacian   (H1 seminorm, beta/2 |grad v|^2),
        DR_REG_H2 = 2 };    /* A = Laplacian^2  (H2 seminorm, beta/2 |Lap v|^2), |k|^4   */
 
 enum { DR_ISOCHORIC = 1u,  /* incompressible variant: v Leray-projected, P = Leray  */
-       DR_FP64 = 2u };     /* all fields are double instead of float                             */
+       DR_FP64 = 2u,       /* all fields are double instead of float                             */
+       DR_FULL_NEWTON = 4u };  /* NEXT-3: dr_hessian_matvec keeps the two lambda terms of Eq. 5c /
+                                  b~; default is Gauss-Newton          */
 
 typedef struct dr_config {
     int32_t n[3];   /* N1 (x1, fastest), N2, N3                                                   */
     int32_t nt;     /* number of time steps n_t, dt = 1/n_t; 1 <= nt <= 64          */
     int32_t reg;    /* DR_REG_H1 or DR_REG_H2                                                     */
-    uint32_t flags; /* DR_ISOCHORIC | DR_FP64                                                     */
+    uint32_t flags; /* DR_ISOCHORIC | DR_FP64 | DR_FULL_NEWTON                                    */
     double beta;    /* regularisation parameter beta > 0 (Eq. 2a)                      */
     int32_t ghost_lo, ghost_hi; /* slab ghost planes below / above (multi-GPU only; 0 -> 4 / 5).  A
                                    gather stencil spans floor(s3)-1 .. floor(s3)+2, so (g, g+1) planes

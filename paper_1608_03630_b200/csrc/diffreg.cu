@@ -62,7 +62,7 @@ dr_status validate(const dr_config* c, int nranks = 1) {
     if (c->nt < 1 || c->nt > 64) return DR_ERR_PARAM;
     if (c->reg != DR_REG_H1 && c->reg != DR_REG_H2) return DR_ERR_PARAM;
     if (!(c->beta > 0.0) || !std::isfinite(c->beta)) return DR_ERR_PARAM;
-    if (c->flags & ~(uint32_t)(DR_ISOCHORIC | DR_FP64)) return DR_ERR_PARAM;
+    if (c->flags & ~(uint32_t)(DR_ISOCHORIC | DR_FP64 | DR_FULL_NEWTON)) return DR_ERR_PARAM;
     if (nranks < 1) return DR_ERR_ARG;
     if (nranks > 1) {  // slabs: P | N3 and P | N2 (x2 blocks of the transposes), slab >= ghost width
         if (c->n[2] % nranks || c->n[1] % nranks) return DR_ERR_GRID;
@@ -101,7 +101,7 @@ int64_t n_tiles(const Grid& g) {
 // zg + n3 + zgh planes; every other slot holds the slab's n3 planes.
 struct Layout {
     size_t F, GF, vstride;
-    size_t kry, rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
+    size_t kry, sN, bN, sc, rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
         plan_m, plan_t, maxext, red, twx, twy, twz, twxd, twyd, twzd, total;
 };
 
@@ -139,6 +139,10 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.stin = take(3 * L.F);                   // host staging in
     L.stout = take(3 * L.F);                  // host staging out
     L.kry = take(4 * 3 * L.F);                // PCG work vectors r, z, p, q (NEXT-2)
+    const bool newton = c->flags & DR_FULL_NEWTON;
+    L.sN = newton ? take((size_t)(nt + 1) * L.GF) : 0;  // NEXT-3: s_k = div(lam_k vt) (gathered: ghosted)
+    L.bN = newton ? take(3 * L.F) : 0;                   // NEXT-3: int lam grad rho~ dt
+    L.sc = newton ? take(L.F) : 0;                       // NEXT-3: rho~_j scratch
     // forward half spectra (complex<double>): 6 (+2 transpose buffers with slabs); inverse-direction
     // (complex<T>): 3 (+2)
     L.specD = take((size_t)(dist ? 8 : 6) * g.S * 16);
@@ -291,6 +295,10 @@ struct Impl {
     T* vc(int a) { return gf(c.L.v) + (size_t)a * gstride(); }
     V3<T> v3() { return V3<T>{{vc(0), vc(1), vc(2)}}; }
     T* vraw() { return c.at<T>(c.L.vin); }
+    T* sN(int k) { return gf(c.L.sN) + (size_t)k * gstride(); }
+    T* bN() { return c.at<T>(c.L.bN); }
+    T* sc() { return c.at<T>(c.L.sc); }
+    bool newton() const { return c.cfg.flags & DR_FULL_NEWTON; }
     T* dplus() { return c.at<T>(c.L.dp); }
     T* dminus() { return c.at<T>(c.L.dm); }
     T* mult() { return c.at<T>(c.L.m); }
@@ -823,6 +831,62 @@ struct Impl {
         if (relres) *relres = gnorm > 0 ? rnorm / gnorm : 0.0;
     }
 
+    template <int QUAD>
+    EpiAdjoint<T, QUAD> adjoint_epi(int k, const T* Gk, T wk, T) {
+        EpiAdjoint<T, QUAD> e{};
+        e.out = lt(k - 1);
+        e.m = mult_or_null();
+        e.b0 = bt(); e.b1 = bt() + g.M; e.b2 = bt() + 2 * g.M;
+        e.G0 = Gk; e.G1 = Gk + g.M; e.G2 = Gk + 2 * g.M;
+        e.w = wk;
+        return e;
+    }
+    template <int QUAD>
+    EpiAdjoint<T, QUAD, true> to_newton(const EpiAdjoint<T, QUAD>& a, int k, T dtt) {
+        EpiAdjoint<T, QUAD, true> e{};
+        e.out = a.out; e.m = a.m; e.scale = a.scale;
+        e.b0 = a.b0; e.b1 = a.b1; e.b2 = a.b2;
+        e.G0 = a.G0; e.G1 = a.G1; e.G2 = a.G2;
+        e.w = a.w; e.nu = a.nu; e.snu = a.snu;
+        e.H0 = a.H0; e.H1 = a.H1; e.H2 = a.H2; e.wn = a.wn;
+        e.D = (c.cfg.flags & DR_ISOCHORIC) ? nullptr : Dv();
+        e.snew = sN(k - 1);
+        e.hdt = T(0.5) * dtt;
+        e.dtt = dtt;
+        return e;
+    }
+    // NEXT-3: the two lambda terms of the full-Newton matvec.  Needs the adjoint slices.
+    //   bN = dt sum_j w_j lam_j grad rho~_j   (rho~_j recovered from the inc-state sweep's g_j)
+    //   s_k = div(lam_k vt), k = 0..nt        (sources of Eq. 5c, gathered by the adjoint sweep)
+    void newton_terms(const T* vt) {
+        const int nt = c.cfg.nt;
+        const T dtt = dt();
+        V3<T> gr = vec(tmp3(), (size_t)g.M);
+        bool first = true;
+        for (int j = 1; j <= nt; ++j) {
+            const T* rtj = rt1();
+            if (j < nt) {
+                PB();
+                k_rt_from_g<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, lt(j), vt, G(j), T(0.5) * dtt, sc());
+                PE("newton_rt");
+                rtj = sc();
+            }
+            grad(rtj, gr);
+            const T w = (j == nt) ? T(0.5) * dtt : dtt;
+            PB();
+            k_acc_lam_grad<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, lam(j), tmp3(), w, bN(), first ? 1 : 0);
+            PE("newton_b");
+            first = false;
+        }
+        if (first) CK(cudaMemsetAsync(bN(), 0, 3 * g.M * sizeof(T), s));
+        for (int k = 0; k <= nt; ++k) {
+            PB();
+            k_lam_vt<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, lam(k), vt, tmp3());
+            PE("newton_flux");
+            div(cvec(gr), sN(k));
+        }
+    }
+
     void hessian_matvec(const T* vt, T* Hvt) {
         const int nt = c.cfg.nt;
         const T dtt = dt();
@@ -837,6 +901,7 @@ struct Impl {
                              last ? T(0.5) * dtt : dtt};
             gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), e);
         }
+        if (newton()) newton_terms(vt);
         // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-); every step
         // also accumulates its term of the b~ trapezoid quadrature in its epilogue
         for (int k = nt; k >= 1; --k) {
@@ -844,29 +909,22 @@ struct Impl {
             const T* Gk = G(k - 1);
             const T wk = (k - 1 == 0) ? T(0.5) * dtt : dtt;
             if (k == nt) {
-                EpiAdjoint<T, 1> e{};
-                e.out = lt(k - 1);
-                e.m = mult_or_null();
+                auto e = adjoint_epi<1>(k, Gk, wk, dtt);
                 e.scale = T(-1);
-                e.b0 = bt(); e.b1 = bt() + g.M; e.b2 = bt() + 2 * g.M;
-                e.G0 = Gk; e.G1 = Gk + g.M; e.G2 = Gk + 2 * g.M;
-                e.w = wk;
                 e.nu = rt1(); e.snu = T(-1);
                 const T* Gn = G(nt);
                 e.H0 = Gn; e.H1 = Gn + g.M; e.H2 = Gn + 2 * g.M;
                 e.wn = T(0.5) * dtt;
-                gather<1>("sl_inc_adjoint_q1", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+                if (newton()) gather<2>("sl_inc_adjoint_n1", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt));
+                else gather<1>("sl_inc_adjoint_q1", Src<T, 1>{{src}}, dminus(), plan_m(), e);
             } else {
-                EpiAdjoint<T, 2> e{};
-                e.out = lt(k - 1);
-                e.m = mult_or_null();
+                auto e = adjoint_epi<2>(k, Gk, wk, dtt);
                 e.scale = T(1);
-                e.b0 = bt(); e.b1 = bt() + g.M; e.b2 = bt() + 2 * g.M;
-                e.G0 = Gk; e.G1 = Gk + g.M; e.G2 = Gk + 2 * g.M;
-                e.w = wk;
-                gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+                if (newton()) gather<2>("sl_inc_adjoint_n2", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt));
+                else gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e);
             }
         }
+        if (newton()) axpby(1.0, bN(), 1.0, bt());  // b~ += int lam grad rho~ dt
         // spectral tail: H vt = beta A vt + P b~
         reg_plus_data(cvec(vec(const_cast<T*>(vt), (size_t)g.M)), cvec(vec(bt(), (size_t)g.M)),
                       vec(Hvt, (size_t)g.M));
@@ -1144,6 +1202,10 @@ dr_status dr_hessian_matvec(dr_ctx* c, const void* vt, void* Hvt) {
         with_output(c, Hvt, V, c->ws + c->L.stout, [&](void* out) {
             dispatch(c, [&](auto& im) {
                 using T = std::remove_pointer_t<decltype(im.rhoR())>;
+                if (im.newton() && !c->have_adjoint) {  // the lambda terms need the adjoint slices
+                    im.adjoint_solve();
+                    c->have_adjoint = true;
+                }
                 im.hessian_matvec(static_cast<const T*>(in), static_cast<T*>(out));
             });
         });
@@ -1201,6 +1263,10 @@ dr_status dr_pcg(dr_ctx* c, const void* g, void* dv, double eta, int maxit, int*
         with_output(c, dv, V, c->ws + c->L.stout, [&](void* out) {
             dispatch(c, [&](auto& im) {
                 using T = std::remove_pointer_t<decltype(im.rhoR())>;
+                if (im.newton() && !c->have_adjoint) {
+                    im.adjoint_solve();
+                    c->have_adjoint = true;
+                }
                 im.pcg(static_cast<const T*>(in), static_cast<T*>(out), eta, maxit, iters, relres);
             });
         });

@@ -29,6 +29,35 @@ __global__ void k_axpby(int64_t n, double a, const T* __restrict__ x, double b, 
         y[i] = (b == 0.0) ? (T)(a * (double)x[i]) : (T)(a * (double)x[i] + b * (double)y[i]);
 }
 
+// NEXT-3 helpers.  rho~_j from the merged inc-state variable g_j = rho~_j + dt/2 f_j, f_j = -vt.G_j:
+// rt = g + c vt.G_j (c = dt/2).
+template <typename T>
+__global__ void k_rt_from_g(int64_t M, const T* __restrict__ gj, const T* __restrict__ vt, const T* __restrict__ Gj,
+                            T c, T* __restrict__ rt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
+        rt[i] = gj[i] + c * (vt[i] * Gj[i] + vt[M + i] * Gj[M + i] + vt[2 * M + i] * Gj[2 * M + i]);
+}
+// out (3 components) = lam * vt, the flux whose divergence is the source s = div(lam vt) of Eq. 5c
+template <typename T>
+__global__ void k_lam_vt(int64_t M, const T* __restrict__ lam, const T* __restrict__ vt, T* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const T l = lam[i];
+        out[i] = l * vt[i];
+        out[M + i] = l * vt[M + i];
+        out[2 * M + i] = l * vt[2 * M + i];
+    }
+}
+// b (3 components) (=|+=) w lam * grad  (the int lam grad rho~ dt term of b~, trapezoid weight w)
+template <typename T>
+__global__ void k_acc_lam_grad(int64_t M, const T* __restrict__ lam, const T* __restrict__ gr, T w,
+                               T* __restrict__ b, int init) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const T l = w * lam[i];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) b[a * M + i] = (init ? T(0) : b[a * M + i]) + l * gr[a * M + i];
+    }
+}
+
 template <typename T>
 __global__ void k_scale(int64_t M, const T* __restrict__ a, T* __restrict__ out, T s) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)

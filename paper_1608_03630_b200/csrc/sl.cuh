@@ -175,7 +175,10 @@ struct EpiStore {  // state solve: rho_{j+1} = I[rho_j](X+)   (Eq. 7 with f = 0)
 // reading A12) step by step, so the streaming sum rides on the gather's shared-memory-bound time:
 // QUAD = 1 (first step, k = nt): b~ = w_nt nu_nt G_nt + w_{nt-1} nu_{nt-1} G_{nt-1}, nu_nt read at x;
 // QUAD = 2 (k < nt): b~ += w_{k-1} nu_{k-1} G_{k-1}.
-template <typename T, int QUAD = 0>
+// NEWTON (NEXT-3, full-Newton incremental adjoint, Eq. 5c with div(lam vt)): the gather carries a
+// second component, I[s_k](X) with s_k = div(lam_k vt) at the old level, and Eq. 7 gives
+//   nu_{k-1} = m I[nu_k](X) + dt/2 (1 + dt D(x)) I[s_k](X) + dt/2 s_{k-1}(x)   (D = div v; 0 isochoric).
+template <typename T, int QUAD = 0, bool NEWTON = false>
 struct EpiAdjoint {
     T* out;        // nu_{k-1}
     const T* m;    // nullable (isochoric: m == 1)
@@ -187,10 +190,18 @@ struct EpiAdjoint {
     const T* nu; T snu;                      // QUAD == 1: nu_nt = snu * nu[x]
     const T* H0; const T* H1; const T* H2;   // QUAD == 1: G_nt
     T wn;                                    // QUAD == 1: dt w_nt
-    struct Late { T m; T g[3]; T b[3]; };
+    // NEWTON operands
+    const T* D;                              // div v at x (nullable: isochoric)
+    const T* snew;                           // s_{k-1} at x
+    T hdt, dtt;                              // dt / 2, dt
+    struct Late { T m; T g[3]; T b[3]; T Dx, sn; };
     __device__ __forceinline__ Late late(uint32_t id) const {
         Late l;
         l.m = m ? scale * __ldg(m + id) : scale;
+        if constexpr (NEWTON) {
+            l.Dx = D ? __ldg(D + id) : T(0);
+            l.sn = __ldg(snew + id);
+        }
         if constexpr (QUAD != 0) {
             l.g[0] = __ldg(G0 + id);
             l.g[1] = __ldg(G1 + id);
@@ -209,7 +220,8 @@ struct EpiAdjoint {
         return l;
     }
     __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
-        const T r = l.m * val[0];
+        T r = l.m * val[0];
+        if constexpr (NEWTON) r += hdt * (T(1) + dtt * l.Dx) * val[1] + hdt * l.sn;
         out[id] = r;
         if constexpr (QUAD != 0) {
             const T wr = w * r;
@@ -288,8 +300,10 @@ template <typename T, int NC>
 struct BoxGeom;
 // MINB: CTAs per SM the register budget must allow.
 template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 3; };   // 58 KB
+template <> struct BoxGeom<float, 2> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };   // 115 KB
 template <> struct BoxGeom<float, 3> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };   // 173 KB
 template <> struct BoxGeom<double, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };  // 115 KB
+template <> struct BoxGeom<double, 2> { static constexpr int BX = 48, BY = 14, BZ = 14, MINB = 1; };  // 150 KB
 template <> struct BoxGeom<double, 3> { static constexpr int BX = 48, BY = 14, BZ = 14, MINB = 1; };  // 221 KB
 
 template <typename T, int NC>

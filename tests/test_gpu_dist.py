@@ -86,18 +86,22 @@ def pipeline(ctx, rT, rR, v, vt):
 
 CASES = [
     # n, nt, iso, velocity (max displacement must stay within the 4/5 ghost planes along x3)
+    # [, full Newton]
     ((32, 32, 32), 4, False, lambda n: synth.smooth_vec(9, n, kmax=4, cells_per_step=2.0, nt=4)),
     ((64, 32, 16), 2, True, lambda n: synth.smooth_vec(5, n, kmax=3, cells_per_step=1.5, nt=2, divfree=True)),
     ((16, 64, 32), 4, False, lambda n: synth.v_star(n)),
+    ((32, 32, 32), 2, False, lambda n: synth.smooth_vec(14, n, kmax=4, cells_per_step=1.5, nt=2), True),
+    ((32, 16, 32), 2, True, lambda n: synth.smooth_vec(15, n, kmax=3, cells_per_step=1.5, nt=2, divfree=True), True),
 ]
 
 
 @pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("case", range(len(CASES)))
 def test_slabs_match_single_rank(dr, P, case):
-    n, nt, iso, vgen = CASES[case]
+    n, nt, iso, vgen = CASES[case][:4]
+    newton = len(CASES[case]) > 4 and CASES[case][4]
     D = dr.dist
-    cfg = dr.Config(n=n, nt=nt, reg=dr.DR_REG_H2, beta=1e-2, isochoric=iso)
+    cfg = dr.Config(n=n, nt=nt, reg=dr.DR_REG_H2, beta=1e-2, isochoric=iso, newton=newton)
     if dr.diffreg.dr_workspace_bytes_dist(cfg, P) == 0:
         pytest.skip("grid not divisible into P slabs")
     rT = synth.round32(synth.blobs(11, n, kcut=6)).cuda()

@@ -348,3 +348,32 @@ def test_pcg_against_oracle(dr, case):
     res = O.hessian_matvec(prob, st, np64(dv)) + g64
     assert rr <= eta and 0 < it < 50
     assert np.sqrt(O.inner(res, res) / O.inner(g64, g64)) < eta + 1e-4
+
+
+# ------------------------------------------------------------------ NEXT-3: full-Newton matvec
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("case", CASES[:3], ids=[c[0] for c in CASES[:3]])
+def test_full_newton_matvec(dr, case, fp64):
+    """DR_FULL_NEWTON: Eq. 5c with div(lam vt) and b~ with lam grad rho~ against the
+    oracle's full-Newton matvec; the images differ (rho_R unrelated to rho(1)), so lambda != 0."""
+    name, n, nt, vgen, iso = case
+    top, tmv = tols(fp64)
+    cfg = dr.Config(n=n, nt=nt, reg=2, beta=1e-2, isochoric=iso, fp64=fp64, newton=True)
+    ctx = dr.Context(cfg)
+    rT, rT64 = prep(synth.blobs(11, n, kcut=10) if name != "cfg1" else synth.rho_t_paper(n), fp64)
+    rR, rR64 = prep(synth.blobs(12, n, kcut=10), fp64)
+    v, v64 = prep(vgen(n), fp64)
+    vt, vt64 = prep(synth.smooth_vec(13, n, kmax=4, divfree=iso), fp64)
+    ctx.set_images(rT.cuda(), rR.cuda())
+    ctx.set_velocity(v.cuda())
+    ctx.forward_solve()
+    Hv = np64(ctx.hessian_matvec(vt.cuda()))
+    prob = O.Problem(rho_T=rT64, rho_R=rR64, nt=nt, reg=2, beta=1e-2, iso=iso)
+    st = O.set_velocity(prob, v64)
+    ref, parts = O.hessian_matvec(prob, st, vt64, parts=True, newton=True)
+    assert rel(np64(ctx.get_field(dr.DR_FIELD_BTILDE)), parts["btilde"]) < tmv
+    assert rel(Hv, ref) < tmv
+    # and it differs from Gauss-Newton by much more than the tolerance
+    gn = O.hessian_matvec(prob, st, vt64)
+    assert rel(gn, ref) > 100 * tmv
