@@ -404,3 +404,102 @@ def pcg(prob: Problem, st: VelocityState, g: np.ndarray, eta: float, maxit: int)
         p = z + (rz_new / rz) * p
         rz = rz_new
     return dv, it, rnorm / gnorm
+
+
+# ------------------------------------------------------------------ NEXT-4: deformation map, det grad y
+
+def deformation(v: np.ndarray, d_plus: np.ndarray, nt: int) -> np.ndarray:
+    """Displacement u_1 = y_1 - x of the deformation map, Eq. 1: d_t y + v.grad y = 0,
+    y(0) = x.  With y = x + u (u periodic): d_t u + v.grad u = -v, u(0) = 0, solved by Eq. 7 with the
+    source f = -v (stationary, independent of u): f0(X) = I[-v](X), f*(x) = -v(x)."""
+    v = _c(v)
+    dt = 1.0 / nt
+    u = np.zeros_like(v)
+    fX = np.stack([sl_gather(-v[a], d_plus) for a in range(3)])
+    for _ in range(nt):
+        u = np.stack([sl_step(u[a], d_plus, dt, f_at_X=lambda _n, a=a: fX[a], f_at_x=lambda _n, a=a: -v[a])
+                      for a in range(3)])
+    return u
+
+
+def det_grad_y(u: np.ndarray) -> np.ndarray:
+    """det(grad y_1) = det(I + grad u_1) pointwise (Fig. 7 caption), grad by D3."""
+    J = np.empty((3, 3) + u.shape[1:])
+    for a in range(3):
+        ga = grad(u[a])
+        for b in range(3):
+            J[a, b] = ga[b] + (1.0 if a == b else 0.0)
+    return (J[0, 0] * (J[1, 1] * J[2, 2] - J[1, 2] * J[2, 1]) - J[0, 1] * (J[1, 0] * J[2, 2] - J[1, 2] * J[2, 0]) +
+            J[0, 2] * (J[1, 0] * J[2, 1] - J[1, 1] * J[2, 0]))
+
+
+# ------------------------------------------------------------------ NEXT-4: Armijo Gauss-Newton-Krylov
+
+def solve(prob: Problem, v0: np.ndarray, gtol: float = 1e-2, max_newton: int = 50, max_krylov: int = 100,
+          c1: float = 1e-4, shrink: float = 0.5, max_backtracks: int = 20, newton: bool = False):
+    """Inexact (Gauss-)Newton-Krylov with Armijo line search:
+      g_k = g(v_k); stop when |g_k| <= gtol |g_0|;  PCG on H dv = -g_k with eta = forcing(|g_k|, |g_0|);
+      alpha = 1, shrink until J(v_k + alpha dv) <= J(v_k) + c1 alpha <g_k, dv>;  v_{k+1} = v_k + alpha dv.
+    Returns (v, history, reason): history rows (J, |g|/|g0|, pcg iterations, alpha, cumulative matvecs)."""
+    v = _c(v0).copy()
+    st = set_velocity(prob, v)
+    J = objective(prob, st)
+    g = gradient(prob, st)
+    g0 = math.sqrt(inner(g, g))
+    hist, matvecs, reason = [], 0, "max_newton"
+    for _ in range(max_newton):
+        gn = math.sqrt(inner(g, g))
+        if gn <= gtol * g0:
+            reason = "converged"
+            break
+        lam = adjoint_solve(prob, st) if newton else None
+        dv, it, _ = _pcg_op(prob, st, g, forcing(gn, g0), max_krylov, newton, lam)
+        matvecs += it
+        slope = inner(g, dv)
+        alpha, accepted = 1.0, False
+        for _ in range(max_backtracks + 1):
+            st_try = set_velocity(prob, v + alpha * dv)
+            J_try = objective(prob, st_try)
+            if J_try <= J + c1 * alpha * slope:
+                accepted = True
+                break
+            alpha *= shrink
+        if not accepted:
+            reason = "line_search_failed"
+            break
+        v = v + alpha * dv
+        st, J = st_try, J_try
+        g = gradient(prob, st)
+        hist.append((J, math.sqrt(inner(g, g)) / g0, it, alpha, matvecs))
+    else:
+        if math.sqrt(inner(g, g)) <= gtol * g0:
+            reason = "converged"
+    return v, hist, reason
+
+
+def _pcg_op(prob, st, g, eta, maxit, newton, lam):
+    """pcg() with the (Gauss-)Newton matvec of the current linearisation."""
+    if not newton:
+        return pcg(prob, st, g, eta, maxit)
+    g = _c(g)
+    dv = np.zeros_like(g)
+    r = -g
+    gnorm = math.sqrt(inner(g, g))
+    z = precond(r, prob.reg, prob.beta, prob.iso)
+    p = z.copy()
+    rz = inner(r, z)
+    it, rnorm = 0, gnorm
+    while it < maxit and rnorm > eta * gnorm:
+        q = hessian_matvec(prob, st, p, newton=True, lam=lam)
+        alpha = rz / inner(p, q)
+        dv = dv + alpha * p
+        r = r - alpha * q
+        it += 1
+        rnorm = math.sqrt(inner(r, r))
+        if rnorm <= eta * gnorm:
+            break
+        z = precond(r, prob.reg, prob.beta, prob.iso)
+        rz_new = inner(r, z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return dv, it, rnorm / gnorm

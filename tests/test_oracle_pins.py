@@ -590,3 +590,45 @@ def test_newton_equals_gauss_newton_at_zero_adjoint():
         a = O.hessian_matvec(prob, st, vt, newton=True)
         b = O.hessian_matvec(prob, st, vt)
         assert np.array_equal(a, b) or rel(a, b) < 1e-15
+
+
+# ------------------------------------------------------------------ NEXT-4: deformation map and solver
+
+def test_deformation_special_cases():
+    """Eq. 1: v = 0 gives y_1 = x (u = 0, det = 1, bitwise); constant v = c gives y_1 = x - c exactly
+    (a constant source transported at constant displacement), det = 1; a divergence-free v preserves
+    volume up to discretisation error, which shrinks under refinement."""
+    n, nt = 16, 4
+    z = np.zeros((3, n, n, n))
+    u = O.deformation(z, O.departure(z, nt, +1), nt)
+    assert np.array_equal(u, z) and np.array_equal(O.det_grad_y(u), np.ones((n, n, n)))
+    c = np.array([0.37, -0.81, 0.55])
+    vc = np.ones((3, n, n, n)) * c[:, None, None, None]
+    u = O.deformation(vc, O.departure(vc, nt, +1), nt)
+    assert np.abs(u + vc).max() < 1e-13
+    assert np.abs(O.det_grad_y(u) - 1).max() < 1e-12
+    errs = []
+    for n, nt in ((16, 4), (32, 8)):
+        v = 0.5 * synth.v_cfg1(n).numpy()  # divergence-free (BJ config 1's field)
+        u = O.deformation(v, O.departure(v, nt, +1), nt)
+        errs.append(np.abs(O.det_grad_y(u) - 1).max())
+    assert errs[1] < errs[0] < 0.05, errs
+
+
+def test_solver_reduces_gradient_on_synthetic_problem():
+    """NEXT-4 on the paper's synthetic problem: rho_T = (sin^2 x1 + sin^2 x2 + sin^2 x3)/3,
+    rho_R = rho_T transported by v*; GN-Krylov with Armijo reaches g_tol = 1e-2, J decreases
+    monotonically, every accepted step satisfies the Armijo condition, det grad y_1 > 0."""
+    n, nt = 16, 4
+    rT = synth.rho_t_paper(n).numpy()
+    vstar = synth.v_star(n).numpy()
+    prob0 = O.Problem(rho_T=rT, rho_R=rT, nt=nt, reg=2, beta=1e-2)
+    rR = O.set_velocity(prob0, vstar).rho[-1]
+    prob = O.Problem(rho_T=rT, rho_R=rR, nt=nt, reg=2, beta=1e-2)
+    J0 = O.objective(prob, O.set_velocity(prob, np.zeros_like(vstar)))
+    v, hist, reason = O.solve(prob, np.zeros_like(vstar), gtol=1e-2, max_newton=20)
+    assert reason == "converged" and hist[-1][1] <= 1e-2
+    Js = [J0] + [h[0] for h in hist]
+    assert all(b < a for a, b in zip(Js[:-1], Js[1:]))
+    st = O.set_velocity(prob, v)
+    assert O.det_grad_y(O.deformation(v, st.d_plus, nt)).min() > 0
