@@ -186,6 +186,41 @@ dr_status dr_objective(dr_ctx* ctx, double* J, double* misfit);
  * the stream once per inner product. */
 dr_status dr_pcg(dr_ctx* ctx, const void* g, void* dv, double eta, int maxit, int* iters, double* relres);
 
+/* NEXT-4: deformation map and its Jacobian determinant.  u = y_1 - x where
+ * d_t y + v.grad y = 0, y(0) = x (Eq. 1; transported like the state, Eq. 7 with the
+ * stationary source -v) and det = det(grad y_1) = det(I + grad u) (Fig. 7 caption, P:L537;
+ * det > 0 everywhere <=> diffeomorphism).  u (vector), det (scalar): nullable, device or host;
+ * det_min / det_max (host, nullable): extrema over all ranks.  Requires dr_set_velocity; clobbers
+ * the incremental fields of the last matvec (dr_get_field INC_* / BTILDE need a new matvec).
+ * Synchronises. */
+dr_status dr_deformation(dr_ctx* ctx, void* u, void* det, double* det_min, double* det_max);
+
+/* NEXT-4: Armijo-globalised inexact (Gauss-)Newton-Krylov registration.
+ * Iterates g_k = g(v_k) (dr_gradient); stops when |g_k| <= gtol |g_0|; Newton step by dr_pcg with the
+ * quadratic forcing eta = min(0.5, |g_k| / |g_0|) (reading A22) and at most max_krylov matvecs;
+ * backtracking alpha = 1, alpha *= shrink until J(v + alpha dv) <= J(v) + c1 alpha <g, dv>.  Uses
+ * the full-Newton matvec when the context has DR_FULL_NEWTON, else Gauss-Newton.
+ * v: DEVICE vector field, in: initial velocity, out: the last accepted iterate (with its state
+ * solved: dr_get_field / dr_deformation apply to it).  opts NULL: {1e-2, 50, 100, 1e-4, 0.5, 20}.
+ * rep (nullable): summary and, if history != NULL, history_len rows of (J, |g|/|g0|, PCG matvecs,
+ * alpha, cumulative matvecs) per Newton iteration.  Requires dr_set_images.  Collective. */
+typedef struct dr_solve_opts {
+    double gtol;         /* relative gradient tolerance g_tol (1e-2)   */
+    int32_t max_newton;  /* Newton iterations                                   */
+    int32_t max_krylov;  /* PCG matvecs per Newton step                         */
+    double c1;           /* Armijo sufficient-decrease constant                 */
+    double shrink;       /* backtracking factor                                 */
+    int32_t max_backtracks;
+} dr_solve_opts;
+enum { DR_SOLVE_CONVERGED = 0, DR_SOLVE_MAX_NEWTON = 1, DR_SOLVE_LINESEARCH_FAILED = 2 };
+typedef struct dr_solve_report {
+    int32_t iterations, matvecs, reason;
+    double J0, J, g0, g;  /* objective and |g| (discrete L2) at the start / end */
+    double* history;      /* caller-owned, 5 * history_len doubles, nullable */
+    int32_t history_len;
+} dr_solve_report;
+dr_status dr_solve(dr_ctx* ctx, void* v, const dr_solve_opts* opts, dr_solve_report* rep);
+
 /* Wait for all work of the context; surfaces asynchronous CUDA errors. */
 dr_status dr_sync(dr_ctx* ctx);
 

@@ -887,6 +887,157 @@ struct Impl {
         }
     }
 
+    // ---------------------------------------------------------------- NEXT-4: deformation map
+    // u_1 = y_1 - x (Eq. 1): d_t u + v.grad u = -v, u(0) = 0, Eq. 7 with the stationary source
+    // f = -v merged into the gather like Algorithm 2: w_0 = -dt/2 v, w_{j+1} = I[w_j](X+) - dt v(x),
+    // u_1 = I[w_{nt-1}](X+) - dt/2 v(x).  Ping-pongs through two ghosted slots (lt(0), rho~(1)).
+    void deformation(V3<T> u) {
+        const int nt = c.cfg.nt;
+        const T dtt = dt();
+        for (int a = 0; a < 3; ++a) {
+            T* w[2] = {lt(0), rt1()};
+            PB();
+            k_scale<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, vc(a), w[0], T(-0.5) * dtt);
+            PE("deform_init");
+            for (int j = 0; j < nt; ++j) {
+                const bool last = (j == nt - 1);
+                T* out = last ? u.c[a] : w[(j + 1) & 1];
+                gather<1>("sl_deform", Src<T, 1>{{w[j & 1]}}, dplus(), plan_p(),
+                          EpiAddScaled<T>{out, vc(a), last ? T(-0.5) * dtt : -dtt});
+            }
+        }
+    }
+    // det grad y_1 = det(I + grad u_1) and its extrema over all ranks
+    void det_grad_y(V3<const T> u, T* det, double* mn, double* mx) {
+        for (int a = 0; a < 3; ++a) grad(u.c[a], vec(kry(a), (size_t)g.M));
+        PB();
+        k_det<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, kry(0), kry(1), kry(2), det);
+        PE("det");
+        double* part = c.at<double>(c.L.red);
+        const int nb = (int)std::min<int64_t>(1024, (g.M + 255) / 256);
+        PB();
+        k_minmax_parts<T><<<nb, 256, 0, s>>>(g.M, det, part);
+        PE("reduce");
+        PB();
+        k_minmax_final<<<1, 256, 0, s>>>(part, nb, part + 2048);
+        PE("reduce");
+        // extrema over ranks: min = -max(-x); gather both per rank through allsum's slots
+        double loc[2];
+        CK(cudaMemcpyAsync(loc, part + 2048, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double lo = loc[0], hi = loc[1];
+        if (c.dist()) {
+            double* slots = c.at<double>(c.L.red) + 3072;  // [P] lows, then [P] highs
+            const int P = c.nranks;
+            CK(cudaMemcpyAsync(slots + c.rank, part + 2048, sizeof(double), cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(slots + 512 + c.rank, part + 2049, sizeof(double), cudaMemcpyDeviceToDevice, s));
+            std::vector<P2P> ops;
+            for (int q = 0; q < P; ++q) {
+                if (q == c.rank) continue;
+                ops.push_back(P2P{true, q, part + 2048, nullptr, sizeof(double)});
+                ops.push_back(P2P{true, q, part + 2049, nullptr, sizeof(double)});
+                ops.push_back(P2P{false, q, nullptr, slots + q, sizeof(double)});
+                ops.push_back(P2P{false, q, nullptr, slots + 512 + q, sizeof(double)});
+            }
+            exchange(ops);
+            std::vector<double> h(2 * 512);
+            CK(cudaMemcpyAsync(h.data(), slots, 1024 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            lo = h[0];
+            hi = h[512];
+            for (int q = 1; q < P; ++q) {
+                lo = std::min(lo, h[q]);
+                hi = std::max(hi, h[512 + q]);
+            }
+        }
+        if (mn) *mn = lo;
+        if (mx) *mx = hi;
+    }
+
+    // ---------------------------------------------------------------- NEXT-4: Armijo (G)N-Krylov solver
+    // g_k = g(v_k); stop at |g_k| <= gtol |g_0|; PCG on H dv = -g_k with the quadratic
+    // forcing eta = min(0.5, |g_k| / |g_0|); alpha = 1, shrink until J(v + alpha dv) <= J + c1 alpha <g, dv>.
+    // v: the current velocity (device, the rank's slab) -- input the initial guess, output the solution.
+    void solve(T* v, const dr_solve_opts& o, dr_solve_report* rep) {
+        const size_t V = 3 * g.M;
+        const double hv = (2.0 * M_PI / g.n1) * (2.0 * M_PI / g.n2) * (2.0 * M_PI / g.n3g);
+        T* gk = stout();  // gradient
+        T* dv = stin();   // Newton step
+        T* vtry = kry(0) + 0;  // trial velocity lives in the PCG's r slot only between PCG calls
+        auto set_and_solve = [&](const T* vel) {
+            set_velocity(vel);
+            c.have_velocity = true;
+            forward_solve();
+            c.have_state = true;
+            c.have_adjoint = false;
+        };
+        set_and_solve(v);
+        double J = 0;
+        objective(&J, nullptr);
+        adjoint_solve();
+        c.have_adjoint = true;
+        gradient(vec(gk, (size_t)g.M));
+        const double g0 = std::sqrt(hv * dot3(gk, gk));
+        double gn = g0;
+        int it = 0, matvecs = 0, reason = DR_SOLVE_MAX_NEWTON;
+        if (rep) {
+            rep->J0 = J;
+            rep->g0 = g0;
+        }
+        for (; it < o.max_newton; ++it) {
+            if (gn <= o.gtol * g0) {
+                reason = DR_SOLVE_CONVERGED;
+                break;
+            }
+            int pit = 0;
+            double rr = 0;
+            const double eta = std::min(0.5, gn / g0);
+            pcg(gk, dv, eta, o.max_krylov, &pit, &rr);
+            matvecs += pit;
+            const double slope = hv * dot3(gk, dv);
+            double alpha = 1.0, Jt = 0;
+            bool ok = false;
+            for (int b = 0; b <= o.max_backtracks; ++b) {
+                CK(cudaMemcpyAsync(vtry, v, V * sizeof(T), cudaMemcpyDeviceToDevice, s));
+                axpby(alpha, dv, 1.0, vtry);
+                set_and_solve(vtry);
+                objective(&Jt, nullptr);
+                if (Jt <= J + o.c1 * alpha * slope) {
+                    ok = true;
+                    break;
+                }
+                alpha *= o.shrink;
+            }
+            if (!ok) {
+                reason = DR_SOLVE_LINESEARCH_FAILED;
+                set_and_solve(v);  // restore the state of the last accepted iterate
+                break;
+            }
+            CK(cudaMemcpyAsync(v, vtry, V * sizeof(T), cudaMemcpyDeviceToDevice, s));
+            J = Jt;
+            adjoint_solve();
+            c.have_adjoint = true;
+            gradient(vec(gk, (size_t)g.M));
+            gn = std::sqrt(hv * dot3(gk, gk));
+            if (rep && rep->history && it < rep->history_len) {
+                double* h = rep->history + 5 * it;
+                h[0] = J;
+                h[1] = gn / g0;
+                h[2] = pit;
+                h[3] = alpha;
+                h[4] = matvecs;
+            }
+        }
+        if (it == o.max_newton && gn <= o.gtol * g0) reason = DR_SOLVE_CONVERGED;
+        if (rep) {
+            rep->iterations = it;
+            rep->matvecs = matvecs;
+            rep->reason = reason;
+            rep->J = J;
+            rep->g = gn;
+        }
+    }
+
     void hessian_matvec(const T* vt, T* Hvt) {
         const int nt = c.cfg.nt;
         const T dtt = dt();
@@ -1271,6 +1422,45 @@ dr_status dr_pcg(dr_ctx* c, const void* g, void* dv, double eta, int maxit, int*
             });
         });
         c->have_matvec = false;  // the matvec test hooks would show the last Krylov matvec
+    });
+}
+
+dr_status dr_deformation(dr_ctx* c, void* u, void* det, double* det_min, double* det_max) {
+    return run(c, [&] {
+        if (!c->have_velocity) fail(DR_ERR_ORDER, "deformation needs set_velocity");
+        const size_t V = 3 * c->g.M * elem_size(c), F = c->g.M * elem_size(c);
+        dispatch(c, [&](auto& im) {
+            using T = std::remove_pointer_t<decltype(im.rhoR())>;
+            T* uo = im.tmp3();
+            im.deformation(vec(uo, (size_t)c->g.M));
+            c->have_matvec = false;  // the deformation reuses the matvec's scratch slices
+            if (det || det_min || det_max) {
+                T* d = im.bt();  // scratch scalar (b~ is not needed afterwards)
+                im.det_grad_y(cvec(vec(uo, (size_t)c->g.M)), d, det_min, det_max);
+                if (det) CK(cudaMemcpyAsync(det, d, F, cudaMemcpyDefault, c->stream));
+            }
+            if (u) CK(cudaMemcpyAsync(u, uo, V, cudaMemcpyDefault, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        });
+    });
+}
+
+dr_status dr_solve(dr_ctx* c, void* v, const dr_solve_opts* opts, dr_solve_report* rep) {
+    return run(c, [&] {
+        if (!v) fail(DR_ERR_ARG, "v must be non-NULL");
+        if (!c->have_images) fail(DR_ERR_ORDER, "solve needs set_images");
+        dr_solve_opts o{1e-2, 50, 100, 1e-4, 0.5, 20};
+        if (opts) o = *opts;
+        if (!(o.gtol > 0) || o.max_newton < 0 || o.max_krylov < 1 || !(o.c1 > 0 && o.c1 < 1) ||
+            !(o.shrink > 0 && o.shrink < 1) || o.max_backtracks < 0)
+            fail(DR_ERR_PARAM, "invalid solver options");
+        if (!is_device_ptr(v)) fail(DR_ERR_ARG, "dr_solve takes a device velocity");
+        dispatch(c, [&](auto& im) {
+            using T = std::remove_pointer_t<decltype(im.rhoR())>;
+            im.solve(static_cast<T*>(v), o, rep);
+        });
+        c->have_matvec = false;
+        CK(cudaStreamSynchronize(c->stream));
     });
 }
 

@@ -58,6 +58,66 @@ __global__ void k_acc_lam_grad(int64_t M, const T* __restrict__ lam, const T* __
     }
 }
 
+// det(I + grad u) pointwise from the nine derivatives d[a][b] = du_a/dx_b (Fig. 7 caption)
+template <typename T>
+__global__ void k_det(int64_t M, const T* __restrict__ d0, const T* __restrict__ d1, const T* __restrict__ d2,
+                      T* __restrict__ det) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const double a00 = 1.0 + (double)d0[i], a01 = d0[M + i], a02 = d0[2 * M + i];
+        const double a10 = d1[i], a11 = 1.0 + (double)d1[M + i], a12 = d1[2 * M + i];
+        const double a20 = d2[i], a21 = d2[M + i], a22 = 1.0 + (double)d2[2 * M + i];
+        det[i] = (T)(a00 * (a11 * a22 - a12 * a21) - a01 * (a10 * a22 - a12 * a20) + a02 * (a10 * a21 - a11 * a20));
+    }
+}
+
+// min / max partials of a field (block b writes part[2b], part[2b+1]); k_minmax_final folds them
+template <typename T>
+__global__ void __launch_bounds__(256) k_minmax_parts(int64_t M, const T* __restrict__ a, double* __restrict__ part) {
+    __shared__ double lo[256], hi[256];
+    double l = 1e308, h = -1e308;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = (double)a[i];
+        l = x < l ? x : l;
+        h = x > h ? x : h;
+    }
+    lo[threadIdx.x] = l;
+    hi[threadIdx.x] = h;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            lo[threadIdx.x] = fmin(lo[threadIdx.x], lo[threadIdx.x + s]);
+            hi[threadIdx.x] = fmax(hi[threadIdx.x], hi[threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = lo[0];
+        part[2 * blockIdx.x + 1] = hi[0];
+    }
+}
+__global__ void __launch_bounds__(256) k_minmax_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double lo[256], hi[256];
+    double l = 1e308, h = -1e308;
+    for (int i = threadIdx.x; i < n; i += 256) {
+        l = fmin(l, part[2 * i]);
+        h = fmax(h, part[2 * i + 1]);
+    }
+    lo[threadIdx.x] = l;
+    hi[threadIdx.x] = h;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            lo[threadIdx.x] = fmin(lo[threadIdx.x], lo[threadIdx.x + s]);
+            hi[threadIdx.x] = fmax(hi[threadIdx.x], hi[threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = lo[0];
+        out[1] = hi[0];
+    }
+}
+
 template <typename T>
 __global__ void k_scale(int64_t M, const T* __restrict__ a, T* __restrict__ out, T s) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)

@@ -233,6 +233,16 @@ struct EpiAdjoint {
 };
 
 template <typename T>
+struct EpiAddScaled {  // out = I[w](X) + c f(x): the merged-source step of the deformation map (NEXT-4)
+    T* out;
+    const T* f;
+    T c;
+    struct Late { T f; };
+    __device__ __forceinline__ Late late(uint32_t id) const { return Late{__ldg(f + id)}; }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const { out[id] = val[0] + c * l.f; }
+};
+
+template <typename T>
 struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+) + c f_{j+1}, f = -vt.G_{j+1}
     T* out;
     const T* vt0; const T* vt1; const T* vt2;  // vt components

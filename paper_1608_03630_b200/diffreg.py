@@ -32,13 +32,27 @@ EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr
            "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry",
            "dr_nccl_get_unique_id", "dr_comm_create_nccl", "dr_hub_create", "dr_hub_destroy",
            "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist",
-           "dr_gradient", "dr_objective", "dr_pcg"]
+           "dr_gradient", "dr_objective", "dr_pcg", "dr_deformation", "dr_solve"]
 
 
 class dr_config(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32 * 3), ("nt", ctypes.c_int32), ("reg", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("beta", ctypes.c_double), ("ghost_lo", ctypes.c_int32),
                 ("ghost_hi", ctypes.c_int32)]
+
+
+class dr_solve_opts(ctypes.Structure):
+    _fields_ = [("gtol", ctypes.c_double), ("max_newton", ctypes.c_int32), ("max_krylov", ctypes.c_int32),
+                ("c1", ctypes.c_double), ("shrink", ctypes.c_double), ("max_backtracks", ctypes.c_int32)]
+
+
+class dr_solve_report(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("matvecs", ctypes.c_int32), ("reason", ctypes.c_int32),
+                ("J0", ctypes.c_double), ("J", ctypes.c_double), ("g0", ctypes.c_double), ("g", ctypes.c_double),
+                ("history", ctypes.POINTER(ctypes.c_double)), ("history_len", ctypes.c_int32)]
+
+
+SOLVE_REASONS = {0: "converged", 1: "max_newton", 2: "line_search_failed"}
 
 
 class DiffRegError(RuntimeError):
@@ -78,7 +92,10 @@ def lib():
         L.dr_workspace_bytes_dist.restype = ctypes.c_size_t
         L.dr_create_dist.argtypes = [ctypes.POINTER(dr_config), vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
         L.dr_create_dist.restype = ctypes.c_int
-        for name, args in [("dr_pcg", [vp, vp, vp, ctypes.c_double, i32, ctypes.POINTER(i32),
+        for name, args in [("dr_deformation", [vp, vp, vp, ctypes.POINTER(ctypes.c_double),
+                                               ctypes.POINTER(ctypes.c_double)]),
+                           ("dr_solve", [vp, vp, ctypes.POINTER(dr_solve_opts), ctypes.POINTER(dr_solve_report)]),
+                           ("dr_pcg", [vp, vp, vp, ctypes.c_double, i32, ctypes.POINTER(i32),
                                        ctypes.POINTER(ctypes.c_double)]),
                            ("dr_gradient", [vp, vp]),
                            ("dr_objective", [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
@@ -312,6 +329,28 @@ class Context:
         it, rr = ctypes.c_int(), ctypes.c_double()
         self._check(lib().dr_pcg(self.h, self._in(g), _ptr(dv), eta, maxit, ctypes.byref(it), ctypes.byref(rr)))
         return dv, it.value, rr.value
+
+    def deformation(self, want_u=True, want_det=True):
+        """(u_1 = y_1 - x or None, det grad y_1 or None, det min, det max)."""
+        u = self.vector() if want_u else None
+        det = self.scalar() if want_det else None
+        lo, hi = ctypes.c_double(), ctypes.c_double()
+        self._check(lib().dr_deformation(self.h, _ptr(u), _ptr(det), ctypes.byref(lo), ctypes.byref(hi)))
+        return u, det, lo.value, hi.value
+
+    def solve(self, v, gtol=1e-2, max_newton=50, max_krylov=100, c1=1e-4, shrink=0.5, max_backtracks=20):
+        """Armijo (G)N-Krylov registration from the device velocity v (updated in place).
+        Returns (report dict, history rows [(J, |g|/|g0|, pcg matvecs, alpha, cumulative matvecs)])."""
+        o = dr_solve_opts(gtol, max_newton, max_krylov, c1, shrink, max_backtracks)
+        hist = (ctypes.c_double * (5 * max(1, max_newton)))()
+        r = dr_solve_report()
+        r.history = hist
+        r.history_len = max_newton
+        self._check(lib().dr_solve(self.h, self._in(v), ctypes.byref(o), ctypes.byref(r)))
+        rows = [tuple(hist[5 * i:5 * i + 5]) for i in range(min(r.iterations, max_newton))]
+        rep = {"iterations": r.iterations, "matvecs": r.matvecs, "reason": SOLVE_REASONS.get(r.reason, r.reason),
+               "J0": r.J0, "J": r.J, "g0": r.g0, "g": r.g}
+        return rep, rows
 
     def objective(self):
         """(J, misfit) as Python floats (collective with slabs)."""

@@ -78,6 +78,8 @@ def pipeline(ctx, rT, rR, v, vt):
     J, mis = ctx.objective()
     dv, it, rr = ctx.pcg(vt, 0.0, 2)
     res["pcg"] = dv
+    u, det, lo, hi = ctx.deformation()
+    res["u"], res["det"] = u, det
     ctx.sync()
     out = {k: t.clone() for k, t in res.items()}
     out["_J"] = (J, mis)

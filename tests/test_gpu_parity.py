@@ -377,3 +377,48 @@ def test_full_newton_matvec(dr, case, fp64):
     # and it differs from Gauss-Newton by much more than the tolerance
     gn = O.hessian_matvec(prob, st, vt64)
     assert rel(gn, ref) > 100 * tmv
+
+
+# ------------------------------------------------------------------ NEXT-4: deformation map and solver
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("case", CASES[:3], ids=[c[0] for c in CASES[:3]])
+def test_deformation_map(dr, case, fp64):
+    """u_1 = y_1 - x (Eq. 1) and det grad y_1 (Fig. 7 caption) against the oracle."""
+    name, n, nt, vgen, iso = case
+    top, tmv = tols(fp64)
+    ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, fp64)
+    st = O.set_velocity(prob, v64)
+    u, det, lo, hi = ctx.deformation()
+    uref = O.deformation(st.v, st.d_plus, nt)
+    dref = O.det_grad_y(uref)
+    assert rel(np64(u), uref) < top
+    # det is stored in the field precision: near-volume-preserving maps (det - 1 ~ 1e-4) are compared
+    # absolutely, not through the relative error of det - 1
+    assert rel(np64(det), dref) < top and np.abs(np64(det) - dref).max() < 10 * top
+    assert abs(lo - dref.min()) < 10 * top and abs(hi - dref.max()) < 10 * top
+
+
+@pytest.mark.parametrize("newton", [False, True])
+def test_solver_on_synthetic_problem(dr, newton):
+    """The paper's synthetic problem at 16^3, n_t = 4, H2, beta = 1e-2, g_tol = 1e-2:
+    the GPU's Armijo (G)N-Krylov run follows the fp64 oracle's run iteration by iteration."""
+    n, nt = 16, 4
+    rT, rT64 = prep(synth.rho_t_paper(n), False)
+    vs, vs64 = prep(synth.v_star(n), False)
+    prob0 = O.Problem(rho_T=rT64, rho_R=rT64, nt=nt, reg=2, beta=1e-2)
+    rR64 = O.set_velocity(prob0, vs64).rho[-1]
+    rR, rR64 = prep(torch.from_numpy(rR64), False)
+    prob = O.Problem(rho_T=rT64, rho_R=rR64, nt=nt, reg=2, beta=1e-2)
+    vref, hist_ref, reason_ref = O.solve(prob, np.zeros_like(vs64), gtol=1e-2, max_newton=20, newton=newton)
+    ctx = dr.Context(dr.Config(n=n, nt=nt, reg=2, beta=1e-2, newton=newton))
+    ctx.set_images(rT.cuda(), rR.cuda())
+    v = torch.zeros((3, n, n, n), dtype=torch.float32, device="cuda")
+    rep, hist = ctx.solve(v, gtol=1e-2, max_newton=20)
+    assert rep["reason"] == reason_ref == "converged"
+    assert rep["iterations"] == len(hist_ref) and [h[2] for h in hist] == [h[2] for h in hist_ref]
+    for a, b in zip(hist, hist_ref):
+        assert abs(a[0] - b[0]) < 1e-4 * abs(b[0]) and abs(a[1] - b[1]) < 1e-3 and a[3] == b[3]
+    assert rel(np64(v), vref) < 1e-3
+    _, det, lo, hi = ctx.deformation(want_u=False)
+    assert lo > 0
