@@ -36,9 +36,14 @@ struct CtaThreads {  // fp64 passes: fewer threads per CTA (large register footp
     static constexpr int V = sizeof(T) == 8 ? 128 : 256;
 };
 // Minimum resident CTAs of a pass for __launch_bounds__: 3 x 256 threads for fp32 compute (<= 80
-// registers); 3 x 128 for fp64 (<= 170 registers for the radix-16 fp64 butterflies).
+// registers); 4 x 128 for fp64 (<= 128 registers for the radix-16 fp64 butterflies), 3 x 128 for the
+// fp64 middle pass (measured: r2c 67 -> 64 us at 128 registers, middle 88 -> 92 us).
 template <typename T, int NT>
 struct MinB {
+    static constexpr int V = sizeof(T) == 8 ? ((512 / NT) > 0 ? 512 / NT : 1) : ((768 / NT) > 0 ? 768 / NT : 1);
+};
+template <typename T, int NT>
+struct MinBMiddle {  // the x3 middle pass keeps 160 registers in fp64 (forward + symbol + fp32 inverse)
     static constexpr int V = sizeof(T) == 8 ? ((384 / NT) > 0 ? 384 / NT : 1) : ((768 / NT) > 0 ? 768 / NT : 1);
 };
 // Row passes: RB rows per CTA.
@@ -588,7 +593,7 @@ struct MiddlePass {
     using CC = ColCfg<L, T, NCI>;
     static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
     static constexpr int TPLO = Tpl<L, To>::V;  // threads per inverse line (fp32: fewer than fp64)
-    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr int MINB = MinBMiddle<T, NT>::V;
     static constexpr size_t BUFI = CC::SMEM;
     static constexpr size_t BUF = BUFI + (size_t)NCO * LINES * LP * sizeof(Cx<To>);
     ColGeom c;

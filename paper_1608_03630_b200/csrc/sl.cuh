@@ -309,7 +309,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <typename T, int NC>
 struct BoxGeom;
 // MINB: CTAs per SM the register budget must allow.
-template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 3; };   // 58 KB
+template <> struct BoxGeom<float, 1> { static constexpr int BX = 64, BY = 15, BZ = 14, MINB = 4; };   // 54 KB
 template <> struct BoxGeom<float, 2> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };   // 115 KB
 template <> struct BoxGeom<float, 3> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };   // 173 KB
 template <> struct BoxGeom<double, 1> { static constexpr int BX = 64, BY = 15, BZ = 15, MINB = 1; };  // 115 KB
@@ -502,8 +502,31 @@ __device__ __forceinline__ void pair_from_box(const Grid& g, const TileCtx<T, NC
 // (C) per pair: issue the next pair's loads, gather the 64 stencil values per point from shared memory
 // -- the two points as one packed fp32x2 pair (FFMA2) -- and finish the step.  Tiles whose box exceeds
 // the compile-time capacity gather from global memory instead (same arithmetic, one point at a time).
+// Resident CTAs per SM of a gather (fp32, one component): 4 (64 registers) unless the epilogue's
+// operands need more registers without spilling (inc-state source, adjoint + quadrature): 3 (80).
+template <class Epi>
+struct EpiMinB {
+    static constexpr int V = 4;
+};
+template <typename T>
+struct EpiMinB<EpiIncState<T>> {
+    static constexpr int V = 3;
+};
+template <typename T, bool N>
+struct EpiMinB<EpiAdjoint<T, 1, N>> {
+    static constexpr int V = 3;
+};
+template <typename T, bool N>
+struct EpiMinB<EpiAdjoint<T, 2, N>> {
+    static constexpr int V = 3;
+};
 template <typename T, int NC, class Epi>
-__global__ void __launch_bounds__(SL_THREADS, BoxGeom<T, NC>::MINB)
+struct GatherMinB {
+    static constexpr int V = (sizeof(T) == 4 && NC == 1) ? EpiMinB<Epi>::V : BoxGeom<T, NC>::MINB;
+};
+
+template <typename T, int NC, class Epi>
+__global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
     k_sl_gather(Grid g, Src<T, NC> src, Disp<T> d, const int* __restrict__ plan, int ntiles, Epi epi) {
     constexpr int H = SL_TZ / 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
