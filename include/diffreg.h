@@ -123,6 +123,10 @@ dr_status dr_hub_create(int nranks, dr_hub** out);
 dr_status dr_hub_destroy(dr_hub* hub);
 dr_status dr_comm_create_loopback(dr_hub* hub, int rank, dr_comm** out);
 dr_status dr_comm_destroy(dr_comm* comm);
+/* Communicator self-test: an all-to-all of rank-stamped 1 KiB chunks (self included) through the same
+ * grouped send/recv path the slab exchanges use, on `stream`; *ok = 1 when every chunk arrived intact.
+ * Collective.  Allocates (and frees) 2 P KiB of device memory. */
+dr_status dr_comm_selftest(dr_comm* comm, void* stream, int* ok);
 
 /* Host-only partition query: the slab [z0, z0 + nz) of `rank` (no GPU needed). */
 dr_status dr_slab(const dr_config* cfg, int nranks, int rank, int* z0, int* nz);

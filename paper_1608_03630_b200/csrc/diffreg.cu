@@ -1262,6 +1262,54 @@ dr_status dr_comm_destroy(dr_comm* c) {
     return DR_OK;
 }
 
+namespace {
+__global__ void k_fill_rank(int* buf, int n, int value) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) buf[i] = value * 1000 + i;
+}
+}  // namespace
+
+dr_status dr_comm_selftest(dr_comm* comm, void* stream, int* ok) {
+    if (!comm || !ok) return DR_ERR_ARG;
+    *ok = 0;
+    Comm& C = *comm->impl;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int P = C.size, n = 256;
+    int *send = nullptr, *recv = nullptr;
+    if (cudaMalloc(&send, (size_t)P * n * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&recv, (size_t)P * n * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        if (send) cudaFree(send);
+        return DR_ERR_OOM;
+    }
+    dr_status st = DR_OK;
+    try {
+        for (int q = 0; q < P; ++q) k_fill_rank<<<1, 256, 0, s>>>(send + q * n, n, C.rank);
+        cudaMemsetAsync(recv, 0xff, (size_t)P * n * sizeof(int), s);
+        std::vector<P2P> ops;
+        for (int q = 0; q < P; ++q) {  // an all-to-all of rank-stamped chunks, self included
+            ops.push_back(P2P{true, q, send + q * n, nullptr, n * sizeof(int)});
+            ops.push_back(P2P{false, q, nullptr, recv + q * n, n * sizeof(int)});
+        }
+        C.group(ops, s);
+        std::vector<int> h((size_t)P * n);
+        if (cudaMemcpyAsync(h.data(), recv, h.size() * sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            st = DR_ERR_CUDA;
+        bool good = st == DR_OK;
+        for (int q = 0; q < P && good; ++q)
+            for (int i = 0; i < n; ++i)
+                if (h[(size_t)q * n + i] != q * 1000 + i) good = false;
+        *ok = good ? 1 : 0;
+        if (!C.check().empty()) st = DR_ERR_NCCL;
+    } catch (const std::exception&) {
+        st = DR_ERR_NCCL;
+    }
+    cudaFree(send);
+    cudaFree(recv);
+    cudaGetLastError();
+    return st;
+}
+
 dr_status dr_create(const dr_config* cfg, void* workspace, size_t workspace_bytes, void* stream, dr_ctx** out) {
     return dr_create_dist(cfg, nullptr, workspace, workspace_bytes, stream, out);
 }

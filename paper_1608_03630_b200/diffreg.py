@@ -32,7 +32,7 @@ EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr
            "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry",
            "dr_nccl_get_unique_id", "dr_comm_create_nccl", "dr_hub_create", "dr_hub_destroy",
            "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist",
-           "dr_gradient", "dr_objective", "dr_pcg", "dr_deformation", "dr_solve"]
+           "dr_gradient", "dr_objective", "dr_pcg", "dr_deformation", "dr_solve", "dr_comm_selftest"]
 
 
 class dr_config(ctypes.Structure):
@@ -92,7 +92,8 @@ def lib():
         L.dr_workspace_bytes_dist.restype = ctypes.c_size_t
         L.dr_create_dist.argtypes = [ctypes.POINTER(dr_config), vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
         L.dr_create_dist.restype = ctypes.c_int
-        for name, args in [("dr_deformation", [vp, vp, vp, ctypes.POINTER(ctypes.c_double),
+        for name, args in [("dr_comm_selftest", [vp, vp, ctypes.POINTER(i32)]),
+                           ("dr_deformation", [vp, vp, vp, ctypes.POINTER(ctypes.c_double),
                                                ctypes.POINTER(ctypes.c_double)]),
                            ("dr_solve", [vp, vp, ctypes.POINTER(dr_solve_opts), ctypes.POINTER(dr_solve_report)]),
                            ("dr_pcg", [vp, vp, vp, ctypes.c_double, i32, ctypes.POINTER(i32),
@@ -193,6 +194,15 @@ class Comm:
         if st != DR_OK:
             raise DiffRegError(st, lib().dr_status_string(st).decode())
         return cls(h, rank, size)
+
+    def selftest(self, stream=None) -> bool:
+        """All-to-all of rank-stamped chunks through the library's exchange path (collective)."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        ok = ctypes.c_int()
+        st = lib().dr_comm_selftest(self.h, ctypes.c_void_p(s.cuda_stream), ctypes.byref(ok))
+        if st != DR_OK:
+            raise DiffRegError(st, lib().dr_status_string(st).decode())
+        return bool(ok.value)
 
     def close(self):
         if getattr(self, "h", None):

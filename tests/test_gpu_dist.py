@@ -197,3 +197,30 @@ def test_slab_rejects_displacement_beyond_ghosts(dr):
         return 0
 
     assert run_ranks(P, rank) == [dr.DR_ERR_PLAN] * P
+
+
+def test_nccl_communicator_single_rank(dr):
+    """The real NCCL backend (dlopen'ed libnccl.so.2, grouped ncclSend/ncclRecv) on the one GPU this box
+    has: a 1-rank communicator passes the exchange self-test and carries a slab context's matvec."""
+    uid = dr.diffreg.nccl_unique_id()
+    comm = dr.diffreg.Comm.nccl(uid, 0, 1)
+    assert comm.selftest()
+    n = (16, 16, 16)
+    cfg = dr.Config(n=n, nt=2)
+    rT = synth.round32(synth.blobs(31, n, kcut=4)).cuda()
+    v = synth.round32(synth.smooth_vec(32, n, kmax=2, cells_per_step=1.0, nt=2)).cuda()
+    vt = synth.round32(synth.smooth_vec(33, n, kmax=3)).cuda()
+    a = pipeline(dr.Context(cfg, comm=comm), rT, rT, v, vt)
+    b = pipeline(dr.Context(cfg), rT, rT, v, vt)
+    for k in b:
+        if k != "_J":
+            assert torch.equal(a[k], b[k]), k
+    comm.close()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_communicator_selftest(dr, P):
+    hub = dr.diffreg.Hub(P)
+    comms = [hub.comm(r) for r in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    assert run_ranks(P, lambda r: comms[r].selftest(streams[r])) == [True] * P
