@@ -101,10 +101,12 @@ dr_status dr_destroy(dr_ctx* ctx);
  * decomposition, and of its ghost-layer interpolation, Algorithm 1).
  * Rank r owns the x3 planes [r N3/P, (r+1) N3/P) of every field; all field arguments of a
  * distributed context are that rank's slab: scalar [N3/P][N2][N1], vector [3][N3/P][N2][N1].
- * Requirements: P | N3, P | N2, N3/P >= ghost_hi (default ghost planes (4, 5) cover x3 displacements
- * of up to 3 cells; dr_config.ghost_lo/hi widen them up to a whole slab; a displacement beyond the
- * ghosts returns DR_ERR_PLAN from dr_set_velocity -- the off-rank departure-point scatter of the
- * paper's Algorithm 1 is not implemented, widened ghosts replace it).  Exchanges: ghost planes before every semi-Lagrangian gather and
+ * Requirements: P | N3, P | N2, P <= 32, N3/P >= ghost_hi.  Ghost planes (default (4, 5), widened
+ * with dr_config.ghost_lo/hi) serve departure points up to ghost_lo - 1 cells away along x3; points
+ * farther out (any distance, several slabs included) are served by the off-rank scatter of the
+ * paper's Algorithm 1: their cells go to the owning rank once per velocity, and every
+ * gather the owners interpolate and return the values.  dr_set_velocity returns DR_ERR_PLAN only if
+ * a rank's remote points exceed the scatter capacity (M/8 per displacement field).  Exchanges: ghost planes before every semi-Lagrangian gather and
  * all-to-all transposes around the x3 FFT pass, stream-ordered on the context stream.  Every rank
  * must make the same sequence of calls (collective semantics).
  *

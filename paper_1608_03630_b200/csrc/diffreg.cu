@@ -101,6 +101,8 @@ int64_t n_tiles(const Grid& g) {
 // zg + n3 + zgh planes; every other slot holds the slab's n3 planes.
 struct Layout {
     size_t F, GF, vstride;
+    int64_t rcap = 0;
+    size_t rem = 0;
     size_t kry, sN, bN, sc, rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
         plan_m, plan_t, maxext, red, twx, twy, twz, twxd, twyd, twzd, total;
 };
@@ -147,6 +149,11 @@ Layout layout(const dr_config* c, int nranks = 1) {
     // (complex<T>): 3 (+2)
     L.specD = take((size_t)(dist ? 8 : 6) * g.S * 16);
     L.specF = take((size_t)(dist ? 5 : 3) * g.S * 2 * es);
+    // off-rank departure points (dist only): per displacement field (d*, d+, d-) ids + records out and in,
+    // values out and in (3 components), capacity M / 8 points each way
+    L.rcap = dist ? std::max<int64_t>(1024, g.M / 8) : 0;
+    const size_t es2 = es;
+    L.rem = dist ? take(3 * (size_t)L.rcap * (2 * 4 + 2 * (12 + 3 * es2) + 2 * 3 * es2) + 3 * 4 * 4 * 64) : 0;
     L.xs = dist ? take(L.F) : 0;              // real-field transpose buffers (x3 derivatives)
     L.xr = dist ? take(L.F) : 0;
     const size_t pb = (size_t)n_tiles(g) * PLAN_INTS * sizeof(int);
@@ -183,6 +190,11 @@ struct dr_ctx {
     cudaStream_t hi = nullptr;                // high-priority stream: the gather sweeps while aux runs
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hi = nullptr;
     bool overlap = false;                     // DR_OVERLAP=1 in the environment at dr_create
+    struct RemotePlanH {                      // host side of an off-rank plan (per displacement field)
+        bool any = false;                     // some rank has remote points for this field
+        std::vector<int> out_cnt, out_off, in_cnt, in_off;
+        int n_out = 0, n_in = 0;
+    } rp[3];
     int num_sms = 148;
     int rank = 0, nranks = 1;
     dr::Comm* comm = nullptr;  // not owned; NULL with one rank
@@ -627,6 +639,111 @@ struct Impl {
         PE("sl_plan");
     }
 
+    // ---------------------------------------------------------------- off-rank departure points
+    // device arrays of remote plan f (0: d*, 1: d+, 2: d-): [ids_out][ids_in][rec_out][rec_in][val_out][val_in]
+    // then 4 int arrays of 64 (cnt, off, cursor, scratch)
+    struct RP {
+        int *ids_out;
+        RemoteRec<T> *rec_out, *rec_in;
+        T *val_out, *val_in;
+        int *cnt, *off, *cur;
+    };
+    RP rp(int f) {
+        const size_t cap = (size_t)c.L.rcap;
+        char* b = c.ws + c.L.rem + (size_t)f * cap * (2 * 4 + 2 * sizeof(RemoteRec<T>) + 2 * 3 * sizeof(T));
+        RP r;
+        r.ids_out = reinterpret_cast<int*>(b);
+        b += 2 * cap * 4;
+        r.rec_out = reinterpret_cast<RemoteRec<T>*>(b);
+        r.rec_in = r.rec_out + cap;
+        b += 2 * cap * sizeof(RemoteRec<T>);
+        r.val_out = reinterpret_cast<T*>(b);
+        r.val_in = r.val_out + 3 * cap;
+        int* ints = reinterpret_cast<int*>(c.ws + c.L.rem + 3 * cap * (2 * 4 + 2 * sizeof(RemoteRec<T>) + 2 * 3 * sizeof(T)));
+        r.cnt = ints + f * 192;
+        r.off = r.cnt + 64;
+        r.cur = r.cnt + 128;
+        return r;
+    }
+    int field_of(const int* plan_buf) { return plan_buf == plan_t() ? 0 : plan_buf == plan_p() ? 1 : 2; }
+    // classify the points of displacement field d whose stencil leaves the slab + ghosts, send their
+    // cells to the owners (counts, then records), once per velocity
+    void remote_plan(int f, const T* d) {
+        auto& H = c.rp[f];
+        H = dr_ctx::RemotePlanH{};
+        if (!c.dist()) return;
+        const int P = c.nranks;
+        RP r = rp(f);
+        const Disp<T> dp{{d, d + g.M, d + 2 * g.M}};
+        CK(cudaMemsetAsync(r.cnt, 0, 192 * sizeof(int), s));
+        PB();
+        k_remote_classify<T><<<grid_1d(g.M), 256, 0, s>>>(g, dp, 0, r.cnt, r.off, r.cur, r.ids_out, r.rec_out, 0);
+        PE("remote_plan");
+        H.out_cnt.assign(P, 0);
+        CK(cudaMemcpyAsync(H.out_cnt.data(), r.cnt, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        H.out_off.assign(P, 0);
+        for (int q = 1; q < P; ++q) H.out_off[q] = H.out_off[q - 1] + H.out_cnt[q - 1];
+        H.n_out = H.out_off[P - 1] + H.out_cnt[P - 1];
+        // counts to the owners (the receiving side learns its in-counts)
+        int* cnt_in = r.cnt + 64 * 0 + 32;  // scratch inside cnt's 64 slots (P <= 32)
+        if (P > 32) fail(DR_ERR_PLAN, "remote plans support at most 32 ranks");
+        {
+            std::vector<P2P> ops;
+            for (int q = 0; q < P; ++q) {
+                ops.push_back(P2P{true, q, r.cnt + q, nullptr, sizeof(int)});
+                ops.push_back(P2P{false, q, nullptr, cnt_in + q, sizeof(int)});
+            }
+            exchange(ops);
+        }
+        H.in_cnt.assign(P, 0);
+        CK(cudaMemcpyAsync(H.in_cnt.data(), cnt_in, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        H.in_off.assign(P, 0);
+        for (int q = 1; q < P; ++q) H.in_off[q] = H.in_off[q - 1] + H.in_cnt[q - 1];
+        H.n_in = H.in_off[P - 1] + H.in_cnt[P - 1];
+        if (H.n_out > c.L.rcap || H.n_in > c.L.rcap)
+            fail(DR_ERR_PLAN, "off-rank departure points exceed the scatter capacity (M/8 per rank)");
+        CK(cudaMemcpyAsync(r.off, H.out_off.data(), P * sizeof(int), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(r.cur, 0, 64 * sizeof(int), s));
+        if (H.n_out > 0) {
+            PB();
+            k_remote_classify<T><<<grid_1d(g.M), 256, 0, s>>>(g, dp, 1, r.cnt, r.off, r.cur, r.ids_out, r.rec_out,
+                                                                (int)c.L.rcap);
+            PE("remote_plan");
+        }
+        {  // records to the owners
+            std::vector<P2P> ops;
+            for (int q = 0; q < P; ++q) {
+                ops.push_back(P2P{true, q, r.rec_out + H.out_off[q], nullptr, H.out_cnt[q] * sizeof(RemoteRec<T>)});
+                ops.push_back(P2P{false, q, nullptr, r.rec_in + H.in_off[q], H.in_cnt[q] * sizeof(RemoteRec<T>)});
+            }
+            exchange(ops);
+        }
+        // does any rank have remote points for this field?  (every rank must join the per-gather exchange)
+        double* tot = c.at<double>(c.L.red) + 4000;
+        const double mine = (double)H.n_out;
+        CK(cudaMemcpyAsync(tot, &mine, sizeof(double), cudaMemcpyHostToDevice, s));
+        H.any = allsum(tot) > 0;
+    }
+    // per gather: owners interpolate the incoming cells, values go back to the requesters
+    template <int NC>
+    void remote_serve(int f, const Src<T, NC>& base_src) {
+        auto& H = c.rp[f];
+        RP r = rp(f);
+        if (H.n_in > 0) {
+            PB();
+            k_remote_eval<T, NC><<<grid_1d(H.n_in), 256, 0, s>>>(g, base_src, r.rec_in, H.n_in, r.val_in);
+            PE("remote_eval");
+        }
+        std::vector<P2P> ops;
+        for (int q = 0; q < c.nranks; ++q) {
+            ops.push_back(P2P{true, q, r.val_in + (size_t)H.in_off[q] * NC, nullptr, (size_t)H.in_cnt[q] * NC * sizeof(T)});
+            ops.push_back(P2P{false, q, nullptr, r.val_out + (size_t)H.out_off[q] * NC, (size_t)H.out_cnt[q] * NC * sizeof(T)});
+        }
+        exchange(ops);
+    }
+
     // gather sources are ghosted fields: the kernel indexes x3 from the slot base (zg planes below)
     template <int NC, class Epi>
     void gather(const char* tag, Src<T, NC> src, const T* d, const int* plan_buf, Epi epi) {
@@ -634,6 +751,9 @@ struct Impl {
             ghosts(const_cast<T*>(src.p[cc]));
             src.p[cc] -= (size_t)g.zg * plane();
         }
+        const int f = field_of(plan_buf);
+        const bool remote = c.dist() && c.rp[f].any;
+        if (remote) remote_serve<NC>(f, src);
         constexpr size_t sm = box_bytes<T, NC>();
         auto k = k_sl_gather<T, NC, Epi>;
         set_smem(k, sm);
@@ -642,6 +762,12 @@ struct Impl {
         PB();
         k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
         PE(tag);
+        if (remote && c.rp[f].n_out > 0) {
+            RP r = rp(f);
+            PB();
+            k_remote_fixup<T, NC, Epi><<<grid_1d(c.rp[f].n_out), 256, 0, s>>>(r.ids_out, r.val_out, c.rp[f].n_out, epi);
+            PE("remote_fixup");
+        }
     }
     int* plan_p() { return c.at<int>(c.L.plan_p); }
     int* plan_m() { return c.at<int>(c.L.plan_m); }
@@ -670,6 +796,7 @@ struct Impl {
                                                     (T)(sg * dtt / h[1]), (T)(sg * dtt / h[2]));
             PE("dstar");
             plan(tmp3(), plan_t());
+            remote_plan(0, tmp3());
             EpiDeparture<T> e;
             e.d0 = dout;
             e.d1 = dout + g.M;
@@ -678,27 +805,15 @@ struct Impl {
             e.v1 = vc(1);
             e.v2 = vc(2);
             for (int a = 0; a < 3; ++a) e.c[a] = (T)(sg * 0.5 * dtt / h[a]);
-            check_plan();
             gather<3>("sl_departure", Src<T, 3>{{vc(0), vc(1), vc(2)}}, tmp3(), plan_t(), e);
             plan(dout, sg > 0 ? plan_p() : plan_m());
+            remote_plan(sg > 0 ? 1 : 2, dout);
         }
-        check_plan();
         if (!(c.cfg.flags & DR_ISOCHORIC)) {
             div(cvec(v3()), Dv());
             gather<1>("sl_multiplier", Src<T, 1>{{Dv()}}, dminus(), plan_m(), EpiMultiplier<T>{mult(), Dv(), dt()});
         }
     }
-    // slabs: every departure stencil must lie in the rank's planes plus ghosts (no off-rank scatter yet)
-    void check_plan() {
-        if (!c.dist()) return;
-        int flag = 0;
-        CK(cudaMemcpyAsync(&flag, c.at<int>(c.L.maxext) + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (flag)
-            fail(DR_ERR_PLAN, "x3 displacement exceeds the slab ghost planes (widen dr_config.ghost_lo/hi; "
-                              "off-rank departure-point scatter is not implemented)");
-    }
-
     void forward_solve() {
         for (int j = 0; j < c.cfg.nt; ++j) gather_scalar_p(rho(j), rho(j + 1));
         for (int j = 0; j <= c.cfg.nt; ++j) grad(rho(j), G3(j));

@@ -395,6 +395,8 @@ __device__ __forceinline__ TileCtx<T, NC> tile_ctx(const Grid& g, const int* __r
     c.ey = q.x;
     c.ez = q.y;
     c.fits = c.ex <= BX && c.ey <= BY && c.ez <= BZ;
+    // slabs: a box leaving the planes + ghosts holds points served by their owner rank (scatter)
+    if (g.ghost && (c.oz - g.z0 + g.zg < 0 || c.oz + c.ez - g.z0 > g.n3 + g.zgh)) c.fits = false;
     return c;
 }
 
@@ -545,12 +547,12 @@ __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
 #pragma unroll 1
         for (int k = 0; k < kmax; ++k) {
             const uint32_t id = id0 + k * plane;
-            const typename Epi::Late lt = epi.late(id);
             int q1, q2, q3;
             T t1, t2, t3;
             cell_of<T>(x, __ldg(d.p[0] + id), q1, t1);
             cell_of<T>(y, __ldg(d.p[1] + id), q2, t2);
             cell_of<T>(c.z0 + k + g.z0, __ldg(d.p[2] + id), q3, t3);
+            if (g.ghost && (q3 - 1 < g.z0 - g.zg || q3 + 2 >= g.z0 + g.n3 + g.zgh)) continue;  // remote point
             T w1[4], w2[4], w3[4];
             lagrange4(t1, w1);
             lagrange4(t2, w2);
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
             T val[NC];
 #pragma unroll
             for (int cc = 0; cc < NC; ++cc) val[cc] = interp_global(src.p[cc], g, q1, q2, q3, w1, w2, w3);
-            epi.store(id, val, lt);
+            epi.store(id, val, epi.late(id));
         }
         return;
     }
@@ -576,6 +578,87 @@ __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
         pair_from_box<T, NC, Epi>(g, c, box, x, y, c.z0 + p, id0 + p * plane, id0 + (p + H) * plane, p + H < kmax,
                                   cur, epi);
         cur = nxt;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Off-rank departure points (slabs; the paper's Algorithm 1, on x3 slabs).  A point whose
+// stencil planes floor(s3)-1 .. floor(s3)+2 leave the rank's planes + ghosts is served by the rank
+// owning plane floor(s3): its cell (q, t) travels there once per velocity (the plan), and every gather
+// the owner interpolates the requested values and returns them; the requester finishes the step with
+// the same epilogue (k_remote_fixup).  Interpolation uses interp_global on both sides of the ghosts,
+// so results are the single-rank arithmetic.
+template <typename T>
+struct RemoteRec {
+    int q[3];
+    T t[3];
+};
+
+__device__ __forceinline__ int remote_owner(const Grid& g, int q3) {
+    int w = q3 % g.n3g;
+    if (w < 0) w += g.n3g;
+    return w / g.n3;
+}
+
+// pass 0: count remote points per owner rank; pass 1: write ids and records (slot = off + cursor)
+template <typename T>
+__global__ void k_remote_classify(Grid g, Disp<T> d, int pass, int* __restrict__ cnt, const int* __restrict__ off,
+                                  int* __restrict__ cursor, int* __restrict__ ids, RemoteRec<T>* __restrict__ rec,
+                                  int cap) {
+    const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.M; e += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(e % g.n1), y = (int)((e / g.n1) % g.n2), z = (int)(e / plane);
+        int q3;
+        T t3;
+        cell_of<T>(z + g.z0, __ldg(d.p[2] + e), q3, t3);
+        if (!(q3 - 1 < g.z0 - g.zg || q3 + 2 >= g.z0 + g.n3 + g.zgh)) continue;
+        const int dst = remote_owner(g, q3);
+        if (pass == 0) {
+            atomicAdd(&cnt[dst], 1);
+            continue;
+        }
+        const int slot = off[dst] + atomicAdd(&cursor[dst], 1);
+        if (slot >= cap) continue;  // capacity is checked on the host before this pass
+        int q1, q2;
+        T t1, t2;
+        cell_of<T>(x, __ldg(d.p[0] + e), q1, t1);
+        cell_of<T>(y, __ldg(d.p[1] + e), q2, t2);
+        ids[slot] = (int)e;
+        RemoteRec<T> r;
+        r.q[0] = q1;
+        r.q[1] = q2;
+        int w = q3 % g.n3g;
+        r.q[2] = w < 0 ? w + g.n3g : w;
+        r.t[0] = t1;
+        r.t[1] = t2;
+        r.t[2] = t3;
+        rec[slot] = r;
+    }
+}
+
+// owner side: interpolate NC ghosted source fields at n incoming cells
+template <typename T, int NC>
+__global__ void k_remote_eval(Grid g, Src<T, NC> src, const RemoteRec<T>* __restrict__ rec, int n, T* __restrict__ val) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const RemoteRec<T> r = rec[i];
+        T w1[4], w2[4], w3[4];
+        lagrange4(r.t[0], w1);
+        lagrange4(r.t[1], w2);
+        lagrange4(r.t[2], w3);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) val[(size_t)i * NC + c] = interp_global(src.p[c], g, r.q[0], r.q[1], r.q[2], w1, w2, w3);
+    }
+}
+
+// requester side: finish the step for its remote points with the returned values
+template <typename T, int NC, class Epi>
+__global__ void k_remote_fixup(const int* __restrict__ ids, const T* __restrict__ val, int n, Epi epi) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t id = (uint32_t)ids[i];
+        T v[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = val[(size_t)i * NC + c];
+        epi.store(id, v, epi.late(id));
     }
 }
 

@@ -176,27 +176,40 @@ def test_widened_ghosts_carry_large_displacement(dr):
         assert torch.equal(dr.dist.assemble([o[k] for o in outs]), full), k
 
 
-def test_slab_rejects_displacement_beyond_ghosts(dr):
-    """|d3| > 3 cells leaves the ghost planes: set_velocity reports DR_ERR_PLAN on every rank."""
-    P, n = 2, (16, 16, 32)
+@pytest.mark.parametrize("P,cells", [(2, 6.0), (4, 9.0)])
+def test_scatter_of_far_departure_points(dr, P, cells):
+    """Displacements beyond the default (4, 5) ghost planes -- up to 9 cells with 8-plane slabs, i.e.
+    owners two slabs away -- go through the off-rank scatter (Alg. 1): owners interpolate
+    the requested cells and return the values; the whole pipeline stays bit-identical to one rank."""
+    n = (16, 16, 32)
     cfg = dr.Config(n=n, nt=2)
-    v = synth.round32(synth.smooth_vec(4, n, kmax=2, cells_per_step=6.0, nt=2)).cuda()
+    rT = synth.round32(synth.blobs(24, n, kcut=5)).cuda()
+    rR = synth.round32(synth.blobs(25, n, kcut=5)).cuda()
+    v = synth.round32(synth.smooth_vec(4, n, kmax=2, cells_per_step=cells, nt=2)).cuda()
+    vt = synth.round32(synth.smooth_vec(26, n, kmax=3)).cuda()
+    ref = pipeline(dr.Context(cfg), rT, rR, v, vt)
     hub = dr.diffreg.Hub(P)
     comms = [hub.comm(r) for r in range(P)]
     streams = [torch.cuda.Stream() for _ in range(P)]
     ctxs = [dr.Context(cfg, stream=streams[r], comm=comms[r]) for r in range(P)]
-    vs = [dr.dist.slab_of(v, cfg, P, r) for r in range(P)]
+    sl = lambda x, r: dr.dist.slab_of(x, cfg, P, r)  # noqa: E731
+    ins = [(sl(rT, r), sl(rR, r), sl(v, r), sl(vt, r)) for r in range(P)]
     torch.cuda.synchronize()
 
     def rank(r):
         with torch.cuda.stream(streams[r]):
-            try:
-                ctxs[r].set_velocity(vs[r])
-            except dr.DiffRegError as e:
-                return e.status
-        return 0
+            out = pipeline(ctxs[r], *ins[r])
+        streams[r].synchronize()
+        return out
 
-    assert run_ranks(P, rank) == [dr.DR_ERR_PLAN] * P
+    outs = run_ranks(P, rank)
+    for k, full in ref.items():
+        if k == "_J":
+            continue
+        got = dr.dist.assemble([o[k] for o in outs])
+        assert rel(got, full) < 1e-6, (k, rel(got, full))
+        if k != "pcg":
+            assert torch.equal(got, full), (k, rel(got, full))
 
 
 def test_nccl_communicator_single_rank(dr):
