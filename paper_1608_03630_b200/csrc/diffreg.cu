@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -432,10 +433,17 @@ struct Impl {
         using PT = RowDerivPass<T, L>;
         stream("row_deriv", PT{g, f, out, acc, twx()}, row_tiles<PT::RB>());
     }
-    template <int L>
-    void row_r2c_L(const T* f, Cx<double>* sp) {
-        using PT = RowR2cPass<T, double, L>;
-        stream("row_r2c", PT{g, f, sp, twxd()}, row_tiles<PT::RB>());
+    // twiddle tables by compute type (the forward spectral passes run in double, or in T for symbols that
+    // damp high wavenumbers -- see spec_forward)
+    template <typename U> const Cx<U>* twx_t() { if constexpr (sizeof(U) == sizeof(double)) return reinterpret_cast<const Cx<U>*>(twxd()); else return reinterpret_cast<const Cx<U>*>(twx()); }
+    template <typename U> const Cx<U>* twy_t() { if constexpr (sizeof(U) == sizeof(double)) return reinterpret_cast<const Cx<U>*>(twyd()); else return reinterpret_cast<const Cx<U>*>(twy()); }
+    template <typename U> const Cx<U>* twz_t() { if constexpr (sizeof(U) == sizeof(double)) return reinterpret_cast<const Cx<U>*>(twzd()); else return reinterpret_cast<const Cx<U>*>(twz()); }
+    template <typename U> Cx<U>* specD_t(int i) { return reinterpret_cast<Cx<U>*>(c.ws + c.L.specD) + (size_t)i * g.S; }
+
+    template <int L, typename Tc>
+    void row_r2c_L(const T* f, Cx<Tc>* sp) {
+        using PT = RowR2cPass<T, Tc, L>;
+        stream("row_r2c", PT{g, f, sp, twx_t<Tc>()}, row_tiles<PT::RB>());
     }
     template <int L>
     void row_c2r_L(const Cx<T>* sp, T* out, const T* add) {
@@ -475,8 +483,9 @@ struct Impl {
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
     }
-    void row_r2c(const T* f, Cx<double>* sp) {
-#define CALL(LL) row_r2c_L<LL>(f, sp)
+    template <typename Tc>
+    void row_r2c(const T* f, Cx<Tc>* sp) {
+#define CALL(LL) row_r2c_L<LL, Tc>(f, sp)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
     }
@@ -536,8 +545,9 @@ struct Impl {
         const ColGeom cg = spec_geom();
         stream(DIR < 0 ? "col_fft_fwd" : "col_fft_inv", PT{cg, src, dst, tw, nb_in, nb_out}, col_tiles<PT>(cg, g.n3));
     }
-    void col_fft_fwd(const Cx<double>* src, Cx<double>* dst, int nb_out) {  // forward along x2, in double
-#define CALL(LL) col_fft_L<double, LL, -1>(src, dst, twyd(), 0, nb_out)
+    template <typename Tc>
+    void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out) {  // forward along x2, in Tc
+#define CALL(LL) col_fft_L<Tc, LL, -1>(src, dst, twy_t<Tc>(), 0, nb_out)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
@@ -547,22 +557,22 @@ struct Impl {
 #undef CALL
     }
 
-    template <int L, int KIND>
-    void middle_L(const ColGeom& cg, Cx<double>* const* in, Cx<T>* const* out) {
-        using PT = MiddlePass<double, T, L, KIND>;
+    template <int L, int KIND, typename Tc>
+    void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out) {
+        using PT = MiddlePass<Tc, T, L, KIND>;
         PT pt;
         pt.c = cg;
         for (int i = 0; i < PT::NCI; ++i) pt.in.p[i] = in[i];
         for (int i = 0; i < PT::NCO; ++i) pt.out.p[i] = out[i];
         pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g)};
-        pt.tw = twzd();
+        pt.tw = twz_t<Tc>();
         pt.two = twz();
         stream("col_middle", pt, col_tiles<PT>(cg, cg.n2));
     }
-    template <int KIND>
-    void middle(Cx<double>* const* in, Cx<T>* const* out) {
+    template <int KIND, typename Tc = double>
+    void middle(Cx<Tc>* const* in, Cx<T>* const* out) {
         const ColGeom cg = c.dist() ? spec_geom_t() : spec_geom();
-#define CALL(LL) middle_L<LL, KIND>(cg, in, out)
+#define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out)
         DR_SWITCH_COL(g.n3g, CALL)
 #undef CALL
     }
@@ -570,15 +580,18 @@ struct Impl {
     // -------------------------------------------------------------------- spectral operators
     // Forward half spectrum of a real slab field into spectrum slot `slot`: x1 r2c, x2 forward FFT and,
     // with slabs, the all-to-all into the transposed layout the x3 middle pass reads.
+    // Tc = double for symbols that amplify high wavenumbers (beta A, reading A20); Tc = T for symbols that
+    // damp them ((beta A)^-1, Leray), where the fp32 rounding noise of the forward passes is harmless.
+    template <typename Tc = double>
     void spec_forward(const T* f, int slot) {
         if (!c.dist()) {
-            row_r2c(f, specD(slot));
-            col_fft_fwd(specD(slot), specD(slot), 0);
+            row_r2c<Tc>(f, specD_t<Tc>(slot));
+            col_fft_fwd<Tc>(specD_t<Tc>(slot), specD_t<Tc>(slot), 0);
             return;
         }
-        row_r2c(f, specD(6));
-        col_fft_fwd(specD(6), specD(7), nb());  // writes the split layout: one contiguous chunk per rank
-        alltoall(specD(7), specD(slot), (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<double>));
+        row_r2c<Tc>(f, specD_t<Tc>(6));
+        col_fft_fwd<Tc>(specD_t<Tc>(6), specD_t<Tc>(7), nb());  // the split layout: one contiguous chunk per rank
+        alltoall(specD_t<Tc>(7), specD_t<Tc>(slot), (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<Tc>));
     }
     // Back from the middle pass's output slot to a real slab field (+ add).
     void spec_inverse(int slot, T* out, const T* add) {
@@ -606,21 +619,23 @@ struct Impl {
     // and the x3 forward transform run in double; the inverse x3 / x2 / x1 passes in T.
     template <int KIND>
     void scalar_symbol3(V3<const T> in, V3<T> out, const V3<const T>* add) {
+        using Tc = std::conditional_t<KIND == 1, T, double>;  // preconditioner: damping symbol
         for (int cc = 0; cc < 3; ++cc) {
-            spec_forward(in.c[cc], 0);
-            Cx<double>* sd = specD(0);
+            spec_forward<Tc>(in.c[cc], 0);
+            Cx<Tc>* sd = specD_t<Tc>(0);
             Cx<T>* sf = specF(0);
-            middle<KIND>(&sd, &sf);
+            middle<KIND, Tc>(&sd, &sf);
             spec_inverse(0, out.c[cc], add ? add->c[cc] : nullptr);
         }
     }
-    // coupled 3-component symbol (KIND 2, 3): out = F^-1[sym F in]
+    // coupled 3-component symbol (KIND 2 Leray, 3 Leray / (beta A)): out = F^-1[sym F in]; both damp or
+    // keep the magnitude of every mode, so the forward passes run in T
     template <int KIND>
     void vector_symbol3(V3<const T> in, V3<T> out) {
-        Cx<double>* sd[3] = {specD(0), specD(1), specD(2)};
+        Cx<T>* sd[3] = {specD_t<T>(0), specD_t<T>(1), specD_t<T>(2)};
         Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
-        for (int cc = 0; cc < 3; ++cc) spec_forward(in.c[cc], cc);
-        middle<KIND>(sd, sf);
+        for (int cc = 0; cc < 3; ++cc) spec_forward<T>(in.c[cc], cc);
+        middle<KIND, T>(sd, sf);
         for (int cc = 0; cc < 3; ++cc) spec_inverse(cc, out.c[cc], nullptr);
     }
     void reg_apply(V3<const T> in, V3<T> out) { scalar_symbol3<0>(in, out, nullptr); }
