@@ -558,21 +558,21 @@ struct Impl {
     }
 
     template <int L, int KIND, typename Tc>
-    void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out) {
+    void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0) {
         using PT = MiddlePass<Tc, T, L, KIND>;
         PT pt;
         pt.c = cg;
         for (int i = 0; i < PT::NCI; ++i) pt.in.p[i] = in[i];
         for (int i = 0; i < PT::NCO; ++i) pt.out.p[i] = out[i];
-        pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g)};
+        pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), comp};
         pt.tw = twz_t<Tc>();
         pt.two = twz();
         stream("col_middle", pt, col_tiles<PT>(cg, cg.n2));
     }
     template <int KIND, typename Tc = double>
-    void middle(Cx<Tc>* const* in, Cx<T>* const* out) {
+    void middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0) {
         const ColGeom cg = c.dist() ? spec_geom_t() : spec_geom();
-#define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out)
+#define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out, comp)
         DR_SWITCH_COL(g.n3g, CALL)
 #undef CALL
     }
@@ -846,14 +846,19 @@ struct Impl {
     // out = beta A u + P b (P = Leray when isochoric, else I): the tail of Eq. 5e and of Eq. 4
     void reg_plus_data(V3<const T> u, V3<const T> b, V3<T> out) {
         if (c.cfg.flags & DR_ISOCHORIC) {
-            Cx<double>* sd[6] = {specD(0), specD(1), specD(2), specD(3), specD(4), specD(5)};
-            Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
+            // L b = b - grad Lap^-1 div b: D = div b by the per-axis derivative passes (its rounding is
+            // damped by k'/|k'|^2), one forward transform of D, then per component a 2 -> 1 middle pass
+            // beta a(k) u_c + i k'_c D/|k'|^2 and the c2r adds b_c
+            T* D = Dv();  // isochoric contexts have no div v: the slot is free
+            div(b, D);
+            spec_forward(D, 1);
             for (int cc = 0; cc < 3; ++cc) {
-                spec_forward(u.c[cc], cc);
-                spec_forward(b.c[cc], 3 + cc);
+                spec_forward(u.c[cc], 0);
+                Cx<double>* sd[2] = {specD(0), specD(1)};
+                Cx<T>* sf = specF(0);
+                middle<6>(sd, &sf, cc);
+                spec_inverse(0, out.c[cc], b.c[cc]);
             }
-            middle<4>(sd, sf);
-            for (int cc = 0; cc < 3; ++cc) spec_inverse(cc, out.c[cc], nullptr);
         } else {
             scalar_symbol3<0>(u, out, &b);
         }

@@ -516,6 +516,7 @@ struct SymInfo {
     int reg;       // 1: a = |k|^2, 2: a = |k|^4
     double beta;
     double norm;
+    int comp = 0;  // kind 6: the output component c
 };
 
 template <typename T>
@@ -527,14 +528,24 @@ __device__ __forceinline__ T sym_a(const SymInfo& s, T kk) { return s.reg == 1 ?
 // kind 3: Y = norm * L_hat X / (beta a_hat(k))    (isochoric preconditioner)
 // kind 4: Y = norm * (beta a(k) V + L_hat B)      (isochoric matvec tail, 6 -> 3)
 // kind 5: Y = norm * L_hat (beta a(k) V + B)      (isochoric gradient from the unprojected v, 6 -> 3)
+// kind 6: Y = norm * (beta a(k) V_c + i k'_c D / |k'|^2)   (isochoric matvec tail per component c, 2 -> 1;
+//         D = F[div b~]: L b~ = b~ - grad Lap^-1 div b~, whose b~ part is added in real space)
 template <typename T, int KIND>
 struct Sym {
-    static constexpr int NCI = (KIND <= 1) ? 1 : (KIND >= 4 ? 6 : 3);
-    static constexpr int NCO = (KIND <= 1) ? 1 : 3;
+    static constexpr int NCI = (KIND <= 1) ? 1 : (KIND == 6 ? 2 : (KIND >= 4 ? 6 : 3));
+    static constexpr int NCO = (KIND <= 1 || KIND == 6) ? 1 : 3;
     static __device__ __forceinline__ void apply(const SymInfo& s, Cx<T>* x, int k1, int k2, int k3, int kp1, int kp2,
                                                  int kp3) {
         const T kk = T(k1) * T(k1) + T(k2) * T(k2) + T(k3) * T(k3);
         const T nrm = (T)s.norm;
+        if (KIND == 6) {
+            const T q1 = T(kp1), q2 = T(kp2), q3 = T(kp3);
+            const T qq = q1 * q1 + q2 * q2 + q3 * q3;
+            const T qc = s.comp == 0 ? q1 : (s.comp == 1 ? q2 : q3);
+            const T f = (qq != T(0)) ? qc / qq : T(0);
+            x[0] = scale(x[0], nrm * (T)s.beta * sym_a<T>(s, kk)) + mul_i(x[1], nrm * f);
+            return;
+        }
         if (KIND == 0) {
             x[0] = scale(x[0], nrm * (T)s.beta * sym_a<T>(s, kk));
         } else if (KIND == 1) {
