@@ -8,7 +8,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libdiffreg.so")
+CHECK = os.environ.get("DR_CHECK", "0") == "1"  # bounds-checked debug variant (device asserts)
+LIB = os.path.join(PKG, "libdiffreg_check.so" if CHECK else "libdiffreg.so")
 SOURCES = [os.path.join(CSRC, "diffreg.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + [
     os.path.join(ROOT, "include", "diffreg.h")]
@@ -30,9 +31,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *SOURCES]
+    cmd = [NVCC, *FLAGS, *(["-DDR_CHECK"] if CHECK else []), "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(PKG, "build.log")
+    log = os.path.join(PKG, "build_check.log" if CHECK else "build.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:

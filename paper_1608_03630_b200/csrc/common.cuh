@@ -3,6 +3,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// DR_CHECK builds (DR_CHECK=1 python paper_1608_03630_b200/build.py -> libdiffreg_check.so) turn on
+// device-side bounds checks of every computed shared-memory and ghosted-field index.
+#ifdef DR_CHECK
+#include <cassert>
+#define DR_ASSERT(c) assert(c)
+#else
+#define DR_ASSERT(c) ((void)0)
+#endif
+
 namespace dr {
 
 template <typename T>

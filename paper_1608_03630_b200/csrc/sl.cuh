@@ -74,6 +74,7 @@ __device__ __forceinline__ T interp_global(const T* __restrict__ f, const Grid& 
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const int j3 = g.ghost ? q3 + c - 1 - g.z0 + g.zg : wrapi(q3 + c - 1, g.n3);
+        DR_ASSERT(j3 >= 0 && j3 < g.n3 + g.zg + g.zgh);
         T accb = T(0);
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
@@ -420,6 +421,7 @@ __device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, 
         const int gz = g.ghost ? c.oz + zz - g.z0 + g.zg : wrapi(c.oz + zz, g.n3);
         const uint32_t gofs = ((uint32_t)gz * g.n2 + gy) * g.n1 + gx;
         T* dst = box + (zz * BY + yy) * BX + ch * VEC;
+        DR_ASSERT(zz < BZ && yy < BY && ch * VEC + VEC <= BX && gz >= 0 && gz < g.n3 + g.zg + g.zgh);
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) cp_async16(dst + cc * SC, src.p[cc] + gofs);
         yy += RSTEP;
@@ -467,6 +469,10 @@ __device__ __forceinline__ void pair_from_box(const Grid& g, const TileCtx<T, NC
     }
     const T* bA = box + ((qA[2] - 1 - c.oz) * BY + (qA[1] - 1 - c.oy)) * BX + (qA[0] - 1 - c.ox);
     const T* bB = box + ((qB[2] - 1 - c.oz) * BY + (qB[1] - 1 - c.oy)) * BX + (qB[0] - 1 - c.ox);
+    DR_ASSERT(qA[0] - 1 - c.ox >= 0 && qA[0] + 2 - c.ox < c.ex && qA[1] - 1 - c.oy >= 0 && qA[1] + 2 - c.oy < c.ey &&
+              qA[2] - 1 - c.oz >= 0 && qA[2] + 2 - c.oz < c.ez);
+    DR_ASSERT(qB[0] - 1 - c.ox >= 0 && qB[0] + 2 - c.ox < c.ex && qB[1] - 1 - c.oy >= 0 && qB[1] + 2 - c.oy < c.ey &&
+              qB[2] - 1 - c.oz >= 0 && qB[2] + 2 - c.oz < c.ez);
     T vA[NC], vB[NC];
     if constexpr (sizeof(T) == 4) {
         float2 w[3][4];

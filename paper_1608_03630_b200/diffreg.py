@@ -15,7 +15,8 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdiffreg.so")
+# DR_CHECK=1 selects the bounds-checked debug build (paper_1608_03630_b200/build.py with DR_CHECK=1)
+LIB_PATH = os.path.join(_PKG, "libdiffreg_check.so" if os.environ.get("DR_CHECK", "0") == "1" else "libdiffreg.so")
 
 DR_OK, DR_ERR_ARG, DR_ERR_GRID, DR_ERR_PARAM, DR_ERR_ORDER, DR_ERR_CUDA, DR_ERR_NCCL, DR_ERR_OOM, \
     DR_ERR_NONFINITE, DR_ERR_PLAN = range(10)
