@@ -68,6 +68,15 @@ def make_inputs(n, device):
     return rT, rR, v, vts
 
 
+def workload_config(n, ws):
+    """The `config` object of both arms' JSON lines (the same workload)."""
+    return {"workload": f"cfg3: {n}^3 nt={NT} H2 beta=1e-2 GN non-isochoric; step = set_velocity + "
+                        f"forward_solve + adjoint_solve + {NMV} x (hessian_matvec + precond_apply)",
+            "grid": [n] * 3, "nt": NT, "reg": "H2", "beta": 1e-2, "isochoric": False, "matvecs_per_step": NMV,
+            "l2": "inputs larger than L2 (working set ~4.8 GB per GPU at 256^3 >> 126 MB; no flush needed)",
+            "parallelism": "single" if ws == 1 else f"x3 slabs x{ws} (NCCL ghost planes + all-to-all)"}
+
+
 # ----------------------------------------------------------------------------- algorithmic bytes per launch
 
 def algo_bytes(tag, n, nt, es=4):
@@ -247,8 +256,7 @@ def run_reference(args, ws, rank):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"cfg3 {n}^3 nt={NT} H2 beta=1e-2 GN non-isochoric (oracle sample)",
-                      "grid": [n] * 3, "nt": NT},
+           "config": workload_config(n, args.gpus if args.gpus else 1),
            "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -397,13 +405,7 @@ def run_ours(args, ws, rank, local):
         out = {"metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": ws, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-               "config": {"workload": f"cfg3: {n}^3 nt={NT} H2 beta=1e-2 GN non-isochoric; step = set_velocity + "
-                                      f"forward_solve + adjoint_solve + {NMV} x (hessian_matvec + precond_apply)",
-                          "grid": [n] * 3, "nt": NT, "reg": "H2", "beta": 1e-2, "isochoric": False,
-                          "matvecs_per_step": NMV,
-                          "l2": "inputs larger than L2 (working set ~%.1f GB per GPU >> 126 MB)" % (
-                              dr.diffreg.dr_workspace_bytes_dist(cfg, ws) / 1e9),
-                          "parallelism": "single" if ws == 1 else f"x3 slabs x{ws} (NCCL ghost planes + all-to-all)"},
+               "config": workload_config(n, ws),
                "voxel_steps_per_s": vox_steps, "matvec_only_ms": mv_ms,
                "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu}
         print(json.dumps(out), flush=True)
