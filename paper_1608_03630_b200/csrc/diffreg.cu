@@ -141,7 +141,7 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.tmp3 = take(3 * L.F);                   // d* and scratch
     L.stin = take(3 * L.F);                   // host staging in
     L.stout = take(3 * L.F);                  // host staging out
-    L.kry = take(4 * 3 * L.F);                // PCG work vectors r, z, p, q (NEXT-2)
+    L.kry = take(5 * 3 * L.F);                // PCG work vectors r, z, p, q, dv (NEXT-2)
     const bool newton = c->flags & DR_FULL_NEWTON;
     L.sN = newton ? take((size_t)(nt + 1) * L.GF) : 0;  // NEXT-3: s_k = div(lam_k vt) (gathered: ghosted)
     L.bN = newton ? take(3 * L.F) : 0;                   // NEXT-3: int lam grad rho~ dt
@@ -191,6 +191,9 @@ struct dr_ctx {
     cudaStream_t hi = nullptr;                // high-priority stream: the gather sweeps while aux runs
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hi = nullptr;
     bool overlap = false;                     // DR_OVERLAP=1 in the environment at dr_create
+    bool graphs = true;                       // DR_GRAPHS=0 disables the CUDA-graph PCG iteration
+    cudaGraphExec_t pcg_graph = nullptr;      // one captured PCG iteration (single rank), reused
+    double* pinned = nullptr;                 // pinned host scalar the graph reports |r|^2 into
     struct RemotePlanH {                      // host side of an off-rank plan (per displacement field)
         bool any = false;                     // some rank has remote points for this field
         std::vector<int> out_cnt, out_off, in_cnt, in_off;
@@ -939,8 +942,15 @@ struct Impl {
         PE("axpby");
     }
     // H dv = -g from dv = 0, preconditioner (beta A)^-1 (+ Leray when isochoric); stop when
-    // |r| <= eta |g| or after maxit matvecs.  Scalars are fp64 on the host (one sync per reduction).
+    // |r| <= eta |g| or after maxit matvecs.  One rank: the iteration (matvec, preconditioner, inner
+    // products into device scalars, vector updates) is one CUDA graph, captured once per context and
+    // replayed, with one small device-to-host read of |r|^2 per iteration -- small grids are launch-
+    // bound otherwise.  Slabs (or profiling): host-scalar loop, one synchronisation per inner product.
     void pcg(const T* gin, T* dv, double eta, int maxit, int* iters, double* relres) {
+        if (!c.dist() && c.graphs && !c.prof) {
+            pcg_graph(gin, dv, eta, maxit, iters, relres);
+            return;
+        }
         T *r = kry(0), *z = kry(1), *p = kry(2), *q = kry(3);
         const size_t V = 3 * g.M;
         CK(cudaMemsetAsync(dv, 0, V * sizeof(T), s));
@@ -966,6 +976,87 @@ struct Impl {
                 rz = rzn;
             }
         }
+        if (iters) *iters = it;
+        if (relres) *relres = gnorm > 0 ? rnorm / gnorm : 0.0;
+    }
+
+    // device scalars of the graph PCG: [0] rz, [1] pq, [2] rr, [3] rz_new, [4] alpha, [5] beta
+    double* psc() { return c.at<double>(c.L.red) + 3840; }
+    void dot_dev(const T* a, const T* b, double* out, int64_t n) {
+        double* part = c.at<double>(c.L.red);
+        const int nb = (int)std::min<int64_t>(2048, (n + 255) / 256);
+        PB();
+        k_dot_parts<T><<<nb, 256, 0, s>>>(n, a, b, nullptr, nullptr, part, 0);
+        PE("reduce");
+        PB();
+        k_sum_parts<<<1, 256, 0, s>>>(part, nb, out);
+        PE("reduce");
+    }
+    void axpby_dev(const double* pa, double sa, const T* x, const double* pb, double cb, T* y) {
+        PB();
+        k_axpby_dev<T><<<grid_1d(3 * g.M), 256, 0, s>>>(3 * g.M, pa, sa, x, pb, cb, y);
+        PE("axpby");
+    }
+    void pcg_iteration_body() {
+        T *r = kry(0), *z = kry(1), *p = kry(2), *q = kry(3), *dv = kry(4);
+        double* sc = psc();
+        const int64_t n = 3 * g.M;
+        hessian_matvec(p, q);
+        dot_dev(p, q, sc + 1, n);
+        PB();
+        k_scalar_ratio<<<1, 32, 0, s>>>(sc, 0, 1, 4, 0);  // alpha = rz / pq
+        PE("pcg_scalar");
+        axpby_dev(sc + 4, 1.0, p, nullptr, 1.0, dv);   // dv += alpha p
+        axpby_dev(sc + 4, -1.0, q, nullptr, 1.0, r);   // r -= alpha q
+        dot_dev(r, r, sc + 2, n);
+        CK(cudaMemcpyAsync(c.pinned, sc + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+        precond(cvec(vec(r, (size_t)g.M)), vec(z, (size_t)g.M));
+        dot_dev(r, z, sc + 3, n);
+        PB();
+        k_scalar_ratio<<<1, 32, 0, s>>>(sc, 3, 0, 5, 1);  // beta = rz_new / rz; rz = rz_new
+        PE("pcg_scalar");
+        axpby_dev(nullptr, 1.0, z, sc + 5, 0.0, p);    // p = z + beta p
+    }
+    void pcg_graph(const T* gin, T* dvout, double eta, int maxit, int* iters, double* relres) {
+        T *r = kry(0), *z = kry(1), *p = kry(2), *dv = kry(4);
+        const size_t V = 3 * g.M;
+        double* sc = psc();
+        if (!c.pinned) CK(cudaMallocHost(&c.pinned, sizeof(double)));
+        CK(cudaMemsetAsync(dv, 0, V * sizeof(T), s));
+        axpby(-1.0, gin, 0.0, r);  // r = -g
+        const double gnorm = std::sqrt(dot3(gin, gin));
+        double rnorm = gnorm;
+        int it = 0;
+        if (gnorm > 0 && maxit > 0 && rnorm > eta * gnorm) {
+            precond(cvec(vec(r, (size_t)g.M)), vec(z, (size_t)g.M));
+            CK(cudaMemcpyAsync(p, z, V * sizeof(T), cudaMemcpyDeviceToDevice, s));
+            dot_dev(r, z, sc + 0, 3 * g.M);
+            if (!c.pcg_graph) {  // capture on an internal stream (the caller's may be the legacy stream)
+                const cudaStream_t user = s;
+                cudaGraph_t gr = nullptr;
+                s = c.hi;
+                CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                try {
+                    pcg_iteration_body();
+                } catch (...) {
+                    cudaStreamEndCapture(s, &gr);
+                    if (gr) cudaGraphDestroy(gr);
+                    s = user;
+                    throw;
+                }
+                CK(cudaStreamEndCapture(s, &gr));
+                s = user;
+                CK(cudaGraphInstantiate(&c.pcg_graph, gr, 0));
+                CK(cudaGraphDestroy(gr));
+            }
+            while (it < maxit && rnorm > eta * gnorm) {
+                CK(cudaGraphLaunch(c.pcg_graph, s));
+                CK(cudaStreamSynchronize(s));
+                ++it;
+                rnorm = std::sqrt(*c.pinned);
+            }
+        }
+        CK(cudaMemcpyAsync(dvout, dv, V * sizeof(T), cudaMemcpyDeviceToDevice, s));
         if (iters) *iters = it;
         if (relres) *relres = gnorm > 0 ? rnorm / gnorm : 0.0;
     }
@@ -1488,6 +1579,8 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
     {
         const char* ov = getenv("DR_OVERLAP");
         c->overlap = ov && ov[0] == '1';
+        const char* gr = getenv("DR_GRAPHS");
+        c->graphs = !(gr && gr[0] == '0');
     }
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
@@ -1523,6 +1616,8 @@ dr_status dr_destroy(dr_ctx* c) {
         cudaStreamDestroy(c->hi);
     }
     if (c->ev_hi) cudaEventDestroy(c->ev_hi);
+    if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
+    if (c->pinned) cudaFreeHost(c->pinned);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

@@ -118,6 +118,25 @@ __global__ void __launch_bounds__(256) k_minmax_final(const double* __restrict__
     }
 }
 
+// Device-scalar variants for the graph-captured PCG iteration: y = a x + b y with
+// a = sa * (*pa or 1), b = (*pb or cb); scalars read once per thread.
+template <typename T>
+__global__ void k_axpby_dev(int64_t n, const double* __restrict__ pa, double sa, const T* __restrict__ x,
+                            const double* __restrict__ pb, double cb, T* __restrict__ y) {
+    const double a = pa ? sa * *pa : sa;
+    const double b = pb ? *pb : cb;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = (T)(a * (double)x[i] + b * (double)y[i]);
+}
+// s[out] = s[num] / s[den]; with `shift`, also s[den] = s[num] (rz <- rz_new)
+__global__ void k_scalar_ratio(double* s, int num, int den, int out, int shift) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const double v = s[num] / s[den];
+        if (shift) s[den] = s[num];
+        s[out] = v;
+    }
+}
+
 template <typename T>
 __global__ void k_scale(int64_t M, const T* __restrict__ a, T* __restrict__ out, T s) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)

@@ -422,3 +422,20 @@ def test_solver_on_synthetic_problem(dr, newton):
     assert rel(np64(v), vref) < 1e-3
     _, det, lo, hi = ctx.deformation(want_u=False)
     assert lo > 0
+
+
+def test_pcg_graph_matches_host_loop(dr, monkeypatch):
+    """The CUDA-graph PCG iteration (device scalars, captured once per context) reproduces the host-scalar
+    loop bit for bit, including a second solve that replays the cached graph."""
+    name, n, nt, vgen, iso = CASES[1]
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("DR_GRAPHS", mode)
+        ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+        ctx.forward_solve()
+        g, _ = prep(synth.smooth_vec(41, n, kmax=6), False)
+        a = ctx.pcg(g.cuda(), 0.05, 20)
+        b = ctx.pcg((2 * g).contiguous().cuda(), 0.05, 20)
+        outs[mode] = (a, b)
+    for (da, ia, ra), (db, ib, rb) in zip(outs["1"], outs["0"]):
+        assert ia == ib and ra == rb and torch.equal(da, db)
