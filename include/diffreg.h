@@ -59,10 +59,10 @@ typedef enum dr_status {
     DR_ERR_PARAM = 3,      /* beta <= 0, nt < 1 or nt > 64, reg not H1/H2                        */
     DR_ERR_ORDER = 4,      /* call sequence violated (see each function)                         */
     DR_ERR_CUDA = 5,       /* CUDA runtime error (message in dr_last_error)                      */
-    DR_ERR_NCCL = 6,       /* reserved: multi-GPU communicator error                             */
+    DR_ERR_NCCL = 6,       /* multi-GPU communicator error (NCCL, or libnccl.so.2 not loadable)   */
     DR_ERR_OOM = 7,        /* workspace smaller than dr_workspace_bytes / cudaMalloc failed       */
     DR_ERR_NONFINITE = 8,  /* reserved                                                           */
-    DR_ERR_PLAN = 9        /* reserved: scatter-plan capacity exceeded (multi-GPU)               */
+    DR_ERR_PLAN = 9        /* multi-GPU: off-rank departure points exceed the scatter capacity    */
 } dr_status;
 
 enum { DR_REG_H1 = 1,      /* A = -Laplacian   (H1 seminorm, beta/2 |grad v|^2), a(k) = |k|^2   */
@@ -106,9 +106,10 @@ dr_status dr_destroy(dr_ctx* ctx);
  * farther out (any distance, several slabs included) are served by the off-rank scatter of the
  * paper's Algorithm 1: their cells go to the owning rank once per velocity, and every
  * gather the owners interpolate and return the values.  dr_set_velocity returns DR_ERR_PLAN only if
- * a rank's remote points exceed the scatter capacity (M/8 per displacement field).  Exchanges: ghost planes before every semi-Lagrangian gather and
- * all-to-all transposes around the x3 FFT pass, stream-ordered on the context stream.  Every rank
- * must make the same sequence of calls (collective semantics).
+ * a rank's remote points exceed the scatter capacity (M/8 per displacement field).  Exchanges:
+ * ghost planes before every semi-Lagrangian gather and all-to-all transposes around the x3 FFT pass,
+ * stream-ordered on the context stream.  Every rank must make the same sequence of calls (collective
+ * semantics).
  *
  * Communicators (owned by the caller, must outlive the contexts that use them):
  *   NCCL     -- one process per GPU: rank 0 calls dr_nccl_get_unique_id, the id is broadcast by the
@@ -163,7 +164,8 @@ dr_status dr_adjoint_solve(dr_ctx* ctx, void* lambda0_out);
 
 /* Gauss-Newton Hessian matvec Hvt = H(v) vt (Eqs. 5a-5e with the lambda terms
  * dropped): incremental state forward (Algorithm 2), incremental adjoint backward,
- * b~ = int lambda~ grad rho dt (trapezoid), Hvt = beta A vt + P b~.  vt, Hvt: vector fields,
+ * b~ = int lambda~ grad rho dt (trapezoid), Hvt = beta A vt + P b~.  With DR_FULL_NEWTON the two
+ * lambda terms are kept (NEXT-3; runs dr_adjoint_solve first if needed).  vt, Hvt: vector fields,
  * must not alias.  Requires dr_forward_solve. */
 dr_status dr_hessian_matvec(dr_ctx* ctx, const void* vt, void* Hvt);
 
@@ -188,8 +190,9 @@ dr_status dr_objective(dr_ctx* ctx, double* J, double* misfit);
  * gradient norm, e.g. the quadratic forcing eta = min(0.5, |g| / |g_0|) of P:L433).  Starts from
  * dv = 0; stops when |r| <= eta |g| (discrete L2 norms, fp64 accumulation, summed over all ranks) or
  * after maxit Hessian matvecs.  g, dv: vector fields (device or host), must not alias.  iters /
- * relres (nullable, host): matvecs used and |r| / |g|.  Requires dr_forward_solve.  Synchronises
- * the stream once per inner product. */
+ * relres (nullable, host): matvecs used and |r| / |g|.  Requires dr_forward_solve.  One rank: each
+ * iteration is a CUDA graph (captured once per context; DR_GRAPHS=0 in the environment at dr_create
+ * disables it) with one 8-byte read-back; slabs: one synchronisation per inner product. */
 dr_status dr_pcg(dr_ctx* ctx, const void* g, void* dv, double eta, int maxit, int* iters, double* relres);
 
 /* NEXT-4: deformation map and its Jacobian determinant.  u = y_1 - x where
