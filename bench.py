@@ -91,7 +91,7 @@ def algo_bytes(tag, n, nt, es=4):
         "sl_state": 5 * es * M,           # gather 1, d+ 3, write 1
         "sl_adjoint": 6 * es * M,
         "sl_multiplier": 6 * es * M,      # gather D 1, d- 3, D 1, write m 1
-        "sl_departure": 12 * es * M,      # gather v 3, d* 3, v 3, write d 3
+        "sl_departure": 6 * es * M,       # per component a: gather v_a 1, d* 3, v_a 1, write d_a 1
         "quadrature": (4 * (nt + 1) + 3) * es * M,
         # inc-adjoint steps carrying the b~ quadrature: gather 1, d- 3, m 1, G_{k-1} 3, write 1, plus
         # first step: rho~(1) at x 1, G_nt 3, write b~ 3; later steps: b~ read 3 + write 3

@@ -815,15 +815,10 @@ struct Impl {
             PE("dstar");
             plan(tmp3(), plan_t());
             remote_plan(0, tmp3());
-            EpiDeparture<T> e;
-            e.d0 = dout;
-            e.d1 = dout + g.M;
-            e.d2 = dout + 2 * g.M;
-            e.v0 = vc(0);
-            e.v1 = vc(1);
-            e.v2 = vc(2);
-            for (int a = 0; a < 3; ++a) e.c[a] = (T)(sg * 0.5 * dtt / h[a]);
-            gather<3>("sl_departure", Src<T, 3>{{vc(0), vc(1), vc(2)}}, tmp3(), plan_t(), e);
+            for (int a = 0; a < 3; ++a) {
+                EpiDeparture1<T> e{dout + (size_t)a * g.M, vc(a), (T)(sg * 0.5 * dtt / h[a])};
+                gather<1>("sl_departure", Src<T, 1>{{vc(a)}}, tmp3(), plan_t(), e);
+            }
             plan(dout, sg > 0 ? plan_p() : plan_m());
             remote_plan(sg > 0 ? 1 : 2, dout);
         }

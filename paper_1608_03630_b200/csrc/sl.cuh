@@ -273,17 +273,14 @@ struct EpiMultiplier {  // m = 1 + dt/2 (Dbar + D + dt Dbar D), Dbar = I[div v](
 };
 
 template <typename T>
-struct EpiDeparture {  // d = sigma dt/2 (v(x) + I[v](X*)) / h  (Eq. 6, cell units)
-    T* d0; T* d1; T* d2;
-    const T* v0; const T* v1; const T* v2;
-    T c[3];  // sigma * dt / (2 h_a)
-    struct Late { T v[3]; };
-    __device__ __forceinline__ Late late(uint32_t id) const { return Late{{__ldg(v0 + id), __ldg(v1 + id), __ldg(v2 + id)}}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
-        d0[id] = c[0] * (l.v[0] + val[0]);
-        d1[id] = c[1] * (l.v[1] + val[1]);
-        d2[id] = c[2] * (l.v[2] + val[2]);
-    }
+struct EpiDeparture1 {  // d_a = sigma dt/2 (v_a(x) + I[v_a](X*)) / h_a  (Eq. 6, cell units), one component a:
+    T* d;               // three one-component gathers (54 KB boxes, 4 CTAs/SM) beat one three-component
+                        // gather (173 KB box, 1 CTA/SM): 3 x ? vs 686 us at 256^3
+    const T* v;
+    T c;
+    struct Late { T v; };
+    __device__ __forceinline__ Late late(uint32_t id) const { return Late{__ldg(v + id)}; }
+    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const { d[id] = c * (l.v + val[0]); }
 };
 
 template <typename T, int NC>
