@@ -21,9 +21,32 @@ namespace dr {
 
 // padded shared-memory index: one pad slot every 16 complex values
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }
-template <int L>
-struct LineGeom {
-    static constexpr int LP = L + L / 16 + 2;  // padded line length (holds index L for r2c)
+// Padded line stride in complex elements: the smallest LP >= P(L) + 1 (holds index L for r2c) with
+// LP = REM (mod MOD).  The stride is chosen per pass from how the lanes of one shared-memory wavefront
+// (128 bytes: W = 128 / sizeof(Cx<T>) lanes) spread over lines, so that they hit distinct banks.
+// Within a line, the lane with thread-in-line index t sits at element offset t (mod 16) in every stage
+// (P pads one slot per 16), so
+//   row passes (TPL consecutive lanes per line, W / TPL lines per wavefront): LP = TPL (mod W);
+//   column passes (XC consecutive lanes = columns, each its own line, W / XC values of t per
+//   wavefront): LP = max(1, W / XC) (mod W).
+template <int L, int MOD, int REM>
+struct PadLP {
+    static constexpr int B = L + L / 16 + 1;
+    static constexpr int V = (MOD <= 1) ? B : B + (((REM - B) % MOD) + MOD) % MOD;
+};
+template <typename T>
+struct WaveLanes {  // lanes of one 128-byte shared-memory wavefront for complex T
+    static constexpr int V = 128 / (int)(2 * sizeof(T));
+};
+template <int L, typename T, int TPL>
+struct RowLP {
+    static constexpr int W = WaveLanes<T>::V;
+    static constexpr int V = (TPL < W) ? PadLP<L, W, TPL>::V : PadLP<L, 1, 0>::V;
+};
+template <int L, typename T, int XC>
+struct ColLP {
+    static constexpr int W = WaveLanes<T>::V;
+    static constexpr int V = PadLP<L, W, (XC >= W) ? 1 : W / XC>::V;
 };
 // Threads per line: each owns the 16 values of one radix-16 butterfly per stage.
 template <int L, typename T>
@@ -52,7 +75,8 @@ struct RowCfg {
     static constexpr int TPL = Tpl<L, Tc>::V;
     static constexpr int RB = (CtaThreads<Tc>::V / TPL) > 0 ? CtaThreads<Tc>::V / TPL : 1;
     static constexpr int NT = RB * TPL;
-    static constexpr size_t SMEM = (size_t)RB * LineGeom<L>::LP * sizeof(Cx<Tc>);
+    static constexpr int LP = RowLP<L, Tc, TPL>::V;
+    static constexpr size_t SMEM = (size_t)RB * LP * sizeof(Cx<Tc>);
 };
 
 // e^{DIR * 2 pi i m / 16}, m compile-time after unrolling
@@ -229,7 +253,7 @@ struct RowSt {  // out = v (+ add) (+ out when acc); nothing when !on
 template <typename T, int L>
 struct RowDerivPass {
     using RC = RowCfg<L, T>;
-    static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int TPL = RC::TPL, LP = RC::LP, RB = RC::RB, NT = RC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr size_t BUF = RC::SMEM;
     Grid g;
@@ -274,7 +298,7 @@ struct RowDerivPass {
 template <typename Ti, typename Tc, int L>
 struct RowR2cPass {
     using RC = RowCfg<L, Tc>;
-    static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int TPL = RC::TPL, LP = RC::LP, RB = RC::RB, NT = RC::NT;
     static constexpr int MINB = MinB<Tc, NT>::V;
     static constexpr size_t BUF = RC::SMEM;
     Grid g;
@@ -313,7 +337,7 @@ struct RowOut {
 template <typename T, int L>
 struct RowC2rPass {
     using RC = RowCfg<L, T>;
-    static constexpr int TPL = RC::TPL, LP = LineGeom<L>::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int TPL = RC::TPL, LP = RC::LP, RB = RC::RB, NT = RC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr size_t BUF = RC::SMEM;
     Grid g;
@@ -422,7 +446,7 @@ template <int L, typename T, int NC = 1>
 struct ColCfg {
     static constexpr int ES = (int)sizeof(Cx<T>);
     static constexpr int TPL = Tpl<L, T>::V;
-    static constexpr int LPB = LineGeom<L>::LP * ES;  // bytes per line
+    static constexpr int LPB = (L + L / 16 + 1 + WaveLanes<T>::V) * ES;  // bytes per line (bound, for sizing)
     static constexpr int XC0 = 128 / ES;
     static constexpr int XC = (NC * XC0 * LPB <= 96 * 1024) ? XC0 : (NC * (XC0 / 2) * LPB <= 96 * 1024) ? XC0 / 2 : XC0 / 4;
     static constexpr int OLT = (XC * TPL >= CtaThreads<T>::V) ? 1 : CtaThreads<T>::V / (XC * TPL);
@@ -431,7 +455,8 @@ struct ColCfg {
     static constexpr int OL = OLT < OLS ? OLT : OLS;
     static constexpr int NT = XC * OL * TPL;
     static constexpr int LINES = XC * OL;
-    static constexpr size_t SMEM = (size_t)NC * LINES * LineGeom<L>::LP * ES;
+    static constexpr int LP = ColLP<L, T, XC>::V;
+    static constexpr size_t SMEM = (size_t)NC * LINES * LP * ES;
 };
 
 // thread -> (column xi, thread-in-line t, transverse line oi); line index oi * XC + xi
@@ -454,7 +479,7 @@ __device__ __forceinline__ void col_origin(const ColGeom& c, int tile, int& x0, 
 template <typename T, int L, int AX>
 struct ColDerivPass {
     using CC = ColCfg<L, T>;
-    static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
+    static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr size_t BUF = CC::SMEM;
     ColGeom c;
@@ -488,7 +513,7 @@ struct ColDerivPass {
 template <typename T, int L, int DIR>
 struct ColFftPass {
     using CC = ColCfg<L, T>;
-    static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
+    static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr size_t BUF = CC::SMEM;
     ColGeom c;
@@ -602,11 +627,12 @@ struct MiddlePass {
     using T = Ti;
     static constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
     using CC = ColCfg<L, T, NCI>;
-    static constexpr int TPL = CC::TPL, LP = LineGeom<L>::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
+    static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
+    static constexpr int LPO = ColLP<L, To, XC>::V;  // stride of the To lines of the inverse
     static constexpr int TPLO = Tpl<L, To>::V;  // threads per inverse line (fp32: fewer than fp64)
     static constexpr int MINB = MinBMiddle<T, NT>::V;
     static constexpr size_t BUFI = CC::SMEM;
-    static constexpr size_t BUF = BUFI + (size_t)NCO * LINES * LP * sizeof(Cx<To>);
+    static constexpr size_t BUF = BUFI + (size_t)NCO * LINES * LPO * sizeof(Cx<To>);
     ColGeom c;
     SpecPtrs<Ti, NCI> in;
     SpecPtrs<To, NCO> out;
@@ -643,7 +669,7 @@ struct MiddlePass {
                 Sym<T, KIND>::apply(s, v, k1, k2, k3, kp1, kp2, kp3);
             }
 #pragma unroll
-            for (int co = 0; co < NCO; ++co) so[co * LINES * LP + ln * LP + P(p)] = cx<To>((To)v[co].re, (To)v[co].im);
+            for (int co = 0; co < NCO; ++co) so[co * LINES * LPO + ln * LPO + P(p)] = cx<To>((To)v[co].re, (To)v[co].im);
         }
         __syncthreads();
         // inverse lines: the CTA's NT threads cover LINES lines of TPLO threads in NT / (LINES * TPLO) rounds
@@ -660,7 +686,7 @@ struct MiddlePass {
                 const int ln = loi * XC + lxi;
                 const bool act = ln < LINES;
                 const bool lon = act && x0 + lxi < c.nx && o0 + loi < c.n2;
-                Cx<To>* buf = so + co * LINES * LP + (act ? ln : 0) * LP;
+                Cx<To>* buf = so + co * LINES * LPO + (act ? ln : 0) * LPO;
                 fft_line_io<To, L, +1, true, false>(buf, lt, two, 1, SmemLine<To>{buf},
                                                     col_acc<3>(out.p[co], c, x0 + lxi, o0 + loi, 0, lon, 0));
             }
