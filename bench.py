@@ -102,11 +102,16 @@ def algo_bytes(tag, n, nt, es=4):
         "dstar": 6 * es * M,
         "row_deriv": 2 * es * M,
         "col_deriv": 2 * es * M,          # (+1 read when accumulating; counted as 2)
-        "row_r2c": es * M + 16 * Sc,
-        "col_fft_fwd": 2 * 16 * Sc,       # forward x2 pass, complex128 in and out
-        "col_fft_inv": 2 * 8 * Sc,        # inverse x2 pass, complex64 in and out
-        "col_middle": 16 * Sc + 8 * Sc,
-        "row_c2r": 8 * Sc + 2 * es * M,   # spectrum in, (b~ in), real out
+        # spectral passes: _f64 = forward passes widened to complex128 (amplifying symbols), _f32 = in T
+        "row_r2c_f64": es * M + 16 * Sc,
+        "row_r2c_f32": es * M + 2 * es * Sc,
+        "col_fft_fwd_f64": 2 * 16 * Sc,   # forward x2 pass, complex128 in and out
+        "col_fft_fwd_f32": 2 * 2 * es * Sc,
+        "col_fft_inv": 2 * 2 * es * Sc,   # inverse x2 pass, complex T in and out
+        "col_middle_f64": 16 * Sc + 2 * es * Sc,   # one-component symbols (KIND 0/1)
+        "col_middle_f32": 2 * es * Sc + 2 * es * Sc,
+        "row_c2r": 2 * es * Sc + es * M,            # spectrum in, real out
+        "row_c2r_add": 2 * es * Sc + 2 * es * M,    # + b~ in
     }
     return table.get(tag)
 

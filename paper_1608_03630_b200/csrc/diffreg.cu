@@ -430,10 +430,28 @@ struct Impl {
     }
     template <int RB>
     int64_t row_tiles() const { return ((int64_t)g.n2 * g.n3 + RB - 1) / RB; }
+    // Launch of a staged row pass (fft.cuh k_rows): persistent, one wave of resident CTAs.
+    template <class PassT>
+    void stream_rows(const char* tag, const PassT& pass) {
+        auto k = k_rows<PassT>;
+        static int per_sm = 0;  // per pass instantiation
+        if (!per_sm) {
+            set_smem(k, PassT::BUF);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, PassT::NT, PassT::BUF));
+            per_sm = std::max(per_sm, 1);
+        }
+        const int64_t nt = row_tiles<PassT::RB>();
+        const int grid = (int)std::min<int64_t>(nt, (int64_t)per_sm * c.num_sms);
+        PB();
+        k<<<grid, PassT::NT, PassT::BUF, s>>>(pass, (int)nt);
+        PE(tag);
+    }
+    // the bulk-copy engine needs 16-byte aligned rows (all workspace fields are; caller buffers may not be)
+    static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
     template <int L>
     void row_deriv_L(const T* f, T* out, int acc) {
-        using PT = RowDerivPass<T, L>;
+        using PT = RowDerivPass<T, L>;  // (a staged variant measured 46 -> 50 us: fewer warps for the compute)
         stream("row_deriv", PT{g, f, out, acc, twx()}, row_tiles<PT::RB>());
     }
     // twiddle tables by compute type (the forward spectral passes run in double, or in T for symbols that
@@ -445,13 +463,25 @@ struct Impl {
 
     template <int L, typename Tc>
     void row_r2c_L(const T* f, Cx<Tc>* sp) {
+        const char* tag = sizeof(Tc) == 8 ? "row_r2c_f64" : "row_r2c_f32";
+        // staged for the widened (complex128) transform; in T the one-tile-per-CTA pass keeps more warps
+        // for the compute (measured 36.8 vs 38.0 us at 256^3)
+        if (sizeof(Tc) > sizeof(T) && al16(f)) {
+            stream_rows(tag, RowR2cStaged<T, Tc, L>{g, f, sp, twx_t<Tc>()});
+            return;
+        }
         using PT = RowR2cPass<T, Tc, L>;
-        stream("row_r2c", PT{g, f, sp, twx_t<Tc>()}, row_tiles<PT::RB>());
+        stream(tag, PT{g, f, sp, twx_t<Tc>()}, row_tiles<PT::RB>());
     }
     template <int L>
     void row_c2r_L(const Cx<T>* sp, T* out, const T* add) {
+        if (al16(sp) && al16(add)) {
+            if (add) stream_rows("row_c2r_add", RowC2rStaged<T, L, true>{g, sp, RowOut<T>{out, add}, twx()});
+            else stream_rows("row_c2r", RowC2rStaged<T, L, false>{g, sp, RowOut<T>{out, nullptr}, twx()});
+            return;
+        }
         using PT = RowC2rPass<T, L>;
-        stream("row_c2r", PT{g, sp, RowOut<T>{out, add}, twx()}, row_tiles<PT::RB>());
+        stream(add ? "row_c2r_add" : "row_c2r", PT{g, sp, RowOut<T>{out, add}, twx()}, row_tiles<PT::RB>());
     }
 
 #define DR_SWITCH_ROW(Lval, call)                          \
@@ -546,7 +576,8 @@ struct Impl {
     void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out) {
         using PT = ColFftPass<U, L, DIR>;
         const ColGeom cg = spec_geom();
-        stream(DIR < 0 ? "col_fft_fwd" : "col_fft_inv", PT{cg, src, dst, tw, nb_in, nb_out}, col_tiles<PT>(cg, g.n3));
+        stream(DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32", PT{cg, src, dst, tw, nb_in, nb_out},
+               col_tiles<PT>(cg, g.n3));
     }
     template <typename Tc>
     void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out) {  // forward along x2, in Tc
@@ -570,7 +601,7 @@ struct Impl {
         pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), comp};
         pt.tw = twz_t<Tc>();
         pt.two = twz();
-        stream("col_middle", pt, col_tiles<PT>(cg, cg.n2));
+        stream(sizeof(Tc) == 8 ? "col_middle_f64" : "col_middle_f32", pt, col_tiles<PT>(cg, cg.n2));
     }
     template <int KIND, typename Tc = double>
     void middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0) {

@@ -367,6 +367,194 @@ struct RowC2rPass {
 };
 
 // ---------------------------------------------------------------------------------------------
+// Staged row passes (persistent CTAs, bulk-copy prefetch).  x1 rows are contiguous, so a tile of RB
+// rows is fetched by the bulk-copy (TMA) engine: warp 0 issues one cp.async.bulk per row into padded
+// shared-memory rows and an mbarrier counts the bytes.  Each CTA loops over tiles (tile += gridDim.x)
+// with two input stages: tile i+1 is in flight while tile i is transformed, so HBM latency is hidden
+// without registers or extra warps.  An epilogue operand (the b~ rows added by the c2r of the matvec)
+// is single-buffered: issued at the start of a tile, consumed by its last stage.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+// Shared-memory row stride (elements of complex E) of a staged row of n elements read by TPL lanes per
+// row: >= n, = TPL (mod W) so the W / TPL rows of one wavefront hit distinct banks, and a multiple of 16
+// bytes (bulk-copy destination alignment).
+template <typename E, int TPL>
+__host__ __device__ constexpr int staged_stride(int n) {
+    constexpr int W = WaveLanes<E>::V;
+    int v = n;
+    if (TPL < W) v = n + (((TPL - n) % W) + W) % W;
+    while ((v * (int)sizeof(Cx<E>)) % 16) ++v;  // (only tiny lines: TPL = 1 and an odd stride)
+    return v;
+}
+
+// Warp 0 (all lanes): fetch rows r0 .. r0 + nr - 1 (bytes per row, global row stride gs bytes) into
+// shared rows of stride ss bytes, completing on mbarrier b.
+__device__ __forceinline__ void issue_rows(unsigned char* dst, const unsigned char* g, int64_t r0, int nr, int64_t gs,
+                                           int ss, unsigned bytes, uint64_t* b, int lane) {
+    if (lane == 0) mbar_expect(b, (unsigned)nr * bytes);
+    __syncwarp();
+    for (int r = lane; r < nr; r += 32) bulk_load(dst + (size_t)r * ss, g + (r0 + r) * gs, bytes, b);
+}
+
+template <int L, typename Tc>
+struct StagedRowCfg {
+    static constexpr int TPL = Tpl<L, Tc>::V;
+    static constexpr int NT = 128;
+    static constexpr int RB = NT / TPL;
+    static constexpr int LP = RowLP<L, Tc, TPL>::V;
+    static constexpr size_t LINES = (size_t)RB * LP * sizeof(Cx<Tc>);
+};
+
+// r2c along x1 (as RowR2cPass) from staged rows of Ti.
+template <typename Ti, typename Tc, int L>
+struct RowR2cStaged {
+    using RC = StagedRowCfg<L, Tc>;
+    static constexpr int TPL = RC::TPL, LP = RC::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = MinB<Tc, NT>::V;
+    static constexpr int SI = staged_stride<Ti, TPL>(L) * (int)sizeof(Cx<Ti>);  // staged row stride, bytes
+    static constexpr size_t STG = (size_t)RB * SI, EPB = 0;
+    static constexpr size_t BUF = 128 + 2 * STG + EPB + RC::LINES;
+    Grid g;
+    const Ti* f;
+    Cx<Tc>* spec;
+    const Cx<Tc>* twN;
+    __device__ __forceinline__ int64_t nrows() const { return (int64_t)g.n2 * g.n3; }
+    __device__ __forceinline__ void issue_in(int tile, unsigned char* dst, uint64_t* b, int lane) const {
+        const int64_t r0 = (int64_t)tile * RB;
+        const int nr = (int)min((int64_t)RB, nrows() - r0);
+        issue_rows(dst, reinterpret_cast<const unsigned char*>(f), r0, nr, (int64_t)L * sizeof(Cx<Ti>), SI,
+                   L * sizeof(Cx<Ti>), b, lane);
+    }
+    __device__ __forceinline__ void issue_ep(int, unsigned char*, uint64_t*, int) const {}
+    __device__ __forceinline__ void run(int tile, const unsigned char* stg, const unsigned char*, uint64_t*, unsigned,
+                                        unsigned char* lines) const {
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        const int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows();
+        Cx<Tc>* buf = reinterpret_cast<Cx<Tc>*>(lines) + line * LP;
+        const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(stg + line * SI);
+        fft_line_io<Tc, L, -1, false, true>(buf, t, twN, 2, RowLd<Ti, Tc>{src}, SmemLine<Tc>{buf});
+        if (!ok) return;
+        Cx<Tc>* out = spec + row * g.n1p;
+        for (int k = t; k <= L / 2; k += TPL) {
+            Cx<Tc> Xk, Xl;
+            r2c_pair(buf[P(k)], buf[P(k == 0 ? 0 : L - k)], twN[k], Xk, Xl);
+            out[k] = Xk;
+            out[L - k] = Xl;
+        }
+    }
+};
+
+// c2r along x1 (as RowC2rPass) from staged spectrum rows; ADD: + staged real rows of epi.add.
+template <typename T, int L, bool ADD>
+struct RowC2rStaged {
+    using RC = StagedRowCfg<L, T>;
+    static constexpr int TPL = RC::TPL, LP = RC::LP, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr int NIN = L + 2;  // complex values fetched per spectrum row (L + 1 used; 16-byte multiple)
+    static constexpr int SI = staged_stride<T, TPL>(NIN) * (int)sizeof(Cx<T>);
+    static constexpr int SA = staged_stride<T, TPL>(L) * (int)sizeof(Cx<T>);
+    static constexpr size_t STG = (size_t)RB * SI, EPB = ADD ? (size_t)RB * SA : 0;
+    static constexpr size_t BUF = 128 + 2 * STG + EPB + RC::LINES;
+    Grid g;
+    const Cx<T>* spec;
+    RowOut<T> epi;
+    const Cx<T>* twN;
+    __device__ __forceinline__ int64_t nrows() const { return (int64_t)g.n2 * g.n3; }
+    __device__ __forceinline__ void issue_in(int tile, unsigned char* dst, uint64_t* b, int lane) const {
+        const int64_t r0 = (int64_t)tile * RB;
+        const int nr = (int)min((int64_t)RB, nrows() - r0);
+        issue_rows(dst, reinterpret_cast<const unsigned char*>(spec), r0, nr, (int64_t)g.n1p * sizeof(Cx<T>), SI,
+                   NIN * sizeof(Cx<T>), b, lane);
+    }
+    __device__ __forceinline__ void issue_ep(int tile, unsigned char* dst, uint64_t* b, int lane) const {
+        if constexpr (ADD) {
+            const int64_t r0 = (int64_t)tile * RB;
+            const int nr = (int)min((int64_t)RB, nrows() - r0);
+            issue_rows(dst, reinterpret_cast<const unsigned char*>(epi.add), r0, nr, (int64_t)L * sizeof(Cx<T>), SA,
+                       L * sizeof(Cx<T>), b, lane);
+        }
+    }
+    __device__ __forceinline__ void run(int tile, const unsigned char* stg, const unsigned char* ep, uint64_t* epb,
+                                        unsigned epar, unsigned char* lines) const {
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        const int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows();
+        Cx<T>* buf = reinterpret_cast<Cx<T>*>(lines) + line * LP;
+        const Cx<T>* in = reinterpret_cast<const Cx<T>*>(stg + line * SI);
+        for (int k = t; k <= L / 2; k += TPL) {
+            Cx<T> Zk, Zl;
+            c2r_pair(in[k], in[L - k], twN[k], Zk, Zl);
+            buf[P(k)] = Zk;
+            if (k != 0 && 2 * k != L) buf[P(L - k)] = Zl;
+        }
+        __syncthreads();
+        const Cx<T>* add = nullptr;
+        if constexpr (ADD) {
+            mbar_wait(epb, epar);
+            add = reinterpret_cast<const Cx<T>*>(ep + line * SA);
+        }
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out) + row * L;
+        fft_line_io<T, L, +1, true, false>(buf, t, twN, 2, SmemLine<T>{buf}, RowSt<T>{dst, add, 0, ok});
+    }
+};
+
+// Persistent driver of a staged row pass: grid = min(tiles, resident CTAs); barriers 0/1 = input stages,
+// 2 = epilogue operand.
+template <class PassT>
+__global__ void __launch_bounds__(PassT::NT, PassT::MINB) k_rows(PassT pass, int ntiles) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* stg = smem_raw + 128;
+    unsigned char* ep = stg + 2 * PassT::STG;
+    unsigned char* lines = ep + PassT::EPB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    int tile = blockIdx.x;
+    if (warp == 0 && tile < ntiles) pass.issue_in(tile, stg, &bar[0], lane);
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const int st = it & 1;
+        if (warp == 0) {
+            // the other stage and the epilogue buffer were last read before the previous trailing barrier
+            if (tile + (int)gridDim.x < ntiles) pass.issue_in(tile + gridDim.x, stg + (st ^ 1) * PassT::STG, &bar[st ^ 1], lane);
+            if (PassT::EPB) pass.issue_ep(tile, ep, &bar[2], lane);
+        }
+        mbar_wait(&bar[st], (unsigned)(it >> 1) & 1u);
+        pass.run(tile, stg + st * PassT::STG, ep, &bar[2], (unsigned)it & 1u, lines);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Column passes along x2 (AX = 2) or x3 (AX = 3) of a complex array with W complex columns per row
 // (W = n1p for spectra, N1/2 for a real field read as pairs) and extents (W, n2, n3).
 // A CTA owns XC consecutive columns x OL lines of the other transverse axis; consecutive lanes own
