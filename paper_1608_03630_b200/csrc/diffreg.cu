@@ -572,12 +572,19 @@ struct Impl {
         PE("unpack");
     }
 
-    template <typename U, int L, int DIR>
-    void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out) {
-        using PT = ColFftPass<U, L, DIR>;
+    template <typename U, int L, int DIR, bool SI, bool SO>
+    void col_fft_LS(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out) {
+        using PT = ColFftPass<U, L, DIR, SI, SO>;
         const ColGeom cg = spec_geom();
         stream(DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32", PT{cg, src, dst, tw, nb_in, nb_out},
                col_tiles<PT>(cg, g.n3));
+    }
+    template <typename U, int L, int DIR>
+    void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out) {
+        // the split layouts only occur on the side facing an all-to-all: out of the forward, into the inverse
+        if (DIR < 0 && nb_out) col_fft_LS<U, L, DIR, false, true>(src, dst, tw, nb_in, nb_out);
+        else if (DIR > 0 && nb_in) col_fft_LS<U, L, DIR, true, false>(src, dst, tw, nb_in, nb_out);
+        else col_fft_LS<U, L, DIR, false, false>(src, dst, tw, nb_in, nb_out);
     }
     template <typename Tc>
     void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out) {  // forward along x2, in Tc

@@ -586,17 +586,22 @@ __device__ __forceinline__ int64_t col_addr(const ColGeom& c, int x, int other, 
     return ((int64_t)p * c.n2 + other) * c.W + x;      // other = i2, p = i3
 }
 
-// Element p of one line of a column array: address base + (p >> sh) * hi + (p & mk) * lo, which covers
-// the plain layouts (sh = 30: one block) and the split layout (blocks of nb = 2^sh lines).
+// Element p of one line of a column array: address base + p * lo in the plain layouts, base +
+// (p >> sh) * hi + (p & mk) * lo in the split layout (blocks of nb = 2^sh lines).  SPLIT is a template
+// flag so the single-GPU passes carry no 64-bit block arithmetic (the plain offset p * lo < 2^31:
+// lo <= n2 * n1p and p < n3 for every supported grid).
 // Out-of-range lines (on = false) read 0 and store nothing.
-template <typename T>
+template <typename T, bool SPLIT = false>
 struct ColAcc {
     Cx<T>* b;
     int64_t hi;
     int lo, sh, mk;
     bool on;
     int acc;
-    __device__ __forceinline__ int64_t at(int p) const { return (int64_t)(p >> sh) * hi + (int64_t)(p & mk) * lo; }
+    __device__ __forceinline__ int64_t at(int p) const {
+        if constexpr (SPLIT) return (int64_t)(p >> sh) * hi + (int64_t)(p & mk) * lo;
+        else return p * lo;
+    }
     __device__ __forceinline__ Cx<T> ld(int p) const { return on ? b[at(p)] : cx(T(0), T(0)); }
     __device__ __forceinline__ void st(int p, const Cx<T>& v) const {
         if (!on) return;
@@ -605,9 +610,9 @@ struct ColAcc {
     }
 };
 
-template <int AX, typename T>
-__device__ __forceinline__ ColAcc<T> col_acc(Cx<T>* a, const ColGeom& c, int x, int o, int nb, bool on, int acc) {
-    ColAcc<T> r;
+template <int AX, typename T, bool SPLIT = false>
+__device__ __forceinline__ ColAcc<T, SPLIT> col_acc(Cx<T>* a, const ColGeom& c, int x, int o, int nb, bool on, int acc) {
+    ColAcc<T, SPLIT> r;
     r.on = on;
     r.acc = acc;
     r.sh = 30;
@@ -720,7 +725,7 @@ struct ColDerivPass {
 // when both layouts are plain: every element is read by its own CTA before that CTA writes it).
 // nb_in / nb_out != 0 select the split layout on that side (the all-to-all chunks of the multi-GPU
 // transposes), fusing the pack / unpack into this pass.
-template <typename T, int L, int DIR>
+template <typename T, int L, int DIR, bool SPLIT_IN = false, bool SPLIT_OUT = false>
 struct ColFftPass {
     using CC = ColCfg<L, T>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
@@ -741,8 +746,9 @@ struct ColFftPass {
         const bool on = x < c.nx && o < c.n3;
         Cx<T>* buf = sm + (oi * XC + xi) * LP;
         const Cx<T>* tw = tw_smem<T, L, NT, TWS>(this->tw, reinterpret_cast<Cx<T>*>(smem + CC::SMEM));
-        fft_line_io<T, L, DIR, false, false>(buf, t, tw, 1, col_acc<2>(const_cast<Cx<T>*>(src), c, x, o, nb_in, on, 0),
-                                             col_acc<2>(dst, c, x, o, nb_out, on, 0));
+        fft_line_io<T, L, DIR, false, false>(buf, t, tw, 1,
+                                             col_acc<2, T, SPLIT_IN>(const_cast<Cx<T>*>(src), c, x, o, nb_in, on, 0),
+                                             col_acc<2, T, SPLIT_OUT>(dst, c, x, o, nb_out, on, 0));
     }
 };
 
