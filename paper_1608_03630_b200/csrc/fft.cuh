@@ -832,6 +832,34 @@ struct Sym {
     }
 };
 
+// Last forward stage of a one-component middle pass with a scalar symbol (KIND 0 / 1: a function of
+// |k|^2 only): the symbol is applied to the stage's outputs in registers and the narrowed values go
+// straight into the inverse's line, so no separate symbol sweep over shared memory is needed.  Same
+// arithmetic as Sym<T, KIND>::apply (kk = (k1^2 + k2^2) + k3^2, factor evaluated in the same order).
+template <typename Ti, typename To, int L, int KIND>
+struct SymSt {
+    Cx<To>* b;  // this line of the inverse's buffer
+    Ti kk12;    // k1^2 + k2^2
+    Ti nrm, beta;
+    int reg;
+    bool live;  // line inside the spectrum (dead lines are stored unscaled and never written out)
+    __device__ __forceinline__ void st(int i, const Cx<Ti>& v) const {
+        Cx<Ti> r = v;
+        if (live) {
+            const Ti k3 = (Ti)wavenum(i, L);
+            const Ti kk = kk12 + k3 * k3;
+            const Ti a = reg == 1 ? kk : kk * kk;
+            if (KIND == 0) {
+                r = scale(v, nrm * beta * a);
+            } else {
+                const Ti ah = (kk == Ti(0)) ? Ti(1) : a;
+                r = scale(v, nrm / (beta * ah));
+            }
+        }
+        b[P(i)] = cx<To>((To)r.re, (To)r.im);
+    }
+};
+
 template <typename T, int NC>
 struct SpecPtrs {
     Cx<T>* p[NC];
@@ -869,6 +897,20 @@ struct MiddlePass {
         const bool on = x0 + xi < c.nx && o0 + oi < c.n2;
         const Cx<T>* tw = tw_smem<T, L, NT, TWS>(this->tw, reinterpret_cast<Cx<T>*>(smem + BUFO));
         const Cx<To>* two = tw_smem<To, L, NT, TWS>(this->two, reinterpret_cast<Cx<To>*>(smem + BUFO + L * sizeof(Cx<T>)));
+        if constexpr (KIND <= 1) {  // scalar symbol fused into the last forward stage
+            const int og = o0 + oi + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
+            const T k1 = (T)(x0 + xi), k2 = (T)wavenum(og, n2g);
+            Cx<T>* buf = sm + line * LP;
+            fft_line_io<T, L, -1, false, true>(
+                buf, t, tw, 1, col_acc<3>(in.p[0], c, x0 + xi, o0 + oi, 0, on, 0),
+                SymSt<T, To, L, KIND>{so + line * LPO, k1 * k1 + k2 * k2, (T)s.norm, (T)s.beta, s.reg, on});
+        } else {
+            forward_and_symbol(x0, o0, xi, t, oi, line, on, tw, sm, so);
+        }
+        inverse(x0, o0, two, so);
+    }
+    __device__ __forceinline__ void forward_and_symbol(int x0, int o0, int xi, int t, int oi, int line, bool on,
+                                                       const Cx<T>* tw, Cx<T>* sm, Cx<To>* so) const {
 #pragma unroll
         for (int ci = 0; ci < NCI; ++ci) {
             Cx<T>* buf = sm + ci * LINES * LP + line * LP;
@@ -894,6 +936,8 @@ struct MiddlePass {
             for (int co = 0; co < NCO; ++co) so[co * LINES * LPO + ln * LPO + P(p)] = cx<To>((To)v[co].re, (To)v[co].im);
         }
         __syncthreads();
+    }
+    __device__ __forceinline__ void inverse(int x0, int o0, const Cx<To>* two, Cx<To>* so) const {
         // inverse lines: the CTA's NT threads cover LINES lines of TPLO threads in NT / (LINES * TPLO) rounds
         static_assert(NT % TPLO == 0, "inverse thread mapping");
         constexpr int PER = NT / TPLO;  // lines per round

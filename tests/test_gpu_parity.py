@@ -82,6 +82,23 @@ def test_spectral_white_noise_nyquist(dr, fp64):
     assert rel(np64(ctx.op_spectral(dr.DR_OP_REG, u.cuda())), O.reg_apply(u64, 2, 1e-2)) < tol
 
 
+@pytest.mark.parametrize("fp64", [False, True])
+def test_spectral_unaligned_input_same_bits(dr, fp64):
+    """An input that is not 16-byte aligned cannot be fetched by the bulk-copy engine (staged row
+    passes); the library then takes the one-tile-per-CTA pass with the same arithmetic: bit-identical."""
+    n = (64, 32, 16)
+    ctx = dr.Context(dr.Config(n=n, nt=2, reg=2, beta=0.37, fp64=fp64))
+    u, _ = prep(synth.smooth_vec(6, n, kmax=5), fp64)
+    u = u.cuda()
+    buf = torch.empty(u.numel() + 1, dtype=u.dtype, device=u.device)
+    ua = buf[1:].view(u.shape)  # 4 / 8 bytes past a 256-byte allocation boundary
+    ua.copy_(u)
+    assert ua.data_ptr() % 16 != 0
+    for op in (dr.DR_OP_REG, dr.DR_OP_PRECOND, dr.DR_OP_GRAD):
+        x, xa = (u[0].contiguous(), buf[1:1 + u[0].numel()].view(u[0].shape)) if op == dr.DR_OP_GRAD else (u, ua)
+        assert torch.equal(ctx.op_spectral(op, x), ctx.op_spectral(op, xa)), op
+
+
 # ------------------------------------------------------------------ interpolation
 
 @pytest.mark.parametrize("fp64", [False, True])
