@@ -29,8 +29,11 @@
  * (pinned or pageable); the library detects which with cudaPointerGetAttributes.  Host inputs
  * are copied into the workspace on the context stream; host outputs are copied back and the call
  * synchronises the stream before it returns.  Device-pointer calls are asynchronous w.r.t. the
- * host and ordered on the context stream (like cuBLAS).  The dr_op_* / dr_get_* test hooks take
- * device pointers only.
+ * host and ordered on the context stream (like cuBLAS).  Kernels read device fields with 16-byte
+ * bulk copies and vector loads: a device pointer that is not 16-byte aligned (e.g. a tensor view at
+ * an odd element offset) is staged through the workspace like a host pointer (one extra device copy)
+ * by the main-path calls and dr_op_spectral.  The other dr_op_* / dr_get_* test hooks take 16-byte
+ * aligned device pointers only.
  *
  * OWNERSHIP.  The caller owns every input, output and the workspace.  Inputs are only read;
  * images and the velocity are copied into the workspace (retained).  Outputs are fully

@@ -1407,22 +1407,26 @@ bool is_device_ptr(const void* p) {
 
 size_t elem_size(const dr_ctx* c) { return (c->cfg.flags & DR_FP64) ? 8 : 4; }
 
-// input: device pointers are used in place, host pointers are staged into `stage`
+bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// input: 16-byte aligned device pointers are used in place; host pointers and unaligned device
+// pointers (the kernels' bulk copies and vector loads need 16 bytes) are staged into `stage`
 const void* stage_in(dr_ctx* c, const void* p, size_t bytes, void* stage) {
-    if (is_device_ptr(p)) return p;
-    CK(cudaMemcpyAsync(stage, p, bytes, cudaMemcpyHostToDevice, c->stream));
+    if (is_device_ptr(p) && aligned16(p)) return p;
+    CK(cudaMemcpyAsync(stage, p, bytes, cudaMemcpyDefault, c->stream));
     return stage;
 }
 
 template <typename F>
 void with_output(dr_ctx* c, void* out, size_t bytes, void* stage, F&& f) {
-    if (is_device_ptr(out)) {
+    const bool dev = is_device_ptr(out);
+    if (dev && aligned16(out)) {
         f(out);
         return;
     }
     f(stage);
-    CK(cudaMemcpyAsync(out, stage, bytes, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(out, stage, bytes, cudaMemcpyDefault, c->stream));
+    if (!dev) CK(cudaStreamSynchronize(c->stream));
 }
 
 template <typename F>
@@ -1906,21 +1910,25 @@ const char* dr_status_string(dr_status s) {
 dr_status dr_op_spectral(dr_ctx* c, int op, const void* in, void* out) {
     return run(c, [&] {
         if (!in || !out) fail(DR_ERR_ARG, "in/out must be non-NULL");
-        dispatch(c, [&](auto& im) {
-            using T = std::remove_pointer_t<decltype(im.rhoR())>;
-            const T* i = static_cast<const T*>(in);
-            T* o = static_cast<T*>(out);
-            const size_t M = c->g.M;
-            const V3<const T> i3 = cvec(vec(const_cast<T*>(i), M));
-            const V3<T> o3 = vec(o, M);
-            switch (op) {
-                case DR_OP_GRAD: im.grad(i, o3); break;
-                case DR_OP_DIV: im.div(i3, o); break;
-                case DR_OP_REG: im.reg_apply(i3, o3); break;
-                case DR_OP_PRECOND: im.precond(i3, o3); break;
-                case DR_OP_LERAY: im.leray(i3, o3); break;
-                default: fail(DR_ERR_ARG, "unknown spectral op");
-            }
+        if (op < DR_OP_GRAD || op > DR_OP_LERAY) fail(DR_ERR_ARG, "unknown spectral op");
+        const size_t F = c->g.M * elem_size(c);
+        const void* ip = stage_in(c, in, op == DR_OP_GRAD ? F : 3 * F, c->ws + c->L.stin);
+        with_output(c, out, op == DR_OP_DIV ? F : 3 * F, c->ws + c->L.stout, [&](void* op_out) {
+            dispatch(c, [&](auto& im) {
+                using T = std::remove_pointer_t<decltype(im.rhoR())>;
+                const T* i = static_cast<const T*>(ip);
+                T* o = static_cast<T*>(op_out);
+                const size_t M = c->g.M;
+                const V3<const T> i3 = cvec(vec(const_cast<T*>(i), M));
+                const V3<T> o3 = vec(o, M);
+                switch (op) {
+                    case DR_OP_GRAD: im.grad(i, o3); break;
+                    case DR_OP_DIV: im.div(i3, o); break;
+                    case DR_OP_REG: im.reg_apply(i3, o3); break;
+                    case DR_OP_PRECOND: im.precond(i3, o3); break;
+                    case DR_OP_LERAY: im.leray(i3, o3); break;
+                }
+            });
         });
     });
 }

@@ -84,8 +84,8 @@ def test_spectral_white_noise_nyquist(dr, fp64):
 
 @pytest.mark.parametrize("fp64", [False, True])
 def test_spectral_unaligned_input_same_bits(dr, fp64):
-    """An input that is not 16-byte aligned cannot be fetched by the bulk-copy engine (staged row
-    passes); the library then takes the one-tile-per-CTA pass with the same arithmetic: bit-identical."""
+    """Device inputs and outputs that are not 16-byte aligned (the kernels' bulk copies and vector
+    loads need 16 bytes) are staged through the workspace: same bits as aligned buffers, no fault."""
     n = (64, 32, 16)
     ctx = dr.Context(dr.Config(n=n, nt=2, reg=2, beta=0.37, fp64=fp64))
     u, _ = prep(synth.smooth_vec(6, n, kmax=5), fp64)
@@ -94,9 +94,16 @@ def test_spectral_unaligned_input_same_bits(dr, fp64):
     ua = buf[1:].view(u.shape)  # 4 / 8 bytes past a 256-byte allocation boundary
     ua.copy_(u)
     assert ua.data_ptr() % 16 != 0
+    obuf = torch.empty_like(buf)
+    oa = obuf[1:].view(u.shape)  # unaligned output as well
     for op in (dr.DR_OP_REG, dr.DR_OP_PRECOND, dr.DR_OP_GRAD):
         x, xa = (u[0].contiguous(), buf[1:1 + u[0].numel()].view(u[0].shape)) if op == dr.DR_OP_GRAD else (u, ua)
-        assert torch.equal(ctx.op_spectral(op, x), ctx.op_spectral(op, xa)), op
+        assert torch.equal(ctx.op_spectral(op, x), ctx.op_spectral(op, xa, out=oa)), op
+    # main path: the matvec with an unaligned input and output
+    ctx.set_images(*(prep(synth.blobs(s_, n, kcut=8), fp64)[0].cuda() for s_ in (1, 2)))
+    ctx.set_velocity(prep(synth.smooth_vec(3, n, kmax=4, cells_per_step=1.5, nt=2), fp64)[0].cuda())
+    ctx.forward_solve()
+    assert torch.equal(ctx.hessian_matvec(u), ctx.hessian_matvec(ua, Hvt=oa))
 
 
 # ------------------------------------------------------------------ interpolation
