@@ -195,10 +195,12 @@ struct EpiAdjoint {
     const T* D;                              // div v at x (nullable: isochoric)
     const T* snew;                           // s_{k-1} at x
     T hdt, dtt;                              // dt / 2, dt
-    struct Late { T m; T g[3]; T b[3]; T Dx, sn; };
+    // late() only loads: arithmetic on a loaded value here would stall the warp on the load right away
+    // instead of a pair later (store() does all of it; same operations in the same order)
+    struct Late { T m; T g[3]; T b[3]; T Dx, sn, nu; };
     __device__ __forceinline__ Late late(uint32_t id) const {
         Late l;
-        l.m = m ? scale * __ldg(m + id) : scale;
+        l.m = m ? __ldg(m + id) : T(1);
         if constexpr (NEWTON) {
             l.Dx = D ? __ldg(D + id) : T(0);
             l.sn = __ldg(snew + id);
@@ -211,24 +213,32 @@ struct EpiAdjoint {
                 l.b[0] = b0[id];
                 l.b[1] = b1[id];
                 l.b[2] = b2[id];
-            } else {
-                const T ln = wn * snu * __ldg(nu + id);
-                l.b[0] = ln * __ldg(H0 + id);
-                l.b[1] = ln * __ldg(H1 + id);
-                l.b[2] = ln * __ldg(H2 + id);
+            } else {  // G_nt (the b~ term of nu_nt) parked in b
+                l.nu = __ldg(nu + id);
+                l.b[0] = __ldg(H0 + id);
+                l.b[1] = __ldg(H1 + id);
+                l.b[2] = __ldg(H2 + id);
             }
         }
         return l;
     }
     __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
-        T r = l.m * val[0];
+        const T mm = m ? scale * l.m : scale;
+        T r = mm * val[0];
         if constexpr (NEWTON) r += hdt * (T(1) + dtt * l.Dx) * val[1] + hdt * l.sn;
         out[id] = r;
         if constexpr (QUAD != 0) {
+            T b[3] = {l.b[0], l.b[1], l.b[2]};
+            if constexpr (QUAD == 1) {
+                const T ln = wn * snu * l.nu;
+                b[0] = ln * l.b[0];
+                b[1] = ln * l.b[1];
+                b[2] = ln * l.b[2];
+            }
             const T wr = w * r;
-            b0[id] = l.b[0] + wr * l.g[0];
-            b1[id] = l.b[1] + wr * l.g[1];
-            b2[id] = l.b[2] + wr * l.g[2];
+            b0[id] = b[0] + wr * l.g[0];
+            b1[id] = b[1] + wr * l.g[1];
+            b2[id] = b[2] + wr * l.g[2];
         }
     }
 };
