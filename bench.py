@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-out", default=None, help="write the per-kernel table (JSON) here")
+    p.add_argument("--profile-steps", type=int, default=2, help="untimed steps with every launch timed")
     return p.parse_args()
 
 
@@ -301,8 +302,26 @@ def run_ours(args, ws, rank, local):
         step(v, vts, Hv, Z)
     torch.cuda.synchronize()
 
-    # ---- timed region (device-resident inputs)
+    # ---- untimed profiling pass: every launch bracketed by CUDA events -> the per-kernel table and the
+    # dominant kernel.  (Timing every launch costs ~2 us of GPU idle per launch, ~6 % of the step, so
+    # the timed region below brackets only the dominant kernel's launches.)
     ctx.profile_reset()
+    ctx.profile_only(None)
+    ctx.profile_enable(True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.profile_steps):
+        step(v, vts, Hv, Z)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof_all, _ = ctx.profile()
+    ctx.profile_enable(False)
+    prof_ms = p0.elapsed_time(p1)
+    dom_tag = max((t for t in prof_all if not t.endswith("@aux")), key=lambda t: prof_all[t][1])
+
+    # ---- timed region (device-resident inputs); the dominant kernel's launches timed live
+    ctx.profile_reset()
+    ctx.profile_only(dom_tag)
     ctx.profile_enable(True)
     clocks = Clocks(local)
     clocks.start()
@@ -319,6 +338,7 @@ def run_ours(args, ws, rank, local):
     clk = clocks.stop()
     prof, launches = ctx.profile()
     ctx.profile_enable(False)
+    ctx.profile_only(None)
     ms_max = max_over_ranks(ms, ws)
     T = ms_max / 1e3
     # every matvec is one collective over all ranks of the whole 256^3 problem (strong scaling)
@@ -337,18 +357,21 @@ def run_ours(args, ws, rank, local):
 
     # ---- dominant kernel roofline (algorithmic bytes / live CUDA-event duration)
     peak, peak_kind = peaks()
-    table = []
-    for tag, (k, tms) in prof.items():
-        b = algo_bytes(tag, n, NT)
-        if b is not None:
-            b = b // ws  # per-rank share of the slab-decomposed launch
-        avg = tms / k
-        table.append({"tag": tag, "launches": k, "total_ms": tms, "avg_ms": avg, "share": tms / ms,
-                      "algo_bytes": b, "gbs": (b / (avg / 1e3) / 1e9) if b else None})
-    table.sort(key=lambda r: -r["total_ms"])
-    # kernels tagged @aux run concurrently with the sweeps on a low-priority stream: their event
-    # durations overlap other kernels', so the dominant (roofline) kernel is chosen among the others
-    dom = next(r for r in table if not r["tag"].endswith("@aux"))
+    def rows(p, total_ms):
+        out = []
+        for tag, (k, tms) in p.items():
+            b = algo_bytes(tag, n, NT)
+            if b is not None:
+                b = b // ws  # per-rank share of the slab-decomposed launch
+            avg = tms / k
+            out.append({"tag": tag, "launches": k, "total_ms": tms, "avg_ms": avg, "share": tms / total_ms,
+                        "algo_bytes": b, "gbs": (b / (avg / 1e3) / 1e9) if b else None})
+        return sorted(out, key=lambda r: -r["total_ms"])
+    # per-kernel table from the profiling pass; the dominant kernel's numbers from the timed region
+    # (kernels tagged @aux run concurrently with the sweeps on a low-priority stream: their event
+    # durations overlap other kernels', so the dominant (roofline) kernel is chosen among the others)
+    table = rows(prof_all, prof_ms)
+    dom = rows({dom_tag: prof[dom_tag]}, ms)[0]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -362,7 +385,8 @@ def run_ours(args, ws, rank, local):
             "share_of_step": dom["share"]}
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as f:
-            json.dump({"step_ms": ms / args.steps, "kernels": table, "matvec_ms": mv_ms}, f, indent=1)
+            json.dump({"step_ms": ms / args.steps, "profiled_step_ms": prof_ms / args.profile_steps,
+                       "kernels": table, "matvec_ms": mv_ms, "dominant_timed": dom}, f, indent=1)
 
     # ---- e2e: the same step through the C ABI with host buffers (copies inside the timed region)
     e2e = None

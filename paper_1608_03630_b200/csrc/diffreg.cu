@@ -41,7 +41,7 @@ void ck(cudaError_t e, const char* what) {
 }
 #define CK(x) ck((x), #x)
 #define CKL(name) ck(cudaGetLastError(), name)
-// launch bracketing: PB() before a kernel launch, PE(tag) after it (error check + accounting + profiling)
+// launch bracketing: PB(tag) before a kernel launch, PE(tag) after it (error check + accounting + profiling)
 
 int ilog2(int n) {
     int l = 0;
@@ -209,6 +209,7 @@ struct dr_ctx {
     // launch accounting and optional per-kernel CUDA-event profiling (dr_profile_*)
     int64_t launches = 0;
     bool prof = false;
+    std::string prof_only;  // non-empty: time only the launches with this tag (dr_profile_only)
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     struct Pending { const char* tag; cudaEvent_t a, b; };
@@ -225,8 +226,9 @@ struct dr_ctx {
         }
         return ev_pool[ev_used++];
     }
-    void prof_begin(cudaStream_t st) {
-        if (prof) {
+    bool prof_on(const char* tag) const { return prof && (prof_only.empty() || prof_only == tag); }
+    void prof_begin(const char* tag, cudaStream_t st) {
+        if (prof_on(tag)) {
             cur_start = take_event();
             cudaEventRecord(cur_start, st);
         }
@@ -240,7 +242,7 @@ struct dr_ctx {
 void dr_ctx::prof_end(const char* tag, cudaStream_t st) {
     ck(cudaGetLastError(), tag);
     ++launches;
-    if (prof) {
+    if (prof_on(tag)) {
         cudaEvent_t e = take_event();
         cudaEventRecord(e, st);
         pending.push_back(Pending{tag, cur_start, e});
@@ -303,7 +305,7 @@ struct Impl {
     const Grid& g;
     cudaStream_t s;
     explicit Impl(dr_ctx& cc) : c(cc), g(cc.g), s(cc.stream) {}
-    void PB() { c.prof_begin(s); }
+    void PB(const char* tag) { c.prof_begin(tag, s); }
     void PE(const char* tag) { c.prof_end(tag, s); }
 
     size_t plane() const { return (size_t)g.n1 * g.n2; }
@@ -353,7 +355,7 @@ struct Impl {
     // -------------------------------------------------------------------- slab exchanges
     int nb() const { return g.n2 / c.nranks; }  // x2 block of one rank in the transposed layout
     void exchange(const std::vector<P2P>& ops) {
-        PB();
+        PB("exchange");
         try {
             c.comm->group(ops, s);
         } catch (const NcclError& e) {
@@ -424,7 +426,7 @@ struct Impl {
             set_smem(k, PassT::BUF);
             attr = true;
         }
-        PB();
+        PB(tag);
         k<<<(unsigned)ntiles, PassT::NT, PassT::BUF, s>>>(pass);
         PE(tag);
     }
@@ -442,7 +444,7 @@ struct Impl {
         }
         const int64_t nt = row_tiles<PassT::RB>();
         const int grid = (int)std::min<int64_t>(nt, (int64_t)per_sm * c.num_sms);
-        PB();
+        PB(tag);
         k<<<grid, PassT::NT, PassT::BUF, s>>>(pass, (int)nt);
         PE(tag);
     }
@@ -559,7 +561,7 @@ struct Impl {
             return;
         }
         const size_t chunk = (size_t)g.n3 * nb() * g.n1 * sizeof(T);
-        PB();
+        PB("pack");
         k_pack_split<T><<<grid_1d(g.M), 256, 0, s>>>(g, f, xs(), nb());
         PE("pack");
         alltoall(xs(), xr(), chunk);
@@ -567,7 +569,7 @@ struct Impl {
         DR_SWITCH_COL(g.n3g, CALL)
 #undef CALL
         alltoall(xr(), xs(), chunk);
-        PB();
+        PB("unpack");
         k_unpack_split<T><<<grid_1d(g.M), 256, 0, s>>>(g, xs(), out, nb(), acc);
         PE("unpack");
     }
@@ -690,7 +692,7 @@ struct Impl {
     // Per-tile gather plan of a displacement field (once per velocity and direction).
     void plan(const T* d, int* plan_buf) {
         int* mx = c.at<int>(c.L.maxext);
-        PB();
+        PB("sl_plan");
         k_sl_plan<T><<<(unsigned)n_tiles(g), SL_THREADS, 0, s>>>(g, d, plan_buf, mx);
         PE("sl_plan");
     }
@@ -732,7 +734,7 @@ struct Impl {
         RP r = rp(f);
         const Disp<T> dp{{d, d + g.M, d + 2 * g.M}};
         CK(cudaMemsetAsync(r.cnt, 0, 192 * sizeof(int), s));
-        PB();
+        PB("remote_plan");
         k_remote_classify<T><<<grid_1d(g.M), 256, 0, s>>>(g, dp, 0, r.cnt, r.off, r.cur, r.ids_out, r.rec_out, 0);
         PE("remote_plan");
         H.out_cnt.assign(P, 0);
@@ -763,7 +765,7 @@ struct Impl {
         CK(cudaMemcpyAsync(r.off, H.out_off.data(), P * sizeof(int), cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(r.cur, 0, 64 * sizeof(int), s));
         if (H.n_out > 0) {
-            PB();
+            PB("remote_plan");
             k_remote_classify<T><<<grid_1d(g.M), 256, 0, s>>>(g, dp, 1, r.cnt, r.off, r.cur, r.ids_out, r.rec_out,
                                                                 (int)c.L.rcap);
             PE("remote_plan");
@@ -788,7 +790,7 @@ struct Impl {
         auto& H = c.rp[f];
         RP r = rp(f);
         if (H.n_in > 0) {
-            PB();
+            PB("remote_eval");
             k_remote_eval<T, NC><<<grid_1d(H.n_in), 256, 0, s>>>(g, base_src, r.rec_in, H.n_in, r.val_in);
             PE("remote_eval");
         }
@@ -815,12 +817,12 @@ struct Impl {
         set_smem(k, sm);
         const Disp<T> dp{{d, d + g.M, d + 2 * g.M}};
         const int nt = (int)n_tiles(g);  // one CTA per tile
-        PB();
+        PB(tag);
         k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
         PE(tag);
         if (remote && c.rp[f].n_out > 0) {
             RP r = rp(f);
-            PB();
+            PB("remote_fixup");
             k_remote_fixup<T, NC, Epi><<<grid_1d(c.rp[f].n_out), 256, 0, s>>>(r.ids_out, r.val_out, c.rp[f].n_out, epi);
             PE("remote_fixup");
         }
@@ -847,7 +849,7 @@ struct Impl {
         const double dtt = 1.0 / c.cfg.nt;
         for (int sg = 1; sg >= -1; sg -= 2) {
             T* dout = sg > 0 ? dplus() : dminus();
-            PB();
+            PB("dstar");
             k_dstar<T><<<grid_1d(g.M), 256, 0, s>>>(g, vc(0), vc(1), vc(2), tmp3(), (T)(sg * dtt / h[0]),
                                                     (T)(sg * dtt / h[1]), (T)(sg * dtt / h[2]));
             PE("dstar");
@@ -872,7 +874,7 @@ struct Impl {
 
     void adjoint_solve() {
         const int nt = c.cfg.nt;
-        PB();
+        PB("sub");
         k_sub<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, rhoR(), rho(nt), lam(nt));
         PE("sub");
         for (int k = nt; k >= 1; --k)
@@ -902,7 +904,7 @@ struct Impl {
 
     // NEXT-1: reduced gradient g = beta A v + P b, b = dt sum_j w_j lambda_j G_j (Eq. 4)
     void gradient(V3<T> gout) {
-        PB();
+        PB("quadrature");
         k_quadrature<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, c.cfg.nt, lam(0), gstride(), G(0), tmp3(), dt());
         PE("quadrature");
         if (c.cfg.flags & DR_ISOCHORIC) {
@@ -945,10 +947,10 @@ struct Impl {
     double reduce(const T* a, const T* b, const T* a2, int mode, int64_t n) {
         double* part = c.at<double>(c.L.red);
         const int nb = (int)std::min<int64_t>(2048, (n + 255) / 256);
-        PB();
+        PB("reduce");
         k_dot_parts<T><<<nb, 256, 0, s>>>(n, a, b, a2, nullptr, part, mode);
         PE("reduce");
-        PB();
+        PB("reduce");
         k_sum_parts<<<1, 256, 0, s>>>(part, nb, part + 2048);
         PE("reduce");
         return allsum(part + 2048);
@@ -970,7 +972,7 @@ struct Impl {
         return reduce(a, b, nullptr, 0, 3 * g.M);
     }
     void axpby(double a, const T* x, double b, T* y) {
-        PB();
+        PB("axpby");
         k_axpby<T><<<grid_1d(3 * g.M), 256, 0, s>>>(3 * g.M, a, x, b, y);
         PE("axpby");
     }
@@ -1018,15 +1020,15 @@ struct Impl {
     void dot_dev(const T* a, const T* b, double* out, int64_t n) {
         double* part = c.at<double>(c.L.red);
         const int nb = (int)std::min<int64_t>(2048, (n + 255) / 256);
-        PB();
+        PB("reduce");
         k_dot_parts<T><<<nb, 256, 0, s>>>(n, a, b, nullptr, nullptr, part, 0);
         PE("reduce");
-        PB();
+        PB("reduce");
         k_sum_parts<<<1, 256, 0, s>>>(part, nb, out);
         PE("reduce");
     }
     void axpby_dev(const double* pa, double sa, const T* x, const double* pb, double cb, T* y) {
-        PB();
+        PB("axpby");
         k_axpby_dev<T><<<grid_1d(3 * g.M), 256, 0, s>>>(3 * g.M, pa, sa, x, pb, cb, y);
         PE("axpby");
     }
@@ -1036,7 +1038,7 @@ struct Impl {
         const int64_t n = 3 * g.M;
         hessian_matvec(p, q);
         dot_dev(p, q, sc + 1, n);
-        PB();
+        PB("pcg_scalar");
         k_scalar_ratio<<<1, 32, 0, s>>>(sc, 0, 1, 4, 0);  // alpha = rz / pq
         PE("pcg_scalar");
         axpby_dev(sc + 4, 1.0, p, nullptr, 1.0, dv);   // dv += alpha p
@@ -1045,7 +1047,7 @@ struct Impl {
         CK(cudaMemcpyAsync(c.pinned, sc + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
         precond(cvec(vec(r, (size_t)g.M)), vec(z, (size_t)g.M));
         dot_dev(r, z, sc + 3, n);
-        PB();
+        PB("pcg_scalar");
         k_scalar_ratio<<<1, 32, 0, s>>>(sc, 3, 0, 5, 1);  // beta = rz_new / rz; rz = rz_new
         PE("pcg_scalar");
         axpby_dev(nullptr, 1.0, z, sc + 5, 0.0, p);    // p = z + beta p
@@ -1129,21 +1131,21 @@ struct Impl {
         for (int j = 1; j <= nt; ++j) {
             const T* rtj = rt1();
             if (j < nt) {
-                PB();
+                PB("newton_rt");
                 k_rt_from_g<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, lt(j), vt, G(j), T(0.5) * dtt, sc());
                 PE("newton_rt");
                 rtj = sc();
             }
             grad(rtj, gr);
             const T w = (j == nt) ? T(0.5) * dtt : dtt;
-            PB();
+            PB("newton_b");
             k_acc_lam_grad<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, lam(j), tmp3(), w, bN(), first ? 1 : 0);
             PE("newton_b");
             first = false;
         }
         if (first) CK(cudaMemsetAsync(bN(), 0, 3 * g.M * sizeof(T), s));
         for (int k = 0; k <= nt; ++k) {
-            PB();
+            PB("newton_flux");
             k_lam_vt<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, lam(k), vt, tmp3());
             PE("newton_flux");
             div(cvec(gr), sN(k));
@@ -1159,7 +1161,7 @@ struct Impl {
         const T dtt = dt();
         for (int a = 0; a < 3; ++a) {
             T* w[2] = {lt(0), rt1()};
-            PB();
+            PB("deform_init");
             k_scale<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, vc(a), w[0], T(-0.5) * dtt);
             PE("deform_init");
             for (int j = 0; j < nt; ++j) {
@@ -1173,15 +1175,15 @@ struct Impl {
     // det grad y_1 = det(I + grad u_1) and its extrema over all ranks
     void det_grad_y(V3<const T> u, T* det, double* mn, double* mx) {
         for (int a = 0; a < 3; ++a) grad(u.c[a], vec(kry(a), (size_t)g.M));
-        PB();
+        PB("det");
         k_det<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, kry(0), kry(1), kry(2), det);
         PE("det");
         double* part = c.at<double>(c.L.red);
         const int nb = (int)std::min<int64_t>(1024, (g.M + 255) / 256);
-        PB();
+        PB("reduce");
         k_minmax_parts<T><<<nb, 256, 0, s>>>(g.M, det, part);
         PE("reduce");
-        PB();
+        PB("reduce");
         k_minmax_final<<<1, 256, 0, s>>>(part, nb, part + 2048);
         PE("reduce");
         // extrema over ranks: min = -max(-x); gather both per rank through allsum's slots
@@ -1329,7 +1331,7 @@ struct Impl {
         }
 
         // incremental state (Algorithm 2, merged gather g_j = rho~_j + dt/2 f_j)
-        PB();
+        PB("inc_init");
         k_inc_init<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, vt, G(0), lt(0), T(0.5) * dtt);
         PE("inc_init");
         for (int j = 0; j < nt; ++j) {
@@ -1849,6 +1851,12 @@ dr_status dr_profile_enable(dr_ctx* c, int enable) {
     });
 }
 
+dr_status dr_profile_only(dr_ctx* c, const char* tag) {
+    if (!c) return DR_ERR_ARG;
+    c->prof_only = tag ? tag : "";
+    return DR_OK;
+}
+
 dr_status dr_profile_reset(dr_ctx* c) {
     return run(c, [&] {
         c->prof_flush();
@@ -1941,7 +1949,7 @@ dr_status dr_op_interp(dr_ctx* c, const void* f, int64_t npts, const void* s, vo
         if (!f || !s || !out) fail(DR_ERR_ARG, "bad interp arguments");
         dispatch(c, [&](auto& im) {
             using T = std::remove_pointer_t<decltype(im.rhoR())>;
-            im.PB();
+            im.PB("interp_points");
             k_interp_points<T><<<im.grid_1d(npts), 256, 0, c->stream>>>(c->g, static_cast<const T*>(f), npts,
                                                                           static_cast<const T*>(s), static_cast<T*>(out));
             im.PE("interp_points");
@@ -1999,7 +2007,7 @@ dr_status dr_get_field(dr_ctx* c, int which, int j, void* out) {
                     need(c->have_matvec, "needs hessian_matvec");
                     jrange();
                     if (j == nt) {  // lambda~(1) = -rho~(1) (Eq. 5d); materialise it
-                        im.PB();
+                        im.PB("scale");
                         k_scale<T><<<im.grid_1d(c->g.M), 256, 0, c->stream>>>(c->g.M, im.rt1(), o, T(-1));
                         im.PE("scale");
                     } else {

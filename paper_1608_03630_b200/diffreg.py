@@ -30,7 +30,7 @@ DR_OP_GRAD, DR_OP_DIV, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY = range(5)
 EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr_set_velocity",
            "dr_forward_solve", "dr_adjoint_solve", "dr_hessian_matvec", "dr_precond_apply", "dr_sync",
            "dr_last_error", "dr_status_string", "dr_op_spectral", "dr_op_interp", "dr_get_departure",
-           "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_count", "dr_profile_entry",
+           "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_only", "dr_profile_count", "dr_profile_entry",
            "dr_nccl_get_unique_id", "dr_comm_create_nccl", "dr_hub_create", "dr_hub_destroy",
            "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist",
            "dr_gradient", "dr_objective", "dr_pcg", "dr_deformation", "dr_solve", "dr_comm_selftest"]
@@ -83,6 +83,7 @@ def lib():
                            ("dr_op_interp", [vp, vp, i64, vp, vp]), ("dr_get_departure", [vp, i32, vp]),
                            ("dr_get_field", [vp, i32, i32, vp]), ("dr_profile_enable", [vp, i32]),
                            ("dr_profile_reset", [vp]),
+                           ("dr_profile_only", [vp, ctypes.c_char_p]),
                            ("dr_profile_count", [vp, ctypes.POINTER(i32), ctypes.POINTER(i64)]),
                            ("dr_profile_entry", [vp, i32, ctypes.c_char_p, i32, ctypes.POINTER(i64),
                                                  ctypes.POINTER(ctypes.c_double)])]:
@@ -375,6 +376,10 @@ class Context:
 
     def profile_reset(self):
         self._check(lib().dr_profile_reset(self.h))
+
+    def profile_only(self, tag=None):
+        """Time only the launches tagged `tag` (None: all)."""
+        self._check(lib().dr_profile_only(self.h, tag.encode() if tag else None))
 
     def profile(self):
         """({tag: (launches, total_ms)}, total kernel launches since the last reset)."""
