@@ -114,6 +114,9 @@ def algo_bytes(tag, n, nt, es=4):
         "row_c2r": 2 * es * Sc + es * M,            # spectrum in, real out
         "row_c2r_add": 2 * es * Sc + 2 * es * M,    # + b~ in
     }
+    if tag.endswith("_x3"):  # the three components of a vector field in one launch (blockIdx.y)
+        b = table.get(tag[:-3])
+        return None if b is None else 3 * b
     return table.get(tag)
 
 

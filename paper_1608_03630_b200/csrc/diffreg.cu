@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <set>
 #include <type_traits>
 #include <string>
 #include <vector>
@@ -418,23 +419,30 @@ struct Impl {
     }
 
     // Launch of an FFT pass: one CTA per tile.
+    // Batched launches (nc > 1, blockIdx.y = component) carry the tag suffix "_x<nc>".
+    static const char* tag_n(const char* tag, int nc) {
+        if (nc == 1) return tag;
+        static std::set<std::string> pool;  // stable storage for composed tags
+        return pool.insert(std::string(tag) + "_x" + std::to_string(nc)).first->c_str();
+    }
     template <class PassT>
-    void stream(const char* tag, const PassT& pass, int64_t ntiles) {
+    void stream(const char* tag, const PassT& pass, int64_t ntiles, int nc = 1) {
         auto k = k_stream<PassT>;
         static bool attr = false;  // per pass instantiation
         if (!attr) {
             set_smem(k, PassT::BUF);
             attr = true;
         }
+        tag = tag_n(tag, nc);
         PB(tag);
-        k<<<(unsigned)ntiles, PassT::NT, PassT::BUF, s>>>(pass);
+        k<<<dim3((unsigned)ntiles, (unsigned)nc), PassT::NT, PassT::BUF, s>>>(pass);
         PE(tag);
     }
     template <int RB>
     int64_t row_tiles() const { return ((int64_t)g.n2 * g.n3 + RB - 1) / RB; }
     // Launch of a staged row pass (fft.cuh k_rows): persistent, one wave of resident CTAs.
     template <class PassT>
-    void stream_rows(const char* tag, const PassT& pass) {
+    void stream_rows(const char* tag, const PassT& pass, int nc = 1) {
         auto k = k_rows<PassT>;
         static int per_sm = 0;  // per pass instantiation
         if (!per_sm) {
@@ -443,9 +451,10 @@ struct Impl {
             per_sm = std::max(per_sm, 1);
         }
         const int64_t nt = row_tiles<PassT::RB>();
-        const int grid = (int)std::min<int64_t>(nt, (int64_t)per_sm * c.num_sms);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)per_sm * c.num_sms / nc));
+        tag = tag_n(tag, nc);
         PB(tag);
-        k<<<grid, PassT::NT, PassT::BUF, s>>>(pass, (int)nt);
+        k<<<dim3(grid, nc), PassT::NT, PassT::BUF, s>>>(pass, (int)nt);
         PE(tag);
     }
     // the bulk-copy engine needs 16-byte aligned rows (all workspace fields are; caller buffers may not be)
@@ -463,27 +472,28 @@ struct Impl {
     template <typename U> const Cx<U>* twz_t() { if constexpr (sizeof(U) == sizeof(double)) return reinterpret_cast<const Cx<U>*>(twzd()); else return reinterpret_cast<const Cx<U>*>(twz()); }
     template <typename U> Cx<U>* specD_t(int i) { return reinterpret_cast<Cx<U>*>(c.ws + c.L.specD) + (size_t)i * g.S; }
 
+    // (nc components at element strides csf (real fields) / css (spectra) in one launch)
     template <int L, typename Tc>
-    void row_r2c_L(const T* f, Cx<Tc>* sp) {
+    void row_r2c_L(const T* f, Cx<Tc>* sp, int nc, int64_t csf, int64_t css) {
         const char* tag = sizeof(Tc) == 8 ? "row_r2c_f64" : "row_r2c_f32";
         // staged for the widened (complex128) transform; in T the one-tile-per-CTA pass keeps more warps
         // for the compute (measured 36.8 vs 38.0 us at 256^3)
         if (sizeof(Tc) > sizeof(T) && al16(f)) {
-            stream_rows(tag, RowR2cStaged<T, Tc, L>{g, f, sp, twx_t<Tc>()});
+            stream_rows(tag, RowR2cStaged<T, Tc, L>{g, f, sp, twx_t<Tc>(), csf, css}, nc);
             return;
         }
         using PT = RowR2cPass<T, Tc, L>;
-        stream(tag, PT{g, f, sp, twx_t<Tc>()}, row_tiles<PT::RB>());
+        stream(tag, PT{g, f, sp, twx_t<Tc>(), csf, css}, row_tiles<PT::RB>(), nc);
     }
     template <int L>
-    void row_c2r_L(const Cx<T>* sp, T* out, const T* add) {
+    void row_c2r_L(const Cx<T>* sp, T* out, const T* add, int nc, int64_t csf, int64_t css) {
         if (al16(sp) && al16(add)) {
-            if (add) stream_rows("row_c2r_add", RowC2rStaged<T, L, true>{g, sp, RowOut<T>{out, add}, twx()});
-            else stream_rows("row_c2r", RowC2rStaged<T, L, false>{g, sp, RowOut<T>{out, nullptr}, twx()});
+            if (add) stream_rows("row_c2r_add", RowC2rStaged<T, L, true>{g, sp, RowOut<T>{out, add}, twx(), csf, css}, nc);
+            else stream_rows("row_c2r", RowC2rStaged<T, L, false>{g, sp, RowOut<T>{out, nullptr}, twx(), csf, css}, nc);
             return;
         }
         using PT = RowC2rPass<T, L>;
-        stream(add ? "row_c2r_add" : "row_c2r", PT{g, sp, RowOut<T>{out, add}, twx()}, row_tiles<PT::RB>());
+        stream(add ? "row_c2r_add" : "row_c2r", PT{g, sp, RowOut<T>{out, add}, twx(), csf, css}, row_tiles<PT::RB>(), nc);
     }
 
 #define DR_SWITCH_ROW(Lval, call)                          \
@@ -519,13 +529,13 @@ struct Impl {
 #undef CALL
     }
     template <typename Tc>
-    void row_r2c(const T* f, Cx<Tc>* sp) {
-#define CALL(LL) row_r2c_L<LL, Tc>(f, sp)
+    void row_r2c(const T* f, Cx<Tc>* sp, int nc = 1, int64_t csf = 0, int64_t css = 0) {
+#define CALL(LL) row_r2c_L<LL, Tc>(f, sp, nc, csf, css)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
     }
-    void row_c2r(const Cx<T>* sp, T* out, const T* add) {
-#define CALL(LL) row_c2r_L<LL>(sp, out, add)
+    void row_c2r(const Cx<T>* sp, T* out, const T* add, int nc = 1, int64_t csf = 0, int64_t css = 0) {
+#define CALL(LL) row_c2r_L<LL>(sp, out, add, nc, csf, css)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
     }
@@ -575,33 +585,33 @@ struct Impl {
     }
 
     template <typename U, int L, int DIR, bool SI, bool SO>
-    void col_fft_LS(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out) {
+    void col_fft_LS(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs) {
         using PT = ColFftPass<U, L, DIR, SI, SO>;
         const ColGeom cg = spec_geom();
-        stream(DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32", PT{cg, src, dst, tw, nb_in, nb_out},
-               col_tiles<PT>(cg, g.n3));
+        stream(DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32",
+               PT{cg, src, dst, tw, nb_in, nb_out, cs}, col_tiles<PT>(cg, g.n3), nc);
     }
     template <typename U, int L, int DIR>
-    void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out) {
+    void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs) {
         // the split layouts only occur on the side facing an all-to-all: out of the forward, into the inverse
-        if (DIR < 0 && nb_out) col_fft_LS<U, L, DIR, false, true>(src, dst, tw, nb_in, nb_out);
-        else if (DIR > 0 && nb_in) col_fft_LS<U, L, DIR, true, false>(src, dst, tw, nb_in, nb_out);
-        else col_fft_LS<U, L, DIR, false, false>(src, dst, tw, nb_in, nb_out);
+        if (DIR < 0 && nb_out) col_fft_LS<U, L, DIR, false, true>(src, dst, tw, nb_in, nb_out, nc, cs);
+        else if (DIR > 0 && nb_in) col_fft_LS<U, L, DIR, true, false>(src, dst, tw, nb_in, nb_out, nc, cs);
+        else col_fft_LS<U, L, DIR, false, false>(src, dst, tw, nb_in, nb_out, nc, cs);
     }
     template <typename Tc>
-    void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out) {  // forward along x2, in Tc
-#define CALL(LL) col_fft_L<Tc, LL, -1>(src, dst, twy_t<Tc>(), 0, nb_out)
+    void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out, int nc = 1, int64_t cs = 0) {  // forward along x2, in Tc
+#define CALL(LL) col_fft_L<Tc, LL, -1>(src, dst, twy_t<Tc>(), 0, nb_out, nc, cs)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
-    void col_fft_inv(const Cx<T>* src, Cx<T>* dst, int nb_in) {  // inverse along x2, in T
-#define CALL(LL) col_fft_L<T, LL, +1>(src, dst, twy(), nb_in, 0)
+    void col_fft_inv(const Cx<T>* src, Cx<T>* dst, int nb_in, int nc = 1, int64_t cs = 0) {  // inverse along x2, in T
+#define CALL(LL) col_fft_L<T, LL, +1>(src, dst, twy(), nb_in, 0, nc, cs)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
 
     template <int L, int KIND, typename Tc>
-    void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0) {
+    void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out, int comp, int nc, int64_t cs) {
         using PT = MiddlePass<Tc, T, L, KIND>;
         PT pt;
         pt.c = cg;
@@ -610,12 +620,13 @@ struct Impl {
         pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), comp};
         pt.tw = twz_t<Tc>();
         pt.two = twz();
-        stream(sizeof(Tc) == 8 ? "col_middle_f64" : "col_middle_f32", pt, col_tiles<PT>(cg, cg.n2));
+        pt.cs = cs;
+        stream(sizeof(Tc) == 8 ? "col_middle_f64" : "col_middle_f32", pt, col_tiles<PT>(cg, cg.n2), nc);
     }
     template <int KIND, typename Tc = double>
-    void middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0) {
+    void middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0, int nc = 1, int64_t cs = 0) {
         const ColGeom cg = c.dist() ? spec_geom_t() : spec_geom();
-#define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out, comp)
+#define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out, comp, nc, cs)
         DR_SWITCH_COL(g.n3g, CALL)
 #undef CALL
     }
@@ -660,9 +671,27 @@ struct Impl {
     }
     // out_c = F^-1[sym F in_c] (+ add_c), componentwise symbol KIND 0/1.  Forward passes (x1 r2c, x2)
     // and the x3 forward transform run in double; the inverse x3 / x2 / x1 passes in T.
+    template <typename P>
+    static int64_t uniform_stride(const P* const* c3) {  // element stride of 3 components, or 0
+        const int64_t a = c3[1] - c3[0], b = c3[2] - c3[1];
+        return (a == b && a > 0) ? a : 0;
+    }
     template <int KIND>
     void scalar_symbol3(V3<const T> in, V3<T> out, const V3<const T>* add) {
         using Tc = std::conditional_t<KIND == 1, T, double>;  // preconditioner: damping symbol
+        // one rank, components at one stride (every SoA vector field): the 3 components go through
+        // each pass in one launch (blockIdx.y), three times the CTAs per wave-quantised launch
+        const int64_t si = uniform_stride(in.c), so = uniform_stride(out.c);
+        if (!c.dist() && si && so && (!add || uniform_stride(add->c) == so)) {
+            row_r2c<Tc>(in.c[0], specD_t<Tc>(0), 3, si, g.S);
+            col_fft_fwd<Tc>(specD_t<Tc>(0), specD_t<Tc>(0), 0, 3, g.S);
+            Cx<Tc>* sd = specD_t<Tc>(0);
+            Cx<T>* sf = specF(0);
+            middle<KIND, Tc>(&sd, &sf, 0, 3, g.S);
+            col_fft_inv(specF(0), specF(0), 0, 3, g.S);
+            row_c2r(specF(0), out.c[0], add ? add->c[0] : nullptr, 3, so, g.S);
+            return;
+        }
         for (int cc = 0; cc < 3; ++cc) {
             spec_forward<Tc>(in.c[cc], 0);
             Cx<Tc>* sd = specD_t<Tc>(0);

@@ -305,6 +305,7 @@ struct RowR2cPass {
     const Ti* f;
     Cx<Tc>* spec;
     const Cx<Tc>* twN;
+    int64_t csf = 0, css = 0;  // component strides (blockIdx.y = component) of f and spec
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<Tc>* sm = reinterpret_cast<Cx<Tc>*>(smem);
         const int64_t nrows = (int64_t)g.n2 * g.n3;
@@ -313,10 +314,10 @@ struct RowR2cPass {
         const bool ok = row < nrows;
         if (!ok) row = nrows - 1;
         Cx<Tc>* buf = sm + line * LP;
-        const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f) + row * L;
+        const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f + blockIdx.y * csf) + row * L;
         fft_line_io<Tc, L, -1, false, true>(buf, t, twN, 2, RowLd<Ti, Tc>{src}, SmemLine<Tc>{buf});
         if (!ok) return;
-        Cx<Tc>* out = spec + row * g.n1p;
+        Cx<Tc>* out = spec + blockIdx.y * css + row * g.n1p;
         for (int k = t; k <= L / 2; k += TPL) {
             Cx<Tc> Xk, Xl;
             r2c_pair(buf[P(k)], buf[P(k == 0 ? 0 : L - k)], twN[k], Xk, Xl);
@@ -344,6 +345,7 @@ struct RowC2rPass {
     const Cx<T>* spec;
     RowOut<T> epi;
     const Cx<T>* twN;
+    int64_t csf = 0, css = 0;  // component strides (blockIdx.y = component) of out/add and spec
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
         const int64_t nrows = (int64_t)g.n2 * g.n3;
@@ -352,7 +354,7 @@ struct RowC2rPass {
         const bool ok = row < nrows;
         if (!ok) row = nrows - 1;
         Cx<T>* buf = sm + line * LP;
-        const Cx<T>* in = spec + row * g.n1p;
+        const Cx<T>* in = spec + blockIdx.y * css + row * g.n1p;
         for (int k = t; k <= L / 2; k += TPL) {
             Cx<T> Zk, Zl;
             c2r_pair(in[k], in[L - k], twN[k], Zk, Zl);
@@ -360,8 +362,8 @@ struct RowC2rPass {
             if (k != 0 && 2 * k != L) buf[P(L - k)] = Zl;
         }
         __syncthreads();
-        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out) + row * L;
-        const Cx<T>* add = epi.add ? reinterpret_cast<const Cx<T>*>(epi.add) + row * L : nullptr;
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out + blockIdx.y * csf) + row * L;
+        const Cx<T>* add = epi.add ? reinterpret_cast<const Cx<T>*>(epi.add + blockIdx.y * csf) + row * L : nullptr;
         fft_line_io<T, L, +1, true, false>(buf, t, twN, 2, SmemLine<T>{buf}, RowSt<T>{dst, add, 0, ok});
     }
 };
@@ -443,12 +445,13 @@ struct RowR2cStaged {
     const Ti* f;
     Cx<Tc>* spec;
     const Cx<Tc>* twN;
+    int64_t csf = 0, css = 0;  // component strides (blockIdx.y = component)
     __device__ __forceinline__ int64_t nrows() const { return (int64_t)g.n2 * g.n3; }
     __device__ __forceinline__ void issue_in(int tile, unsigned char* dst, uint64_t* b, int lane) const {
         const int64_t r0 = (int64_t)tile * RB;
         const int nr = (int)min((int64_t)RB, nrows() - r0);
-        issue_rows(dst, reinterpret_cast<const unsigned char*>(f), r0, nr, (int64_t)L * sizeof(Cx<Ti>), SI,
-                   L * sizeof(Cx<Ti>), b, lane);
+        issue_rows(dst, reinterpret_cast<const unsigned char*>(f + blockIdx.y * csf), r0, nr,
+                   (int64_t)L * sizeof(Cx<Ti>), SI, L * sizeof(Cx<Ti>), b, lane);
     }
     __device__ __forceinline__ void issue_ep(int, unsigned char*, uint64_t*, int) const {}
     __device__ __forceinline__ void run(int tile, const unsigned char* stg, const unsigned char*, uint64_t*, unsigned,
@@ -460,7 +463,7 @@ struct RowR2cStaged {
         const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(stg + line * SI);
         fft_line_io<Tc, L, -1, false, true>(buf, t, twN, 2, RowLd<Ti, Tc>{src}, SmemLine<Tc>{buf});
         if (!ok) return;
-        Cx<Tc>* out = spec + row * g.n1p;
+        Cx<Tc>* out = spec + blockIdx.y * css + row * g.n1p;
         for (int k = t; k <= L / 2; k += TPL) {
             Cx<Tc> Xk, Xl;
             r2c_pair(buf[P(k)], buf[P(k == 0 ? 0 : L - k)], twN[k], Xk, Xl);
@@ -487,19 +490,20 @@ struct RowC2rStaged {
     const Cx<T>* spec;
     RowOut<T> epi;
     const Cx<T>* twN;
+    int64_t csf = 0, css = 0;  // component strides (blockIdx.y = component) of out/add and spec
     __device__ __forceinline__ int64_t nrows() const { return (int64_t)g.n2 * g.n3; }
     __device__ __forceinline__ void issue_in(int tile, unsigned char* dst, uint64_t* b, int lane) const {
         const int64_t r0 = (int64_t)tile * RB;
         const int nr = (int)min((int64_t)RB, nrows() - r0);
-        issue_rows(dst, reinterpret_cast<const unsigned char*>(spec), r0, nr, (int64_t)g.n1p * sizeof(Cx<T>), SI,
-                   NIN * sizeof(Cx<T>), b, lane);
+        issue_rows(dst, reinterpret_cast<const unsigned char*>(spec + blockIdx.y * css), r0, nr,
+                   (int64_t)g.n1p * sizeof(Cx<T>), SI, NIN * sizeof(Cx<T>), b, lane);
     }
     __device__ __forceinline__ void issue_ep(int tile, unsigned char* dst, uint64_t* b, int lane) const {
         if constexpr (ADD) {
             const int64_t r0 = (int64_t)tile * RB;
             const int nr = (int)min((int64_t)RB, nrows() - r0);
-            issue_rows(dst, reinterpret_cast<const unsigned char*>(epi.add), r0, nr, (int64_t)L * sizeof(Cx<T>), SA,
-                       L * sizeof(Cx<T>), b, lane);
+            issue_rows(dst, reinterpret_cast<const unsigned char*>(epi.add + blockIdx.y * csf), r0, nr,
+                       (int64_t)L * sizeof(Cx<T>), SA, L * sizeof(Cx<T>), b, lane);
         }
     }
     __device__ __forceinline__ void run(int tile, const unsigned char* stg, const unsigned char* ep, uint64_t* epb,
@@ -521,7 +525,7 @@ struct RowC2rStaged {
             mbar_wait(epb, epar);
             add = reinterpret_cast<const Cx<T>*>(ep + line * SA);
         }
-        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out) + row * L;
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out + blockIdx.y * csf) + row * L;
         fft_line_io<T, L, +1, true, false>(buf, t, twN, 2, SmemLine<T>{buf}, RowSt<T>{dst, add, 0, ok});
     }
 };
@@ -737,6 +741,7 @@ struct ColFftPass {
     Cx<T>* dst;
     const Cx<T>* tw;
     int nb_in, nb_out;
+    int64_t cs = 0;  // component stride (blockIdx.y = component) of src and dst
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
         int x0, o0, xi, t, oi;
@@ -747,8 +752,8 @@ struct ColFftPass {
         Cx<T>* buf = sm + (oi * XC + xi) * LP;
         const Cx<T>* tw = tw_smem<T, L, NT, TWS>(this->tw, reinterpret_cast<Cx<T>*>(smem + CC::SMEM));
         fft_line_io<T, L, DIR, false, false>(buf, t, tw, 1,
-                                             col_acc<2, T, SPLIT_IN>(const_cast<Cx<T>*>(src), c, x, o, nb_in, on, 0),
-                                             col_acc<2, T, SPLIT_OUT>(dst, c, x, o, nb_out, on, 0));
+                                             col_acc<2, T, SPLIT_IN>(const_cast<Cx<T>*>(src) + blockIdx.y * cs, c, x, o, nb_in, on, 0),
+                                             col_acc<2, T, SPLIT_OUT>(dst + blockIdx.y * cs, c, x, o, nb_out, on, 0));
     }
 };
 
@@ -887,6 +892,7 @@ struct MiddlePass {
     SymInfo s;
     const Cx<Ti>* tw;
     const Cx<To>* two;  // inverse twiddles in To
+    int64_t cs = 0;     // component stride of in / out (blockIdx.y = component; one-component symbols)
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
         Cx<To>* so = reinterpret_cast<Cx<To>*>(smem + BUFI);
@@ -902,7 +908,7 @@ struct MiddlePass {
             const T k1 = (T)(x0 + xi), k2 = (T)wavenum(og, n2g);
             Cx<T>* buf = sm + line * LP;
             fft_line_io<T, L, -1, false, true>(
-                buf, t, tw, 1, col_acc<3>(in.p[0], c, x0 + xi, o0 + oi, 0, on, 0),
+                buf, t, tw, 1, col_acc<3>(in.p[0] + blockIdx.y * cs, c, x0 + xi, o0 + oi, 0, on, 0),
                 SymSt<T, To, L, KIND>{so + line * LPO, k1 * k1 + k2 * k2, (T)s.norm, (T)s.beta, s.reg, on});
         } else {
             forward_and_symbol(x0, o0, xi, t, oi, line, on, tw, sm, so);
@@ -954,7 +960,7 @@ struct MiddlePass {
                 const bool lon = act && x0 + lxi < c.nx && o0 + loi < c.n2;
                 Cx<To>* buf = so + co * LINES * LPO + (act ? ln : 0) * LPO;
                 fft_line_io<To, L, +1, true, false>(buf, lt, two, 1, SmemLine<To>{buf},
-                                                    col_acc<3>(out.p[co], c, x0 + lxi, o0 + loi, 0, lon, 0));
+                                                    col_acc<3>(out.p[co] + blockIdx.y * cs, c, x0 + lxi, o0 + loi, 0, lon, 0));
             }
         }
     }
