@@ -1338,20 +1338,20 @@ struct Impl {
         // Optional (DR_OVERLAP=1), non-isochoric, one rank: beta A vt does not depend on the transport
         // sweeps, so its x1/x2/x3 transforms run on a low-priority stream while the gathers (bound by the
         // shared-memory datapath, HBM ~40 % busy) run on a high-priority one; only the final c2r (+ b~)
-        // waits for both.  Measured 2.97 -> 2.89 ms per 256^3 matvec: off by default, because concurrent
-        // kernels' event durations no longer describe each kernel (bench.py's per-kernel roofline).
+        // waits for both.  Off by default: with the three components batched per pass the overlap is
+        // slower (bench step 278.8 -> 274 matvecs/s at 256^3: the gathers fill every SM, so the spectral
+        // CTAs only slow their tail); it measured 2.97 -> 2.89 ms per matvec before the batching.
         const bool overlap = c.overlap && !(c.cfg.flags & DR_ISOCHORIC) && !c.dist();
         if (overlap) {
             CK(cudaEventRecord(c.ev_fork, s));
             CK(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
             s = c.aux;
-            for (int cc = 0; cc < 3; ++cc) {
-                spec_forward(vt + (size_t)cc * g.M, cc);
-                Cx<double>* sd = specD(cc);
-                Cx<T>* sf = specF(cc);
-                middle<0>(&sd, &sf);
-                col_fft_inv(specF(cc), specF(cc), 0);
-            }
+            row_r2c<double>(vt, specD(0), 3, (int64_t)g.M, g.S);
+            col_fft_fwd<double>(specD(0), specD(0), 0, 3, g.S);
+            Cx<double>* sd = specD(0);
+            Cx<T>* sf = specF(0);
+            middle<0>(&sd, &sf, 0, 3, g.S);
+            col_fft_inv(specF(0), specF(0), 0, 3, g.S);
             CK(cudaEventRecord(c.ev_join, s));
             // the sweeps go to the high-priority stream so their CTAs are scheduled first and the
             // spectral CTAs fill the remaining SM resources
@@ -1400,7 +1400,7 @@ struct Impl {
             s = c.stream;
             CK(cudaStreamWaitEvent(s, c.ev_hi, 0));
             CK(cudaStreamWaitEvent(s, c.ev_join, 0));
-            for (int cc = 0; cc < 3; ++cc) row_c2r(specF(cc), Hvt + (size_t)cc * g.M, bt() + (size_t)cc * g.M);
+            row_c2r(specF(0), Hvt, bt(), 3, (int64_t)g.M, g.S);
         } else {
             reg_plus_data(cvec(vec(const_cast<T*>(vt), (size_t)g.M)), cvec(vec(bt(), (size_t)g.M)),
                           vec(Hvt, (size_t)g.M));
