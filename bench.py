@@ -87,6 +87,7 @@ def algo_bytes(tag, n, nt, es=4):
     Sc = (n // 2 + 1) * n * n
     table = {
         "sl_inc_state": 11 * es * M,      # gather g_j 1, d+ 3, vt 3, G_{j+1} 3, write 1
+        "sl_inc_state_b": 14 * es * M,    # last step: + b~'s k = nt term written (3)
         "sl_inc_adjoint": 6 * es * M,     # gather 1, d- 3, m 1, write 1
         "quad_term@aux": 10 * es * M,     # b~ += w lambda~ G: lambda~ 1, G 3, b~ read 3 + write 3
         "sl_state": 5 * es * M,           # gather 1, d+ 3, write 1
@@ -95,7 +96,8 @@ def algo_bytes(tag, n, nt, es=4):
         "sl_departure": 6 * es * M,       # per component a: gather v_a 1, d* 3, v_a 1, write d_a 1
         "quadrature": (4 * (nt + 1) + 3) * es * M,
         # inc-adjoint steps carrying the b~ quadrature: gather 1, d- 3, m 1, G_{k-1} 3, write 1, plus
-        # first step: rho~(1) at x 1, G_nt 3, write b~ 3; later steps: b~ read 3 + write 3
+        # b~ read 3 + write 3 (q2: every GN step, b~ started by sl_inc_state_b); q1 (full Newton's first
+        # step): rho~(1) at x 1, G_nt 3, write b~ 3
         "sl_inc_adjoint_q1": 16 * es * M,
         "sl_inc_adjoint_q2": 15 * es * M,
         "inc_init": 7 * es * M,

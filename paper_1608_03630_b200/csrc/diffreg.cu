@@ -1368,7 +1368,13 @@ struct Impl {
             const T* Gj = G(j + 1);
             EpiIncState<T> e{last ? rt1() : lt(j + 1), vt, vt + g.M, vt + 2 * g.M, Gj, Gj + g.M, Gj + 2 * g.M,
                              last ? T(0.5) * dtt : dtt};
-            gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), e);
+            if (last && !newton()) {  // GN: the last step also writes b~'s k = nt term (EpiIncState WB)
+                EpiIncState<T, true> eb{e.out, e.vt0, e.vt1, e.vt2, e.G0, e.G1, e.G2, e.c,
+                                        bt(), bt() + g.M, bt() + 2 * g.M, T(0.5) * dtt * T(-1)};
+                gather<1>("sl_inc_state_b", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), eb);
+            } else {
+                gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), e);
+            }
         }
         if (newton()) newton_terms(vt);
         // incremental adjoint (GN): lambda~_nt = -rho~(1), lambda~_{k-1} = m I[lambda~_k](X-); every step
@@ -1377,15 +1383,18 @@ struct Impl {
             T* src = (k == nt) ? rt1() : lt(k);
             const T* Gk = G(k - 1);
             const T wk = (k - 1 == 0) ? T(0.5) * dtt : dtt;
-            if (k == nt) {
+            if (k == nt && !newton()) {  // b~ already holds the k = nt term (sl_inc_state_b)
+                auto e = adjoint_epi<2>(k, Gk, wk, dtt);
+                e.scale = T(-1);
+                gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+            } else if (k == nt) {
                 auto e = adjoint_epi<1>(k, Gk, wk, dtt);
                 e.scale = T(-1);
                 e.nu = rt1(); e.snu = T(-1);
                 const T* Gn = G(nt);
                 e.H0 = Gn; e.H1 = Gn + g.M; e.H2 = Gn + 2 * g.M;
                 e.wn = T(0.5) * dtt;
-                if (newton()) gather<2>("sl_inc_adjoint_n1", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt));
-                else gather<1>("sl_inc_adjoint_q1", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+                gather<2>("sl_inc_adjoint_n1", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt));
             } else {
                 auto e = adjoint_epi<2>(k, Gk, wk, dtt);
                 e.scale = T(1);

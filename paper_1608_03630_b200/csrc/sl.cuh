@@ -253,19 +253,32 @@ struct EpiAddScaled {  // out = I[w](X) + c f(x): the merged-source step of the 
     __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const { out[id] = val[0] + c * l.f; }
 };
 
-template <typename T>
+// WB (last step, j + 1 = nt): also starts the b~ quadrature with its k = nt term
+// w_nt lambda~_nt G_nt, lambda~_nt = -rho~_nt: b~ = (wq rho~_nt) G_nt with wq = -w_nt = -dt/2.  G_nt is
+// this step's source gradient, already in registers, so the term costs three stores here instead of
+// four loads in the first adjoint step.
+template <typename T, bool WB = false>
 struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+) + c f_{j+1}, f = -vt.G_{j+1}
     T* out;
     const T* vt0; const T* vt1; const T* vt2;  // vt components
     const T* G0; const T* G1; const T* G2;     // grad rho_{j+1} components
     T c;
+    T* b0 = nullptr; T* b1 = nullptr; T* b2 = nullptr;  // WB: b~ components
+    T wq = T(0);                                        // WB: w_nt * snu
     struct Late { T v[3], g[3]; };
     __device__ __forceinline__ Late late(uint32_t id) const {
         return Late{{__ldg(vt0 + id), __ldg(vt1 + id), __ldg(vt2 + id)}, {__ldg(G0 + id), __ldg(G1 + id), __ldg(G2 + id)}};
     }
     __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
         const T f = l.v[0] * l.g[0] + l.v[1] * l.g[1] + l.v[2] * l.g[2];
-        out[id] = val[0] - c * f;
+        const T r = val[0] - c * f;
+        out[id] = r;
+        if constexpr (WB) {  // same products as EpiAdjoint<T, 1>::store
+            const T ln = wq * r;
+            b0[id] = ln * l.g[0];
+            b1[id] = ln * l.g[1];
+            b2[id] = ln * l.g[2];
+        }
     }
 };
 
@@ -523,8 +536,8 @@ template <class Epi>
 struct EpiMinB {
     static constexpr int V = 4;
 };
-template <typename T>
-struct EpiMinB<EpiIncState<T>> {
+template <typename T, bool WB>
+struct EpiMinB<EpiIncState<T, WB>> {
     static constexpr int V = 3;
 };
 template <typename T, bool N>
