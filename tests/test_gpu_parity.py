@@ -275,6 +275,30 @@ def test_host_buffers_match_device_buffers(dr):
     assert torch.equal(z_host, ctx.precond_apply(vt.cuda()).cpu())
 
 
+def test_profiler_tag_filter(dr):
+    """dr_profile_only(tag): only that tag's launches are timed; the launch counter still counts all."""
+    n = (32, 16, 64)
+    ctx, prob, v64 = setup_case(dr, "smooth_aniso", n, 4, lambda n_: synth.smooth_vec(9, n_, kmax=4, cells_per_step=2.0, nt=4),
+                                False, False)
+    ctx.forward_solve()
+    vt = synth.round32(synth.smooth_vec(21, n, kmax=5)).contiguous().cuda()
+    for only in (None, "sl_inc_adjoint_q2"):
+        ctx.profile_reset()
+        ctx.profile_only(only)
+        ctx.profile_enable(True)
+        ctx.hessian_matvec(vt)
+        prof, launches = ctx.profile()
+        ctx.profile_enable(False)
+        if only is None:
+            assert {"sl_inc_state", "sl_inc_state_b", "sl_inc_adjoint_q2", "inc_init"} <= set(prof)
+            assert sum(k for k, _ in prof.values()) == launches
+            full = launches
+        else:
+            assert set(prof) == {only} and prof[only][0] == 4 and prof[only][1] > 0
+            assert launches == full
+    ctx.profile_only(None)
+
+
 def test_call_order_and_argument_errors(dr):
     n = 16
     ctx = dr.Context(dr.Config(n=n, nt=2))
