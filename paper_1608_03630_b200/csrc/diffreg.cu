@@ -4,6 +4,7 @@
 // sizes the workspace, validates arguments and call order, and launches.  See DESIGN.md for the data
 // layout and the dataflow.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <climits>
@@ -676,6 +677,47 @@ struct Impl {
         const int64_t a = c3[1] - c3[0], b = c3[2] - c3[1];
         return (a == b && a > 0) ? a : 0;
     }
+    // x3 middle pass through tensor-map TMA tiles (fft.cuh MiddleTma); false if unavailable
+    template <int L, int KIND>
+    bool middle_tma(Cx<float>* in, Cx<float>* out, int nc) {
+        using P = MiddleTma<L, KIND>;
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult q;
+            void* fn = nullptr;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+                cudaGetLastError();
+                return false;
+            }
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }
+        const ColGeom cg = spec_geom();
+        CUtensorMap tm;
+        const cuuint64_t dims[4] = {(cuuint64_t)2 * cg.W, (cuuint64_t)cg.n2, (cuuint64_t)g.n3, (cuuint64_t)nc};
+        const cuuint64_t strides[3] = {(cuuint64_t)cg.W * 8, (cuuint64_t)cg.n2 * cg.W * 8, (cuuint64_t)g.S * 8};
+        const cuuint32_t box[4] = {(cuuint32_t)(2 * P::XC), 1, (cuuint32_t)L, 1};
+        const cuuint32_t es[4] = {1, 1, 1, 1};
+        if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+        auto k = k_middle_tma<L, KIND>;
+        static int per_sm = 0;
+        if (!per_sm) {
+            set_smem(k, P::BUF);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NT, P::BUF));
+            per_sm = std::max(per_sm, 1);
+        }
+        const int64_t nt = (int64_t)((cg.nx + P::XC - 1) / P::XC) * cg.n2;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)per_sm * c.num_sms / nc));
+        P pass{cg, out, g.S, SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), 0}, twz()};
+        const char* tag = tag_n("col_middle_f32", nc);
+        PB(tag);
+        k<<<dim3(grid, nc), P::NT, P::BUF, s>>>(tm, pass, (int)nt);
+        PE(tag);
+        return true;
+    }
+    bool tma_middle = getenv("DR_TMA_MIDDLE") == nullptr || getenv("DR_TMA_MIDDLE")[0] != '0';
+
     template <int KIND>
     void scalar_symbol3(V3<const T> in, V3<T> out, const V3<const T>* add) {
         using Tc = std::conditional_t<KIND == 1, T, double>;  // preconditioner: damping symbol
@@ -687,7 +729,11 @@ struct Impl {
             col_fft_fwd<Tc>(specD_t<Tc>(0), specD_t<Tc>(0), 0, 3, g.S);
             Cx<Tc>* sd = specD_t<Tc>(0);
             Cx<T>* sf = specF(0);
+            if constexpr (std::is_same_v<Tc, float> && std::is_same_v<T, float>) {
+                if (tma_middle && g.n3g == 256 && middle_tma<256, KIND>(sd, sf, 3)) goto inverse;
+            }
             middle<KIND, Tc>(&sd, &sf, 0, 3, g.S);
+        inverse:
             col_fft_inv(specF(0), specF(0), 0, 3, g.S);
             row_c2r(specF(0), out.c[0], add ? add->c[0] : nullptr, 3, so, g.S);
             return;

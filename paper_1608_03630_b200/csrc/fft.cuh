@@ -15,6 +15,7 @@
 //   col_middle     x3 lines of NCI spectra: forward FFT, pointwise symbol (NCI -> NCO), inverse FFT
 // Normalisation: forward transforms are unnormalised; every symbol carries the inverse factor.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the tensor map is encoded on the host through the runtime's driver entry point)
 #include "common.cuh"
 
 namespace dr {
@@ -965,6 +966,145 @@ struct MiddlePass {
         }
     }
 };
+
+// Line FFT with an arbitrary shared-memory line accessor, in place (source = intermediate = line).
+template <typename T, int L, int DIR, int TPL, int R, int Ns, bool DST_SMEM, class LineT, class Dst>
+__device__ __forceinline__ void stages_rest_l(const LineT& line, int t, const Cx<T>* __restrict__ tw, int tws,
+                                              const Dst& dst) {
+    if constexpr (Ns * R >= L) {
+        stage_io<T, L, L / Ns, Ns, DIR, TPL, DST_SMEM>(t, tw, tws, line, dst);
+        if (DST_SMEM) __syncthreads();
+    } else {
+        stage_io<T, L, R, Ns, DIR, TPL, true>(t, tw, tws, line, line);
+        __syncthreads();
+        stages_rest_l<T, L, DIR, TPL, R, Ns * R, DST_SMEM>(line, t, tw, tws, dst);
+    }
+}
+template <typename T, int L, int DIR, bool DST_SMEM, class LineT, class Dst>
+__device__ __forceinline__ void fft_line_inplace(const LineT& line, int t, const Cx<T>* __restrict__ tw, int tws,
+                                                 const Dst& dst) {
+    constexpr int TPL = Tpl<L, T>::V, R = Tpl<L, T>::R;
+    if constexpr (L <= R) {
+        stage_io<T, L, L, 1, DIR, TPL, true>(t, tw, tws, line, dst);
+        if (DST_SMEM) __syncthreads();
+    } else {
+        stage_io<T, L, R, 1, DIR, TPL, true>(t, tw, tws, line, line);
+        __syncthreads();
+        stages_rest_l<T, L, DIR, TPL, R, R, DST_SMEM>(line, t, tw, tws, dst);
+    }
+}
+// line xi of a staged column tile: element p at row p (row = XC consecutive columns, 128 bytes)
+template <typename T, int XC>
+struct StgLine {
+    Cx<T>* b;
+    __device__ __forceinline__ Cx<T> ld(int i) const { return b[i * XC]; }
+    __device__ __forceinline__ void st(int i, const Cx<T>& v) const { b[i * XC] = v; }
+};
+
+// fp32 x3 middle pass with a scalar symbol (KIND 0 / 1), tiles fetched by the tensor-map TMA engine:
+// one cp.async.bulk.tensor request per tile (XC columns x one k2 line x all L planes, 32 KB) lands as
+// [p][XC columns] rows of 128 bytes, and the forward FFT, the symbol (in the last forward stage) and
+// the inverse FFT all run in place there.  Persistent CTAs, two stages: tile i+1 is in flight while
+// tile i is transformed.  The 4-D map is (2 W floats, n2, n3, components).
+template <int L, int KIND>
+struct MiddleTma {
+    using T = float;
+    using CC = ColCfg<L, T>;
+    static constexpr int TPL = CC::TPL, XC = CC::XC, NT = CC::NT;
+    static_assert(CC::OL == 1 && XC * sizeof(Cx<T>) == 128, "one 128-byte row per plane");
+    static constexpr int MINB = MinBMiddle<T, NT>::V;
+    static constexpr size_t STG = (size_t)L * XC * sizeof(Cx<T>);
+    static constexpr size_t BUF = 128 + 2 * STG + L * sizeof(Cx<T>);
+    ColGeom c;
+    Cx<T>* out;
+    int64_t cs;  // output component stride
+    SymInfo s;
+    const Cx<T>* tw;
+    __device__ __forceinline__ void origin(int tile, int& x0, int& o) const {
+        const int nxb = (c.nx + XC - 1) / XC;
+        x0 = (tile % nxb) * XC;
+        o = tile / nxb;
+    }
+};
+
+// in-place SymSt on a staged line
+template <typename T, int L, int XC, int KIND>
+struct SymStStg {
+    Cx<T>* b;
+    T kk12, nrm, beta;
+    int reg;
+    bool live;
+    __device__ __forceinline__ void st(int i, const Cx<T>& v) const {
+        Cx<T> r = v;
+        if (live) {
+            const T k3 = (T)wavenum(i, L);
+            const T kk = kk12 + k3 * k3;
+            const T a = reg == 1 ? kk : kk * kk;
+            if (KIND == 0) {
+                r = scale(v, nrm * beta * a);
+            } else {
+                const T ah = (kk == T(0)) ? T(1) : a;
+                r = scale(v, nrm / (beta * ah));
+            }
+        }
+        b[i * XC] = r;
+    }
+};
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int L, int KIND>
+__global__ void __launch_bounds__(MiddleTma<L, KIND>::NT, MiddleTma<L, KIND>::MINB)
+    k_middle_tma(const __grid_constant__ CUtensorMap tmap, MiddleTma<L, KIND> pass, int ntiles) {
+    using P = MiddleTma<L, KIND>;
+    using T = float;
+    constexpr int XC = P::XC, TPL = P::TPL;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* stg = smem_raw + 128;
+    Cx<T>* tw = reinterpret_cast<Cx<T>*>(stg + 2 * P::STG);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    for (int i = threadIdx.x; i < L; i += P::NT) tw[i] = pass.tw[i];
+    __syncthreads();
+    auto issue = [&](int tile, int st) {
+        int x0, o;
+        pass.origin(tile, x0, o);
+        mbar_expect(&bar[st], (unsigned)P::STG);
+        tma_load_4d(stg + st * P::STG, &tmap, 2 * x0, o, 0, blockIdx.y, &bar[st]);
+    };
+    int tile = blockIdx.x;
+    if (threadIdx.x == 0 && tile < ntiles) issue(tile, 0);
+    int xi, t, oi;
+    col_thread<XC, TPL>(xi, t, oi);
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const int st = it & 1;
+        if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, st ^ 1);
+        mbar_wait(&bar[st], (unsigned)(it >> 1) & 1u);
+        int x0, o;
+        pass.origin(tile, x0, o);
+        const int x = x0 + xi;
+        const bool on = x < pass.c.nx && o < pass.c.n2;
+        const StgLine<T, XC> line{reinterpret_cast<Cx<T>*>(stg + st * P::STG) + xi};
+        const int og = o + pass.c.k2off, n2g = pass.c.n2g ? pass.c.n2g : pass.c.n2;
+        const T k1 = (T)x, k2 = (T)wavenum(og, n2g);
+        fft_line_inplace<T, L, -1, true>(line, t, tw, 1,
+                                         SymStStg<T, L, XC, KIND>{line.b, k1 * k1 + k2 * k2, (T)pass.s.norm,
+                                                                  (T)pass.s.beta, pass.s.reg, on});
+        fft_line_inplace<T, L, +1, false>(line, t, tw, 1,
+                                          col_acc<3, T, false>(pass.out + blockIdx.y * pass.cs, pass.c, x, o, 0, on, 0));
+        __syncthreads();  // the stage is refilled two iterations later
+    }
+}
 
 // One CTA per tile of a pass.
 template <class PassT>
