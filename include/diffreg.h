@@ -35,6 +35,11 @@
  * by the main-path calls and dr_op_spectral.  The other dr_op_* / dr_get_* test hooks take 16-byte
  * aligned device pointers only.
  *
+ * ENVIRONMENT (read by dr_create / dr_create_dist; A/B switches, defaults are the measured best):
+ * DR_OVERLAP=1 transforms beta A vt on a second stream concurrently with the transport sweeps
+ * (measured slower, off); DR_TMA_MIDDLE=0 replaces the tensor-map TMA fp32 x3 middle pass by the
+ * one-tile-per-CTA pass.  Results are bit-identical either way.
+ *
  * OWNERSHIP.  The caller owns every input, output and the workspace.  Inputs are only read;
  * images and the velocity are copied into the workspace (retained).  Outputs are fully
  * overwritten.  The library allocates no device memory after dr_create (and none at all when a

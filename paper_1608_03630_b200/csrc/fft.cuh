@@ -1001,25 +1001,30 @@ struct StgLine {
     __device__ __forceinline__ void st(int i, const Cx<T>& v) const { b[i * XC] = v; }
 };
 
-// fp32 x3 middle pass with a scalar symbol (KIND 0 / 1), tiles fetched by the tensor-map TMA engine:
-// one cp.async.bulk.tensor request per tile (XC columns x one k2 line x all L planes, 32 KB) lands as
-// [p][XC columns] rows of 128 bytes, and the forward FFT, the symbol (in the last forward stage) and
-// the inverse FFT all run in place there.  Persistent CTAs, two stages: tile i+1 is in flight while
-// tile i is transformed.  The 4-D map is (2 W floats, n2, n3, components).
-template <int L, int KIND>
+// x3 middle pass with a scalar symbol (KIND 0 / 1), tiles fetched by the tensor-map TMA engine: one
+// cp.async.bulk.tensor request per tile (XC columns x one k2 line x all L planes, 32 KB) lands as
+// [p][XC columns] rows of 128 bytes; the forward FFT in Ti, the symbol (in the last forward stage) and
+// the fp32 inverse all run in place there (a narrowed fp32 value takes the first half of its fp64
+// slot).  Persistent CTAs, two stages: tile i+1 is in flight while tile i is transformed.  The 4-D
+// tensor map is (2 W scalars, n2, n3, components).
+template <typename Ti, int L, int KIND>
 struct MiddleTma {
-    using T = float;
+    using T = Ti;
     using CC = ColCfg<L, T>;
     static constexpr int TPL = CC::TPL, XC = CC::XC, NT = CC::NT;
     static_assert(CC::OL == 1 && XC * sizeof(Cx<T>) == 128, "one 128-byte row per plane");
+    static_assert(Tpl<L, float>::V == TPL, "the fp32 inverse keeps the thread -> (column, t) map");
     static constexpr int MINB = MinBMiddle<T, NT>::V;
     static constexpr size_t STG = (size_t)L * XC * sizeof(Cx<T>);
-    static constexpr size_t BUF = 128 + 2 * STG + L * sizeof(Cx<T>);
+    static constexpr bool TWS = sizeof(T) == 4;  // fp32: twiddles in shared memory (fp64: L1, as MiddlePass)
+    static constexpr size_t BUF = 128 + 2 * STG + (TWS ? L * sizeof(Cx<T>) : 0);
+    static constexpr int XO = (int)(sizeof(Cx<T>) / sizeof(Cx<float>));  // fp32 slots per Ti slot
     ColGeom c;
-    Cx<T>* out;
+    Cx<float>* out;
     int64_t cs;  // output component stride
     SymInfo s;
     const Cx<T>* tw;
+    const Cx<float>* two;
     __device__ __forceinline__ void origin(int tile, int& x0, int& o) const {
         const int nxb = (c.nx + XC - 1) / XC;
         x0 = (tile % nxb) * XC;
@@ -1027,10 +1032,10 @@ struct MiddleTma {
     }
 };
 
-// in-place SymSt on a staged line
-template <typename T, int L, int XC, int KIND>
+// the last forward stage of a staged line: symbol in registers, narrowed in place (first half of the slot)
+template <typename T, int L, int RS, int KIND>
 struct SymStStg {
-    Cx<T>* b;
+    Cx<float>* b;  // line base as fp32 slots, row stride RS fp32 slots
     T kk12, nrm, beta;
     int reg;
     bool live;
@@ -1047,9 +1052,13 @@ struct SymStStg {
                 r = scale(v, nrm / (beta * ah));
             }
         }
-        b[i * XC] = r;
+        b[i * RS] = cx<float>((float)r.re, (float)r.im);
     }
 };
+
+template <typename T> struct TmaType;
+template <> struct TmaType<float> { static constexpr CUtensorMapDataType V = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; };
+template <> struct TmaType<double> { static constexpr CUtensorMapDataType V = CU_TENSOR_MAP_DATA_TYPE_FLOAT64; };
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
     asm volatile(
@@ -1059,22 +1068,28 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0,
         : "memory");
 }
 
-template <int L, int KIND>
-__global__ void __launch_bounds__(MiddleTma<L, KIND>::NT, MiddleTma<L, KIND>::MINB)
-    k_middle_tma(const __grid_constant__ CUtensorMap tmap, MiddleTma<L, KIND> pass, int ntiles) {
-    using P = MiddleTma<L, KIND>;
-    using T = float;
-    constexpr int XC = P::XC, TPL = P::TPL;
+template <typename Ti, int L, int KIND>
+__global__ void __launch_bounds__(MiddleTma<Ti, L, KIND>::NT, MiddleTma<Ti, L, KIND>::MINB)
+    k_middle_tma(const __grid_constant__ CUtensorMap tmap, MiddleTma<Ti, L, KIND> pass, int ntiles) {
+    using P = MiddleTma<Ti, L, KIND>;
+    using T = Ti;
+    constexpr int XC = P::XC, TPL = P::TPL, XO = P::XO;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     unsigned char* stg = smem_raw + 128;
-    Cx<T>* tw = reinterpret_cast<Cx<T>*>(stg + 2 * P::STG);
+    const Cx<T>* tw = pass.tw;
+    const Cx<float>* two = pass.two;
+    if constexpr (P::TWS) {
+        Cx<T>* tws = reinterpret_cast<Cx<T>*>(stg + 2 * P::STG);
+        for (int i = threadIdx.x; i < L; i += P::NT) tws[i] = pass.tw[i];
+        tw = tws;
+        two = reinterpret_cast<const Cx<float>*>(tws);  // fp32: the same table
+    }
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
-    for (int i = threadIdx.x; i < L; i += P::NT) tw[i] = pass.tw[i];
     __syncthreads();
     auto issue = [&](int tile, int st) {
         int x0, o;
@@ -1094,14 +1109,16 @@ __global__ void __launch_bounds__(MiddleTma<L, KIND>::NT, MiddleTma<L, KIND>::MI
         pass.origin(tile, x0, o);
         const int x = x0 + xi;
         const bool on = x < pass.c.nx && o < pass.c.n2;
-        const StgLine<T, XC> line{reinterpret_cast<Cx<T>*>(stg + st * P::STG) + xi};
+        Cx<T>* base = reinterpret_cast<Cx<T>*>(stg + st * P::STG);
+        const StgLine<T, XC> line{base + xi};
+        Cx<float>* fb = reinterpret_cast<Cx<float>*>(base) + XO * xi;  // fp32 view of the line
         const int og = o + pass.c.k2off, n2g = pass.c.n2g ? pass.c.n2g : pass.c.n2;
         const T k1 = (T)x, k2 = (T)wavenum(og, n2g);
         fft_line_inplace<T, L, -1, true>(line, t, tw, 1,
-                                         SymStStg<T, L, XC, KIND>{line.b, k1 * k1 + k2 * k2, (T)pass.s.norm,
-                                                                  (T)pass.s.beta, pass.s.reg, on});
-        fft_line_inplace<T, L, +1, false>(line, t, tw, 1,
-                                          col_acc<3, T, false>(pass.out + blockIdx.y * pass.cs, pass.c, x, o, 0, on, 0));
+                                         SymStStg<T, L, XO * XC, KIND>{fb, k1 * k1 + k2 * k2, (T)pass.s.norm,
+                                                                       (T)pass.s.beta, pass.s.reg, on});
+        fft_line_inplace<float, L, +1, false>(StgLine<float, XO * XC>{fb}, t, two, 1,
+                                              col_acc<3, float, false>(pass.out + blockIdx.y * pass.cs, pass.c, x, o, 0, on, 0));
         __syncthreads();  // the stage is refilled two iterations later
     }
 }

@@ -487,6 +487,19 @@ def test_overlap_stream_matvec_same_bits(dr, monkeypatch):
     assert torch.equal(out[0], out[1])
 
 
+def test_tma_middle_same_bits(dr, monkeypatch):
+    """The preconditioner's fp32 x3 middle pass through tensor-map TMA tiles (256 planes) against the
+    one-tile-per-CTA pass: same arithmetic, bit-identical z."""
+    n = (64, 32, 256)
+    u = synth.round32(synth.smooth_vec(6, n, kmax=5)).contiguous().cuda()
+    out = []
+    for tm in ("0", "1"):
+        monkeypatch.setenv("DR_TMA_MIDDLE", tm)  # read at dr_create
+        ctx = dr.Context(dr.Config(n=n, nt=2, reg=2, beta=0.37))
+        out.append(ctx.precond_apply(u))
+    assert torch.equal(out[0], out[1])
+
+
 def test_pcg_graph_matches_host_loop(dr, monkeypatch):
     """The CUDA-graph PCG iteration (device scalars, captured once per context) reproduces the host-scalar
     loop bit for bit, including a second solve that replays the cached graph."""
