@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <type_traits>
 #include <string>
@@ -424,17 +425,27 @@ struct Impl {
     // Batched launches (nc > 1, blockIdx.y = component) carry the tag suffix "_x<nc>".
     static const char* tag_n(const char* tag, int nc) {
         if (nc == 1) return tag;
+        static std::mutex mu;               // contexts may be driven from several host threads
         static std::set<std::string> pool;  // stable storage for composed tags
+        std::lock_guard<std::mutex> lock(mu);
         return pool.insert(std::string(tag) + "_x" + std::to_string(nc)).first->c_str();
+    }
+    // resident CTAs per SM of a kernel with `smem` dynamic shared memory (sets the smem attribute)
+    template <class K>
+    static int occupancy(K k, int nt, size_t smem) {
+        set_smem(k, smem);
+        int n = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, nt, smem));
+        return std::max(n, 1);
     }
     template <class PassT>
     void stream(const char* tag, const PassT& pass, int64_t ntiles, int nc = 1) {
         auto k = k_stream<PassT>;
-        static bool attr = false;  // per pass instantiation
-        if (!attr) {
+        static const bool attr = [&] {  // once per pass instantiation (thread-safe static init)
             set_smem(k, PassT::BUF);
-            attr = true;
-        }
+            return true;
+        }();
+        (void)attr;
         tag = tag_n(tag, nc);
         PB(tag);
         k<<<dim3((unsigned)ntiles, (unsigned)nc), PassT::NT, PassT::BUF, s>>>(pass);
@@ -446,12 +457,7 @@ struct Impl {
     template <class PassT>
     void stream_rows(const char* tag, const PassT& pass, int nc = 1) {
         auto k = k_rows<PassT>;
-        static int per_sm = 0;  // per pass instantiation
-        if (!per_sm) {
-            set_smem(k, PassT::BUF);
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, PassT::NT, PassT::BUF));
-            per_sm = std::max(per_sm, 1);
-        }
+        static const int per_sm = occupancy(k, PassT::NT, PassT::BUF);  // once per pass instantiation
         const int64_t nt = row_tiles<PassT::RB>();
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)per_sm * c.num_sms / nc));
         tag = tag_n(tag, nc);
@@ -678,20 +684,20 @@ struct Impl {
         const int64_t a = c3[1] - c3[0], b = c3[2] - c3[1];
         return (a == b && a > 0) ? a : 0;
     }
-    // Tensor-map TMA tiles (fft.cuh MiddleTma / ColTma): a 4-D map (2 W scalars, n2, n3, components)
+    // Tensor-map TMA tiles (fft.cuh MiddleTma): a 4-D map (2 W scalars, n2, n3, components)
     // over spectrum slots `base` .. (component stride S); false if the driver entry point is missing.
     template <typename U>
     bool tensor_map(CUtensorMap* tm, const void* base, int nc, cuuint32_t box0, cuuint32_t box1, cuuint32_t box2) {
-        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-        if (!encode) {
+        static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
             cudaDriverEntryPointQueryResult q;
             void* fn = nullptr;
-            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) {
                 cudaGetLastError();
-                return false;
+                fn = nullptr;
             }
-            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-        }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }();
+        if (!encode) return false;
         const ColGeom cg = spec_geom();
         const cuuint64_t es = sizeof(U);
         const cuuint64_t dims[4] = {(cuuint64_t)2 * cg.W, (cuuint64_t)cg.n2, (cuuint64_t)cg.n3, (cuuint64_t)nc};
@@ -702,13 +708,7 @@ struct Impl {
                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
-    template <class K>
-    int persistent_grid(K k, int nt, size_t smem, int64_t ntiles, int nc, int& per_sm) {
-        if (!per_sm) {
-            set_smem(k, smem);
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, nt, smem));
-            per_sm = std::max(per_sm, 1);
-        }
+    int persistent_grid(int per_sm, int64_t ntiles, int nc) const {
         return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * c.num_sms / nc));
     }
     // x3 middle pass of a scalar symbol over nc spectra (one 256-plane line per tile)
@@ -719,9 +719,9 @@ struct Impl {
         if (!tensor_map<Ti>(&tm, in, nc, 2 * P::XC, 1, L)) return false;
         const ColGeom cg = spec_geom();
         const int64_t nt = (int64_t)((cg.nx + P::XC - 1) / P::XC) * cg.n2;
-        static int per_sm = 0;
         auto k = k_middle_tma<Ti, L, KIND>;
-        const int grid = persistent_grid(k, P::NT, P::BUF, nt, nc, per_sm);
+        static const int per_sm = occupancy(k, P::NT, P::BUF);
+        const int grid = persistent_grid(per_sm, nt, nc);
         P pass{cg, out, g.S, SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), 0}, twz_t<Ti>(),
                reinterpret_cast<const Cx<float>*>(twz())};
         const char* tag = tag_n(sizeof(Ti) == 8 ? "col_middle_f64" : "col_middle_f32", nc);
@@ -744,11 +744,11 @@ struct Impl {
             Cx<T>* sf = specF(0);
             // fp32 spectra: the TMA-tile middle pass (152 -> 118 us for three components at 256^3); the
             // fp64-input middle and the x2 passes through TMA tiles measured no gain / slower
+            bool done = false;
             if constexpr (std::is_same_v<Tc, float> && std::is_same_v<T, float>) {
-                if (c.tma_middle && g.n3g == 256 && middle_tma<Tc, 256, KIND>(sd, sf, 3)) goto inverse;
+                done = c.tma_middle && g.n3g == 256 && middle_tma<Tc, 256, KIND>(sd, sf, 3);
             }
-            middle<KIND, Tc>(&sd, &sf, 0, 3, g.S);
-        inverse:
+            if (!done) middle<KIND, Tc>(&sd, &sf, 0, 3, g.S);
             col_fft_inv(specF(0), specF(0), 0, 3, g.S);
             row_c2r(specF(0), out.c[0], add ? add->c[0] : nullptr, 3, so, g.S);
             return;
