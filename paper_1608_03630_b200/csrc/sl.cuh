@@ -174,8 +174,9 @@ struct EpiStore {  // state solve: rho_{j+1} = I[rho_j](X+)   (Eq. 7 with f = 0)
 // Adjoint-like step: nu_{k-1} = scale * m * I[nu_k](X-)  (Eq. 7 with f = nu div v; D7).
 // QUAD != 0 also accumulates the trapezoid quadrature b~ = dt sum_j w_j lambda~_j G_j (P:L196-198,
 // reading A12) step by step, so the streaming sum rides on the gather's shared-memory-bound time:
-// QUAD = 1 (first step, k = nt): b~ = w_nt nu_nt G_nt + w_{nt-1} nu_{nt-1} G_{nt-1}, nu_nt read at x;
-// QUAD = 2 (k < nt): b~ += w_{k-1} nu_{k-1} G_{k-1}.
+// QUAD = 1 (first step, k = nt, full Newton): b~ = w_nt nu_nt G_nt + w_{nt-1} nu_{nt-1} G_{nt-1}, nu_nt
+// read at x; QUAD = 2: b~ += w_{k-1} nu_{k-1} G_{k-1} (every GN step: the k = nt term was written by the
+// last incremental-state step, EpiIncState<T, true>).
 // NEWTON (NEXT-3, full-Newton incremental adjoint, Eq. 5c with div(lam vt)): the gather carries a
 // second component, I[s_k](X) with s_k = div(lam_k vt) at the old level, and Eq. 7 gives
 //   nu_{k-1} = m I[nu_k](X) + dt/2 (1 + dt D(x)) I[s_k](X) + dt/2 s_{k-1}(x)   (D = div v; 0 isochoric).
