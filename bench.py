@@ -122,6 +122,31 @@ def algo_bytes(tag, n, nt, es=4):
     return table.get(tag)
 
 
+# ----------------------------------------------------------------------------- ncu evidence
+
+NCU_SUMMARY = {"sl_inc_adjoint_q2": "EpiAdjoint", "sl_inc_state": "EpiIncState", "col_middle_f64_x3": "MiddlePass_double",
+               "row_r2c_f64_x3": "RowR2cStaged", "row_c2r_add_x3": "RowC2rStaged", "col_fft_fwd_f64_x3": "ColFftPass_double"}
+
+
+def ncu_limiter(tag):
+    """What bounds the dominant kernel besides HBM, from its committed `ncu --set full` summary
+    (profiles/ncu_full_<round>_<kernel>.txt, written by tools/final_profile.sh + tools/ncu_summary.py):
+    L1/TEX (shared-memory datapath) and DRAM throughput in % of peak.  None if not captured."""
+    import glob
+    key = NCU_SUMMARY.get(tag)
+    if not key:
+        return None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_full_*_{key}.txt")))  # round tags sort
+    if not files:
+        return None
+    out = {"source": os.path.relpath(files[-1], ROOT)}
+    for line in open(files[-1]):
+        for name, k in (("L1/TEX Cache Throughput", "l1tex_pct"), ("DRAM Throughput", "dram_pct")):
+            if line.startswith(name) and line.split()[-1].replace(".", "", 1).isdigit():
+                out[k] = float(line.split()[-1])
+    return out
+
+
 # ----------------------------------------------------------------------------- clocks
 
 class Clocks:
@@ -387,7 +412,7 @@ def run_ours(args, ws, rank, local):
     roof = {"bound": "hbm", "kernel": dom["tag"], "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
             "frac": dom["gbs"] / peak if dom["gbs"] else None, "traffic": traffic,
             "peak_kind": peak_kind, "algo_bytes_per_launch": dom["algo_bytes"], "avg_launch_ms": dom["avg_ms"],
-            "share_of_step": dom["share"]}
+            "share_of_step": dom["share"], "ncu": ncu_limiter(dom["tag"])}
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as f:
             json.dump({"step_ms": ms / args.steps, "profiled_step_ms": prof_ms / args.profile_steps,
