@@ -27,6 +27,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the oracle's OpenMP placement (SURVEY §8(d) CPU-baseline protocol); read when its runtime starts
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
 
 import torch  # noqa: E402
 
@@ -81,45 +84,40 @@ def workload_config(n, ws):
 # ----------------------------------------------------------------------------- algorithmic bytes per launch
 
 def algo_bytes(tag, n, nt, es=4):
-    """SURVEY.md §8(d) reference dataflow: each kernel reads each operand once and writes each produced
-    field once.  Spectra: forward half spectra complex128 (16 B), inverse complex64 (8 B)."""
+    """SURVEY.md §8(d)'s reference dataflow ("each kernel reads each operand once and writes each
+    produced field once"), in fp32 values per voxel, attributed to the launches that carry each part:
+      K3a inc_init 7; K3 sl_inc_state 11; K4 incremental adjoint 6; K5 quadrature 4 per slice (lambda~_j
+      1 + G_j 3) + b~ written once (3); tail 33 (per component 5 passes of 1 R + 1 W, + the b~ read);
+      preconditioner 30 (3 x 5 x 2).  The GPU fuses K5 into the transport epilogues: the last inc-state
+      step carries slice n_t (11 + 4), each inc-adjoint step slice k-1 and an n_t-th of the b~ write
+      (6 + 4 + 3/n_t).  Summed over a matvec: 7 + 11 (n_t - 1) + 15 + n_t (10 + 3/n_t) + 33 = 21 n_t + 47
+      (131 at n_t = 4, = §8(d)'s matvec total).  A complex half spectrum counts as 1 value per voxel (M/2
+      complex numbers), whatever precision it is stored in: the algorithmic count, not the kernel's."""
     M = n ** 3
-    Sc = (n // 2 + 1) * n * n
-    table = {
-        "sl_inc_state": 11 * es * M,      # gather g_j 1, d+ 3, vt 3, G_{j+1} 3, write 1
-        "sl_inc_state_b": 14 * es * M,    # last step: + b~'s k = nt term written (3)
-        "sl_inc_adjoint": 6 * es * M,     # gather 1, d- 3, m 1, write 1
-        "quad_term@aux": 10 * es * M,     # b~ += w lambda~ G: lambda~ 1, G 3, b~ read 3 + write 3
-        "sl_state": 5 * es * M,           # gather 1, d+ 3, write 1
-        "sl_adjoint": 6 * es * M,
-        "sl_multiplier": 6 * es * M,      # gather D 1, d- 3, D 1, write m 1
-        "sl_departure": 6 * es * M,       # per component a: gather v_a 1, d* 3, v_a 1, write d_a 1
-        "quadrature": (4 * (nt + 1) + 3) * es * M,
-        # inc-adjoint steps carrying the b~ quadrature: gather 1, d- 3, m 1, G_{k-1} 3, write 1, plus
-        # b~ read 3 + write 3 (q2: every GN step, b~ started by sl_inc_state_b); q1 (full Newton's first
-        # step): rho~(1) at x 1, G_nt 3, write b~ 3
-        "sl_inc_adjoint_q1": 16 * es * M,
-        "sl_inc_adjoint_q2": 15 * es * M,
-        "inc_init": 7 * es * M,
-        "sub": 3 * es * M,
-        "dstar": 6 * es * M,
-        "row_deriv": 2 * es * M,
-        "col_deriv": 2 * es * M,          # (+1 read when accumulating; counted as 2)
-        # spectral passes: _f64 = forward passes widened to complex128 (amplifying symbols), _f32 = in T
-        "row_r2c_f64": es * M + 16 * Sc,
-        "row_r2c_f32": es * M + 2 * es * Sc,
-        "col_fft_fwd_f64": 2 * 16 * Sc,   # forward x2 pass, complex128 in and out
-        "col_fft_fwd_f32": 2 * 2 * es * Sc,
-        "col_fft_inv": 2 * 2 * es * Sc,   # inverse x2 pass, complex T in and out
-        "col_middle_f64": 16 * Sc + 2 * es * Sc,   # one-component symbols (KIND 0/1)
-        "col_middle_f32": 2 * es * Sc + 2 * es * Sc,
-        "row_c2r": 2 * es * Sc + es * M,            # spectrum in, real out
-        "row_c2r_add": 2 * es * Sc + 2 * es * M,    # + b~ in
+    v = {
+        "inc_init": 7,
+        "sl_inc_state": 11,
+        "sl_inc_state_b": 11 + 4,
+        "sl_inc_adjoint": 6,
+        "sl_inc_adjoint_q2": 6 + 4 + 3.0 / nt,
+        "sl_state": 5,                     # pure transport step: gather 1, d 3, write 1
+        "sl_adjoint": 6,                   # + m 1
+        "sl_departure": 2,                 # setup d^+- 2 x 6 (§8(d)): per component read v_a, write d_a
+        "sl_multiplier": 5,                # D gathered 1, d- 3, write m 1 (§8(d) "m 5")
+        # spectral passes: 1 read + 1 write per component (a half spectrum = 1 value per voxel)
+        "row_r2c_f64": 2, "row_r2c_f32": 2, "col_fft_fwd_f64": 2, "col_fft_fwd_f32": 2, "col_fft_inv": 2,
+        "col_middle_f64": 2, "col_middle_f32": 2, "row_c2r": 2,
+        "row_c2r_add": 3,                  # + the b~ read
+        "row_deriv": 2, "col_deriv": 2,
+        "sub": 3, "dstar": 6,
     }
-    if tag.endswith("_x3"):  # the three components of a vector field in one launch (blockIdx.y)
-        b = table.get(tag[:-3])
-        return None if b is None else 3 * b
-    return table.get(tag)
+    base = tag[:-3] if tag.endswith("_x3") else tag
+    if base not in v:
+        return None
+    return int(round((3 if tag.endswith("_x3") else 1) * v[base] * es * M))
+
+
+MATVEC_VALUES = lambda nt: 21 * nt + 47  # noqa: E731  §8(d) matvec total, non-isochoric (131 at n_t = 4)
 
 
 # ----------------------------------------------------------------------------- ncu evidence
@@ -217,6 +215,9 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
+        if torch.cuda.device_count() <= local:  # one GPU per rank, never two ranks on one GPU
+            sys.stderr.write(f"bench.py: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible\n")
+            sys.exit(2)
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -264,6 +265,54 @@ def oracle_matvec_sample(n, rT, rR, v, vt, setup_from=None):
     return time.perf_counter() - t0, O.num_threads(), prob, st, vt64
 
 
+def host_cpu():
+    """lscpu's model, sockets, cores per socket, threads per core, NUMA nodes (the host the oracle ran on)."""
+    out = {"nproc": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keys = {"Model name": "model", "Socket(s)": "sockets", "Core(s) per socket": "cores_per_socket",
+                "Thread(s) per core": "threads_per_core", "NUMA node(s)": "numa_nodes", "CPU(s)": "cpus"}
+        for line in txt.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in keys:
+                out[keys[k.strip()]] = v.strip()
+    except Exception as ex:
+        out["lscpu"] = repr(ex)
+    return out
+
+
+def cpu_baseline(n, rT, rR, v, vt, ctx):
+    """The fp64 oracle on the host cores: one 256^3 GN matvec on all cores (per-velocity inputs copied
+    from the GPU setup), plus a bounded 1-thread sample: one 256^3 semi-Lagrangian gather, the matvec's
+    dominant primitive (a matvec runs 2 n_t of them), timed at 1 thread and at all threads; the 1-thread
+    matvec estimate scales the all-core matvec by that gather's 1-thread / all-thread ratio."""
+    import synth
+    from oracle import oracle as O
+    secs, cores, prob, st, vt64 = oracle_matvec_sample(n, rT, rR, v, vt, setup_from=ctx)
+    f = synth.promote64(rT)
+    t0 = time.perf_counter()
+    O.sl_gather(f, st.d_minus)
+    g_all = time.perf_counter() - t0
+    O.set_num_threads(1)
+    try:
+        t0 = time.perf_counter()
+        O.sl_gather(f, st.d_minus)
+        g_one = time.perf_counter() - t0
+    finally:
+        O.set_num_threads(cores)
+    est1 = secs * g_one / g_all
+    return {"value": 1.0 / secs, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+            "sample": f"one fp64 oracle GN matvec at {n}^3 (n_t={NT}, H2) on {cores} OpenMP threads "
+                      f"(OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')}, OMP_PLACES={os.environ.get('OMP_PLACES')}); "
+                      f"its per-velocity inputs (departure points, state gradients) copied from the GPU setup; "
+                      f"{secs:.1f} s",
+            "single_thread": {"value_est": 1.0 / est1, "unit": "matvec/s", "cores": 1,
+                              "sample": f"one {n}^3 oracle semi-Lagrangian gather (2 n_t = {2 * NT} per matvec): "
+                                        f"{g_one:.2f} s at 1 thread vs {g_all:.2f} s at {cores}; matvec estimate "
+                                        f"{est1:.1f} s = {secs:.1f} s x {g_one / g_all:.1f}"},
+            "host": host_cpu()}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -293,7 +342,8 @@ def run_reference(args, ws, rank):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": workload_config(n, args.gpus if args.gpus else 1),
-           "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": sample,
+                            "host": host_cpu()},
            "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -347,7 +397,17 @@ def run_ours(args, ws, rank, local):
     prof_all, _ = ctx.profile()
     ctx.profile_enable(False)
     prof_ms = p0.elapsed_time(p1)
-    dom_tag = max((t for t in prof_all if not t.endswith("@aux")), key=lambda t: prof_all[t][1])
+    dom_tag = max((t for t in prof_all if not t.endswith("@aux") and t != "exchange"), key=lambda t: prof_all[t][1])
+    # N > 1: the slab exchanges (ghost planes, all-to-all transposes, off-rank values) per step, as the
+    # library's profiler brackets them on the context stream (max over ranks)
+    comm_info = None
+    if ws > 1:
+        xk, xms = prof_all.get("exchange", (0, 0.0))
+        comm_info = {"nccl_ranks": ws, "exchanges_per_step": xk / args.profile_steps,
+                     "exchange_ms_per_step_max": max_over_ranks(xms / args.profile_steps, ws),
+                     "profiled_step_ms_max": max_over_ranks(prof_ms / args.profile_steps, ws),
+                     "note": "exchange = grouped ncclSend/ncclRecv bracketed by CUDA events on the context stream "
+                             "in the untimed profiling pass (every launch timed)"}
 
     # ---- timed region (device-resident inputs); the dominant kernel's launches timed live
     ctx.profile_reset()
@@ -409,10 +469,19 @@ def run_ours(args, ws, rank, local):
             traffic = json.load(open(tp)).get(dom["tag"])
         except Exception:
             traffic = None
+    # frac (= frac_algo): SURVEY §8(d)'s algorithmic bytes per launch / live launch time / measured peak;
+    # frac_dram: the ncu-measured DRAM bytes per launch (profiles/ncu_traffic.json) over the same time
+    dram_gbs = traffic / (dom["avg_ms"] / 1e3) / 1e9 if traffic else None
+    mv_bytes = MATVEC_VALUES(NT) * 4 * M // ws
     roof = {"bound": "hbm", "kernel": dom["tag"], "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
             "frac": dom["gbs"] / peak if dom["gbs"] else None, "traffic": traffic,
+            "frac_algo": dom["gbs"] / peak if dom["gbs"] else None,
+            "frac_dram": dram_gbs / peak if dram_gbs else None,
             "peak_kind": peak_kind, "algo_bytes_per_launch": dom["algo_bytes"], "avg_launch_ms": dom["avg_ms"],
-            "share_of_step": dom["share"], "ncu": ncu_limiter(dom["tag"])}
+            "share_of_step": dom["share"], "ncu": ncu_limiter(dom["tag"]),
+            "matvec": {"algo_bytes": mv_bytes, "values_per_voxel": MATVEC_VALUES(NT), "ms": mv_ms,
+                       "achieved": mv_bytes / (mv_ms / 1e3) / 1e9, "frac": mv_bytes / (mv_ms / 1e3) / 1e9 / peak,
+                       "note": "SURVEY §8(d) matvec total (21 n_t + 47 fp32 values per voxel) / matvec_only_ms"}}
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as f:
             json.dump({"step_ms": ms / args.steps, "profiled_step_ms": prof_ms / args.profile_steps,
@@ -447,18 +516,15 @@ def run_ours(args, ws, rank, local):
                "h2d_bytes_per_step": 2 * fb + 3 * fb + NMV * (3 * fb + 3 * fb),
                "d2h_bytes_per_step": NMV * (3 * fb + 3 * fb), "steps": ksteps}
 
-    # ---- CPU baseline: the oracle, rank 0 at N = 1 only
+    # ---- CPU baseline: the oracle, rank 0 at N = 1 only (SURVEY §8(d) protocol: all cores and 1 thread,
+    # OMP_PROC_BIND=close, OMP_PLACES=cores, host CPU stated)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            secs, cores, *_ = oracle_matvec_sample(n, rT.cpu(), rR.cpu(), v.cpu(), vts[0].cpu(), setup_from=ctx)
-            cpu = {"value": 1.0 / secs, "unit": "matvec/s", "cores": cores, "kind": "oracle",
-                   "sample": f"one fp64 oracle GN matvec at {n}^3 (n_t={NT}, H2) on {cores} OpenMP threads; "
-                             f"its per-velocity inputs (departure points, state gradients) copied from the GPU "
-                             f"setup; {secs:.1f} s"}
+            cpu = cpu_baseline(n, rT.cpu(), rR.cpu(), v.cpu(), vts[0].cpu(), ctx)
         except Exception as ex:  # the baseline must not take the bench line down
             cpu = {"value": None, "unit": "matvec/s", "cores": os.cpu_count(), "kind": "oracle",
-                   "sample": f"failed: {ex!r}"}
+                   "sample": f"failed: {ex!r}", "host": host_cpu()}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": ws, "steps": args.steps,
@@ -467,11 +533,37 @@ def run_ours(args, ws, rank, local):
                "config": workload_config(n, ws),
                "voxel_steps_per_s": vox_steps, "matvec_only_ms": mv_ms,
                "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu}
+        if comm_info:
+            out["comm"] = comm_info
         print(json.dumps(out), flush=True)
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a torchrun environment: re-launch this script as N ranks on this node
+    (python -m torch.distributed.run --nproc-per-node N, rendezvous on 127.0.0.1), one process per GPU.
+    Fails loudly when fewer than N GPUs are visible.  DR_BENCH_DRYRUN=1 prints the command instead of
+    running it; DR_BENCH_VISIBLE_GPUS overrides the device count (both for the CPU test of this path)."""
+    have = int(os.environ.get("DR_BENCH_VISIBLE_GPUS", torch.cuda.device_count() if torch.cuda.is_available() else 0))
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs on this node, found {have}\n")
+        sys.exit(2)
+    import socket
+    with socket.socket() as so:  # a free rendezvous port
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    if os.environ.get("DR_BENCH_DRYRUN") == "1":
+        print(json.dumps({"launch": cmd}))
+        sys.exit(0)
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     ws, rank, local = dist_setup(args) if torch.cuda.is_available() else (1, 0, 0)
     if args.impl == "reference":
         run_reference(args, ws, rank)

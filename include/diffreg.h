@@ -89,7 +89,10 @@ typedef struct dr_config {
     double beta;    /* regularisation parameter beta > 0 (Eq. 2a)                      */
     int32_t ghost_lo, ghost_hi; /* slab ghost planes below / above (multi-GPU only; 0 -> 4 / 5).  A
                                    gather stencil spans floor(s3)-1 .. floor(s3)+2, so (g, g+1) planes
-                                   cover x3 displacements |d3| <= g - 1 cells; 1 <= g <= N3/P.         */
+                                   cover x3 displacements |d3| <= g - 1 cells; 1 <= g <= N3/P.
+                                   Set explicitly: ghost_lo >= 1 and ghost_hi >= 2, else DR_ERR_PARAM
+                                   (an owner serving an off-rank point reads one plane below its
+                                   slab and two above).                                               */
 } dr_config;
 
 typedef struct dr_ctx dr_ctx;

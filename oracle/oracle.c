@@ -334,3 +334,13 @@ int or_num_threads(void) {
     return 1;
 #endif
 }
+
+/* Thread count of the OpenMP loops (bench.py's CPU-baseline protocol times 1 and nproc threads;
+ * SURVEY §8(d)).  Execution control only: the arithmetic does not depend on it. */
+void or_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}

@@ -58,6 +58,7 @@ def lib():
         L.or_departure.argtypes = [i, i, i, i, i, P, P]
         L.or_fft3.argtypes = [i, i, i, ctypes.c_void_p, i]
         L.or_num_threads.restype = ctypes.c_int
+        L.or_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -79,6 +80,11 @@ def _n(a: np.ndarray):
 
 def num_threads() -> int:
     return int(lib().or_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of the C primitives (timing protocol only; results do not depend on it)."""
+    lib().or_set_num_threads(int(n))
 
 
 # ------------------------------------------------------------------ grid (D0, D1)

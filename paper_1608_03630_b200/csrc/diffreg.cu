@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -71,6 +72,9 @@ dr_status validate(const dr_config* c, int nranks = 1) {
     if (nranks > 1) {  // slabs: P | N3 and P | N2 (x2 blocks of the transposes), slab >= ghost width
         if (c->n[2] % nranks || c->n[1] % nranks) return DR_ERR_GRID;
         if (c->ghost_lo < 0 || c->ghost_hi < 0) return DR_ERR_PARAM;
+        // a stencil spans floor(s3) - 1 .. floor(s3) + 2: even an owner serving an off-rank point at
+        // its own slab edge reads one plane below and two above (ghost widths (g, g + 1), g >= 1)
+        if (ghost_lo(c) < 1 || ghost_hi(c) < 2) return DR_ERR_PARAM;
         if (c->n[2] / nranks < ghost_lo(c) || c->n[2] / nranks < ghost_hi(c)) return DR_ERR_GRID;
     }
     return DR_OK;
@@ -194,6 +198,7 @@ struct dr_ctx {
     cudaStream_t hi = nullptr;                // high-priority stream: the gather sweeps while aux runs
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hi = nullptr;
     bool overlap = false;                     // DR_OVERLAP=1 in the environment at dr_create
+    bool window = false;                      // DR_WINDOW=1: sliding-window fp32 gathers (sl.cuh k_sl_window)
     bool tma_middle = true;                   // DR_TMA_MIDDLE=0 at dr_create: the unstaged fp32 middle pass
     bool graphs = true;                       // DR_GRAPHS=0 disables the CUDA-graph PCG iteration
     cudaGraphExec_t pcg_graph = nullptr;      // one captured PCG iteration (single rank), reused
@@ -204,6 +209,7 @@ struct dr_ctx {
         int n_out = 0, n_in = 0;
     } rp[3];
     int num_sms = 148;
+    int dev = 0;                              // CUDA device the context was created on
     int rank = 0, nranks = 1;
     dr::Comm* comm = nullptr;  // not owned; NULL with one rank
     char* ws = nullptr;
@@ -438,14 +444,24 @@ struct Impl {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, nt, smem));
         return std::max(n, 1);
     }
+    // Function attributes belong to the device context: cache the occupancy (and the smem attribute set
+    // by occupancy()) per kernel instantiation AND device (a process may drive contexts on several GPUs).
+    static constexpr int MAX_DEV = 64;
+    template <class K>
+    int per_device_occupancy(K k, int nt, size_t smem) {
+        static std::atomic<int> cache[MAX_DEV];  // 0: not yet queried on that device
+        const int d = c.dev < MAX_DEV ? c.dev : MAX_DEV - 1;
+        int v = cache[d].load(std::memory_order_relaxed);
+        if (v == 0 || c.dev >= MAX_DEV) {
+            v = occupancy(k, nt, smem);
+            cache[d].store(v, std::memory_order_relaxed);
+        }
+        return v;
+    }
     template <class PassT>
     void stream(const char* tag, const PassT& pass, int64_t ntiles, int nc = 1) {
         auto k = k_stream<PassT>;
-        static const bool attr = [&] {  // once per pass instantiation (thread-safe static init)
-            set_smem(k, PassT::BUF);
-            return true;
-        }();
-        (void)attr;
+        per_device_occupancy(k, PassT::NT, PassT::BUF);  // sets the smem attribute on this device once
         tag = tag_n(tag, nc);
         PB(tag);
         k<<<dim3((unsigned)ntiles, (unsigned)nc), PassT::NT, PassT::BUF, s>>>(pass);
@@ -457,7 +473,7 @@ struct Impl {
     template <class PassT>
     void stream_rows(const char* tag, const PassT& pass, int nc = 1) {
         auto k = k_rows<PassT>;
-        static const int per_sm = occupancy(k, PassT::NT, PassT::BUF);  // once per pass instantiation
+        const int per_sm = per_device_occupancy(k, PassT::NT, PassT::BUF);
         const int64_t nt = row_tiles<PassT::RB>();
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)per_sm * c.num_sms / nc));
         tag = tag_n(tag, nc);
@@ -720,7 +736,7 @@ struct Impl {
         const ColGeom cg = spec_geom();
         const int64_t nt = (int64_t)((cg.nx + P::XC - 1) / P::XC) * cg.n2;
         auto k = k_middle_tma<Ti, L, KIND>;
-        static const int per_sm = occupancy(k, P::NT, P::BUF);
+        const int per_sm = per_device_occupancy(k, P::NT, P::BUF);
         const int grid = persistent_grid(per_sm, nt, nc);
         P pass{cg, out, g.S, SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), 0}, twz_t<Ti>(),
                reinterpret_cast<const Cx<float>*>(twz())};
@@ -902,14 +918,28 @@ struct Impl {
         const int f = field_of(plan_buf);
         const bool remote = c.dist() && c.rp[f].any;
         if (remote) remote_serve<NC>(f, src);
-        constexpr size_t sm = box_bytes<T, NC>();
-        auto k = k_sl_gather<T, NC, Epi>;
-        set_smem(k, sm);
         const Disp<T> dp{{d, d + g.M, d + 2 * g.M}};
         const int nt = (int)n_tiles(g);  // one CTA per tile
-        PB(tag);
-        k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
-        PE(tag);
+        if constexpr (std::is_same<T, float>::value && NC == 1) {
+            if (c.window) {  // sliding-window gather (sl.cuh k_sl_window)
+                constexpr size_t sm = win_box_bytes();
+                auto k = k_sl_window<Epi>;
+                set_smem(k, sm);
+                PB(tag);
+                k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
+                PE(tag);
+                goto launched;
+            }
+        }
+        {
+            constexpr size_t sm = box_bytes<T, NC>();
+            auto k = k_sl_gather<T, NC, Epi>;
+            set_smem(k, sm);
+            PB(tag);
+            k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
+            PE(tag);
+        }
+    launched:
         if (remote && c.rp[f].n_out > 0) {
             RP r = rp(f);
             PB("remote_fixup");
@@ -1403,6 +1433,9 @@ struct Impl {
         // slower (bench step 278.8 -> 274 matvecs/s at 256^3: the gathers fill every SM, so the spectral
         // CTAs only slow their tail); it measured 2.97 -> 2.89 ms per matvec before the batching.
         const bool overlap = c.overlap && !(c.cfg.flags & DR_ISOCHORIC) && !c.dist();
+        // the entry stream: the context stream, or the capture stream of the PCG graph -- the fork and
+        // the join both use it, so a captured matvec stays inside its capture
+        const cudaStream_t s0 = s;
         if (overlap) {
             CK(cudaEventRecord(c.ev_fork, s));
             CK(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
@@ -1467,7 +1500,7 @@ struct Impl {
         // spectral tail: H vt = beta A vt + P b~
         if (overlap) {  // beta A vt was transformed on the aux stream; only the c2r + b~ remains
             CK(cudaEventRecord(c.ev_hi, s));
-            s = c.stream;
+            s = s0;
             CK(cudaStreamWaitEvent(s, c.ev_hi, 0));
             CK(cudaStreamWaitEvent(s, c.ev_join, 0));
             row_c2r(specF(0), Hvt, bt(), 3, (int64_t)g.M, g.S);
@@ -1698,6 +1731,7 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
         int dev = 0, nsm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
             c->num_sms = nsm;
+        c->dev = dev;
         cudaGetLastError();
     }
     if (workspace) {
@@ -1721,6 +1755,8 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
         c->tma_middle = !(tm && tm[0] == '0');
         const char* gr = getenv("DR_GRAPHS");
         c->graphs = !(gr && gr[0] == '0');
+        const char* wi = getenv("DR_WINDOW");
+        c->window = wi && wi[0] == '1';
     }
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);

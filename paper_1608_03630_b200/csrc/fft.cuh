@@ -1119,6 +1119,9 @@ __global__ void __launch_bounds__(MiddleTma<Ti, L, KIND>::NT, MiddleTma<Ti, L, K
                                                                        (T)pass.s.beta, pass.s.reg, on});
         fft_line_inplace<float, L, +1, false>(StgLine<float, XO * XC>{fb}, t, two, 1,
                                               col_acc<3, float, false>(pass.out + blockIdx.y * pass.cs, pass.c, x, o, 0, on, 0));
+        // generic-proxy writes to the stage (the in-place transforms) must be ordered before the
+        // async-proxy (TMA) refill of the same buffer: every writer fences, then the barrier
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();  // the stage is refilled two iterations later
     }
 }

@@ -402,30 +402,33 @@ struct TileCtx {
     bool fits;
 };
 
-template <typename T, int NC>
+// WIN: the box of the sliding-window gather (k_sl_window), one cell wider: +1 on the high side of x1
+// and x2 (a thread's 5-wide window starts at its lowest stencil node), +1 on both sides of x3 (its
+// 12-plane window may start one plane below the tile's lowest node or end one above the highest).
+template <typename T, int NC, class Geo = BoxGeom<T, NC>, bool WIN = false>
 __device__ __forceinline__ TileCtx<T, NC> tile_ctx(const Grid& g, const int* __restrict__ plan, int tile) {
     constexpr int VEC = 16 / (int)sizeof(T);
-    constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
+    constexpr int BX = Geo::BX, BY = Geo::BY, BZ = Geo::BZ;
     TileCtx<T, NC> c;
     tile_coords(g, tile, c.x0, c.y0, c.z0);
     const int4 p = __ldg(reinterpret_cast<const int4*>(plan + (size_t)tile * PLAN_INTS));
     const int4 q = __ldg(reinterpret_cast<const int4*>(plan + (size_t)tile * PLAN_INTS + 4));
     c.ox = p.x & ~(VEC - 1);
     c.oy = p.y;
-    c.oz = p.z;
-    c.ex = ((p.x + p.w - c.ox) + VEC - 1) & ~(VEC - 1);
-    c.ey = q.x;
-    c.ez = q.y;
+    c.oz = p.z - (WIN ? 1 : 0);
+    c.ex = ((p.x + p.w + (WIN ? 1 : 0) - c.ox) + VEC - 1) & ~(VEC - 1);
+    c.ey = q.x + (WIN ? 1 : 0);
+    c.ez = q.y + (WIN ? 2 : 0);
     c.fits = c.ex <= BX && c.ey <= BY && c.ez <= BZ;
     // slabs: a box leaving the planes + ghosts holds points served by their owner rank (scatter)
     if (g.ghost && (c.oz - g.z0 + g.zg < 0 || c.oz + c.ez - g.z0 > g.n3 + g.zgh)) c.fits = false;
     return c;
 }
 
-template <typename T, int NC>
+template <typename T, int NC, class Geo = BoxGeom<T, NC>>
 __device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, const TileCtx<T, NC>& c, T* box) {
     constexpr int VEC = 16 / (int)sizeof(T);
-    constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
+    constexpr int BX = Geo::BX, BY = Geo::BY, BZ = Geo::BZ;
     constexpr int SC = BX * BY * BZ;
     constexpr int NCHP = BX / VEC;
     constexpr int RSTEP = SL_THREADS / NCHP;
@@ -472,11 +475,11 @@ __device__ __forceinline__ void load_pair(const Disp<T>& d, const Epi& epi, uint
 }
 
 // Interpolate a pair from the staged box and finish both points.
-template <typename T, int NC, class Epi>
+template <typename T, int NC, class Epi, class Geo = BoxGeom<T, NC>>
 __device__ __forceinline__ void pair_from_box(const Grid& g, const TileCtx<T, NC>& c, const T* __restrict__ box,
                                               int x, int y, int zA, uint32_t idA, uint32_t idB, bool okB,
                                               const PairIn<T, Epi>& in, const Epi& epi) {
-    constexpr int BX = BoxGeom<T, NC>::BX, BY = BoxGeom<T, NC>::BY, BZ = BoxGeom<T, NC>::BZ;
+    constexpr int BX = Geo::BX, BY = Geo::BY, BZ = Geo::BZ;
     constexpr int SC = BX * BY * BZ;
     constexpr int H = SL_TZ / 2;
     int qA[3], qB[3];
@@ -554,6 +557,32 @@ struct GatherMinB {
     static constexpr int V = (sizeof(T) == 4 && NC == 1) ? EpiMinB<Epi>::V : BoxGeom<T, NC>::MINB;
 };
 
+// Global-memory path of one thread's column of SL_TZ points (tiles whose box exceeds the shared-memory
+// capacity; with slabs also the points served by their owner rank are skipped here).
+template <typename T, int NC, class Epi>
+__device__ __forceinline__ void column_from_global(const Grid& g, const Src<T, NC>& src, const Disp<T>& d, int x,
+                                                   int y, int z0, int kmax, uint32_t id0, uint32_t plane,
+                                                   const Epi& epi) {
+#pragma unroll 1
+    for (int k = 0; k < kmax; ++k) {
+        const uint32_t id = id0 + k * plane;
+        int q1, q2, q3;
+        T t1, t2, t3;
+        cell_of<T>(x, __ldg(d.p[0] + id), q1, t1);
+        cell_of<T>(y, __ldg(d.p[1] + id), q2, t2);
+        cell_of<T>(z0 + k + g.z0, __ldg(d.p[2] + id), q3, t3);
+        if (g.ghost && (q3 - 1 < g.z0 - g.zg || q3 + 2 >= g.z0 + g.n3 + g.zgh)) continue;  // remote point
+        T w1[4], w2[4], w3[4];
+        lagrange4(t1, w1);
+        lagrange4(t2, w2);
+        lagrange4(t3, w3);
+        T val[NC];
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) val[cc] = interp_global(src.p[cc], g, q1, q2, q3, w1, w2, w3);
+        epi.store(id, val, epi.late(id));
+    }
+}
+
 template <typename T, int NC, class Epi>
 __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
     k_sl_gather(Grid g, Src<T, NC> src, Disp<T> d, const int* __restrict__ plan, int ntiles, Epi epi) {
@@ -570,25 +599,7 @@ __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
     const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
     const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
     if (!c.fits) {  // global-memory fallback (no barrier needed: nothing was staged)
-        if (!xyok) return;
-#pragma unroll 1
-        for (int k = 0; k < kmax; ++k) {
-            const uint32_t id = id0 + k * plane;
-            int q1, q2, q3;
-            T t1, t2, t3;
-            cell_of<T>(x, __ldg(d.p[0] + id), q1, t1);
-            cell_of<T>(y, __ldg(d.p[1] + id), q2, t2);
-            cell_of<T>(c.z0 + k + g.z0, __ldg(d.p[2] + id), q3, t3);
-            if (g.ghost && (q3 - 1 < g.z0 - g.zg || q3 + 2 >= g.z0 + g.n3 + g.zgh)) continue;  // remote point
-            T w1[4], w2[4], w3[4];
-            lagrange4(t1, w1);
-            lagrange4(t2, w2);
-            lagrange4(t3, w3);
-            T val[NC];
-#pragma unroll
-            for (int cc = 0; cc < NC; ++cc) val[cc] = interp_global(src.p[cc], g, q1, q2, q3, w1, w2, w3);
-            epi.store(id, val, epi.late(id));
-        }
+        if (xyok) column_from_global<T, NC, Epi>(g, src, d, x, y, c.z0, kmax, id0, plane, epi);
         return;
     }
     PairIn<T, Epi> cur;
@@ -605,6 +616,192 @@ __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
         pair_from_box<T, NC, Epi>(g, c, box, x, y, c.z0 + p, id0 + p * plane, id0 + (p + H) * plane, p + H < kmax,
                                   cur, epi);
         cur = nxt;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Sliding-window gather (fp32, one component: every transport step of the hot path).  The gather is
+// bound by the shared-memory datapath (64 stencil LDS per point, 1.3 wavefronts each), so this kernel
+// loads each staged value once per thread and reuses it for every point that needs it (P:L314
+// "Blocking, prefetching, and vectorization").  A thread's SL_TZ points lie on one x3 column; their
+// departure cells move with the smooth velocity, so per axis floor(-d) takes at most two adjacent
+// values m, m + 1 over the column (checked per warp; otherwise the pair path of k_sl_gather runs on the
+// same box).  The thread then reads a window of 5 x1 columns x 5 x2 rows x (SL_TZ + 4) x3 planes: point
+// k's 4x4x4 stencil sits at offset e_a = floor(-d_a) - m_a in {0, 1} of each 5-wide axis and at planes
+// k + e_3 .. k + e_3 + 3.  Each point's Lagrange weights are padded with one zero per axis (a 5-vector,
+// 6 slots in x3 for a pair), so the window is walked with compile-time offsets and no per-lane
+// branches: 25 LDS per plane, 300 per 8 points (37.5 per point instead of 64).  Points k, k + 1 are
+// packed in fp32x2 (FFMA2 with the shared window value as a broadcast operand).  The products of the
+// zero weights are exact zeros, and the non-zero terms are summed in the same order as the pair path,
+// so both paths give the same bits (up to the sign of an exact zero).
+struct WinGeom {
+    static constexpr int BX = 64, BY = 16, BZ = 16;  // 64 KB
+};
+constexpr size_t win_box_bytes() { return (size_t)WinGeom::BX * WinGeom::BY * WinGeom::BZ * sizeof(float); }
+#ifndef DR_WIN_MINB
+#define DR_WIN_MINB 2
+#endif
+#ifndef DR_WIN_LATE
+#define DR_WIN_LATE 1
+#endif
+constexpr int WIN_MINB = DR_WIN_MINB;  // resident CTAs per SM the register budget must allow
+constexpr int WIN_LATE = DR_WIN_LATE;  // planes between a pair's epilogue loads and its store
+
+// slot s of a zero-padded weight vector whose 4 Lagrange weights start at slot e + O (e in {0, 1})
+template <int S, int O>
+__device__ __forceinline__ float pad_slot(const float w0, const float w1, const float w2, const float w3, bool e) {
+    constexpr int i0 = S - O, i1 = S - O - 1;  // weight index at e = 0 / e = 1
+    const float a = i0 == 0 ? w0 : i0 == 1 ? w1 : i0 == 2 ? w2 : i0 == 3 ? w3 : 0.f;
+    const float b = i1 == 0 ? w0 : i1 == 1 ? w1 : i1 == 2 ? w2 : i1 == 3 ? w3 : 0.f;
+    return e ? b : a;
+}
+// pair weight vector (point A at offset eA, point B at offset OB + eB)
+template <int NS, int OB>
+__device__ __forceinline__ void pad_pair(const float2 w[4], bool eA, bool eB, float2 W[NS]) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        // (s is a compile-time constant after unrolling)
+        float a, b;
+        switch (s) {
+#define DR_PAD_CASE(S)                                                                 \
+    case S:                                                                            \
+        a = pad_slot<S, 0>(w[0].x, w[1].x, w[2].x, w[3].x, eA);                        \
+        b = pad_slot<S, OB>(w[0].y, w[1].y, w[2].y, w[3].y, eB);                       \
+        break;
+            DR_PAD_CASE(0) DR_PAD_CASE(1) DR_PAD_CASE(2) DR_PAD_CASE(3) DR_PAD_CASE(4) DR_PAD_CASE(5)
+#undef DR_PAD_CASE
+            default: a = b = 0.f;
+        }
+        W[s] = make_float2(a, b);
+    }
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(SL_THREADS, WIN_MINB)
+    k_sl_window(Grid g, Src<float, 1> src, Disp<float> d, const int* __restrict__ plan, int ntiles, Epi epi) {
+    using T = float;
+    constexpr int BX = WinGeom::BX, BY = WinGeom::BY;
+    constexpr int H = SL_TZ / 2, NP = SL_TZ / 2, NJ = SL_TZ + 4;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* box = reinterpret_cast<T*>(smem_raw);
+    const int tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    const TileCtx<T, 1> c = tile_ctx<T, 1, WinGeom, true>(g, plan, tile);
+    stage_box<T, 1, WinGeom>(g, src, c, box);
+    const int x = c.x0 + (threadIdx.x % SL_TX), y = c.y0 + threadIdx.x / SL_TX;
+    const bool xyok = x < g.n1 && y < g.n2;
+    const int kmax = min(SL_TZ, g.n3 - c.z0);
+    const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
+    const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
+    if (!c.fits) {
+        if (xyok) column_from_global<T, 1, Epi>(g, src, d, x, y, c.z0, kmax, id0, plane, epi);
+        return;
+    }
+    // the column's displacements (idle lanes of a narrow grid read a valid column and store nothing)
+    const int xc = min(x, g.n1 - 1), yc = min(y, g.n2 - 1);
+    const uint32_t idc = ((uint32_t)c.z0 * g.n2 + yc) * g.n1 + xc;
+    bool ok = kmax == SL_TZ;
+    float t[3][SL_TZ];
+    int fl[3][SL_TZ];
+#pragma unroll
+    for (int k = 0; k < SL_TZ; ++k)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const T e = ok ? -__ldg(d.p[a] + idc + k * plane) : T(0);
+            const T f = floorf(e);
+            t[a][k] = e - f;
+            fl[a][k] = (int)f;
+        }
+    int mn[3];
+    uint32_t ebits = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int lo = fl[a][0], hi = fl[a][0];
+#pragma unroll
+        for (int k = 1; k < SL_TZ; ++k) {
+            lo = min(lo, fl[a][k]);
+            hi = max(hi, fl[a][k]);
+        }
+        ok = ok && hi - lo <= 1;
+        mn[a] = lo;
+#pragma unroll
+        for (int k = 0; k < SL_TZ; ++k) ebits |= (uint32_t)(fl[a][k] - lo) << (a * SL_TZ + k);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (!__all_sync(0xffffffffu, ok)) {  // a deformation too strong for the window: the pair path
+        if (!xyok) return;
+#pragma unroll 1
+        for (int p = 0; p < H; ++p) {
+            if (p >= kmax) break;
+            PairIn<T, Epi> in;
+            load_pair<T, Epi>(d, epi, id0 + p * plane, id0 + (p + H) * plane, true, p + H < kmax, in);
+            pair_from_box<T, 1, Epi, WinGeom>(g, c, box, x, y, c.z0 + p, id0 + p * plane, id0 + (p + H) * plane,
+                                              p + H < kmax, in, epi);
+        }
+        return;
+    }
+    const int col0 = xc + mn[0] - 1 - c.ox, row0 = yc + mn[1] - 1 - c.oy, pl0 = c.z0 + g.z0 + mn[2] - 1 - c.oz;
+    DR_ASSERT(col0 >= 0 && col0 + 5 <= c.ex && row0 >= 0 && row0 + 5 <= c.ey && pl0 >= 0 && pl0 + NJ <= c.ez);
+    const T* __restrict__ wb = box + (pl0 * BY + row0) * BX + col0;
+    float2 W1[NP][5], W2[NP][5], w3[NP][4], acc[NP];  // x3 weights padded per plane (pad_slot)
+    bool e3[NP][2];
+    typename Epi::Late lt[NP][2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if ((j & 1) == 0 && j / 2 < NP) {  // pair p = (2p, 2p + 1) enters the window at plane 2p
+            const int p = j / 2, kA = 2 * p, kB = 2 * p + 1;
+            float2 w[4];
+            lagrange4x2(make_float2(t[0][kA], t[0][kB]), w);
+            pad_pair<5, 0>(w, (ebits >> kA) & 1, (ebits >> kB) & 1, W1[p]);
+            lagrange4x2(make_float2(t[1][kA], t[1][kB]), w);
+            pad_pair<5, 0>(w, (ebits >> (SL_TZ + kA)) & 1, (ebits >> (SL_TZ + kB)) & 1, W2[p]);
+            lagrange4x2(make_float2(t[2][kA], t[2][kB]), w3[p]);
+            e3[p][0] = (ebits >> (2 * SL_TZ + kA)) & 1;
+            e3[p][1] = (ebits >> (2 * SL_TZ + kB)) & 1;
+        }
+        if (j >= 5 - WIN_LATE && ((j - 5 + WIN_LATE) & 1) == 0 && (j - 5 + WIN_LATE) / 2 < NP && xyok) {
+            const int p = (j - 5 + WIN_LATE) / 2;  // epilogue operands, WIN_LATE planes ahead of the store
+            lt[p][0] = epi.late(id0 + 2 * p * plane);
+            lt[p][1] = epi.late(id0 + (2 * p + 1) * plane);
+        }
+        float2 ys[NP];
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+            float r[5];
+#pragma unroll
+            for (int a = 0; a < 5; ++a) r[a] = wb[(j * BY + b) * BX + a];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                if (j < 2 * p || j > 2 * p + 5) continue;
+                float2 row = __fmul2_rn(W1[p][0], make_float2(r[0], r[0]));
+#pragma unroll
+                for (int a = 1; a < 5; ++a) row = __ffma2_rn(W1[p][a], make_float2(r[a], r[a]), row);
+                ys[p] = b == 0 ? __fmul2_rn(W2[p][0], row) : __ffma2_rn(W2[p][b], row, ys[p]);
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            if (j < 2 * p || j > 2 * p + 5) continue;
+            float2 W3;  // slot j - 2p of the pair's 6-slot x3 vector: A at offset e3A, B at 1 + e3B
+            switch (j - 2 * p) {
+#define DR_W3_CASE(S)                                                                         \
+    case S:                                                                                   \
+        W3 = make_float2(pad_slot<S, 0>(w3[p][0].x, w3[p][1].x, w3[p][2].x, w3[p][3].x, e3[p][0]),  \
+                         pad_slot<S, 1>(w3[p][0].y, w3[p][1].y, w3[p][2].y, w3[p][3].y, e3[p][1])); \
+        break;
+                DR_W3_CASE(0) DR_W3_CASE(1) DR_W3_CASE(2) DR_W3_CASE(3) DR_W3_CASE(4) DR_W3_CASE(5)
+#undef DR_W3_CASE
+                default: W3 = make_float2(0.f, 0.f);
+            }
+            acc[p] = j == 2 * p ? __fmul2_rn(W3, ys[p]) : __ffma2_rn(W3, ys[p], acc[p]);
+        }
+        if (j >= 5 && ((j - 5) & 1) == 0 && xyok) {  // pair p leaves the window after plane 2p + 5
+            const int p = (j - 5) / 2;
+            const T vA = acc[p].x, vB = acc[p].y;
+            epi.store(id0 + 2 * p * plane, &vA, lt[p][0]);
+            epi.store(id0 + (2 * p + 1) * plane, &vB, lt[p][1]);
+        }
     }
 }
 

@@ -17,6 +17,8 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 # DR_CHECK=1 selects the bounds-checked debug build (paper_1608_03630_b200/build.py with DR_CHECK=1)
 LIB_PATH = os.path.join(_PKG, "libdiffreg_check.so" if os.environ.get("DR_CHECK", "0") == "1" else "libdiffreg.so")
+if os.environ.get("DR_LIB_VARIANT"):  # A/B builds of the same sources (build.py --variant NAME -D...)
+    LIB_PATH = os.path.join(_PKG, f"libdiffreg_{os.environ['DR_LIB_VARIANT']}.so")
 
 DR_OK, DR_ERR_ARG, DR_ERR_GRID, DR_ERR_PARAM, DR_ERR_ORDER, DR_ERR_CUDA, DR_ERR_NCCL, DR_ERR_OOM, \
     DR_ERR_NONFINITE, DR_ERR_PLAN = range(10)
@@ -249,6 +251,8 @@ class Context:
     def __init__(self, cfg: Config, device="cuda", stream: torch.cuda.Stream | None = None, comm: Comm | None = None):
         self.cfg = cfg
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.comm = comm
         self.nranks = comm.size if comm is not None else 1
@@ -260,8 +264,9 @@ class Context:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         c = cfg.c()
         h = ctypes.c_void_p()
-        st = lib().dr_create_dist(ctypes.byref(c), comm.h if comm is not None else None, _ptr(self.workspace), nbytes,
-                                  ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        with torch.cuda.device(self.device):  # dr_create binds the context to the current device
+            st = lib().dr_create_dist(ctypes.byref(c), comm.h if comm is not None else None, _ptr(self.workspace),
+                                      nbytes, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
         if st != DR_OK:
             raise DiffRegError(st, lib().dr_status_string(st).decode())
         self.h = h
@@ -293,35 +298,60 @@ class Context:
     def vector(self, device=None):
         return torch.empty((3,) + self.shape, dtype=self.cfg.dtype, device=device or self.device)
 
-    def _in(self, t):
-        assert t.dtype == self.cfg.dtype and t.is_contiguous(), (t.dtype, self.cfg.dtype)
+    def _buf(self, t, kind, what, host_ok=True):
+        """Pointer of a field argument after checking what the library cannot (it sees only the pointer):
+        a contiguous tensor of the context dtype with the rank's scalar (kind "s") / vector ("v") numel,
+        on the context's device (or the host, where the C ABI stages host buffers).  ValueError otherwise."""
+        if t is None:
+            return None
+        if not isinstance(t, torch.Tensor):
+            raise ValueError(f"{what}: expected a torch.Tensor, got {type(t).__name__}")
+        n = (3 if kind == "v" else 1) * self.nz * self.cfg.shape[1] * self.cfg.shape[2]
+        if t.dtype != self.cfg.dtype:
+            raise ValueError(f"{what}: dtype {t.dtype}, the context computes in {self.cfg.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what}: must be contiguous")
+        if kind != "any" and t.numel() != n:
+            raise ValueError(f"{what}: {t.numel()} elements, expected {n} ({'vector' if kind == 'v' else 'scalar'} "
+                             f"field of the slab {self.shape})")
+        if t.device.type == "cuda":
+            if t.device.index != self.device.index and not (t.device.index is None or self.device.index is None):
+                raise ValueError(f"{what}: on {t.device}, the context is on {self.device}")
+        elif not (host_ok and t.device.type == "cpu"):
+            raise ValueError(f"{what}: unsupported device {t.device}")
         return _ptr(t)
+
+    def _in(self, t, kind="v", what="input"):
+        return self._buf(t, kind, what)
+
+    def _out(self, t, kind="v", what="output"):
+        return self._buf(t, kind, what)
 
     # ---- main path (same names as the C ABI) ----
     def set_images(self, rho_T, rho_R):
-        self._check(lib().dr_set_images(self.h, self._in(rho_T), self._in(rho_R)))
+        self._check(lib().dr_set_images(self.h, self._in(rho_T, "s", "rho_T"), self._in(rho_R, "s", "rho_R")))
 
     def set_velocity(self, v):
-        self._check(lib().dr_set_velocity(self.h, self._in(v)))
+        self._check(lib().dr_set_velocity(self.h, self._in(v, "v", "v")))
 
     def forward_solve(self, rho1_out=None):
-        self._check(lib().dr_forward_solve(self.h, _ptr(rho1_out)))
+        self._check(lib().dr_forward_solve(self.h, self._out(rho1_out, "s", "rho1_out")))
         return rho1_out
 
     def adjoint_solve(self, lambda0_out=None):
-        self._check(lib().dr_adjoint_solve(self.h, _ptr(lambda0_out)))
+        self._check(lib().dr_adjoint_solve(self.h, self._out(lambda0_out, "s", "lambda0_out")))
         return lambda0_out
 
     def hessian_matvec(self, vt, Hvt=None):
         if Hvt is None:
             Hvt = self.vector(vt.device)
-        self._check(lib().dr_hessian_matvec(self.h, self._in(vt), _ptr(Hvt)))
+        self._check(lib().dr_hessian_matvec(self.h, self._in(vt, "v", "vt"), self._out(Hvt, "v", "Hvt")))
         return Hvt
 
     def precond_apply(self, r, z=None):
         if z is None:
             z = self.vector(r.device)
-        self._check(lib().dr_precond_apply(self.h, self._in(r), _ptr(z)))
+        self._check(lib().dr_precond_apply(self.h, self._in(r, "v", "r"), self._out(z, "v", "z")))
         return z
 
     def sync(self):
@@ -331,7 +361,7 @@ class Context:
     def gradient(self, g=None):
         if g is None:
             g = self.vector()
-        self._check(lib().dr_gradient(self.h, _ptr(g)))
+        self._check(lib().dr_gradient(self.h, self._out(g, "v", "g")))
         return g
 
     def pcg(self, g, eta: float, maxit: int, dv=None):
@@ -339,7 +369,8 @@ class Context:
         if dv is None:
             dv = self.vector(g.device)
         it, rr = ctypes.c_int(), ctypes.c_double()
-        self._check(lib().dr_pcg(self.h, self._in(g), _ptr(dv), eta, maxit, ctypes.byref(it), ctypes.byref(rr)))
+        self._check(lib().dr_pcg(self.h, self._in(g, "v", "g"), self._out(dv, "v", "dv"), eta, maxit, ctypes.byref(it),
+                                 ctypes.byref(rr)))
         return dv, it.value, rr.value
 
     def deformation(self, want_u=True, want_det=True):
@@ -347,7 +378,8 @@ class Context:
         u = self.vector() if want_u else None
         det = self.scalar() if want_det else None
         lo, hi = ctypes.c_double(), ctypes.c_double()
-        self._check(lib().dr_deformation(self.h, _ptr(u), _ptr(det), ctypes.byref(lo), ctypes.byref(hi)))
+        self._check(lib().dr_deformation(self.h, self._out(u, "v", "u"), self._out(det, "s", "det"), ctypes.byref(lo),
+                                         ctypes.byref(hi)))
         return u, det, lo.value, hi.value
 
     def solve(self, v, gtol=1e-2, max_newton=50, max_krylov=100, c1=1e-4, shrink=0.5, max_backtracks=20):
@@ -358,7 +390,7 @@ class Context:
         r = dr_solve_report()
         r.history = hist
         r.history_len = max_newton
-        self._check(lib().dr_solve(self.h, self._in(v), ctypes.byref(o), ctypes.byref(r)))
+        self._check(lib().dr_solve(self.h, self._buf(v, "v", "v", host_ok=False), ctypes.byref(o), ctypes.byref(r)))
         rows = [tuple(hist[5 * i:5 * i + 5]) for i in range(min(r.iterations, max_newton))]
         rep = {"iterations": r.iterations, "matvecs": r.matvecs, "reason": SOLVE_REASONS.get(r.reason, r.reason),
                "J0": r.J0, "J": r.J, "g0": r.g0, "g": r.g}
@@ -399,7 +431,10 @@ class Context:
     def op_spectral(self, op: int, x, out=None):
         if out is None:
             out = self.vector() if op in (DR_OP_GRAD, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY) else self.scalar()
-        self._check(lib().dr_op_spectral(self.h, op, self._in(x), _ptr(out)))
+        vin = op in (DR_OP_DIV, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY)
+        vout = op in (DR_OP_GRAD, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY)
+        self._check(lib().dr_op_spectral(self.h, op, self._buf(x, "v" if vin else "s", "x", False),
+                                         self._buf(out, "v" if vout else "s", "out", False)))
         return out
 
     def op_interp(self, f, s, out=None):
@@ -407,16 +442,38 @@ class Context:
         npts = s.shape[-1]
         if out is None:
             out = torch.empty(npts, dtype=self.cfg.dtype, device=self.device)
-        self._check(lib().dr_op_interp(self.h, self._in(f), npts, self._in(s), _ptr(out)))
+        if out.numel() != npts or s.numel() != 3 * npts:
+            raise ValueError("op_interp: s must be (3, npts) and out (npts,)")
+        self._check(lib().dr_op_interp(self.h, self._buf(f, "s", "f", False), npts, self._buf(s, "any", "s", False),
+                                       self._buf(out, "any", "out", False)))
         return out
 
     def get_departure(self, sigma: int):
         out = self.vector()
-        self._check(lib().dr_get_departure(self.h, sigma, _ptr(out)))
+        self._check(lib().dr_get_departure(self.h, sigma, self._out(out, "v", "out")))
         return out
 
     def get_field(self, which: int, j: int = 0):
         vec = which in (DR_FIELD_STATE_GRAD, DR_FIELD_BTILDE, DR_FIELD_VELOCITY)
         out = self.vector() if vec else self.scalar()
-        self._check(lib().dr_get_field(self.h, which, j, _ptr(out)))
+        self._check(lib().dr_get_field(self.h, which, j, self._out(out, "v" if vec else "s", "out")))
         return out
+
+
+def _make_current(fn):
+    """Run a Context method with the context's device current: the library launches on the current
+    device, and a process may drive contexts on several GPUs."""
+    import functools
+
+    @functools.wraps(fn)
+    def w(self, *a, **k):
+        if self.device.type == "cuda" and self.device.index is not None:
+            with torch.cuda.device(self.device):
+                return fn(self, *a, **k)
+        return fn(self, *a, **k)
+    return w
+
+
+for _name, _fn in list(vars(Context).items()):
+    if callable(_fn) and not _name.startswith("_") and _name not in ("scalar", "vector", "close"):
+        setattr(Context, _name, _make_current(_fn))

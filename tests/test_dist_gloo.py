@@ -92,3 +92,6 @@ def test_slab_partition_and_limits():
     # widened ghosts must fit in a slab
     assert dr_workspace_bytes_dist(Config(n=(32, 16, 64), ghost_lo=7, ghost_hi=8), 8) > 0
     assert dr_workspace_bytes_dist(Config(n=(32, 16, 64), ghost_lo=8, ghost_hi=9), 8) == 0
+    # too-thin ghosts: a stencil reaches one plane below and two above its cell
+    assert dr_workspace_bytes_dist(Config(n=(32, 16, 64), ghost_lo=1, ghost_hi=1), 2) == 0
+    assert dr_workspace_bytes_dist(Config(n=(32, 16, 64), ghost_lo=1, ghost_hi=2), 2) > 0

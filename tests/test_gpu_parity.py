@@ -46,6 +46,21 @@ def tols(fp64):
     return (TOL64_OP, TOL64_MV) if fp64 else (TOL32_OP, TOL32_MV)
 
 
+def amp_tol(tol, shape, reg, beta, u64, Au64, fp64):
+    """Tolerance of an amplifying operator (beta A, a(k) = |k|^(2 reg)) in fp64: both sides' FFT rounding
+    (~eps |u| spread over every mode) is multiplied by a(k) up to the grid's largest |k|, while the signal
+    is amplified only by its own modes'.  Relative error ~ eps * rms_k a(k) / (|A u| / |u|): on 1024-long
+    lines with |k| <= 4 probes that is ~1e-8 for H2, far above 1e-12 (reading A20's conditioning argument,
+    in fp64).  fp32 contexts run these forward passes in fp64 too, so their 1e-5 bar is unaffected."""
+    if not fp64:
+        return tol
+    k = np.meshgrid(*[np.fft.fftfreq(N, 1.0 / N) for N in shape], indexing="ij")
+    a = (k[0] ** 2 + k[1] ** 2 + k[2] ** 2) ** reg
+    rms_a = float(np.sqrt(np.mean(a.astype(np.float64) ** 2)))
+    eff = np.linalg.norm(Au64) / (beta * np.linalg.norm(u64))
+    return max(tol, 32 * 2.0 ** -53 * rms_a / eff)
+
+
 # ------------------------------------------------------------------ spectral operators
 
 @pytest.mark.parametrize("fp64", [False, True])
@@ -65,6 +80,54 @@ def test_spectral_ops(dr, n, fp64):
         assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, u)), O.leray(u64)) < tol
         ci = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37, fp64=fp64, isochoric=True))
         assert rel(np64(ci.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, True)) < tol
+
+
+# FFT line lengths 128 (radix plan 16 x 8), 512 (16 x 16 x 2) and 1024 (16 x 16 x 4) on each axis, on
+# anisotropic grids the oracle finishes in seconds (BJ configs 4-5 run 512- and 1024-long lines)
+LONG_GRIDS = [(1024, 16, 16), (16, 1024, 16), (16, 16, 1024), (128, 32, 64), (512, 16, 32)]
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("n", LONG_GRIDS, ids=["x".join(map(str, g)) for g in LONG_GRIDS])
+def test_spectral_ops_long_lines(dr, n, fp64):
+    """grad, div, beta A (H1, H2), (beta A)^-1 (isochoric and not) and the Leray projection with long
+    lines on every axis, in both precisions; the inputs carry modes up to |k| = min(n)/3 on every axis."""
+    tol = tols(fp64)[0]
+    kc = min(n) // 3
+    f, f64 = prep(synth.blobs(5, n, kcut=kc), fp64)
+    u, u64 = prep(synth.smooth_vec(6, n, kmax=kc), fp64)
+    f, u = f.cuda(), u.cuda()
+    for reg in (1, 2):
+        ctx = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37, fp64=fp64))
+        if reg == 1:
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_GRAD, f)), O.grad(f64)) < tol
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_DIV, u)), O.div(u64)) < tol
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, u)), O.leray(u64)) < tol
+        Au = O.reg_apply(u64, reg, 0.37)
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_REG, u)), Au) < amp_tol(tol, u64.shape[1:], reg, 0.37, u64, Au, fp64)
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, False)) < tol
+        ci = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37, fp64=fp64, isochoric=True))
+        assert rel(np64(ci.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, True)) < tol
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("iso", [False, True])
+@pytest.mark.parametrize("n", LONG_GRIDS, ids=["x".join(map(str, g)) for g in LONG_GRIDS])
+def test_matvec_long_lines(dr, n, iso, fp64):
+    """One GN matvec per mode on the long-line grids (the isochoric data term goes through the x3
+    middle pass KIND 6, the non-isochoric one through the staged row passes with b~ added)."""
+    top, tmv = tols(fp64)
+    kc = min(n) // 3
+    nt = 2
+    ctx = dr.Context(dr.Config(n=n, nt=nt, reg=2, beta=1e-2, isochoric=iso, fp64=fp64))
+    rT, rT64 = prep(synth.blobs(11, n, kcut=kc), fp64)
+    rR, rR64 = prep(synth.blobs(12, n, kcut=kc), fp64)
+    v, v64 = prep(synth.smooth_vec(9, n, kmax=min(kc, 4), divfree=iso, cells_per_step=1.5, nt=nt), fp64)
+    ctx.set_images(rT.cuda(), rR.cuda())
+    ctx.set_velocity(v.cuda())
+    prob = O.Problem(rho_T=rT64, rho_R=rR64, nt=nt, reg=2, beta=1e-2, iso=iso)
+    vt, vt64 = prep(synth.smooth_vec(21, n, kmax=min(kc, 4), divfree=iso), fp64)
+    check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, iso)
 
 
 @pytest.mark.parametrize("fp64", [False, True])
@@ -206,8 +269,10 @@ def check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, iso):
     for j in range(prob.nt + 1):
         assert rel(np64(ctx.get_field(dr.DR_FIELD_INC_ADJOINT, j)), parts["lam_tilde"][j]) < tmv, j
     reg = np64(ctx.op_spectral(dr.DR_OP_REG, vt.cuda()))
-    assert rel(reg, parts["reg"]) < top
-    assert rel(Hv, ref) < tmv
+    shape = vt64.shape[1:]
+    atol = amp_tol(top, shape, prob.reg, prob.beta, vt64, parts["reg"], fp64)
+    assert rel(reg, parts["reg"]) < atol
+    assert rel(Hv, ref) < max(tmv, atol)
     return Hv
 
 
@@ -373,6 +438,34 @@ def test_gradient_objective(dr, case, fp64):
     assert abs(J - Jref) <= (1e-12 if fp64 else 1e-5) * abs(Jref)
 
 
+@pytest.mark.parametrize("fp64", [False, True])
+def test_objective_absolute_closed_forms(dr, fp64):
+    """The GPU's J (Eq. 2a) against closed forms, not only against the oracle's J:
+    rho_T = G1, rho_R = 0, v = 0 gives J = 7 (2 pi)^3 / 48; constant images with v = (sin 2x2, 0, 0)
+    and H2 give J = 4 beta (2 pi)^3 (both exact on the grid for N >= 8)."""
+    n = (16, 8, 32)
+    tol = 1e-12 if fp64 else 1e-6
+    x1, x2, x3 = synth.grid_coords(n)
+    rT = ((torch.sin(x1) ** 2 + torch.sin(x2) ** 2 + torch.sin(x3) ** 2) / 3).expand(32, 8, 16)
+    dt_ = torch.float64 if fp64 else torch.float32
+    ctx = dr.Context(dr.Config(n=n, nt=4, reg=2, beta=1e-2, fp64=fp64))
+    ctx.set_images(rT.to(dt_).contiguous().cuda(), torch.zeros_like(rT, dtype=dt_).cuda())
+    ctx.set_velocity(torch.zeros((3, 32, 8, 16), dtype=dt_, device="cuda"))
+    ctx.forward_solve()
+    J, mis = ctx.objective()
+    assert abs(J - 7 * (2 * np.pi) ** 3 / 48) < tol * J and J == mis
+    beta = 0.37
+    ctx = dr.Context(dr.Config(n=n, nt=3, reg=2, beta=beta, fp64=fp64))
+    c = torch.full((32, 8, 16), 0.25, dtype=dt_, device="cuda")
+    ctx.set_images(c, c.clone())
+    v = torch.zeros((3, 32, 8, 16), dtype=torch.float64)
+    v[0] = torch.sin(2 * x2).expand(32, 8, 16)
+    ctx.set_velocity(v.to(dt_).contiguous().cuda())
+    ctx.forward_solve()
+    J, mis = ctx.objective()
+    assert abs(J - 4 * beta * (2 * np.pi) ** 3) < tol * J and abs(mis) < tol * J
+
+
 # ------------------------------------------------------------------ NEXT-2: PCG
 
 @pytest.mark.parametrize("case", [CASES[1], CASES[0]], ids=["vstar64", "cfg1"])
@@ -515,3 +608,41 @@ def test_pcg_graph_matches_host_loop(dr, monkeypatch):
         outs[mode] = (a, b)
     for (da, ia, ra), (db, ib, rb) in zip(outs["1"], outs["0"]):
         assert ia == ib and ra == rb and torch.equal(da, db)
+
+
+def test_pcg_graph_with_overlap_stream(dr, monkeypatch):
+    """DR_OVERLAP=1 inside the captured PCG iteration: the matvec forks beta A vt onto the aux stream
+    and joins back into the capture stream (it used to join into the context stream, which
+    broke the capture).  Same bits as the serial matvec, and the cached graph replays."""
+    name, n, nt, vgen, iso = CASES[2]
+    outs = {}
+    for ov in ("0", "1"):
+        monkeypatch.setenv("DR_OVERLAP", ov)
+        monkeypatch.setenv("DR_GRAPHS", "1")
+        ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+        ctx.forward_solve()
+        g, _ = prep(synth.smooth_vec(41, n, kmax=6), False)
+        outs[ov] = (ctx.pcg(g.cuda(), 0.05, 20), ctx.pcg((2 * g).contiguous().cuda(), 0.05, 20))
+    for (da, ia, ra), (db, ib, rb) in zip(outs["0"], outs["1"]):
+        assert ia == ib and ra == rb and torch.equal(da, db)
+
+
+def test_window_gather_same_bits_as_pair_path(dr, monkeypatch):
+    """The sliding-window fp32 gather (k_sl_window) against the pair path (k_sl_gather, DR_WINDOW=0) on
+    every transport of the hot path (departure points, multiplier, state, adjoint, matvec): the zero-
+    padded weights add exact zeros and the non-zero terms are summed in the same order, so the bits
+    agree.  The stress case (9 cells/step) mixes window warps, pair-path warps and global tiles."""
+    for case in (CASES[1], CASES[2], CASES[3]):
+        name, n, nt, vgen, iso = case
+        res = {}
+        for w in ("0", "1"):
+            monkeypatch.setenv("DR_WINDOW", w)
+            ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+            ctx.forward_solve()
+            ctx.adjoint_solve()
+            vt = synth.round32(synth.smooth_vec(21, n, kmax=5)).contiguous().cuda()
+            res[w] = [ctx.get_departure(1), ctx.get_departure(-1), ctx.get_field(dr.DR_FIELD_MULTIPLIER),
+                      ctx.get_field(dr.DR_FIELD_STATE, nt), ctx.get_field(dr.DR_FIELD_ADJOINT, 0),
+                      ctx.hessian_matvec(vt), ctx.get_field(dr.DR_FIELD_BTILDE)]
+        for a, b in zip(res["0"], res["1"]):
+            assert torch.equal(a, b), name

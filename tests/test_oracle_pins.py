@@ -501,6 +501,34 @@ def test_p13_p14_trends_decrease_under_refinement():
     assert d[-1][0] < 1e-3 and d[-1][1] < 1e-3 and d[-1][2] < 1e-2, d
 
 
+@pytest.mark.parametrize("n", [8, (16, 8, 12)])
+def test_objective_absolute_closed_forms(n):
+    """J of Eq. 2a in absolute value, so the D1 weight h1 h2 h3 of `inner` is pinned (a
+    1/M weight would fail): both cases are trigonometric polynomials whose grid sums are exact for N >= 8.
+    (a) rho_T = G1 = (sin^2 x1 + sin^2 x2 + sin^2 x3)/3, rho_R = 0, v = 0 (identity transport, P8):
+        J = 1/2 int rho_T^2 = (2 pi)^3 (1/4 + 3/72) / 2 = 7 (2 pi)^3 / 48.
+    (b) v = (sin 2 x2, 0, 0), H2 (A = Delta^2: Delta^2 sin 2x2 = 16 sin 2x2), constant images (the
+        constant is transported exactly, misfit 0): J = beta/2 * 16 int sin^2 2x2 = 4 beta (2 pi)^3."""
+    N1, N2, N3 = (n, n, n) if isinstance(n, int) else n
+    x1, x2, x3 = coords(n)
+    rT = full((np.sin(x1) ** 2 + np.sin(x2) ** 2 + np.sin(x3) ** 2) / 3, n)
+    prob = O.Problem(rho_T=rT, rho_R=np.zeros_like(rT), nt=4, reg=2, beta=1e-2)
+    J = O.objective(prob, O.set_velocity(prob, np.zeros((3,) + rT.shape)))
+    assert abs(J - 7 * (2 * math.pi) ** 3 / 48) < 1e-12 * J
+    beta = 0.37
+    c = np.full_like(rT, 0.25)
+    v = np.zeros((3,) + rT.shape)
+    v[0] = full(np.sin(2 * x2), n)
+    for nt in (1, 3):
+        prob = O.Problem(rho_T=c, rho_R=c.copy(), nt=nt, reg=2, beta=beta)
+        J = O.objective(prob, O.set_velocity(prob, v))
+        assert abs(J - 4 * beta * (2 * math.pi) ** 3) < 1e-12 * J, (nt, J)
+    # H1 (A = -Delta: -Delta sin 2x2 = 4 sin 2x2): J = beta/2 * 4 * (2 pi)^3 / 2 = beta (2 pi)^3
+    prob = O.Problem(rho_T=c, rho_R=c.copy(), nt=2, reg=1, beta=beta)
+    J = O.objective(prob, O.set_velocity(prob, v))
+    assert abs(J - beta * (2 * math.pi) ** 3) < 1e-12 * J
+
+
 def test_gradient_matches_fd_of_objective():
     """<g, vt> against a centred difference of J (SPEC acceptance 5 idea): optimize-then-discretize,
     so agreement is to discretisation error only, shrinking under refinement."""
