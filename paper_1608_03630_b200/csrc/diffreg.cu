@@ -201,6 +201,7 @@ struct dr_ctx {
     bool window = false;                      // DR_WINDOW=1: sliding-window fp32 gathers (sl.cuh k_sl_window)
     bool tma_middle = true;                   // DR_TMA_MIDDLE=0 at dr_create: the unstaged fp32 middle pass
     bool graphs = true;                       // DR_GRAPHS=0 disables the CUDA-graph PCG iteration
+    int chunk = 0;                            // DR_CHUNK=P: x1/x2 pass pairs run per P planes (L2 reuse)
     cudaGraphExec_t pcg_graph = nullptr;      // one captured PCG iteration (single rank), reused
     double* pinned = nullptr;                 // pinned host scalar the graph reports |r|^2 into
     struct RemotePlanH {                      // host side of an off-rank plan (per displacement field)
@@ -315,6 +316,7 @@ struct Impl {
     const Grid& g;
     cudaStream_t s;
     explicit Impl(dr_ctx& cc) : c(cc), g(cc.g), s(cc.stream) {}
+    Impl(dr_ctx& cc, const Grid& gg, cudaStream_t st) : c(cc), g(gg), s(st) {}  // a plane range of the grid
     void PB(const char* tag) { c.prof_begin(tag, s); }
     void PE(const char* tag) { c.prof_end(tag, s); }
 
@@ -754,8 +756,21 @@ struct Impl {
         // each pass in one launch (blockIdx.y), three times the CTAs per wave-quantised launch
         const int64_t si = uniform_stride(in.c), so = uniform_stride(out.c);
         if (!c.dist() && si && so && (!add || uniform_stride(add->c) == so)) {
-            row_r2c<Tc>(in.c[0], specD_t<Tc>(0), 3, si, g.S);
-            col_fft_fwd<Tc>(specD_t<Tc>(0), specD_t<Tc>(0), 0, 3, g.S);
+            if (c.chunk > 0 && g.n3 % c.chunk == 0 && c.chunk < g.n3) {
+                // plane chunks: each chunk's x1 output is still in L2 when its x2 pass reads it
+                Grid gc = g;
+                gc.n3 = c.chunk;
+                gc.M = (int64_t)g.n1 * g.n2 * gc.n3;
+                Impl sub(c, gc, s);
+                for (int z = 0; z < g.n3; z += c.chunk) {
+                    Cx<Tc>* sp = specD_t<Tc>(0) + (size_t)z * g.n2 * g.n1p;
+                    sub.template row_r2c<Tc>(in.c[0] + (size_t)z * plane(), sp, 3, si, g.S);
+                    sub.template col_fft_fwd<Tc>(sp, sp, 0, 3, g.S);
+                }
+            } else {
+                row_r2c<Tc>(in.c[0], specD_t<Tc>(0), 3, si, g.S);
+                col_fft_fwd<Tc>(specD_t<Tc>(0), specD_t<Tc>(0), 0, 3, g.S);
+            }
             Cx<Tc>* sd = specD_t<Tc>(0);
             Cx<T>* sf = specF(0);
             // fp32 spectra: the TMA-tile middle pass (152 -> 118 us for three components at 256^3); the
@@ -765,6 +780,19 @@ struct Impl {
                 done = c.tma_middle && g.n3g == 256 && middle_tma<Tc, 256, KIND>(sd, sf, 3);
             }
             if (!done) middle<KIND, Tc>(&sd, &sf, 0, 3, g.S);
+            if (c.chunk > 0 && g.n3 % c.chunk == 0 && c.chunk < g.n3) {
+                Grid gc = g;
+                gc.n3 = c.chunk;
+                gc.M = (int64_t)g.n1 * g.n2 * gc.n3;
+                Impl sub(c, gc, s);
+                for (int z = 0; z < g.n3; z += c.chunk) {
+                    Cx<T>* sp = specF(0) + (size_t)z * g.n2 * g.n1p;
+                    const size_t off = (size_t)z * plane();
+                    sub.col_fft_inv(sp, sp, 0, 3, g.S);
+                    sub.row_c2r(sp, out.c[0] + off, add ? add->c[0] + off : nullptr, 3, so, g.S);
+                }
+                return;
+            }
             col_fft_inv(specF(0), specF(0), 0, 3, g.S);
             row_c2r(specF(0), out.c[0], add ? add->c[0] : nullptr, 3, so, g.S);
             return;
@@ -1755,6 +1783,8 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
         c->tma_middle = !(tm && tm[0] == '0');
         const char* gr = getenv("DR_GRAPHS");
         c->graphs = !(gr && gr[0] == '0');
+        const char* ch = getenv("DR_CHUNK");
+        c->chunk = ch ? atoi(ch) : 0;
         const char* wi = getenv("DR_WINDOW");
         c->window = wi && wi[0] == '1';
     }
