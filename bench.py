@@ -409,10 +409,14 @@ def run_ours(args, ws, rank, local):
                      "note": "exchange = grouped ncclSend/ncclRecv bracketed by CUDA events on the context stream "
                              "in the untimed profiling pass (every launch timed)"}
 
-    # ---- timed region (device-resident inputs); the dominant kernel's launches timed live
-    ctx.profile_reset()
+    # ---- timed region (device-resident inputs); the dominant kernel's launches timed live.  One untimed
+    # step first: the library replays matvec / preconditioner calls from CUDA graphs captured per profiler
+    # setting, so the capture for this setting happens outside the timed region
     ctx.profile_only(dom_tag)
     ctx.profile_enable(True)
+    step(v, vts, Hv, Z)
+    torch.cuda.synchronize()
+    ctx.profile_reset()
     clocks = Clocks(local)
     clocks.start()
     barrier(ws)
@@ -435,7 +439,9 @@ def run_ours(args, ws, rank, local):
     value = args.steps * NMV / T
     vox_steps = args.steps * (NT * M + NT * M + NMV * 2 * NT * M) / T
 
-    # ---- matvec-only throughput (secondary)
+    # ---- matvec-only throughput (secondary; one untimed pass re-captures the graphs without profiling)
+    for i in range(NMV):
+        ctx.hessian_matvec(vts[i], Hv[i])
     torch.cuda.synchronize()
     m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     m0.record(stream)

@@ -40,6 +40,7 @@ struct Comm {
     // matched in the order they appear in the two ranks' lists (NCCL semantics).
     virtual void group(const std::vector<P2P>& ops, cudaStream_t s) = 0;
     virtual std::string check() { return ""; }  // asynchronous error, empty if none
+    virtual bool capturable() const { return false; }  // group() may be recorded into a CUDA graph
 };
 
 // ----------------------------------------------------------------------------------------------- NCCL
@@ -124,6 +125,7 @@ struct NcclComm : Comm {
         }
         nccl_ck(A.GroupEnd(), "ncclGroupEnd");
     }
+    bool capturable() const override { return true; }  // NCCL kernels under stream capture
     std::string check() override {
         int e = 0;
         NcclApi& A = NcclApi::get();

@@ -225,6 +225,28 @@ struct dr_ctx {
     size_t ev_used = 0;
     struct Pending { const char* tag; cudaEvent_t a, b; };
     std::vector<Pending> pending;
+    // Captured matvec / preconditioner calls (dr_hessian_matvec, dr_precond_apply), keyed by their
+    // argument pointers; the CUDA graph holds every launch of the call (and, with NCCL slabs, its
+    // send/recv), replayed with one cudaGraphLaunch.  Invalidated by set_images / set_velocity (the
+    // off-rank plans' host counts are baked into the launches) and by profiler changes.
+    struct CallGraph {
+        int kind = 0;
+        const void* a = nullptr;
+        const void* b = nullptr;
+        uint64_t epoch = 0;
+        std::string prof_sig;
+        cudaGraph_t graph = nullptr;          // kept: its event-record nodes are retargeted per replay
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;                 // kernel launches one replay performs
+        struct EvNode { const char* tag; cudaGraphNode_t a, b; };
+        std::vector<EvNode> ev;               // profiled launches: start / end event-record nodes
+        std::vector<cudaEvent_t> own;         // the events recorded at capture (identify the nodes)
+    };
+    std::vector<CallGraph> call_graphs;
+    uint64_t graph_epoch = 1;
+    bool capturing = false;                   // profiler events go to cap_ev, not the pending list
+    std::vector<Pending> cap_ev;
+    std::vector<cudaEvent_t> graph_events;    // events recorded by the PCG graph's nodes
     struct Acc { std::string tag; int64_t n = 0; double ms = 0; };
     std::vector<Acc> acc;
     cudaEvent_t cur_start = nullptr;
@@ -240,8 +262,13 @@ struct dr_ctx {
     bool prof_on(const char* tag) const { return prof && (prof_only.empty() || prof_only == tag); }
     void prof_begin(const char* tag, cudaStream_t st) {
         if (prof_on(tag)) {
-            cur_start = take_event();
-            cudaEventRecord(cur_start, st);
+            if (capturing) {  // a dedicated event, recorded as a graph node (retargeted at every replay)
+                cudaEventCreate(&cur_start);
+                cudaEventRecordWithFlags(cur_start, st, cudaEventRecordExternal);
+            } else {
+                cur_start = take_event();
+                cudaEventRecord(cur_start, st);
+            }
         }
     }
     void prof_end(const char* tag, cudaStream_t st);
@@ -254,9 +281,15 @@ void dr_ctx::prof_end(const char* tag, cudaStream_t st) {
     ck(cudaGetLastError(), tag);
     ++launches;
     if (prof_on(tag)) {
-        cudaEvent_t e = take_event();
-        cudaEventRecord(e, st);
-        pending.push_back(Pending{tag, cur_start, e});
+        cudaEvent_t e;
+        if (capturing) {
+            cudaEventCreate(&e);
+            cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+        } else {
+            e = take_event();
+            cudaEventRecord(e, st);
+        }
+        (capturing ? cap_ev : pending).push_back(Pending{tag, cur_start, e});
     }
 }
 
@@ -1219,14 +1252,23 @@ struct Impl {
                 cudaGraph_t gr = nullptr;
                 s = c.hi;
                 CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                c.capturing = true;
+                c.cap_ev.clear();
                 try {
                     pcg_iteration_body();
                 } catch (...) {
+                    c.capturing = false;
                     cudaStreamEndCapture(s, &gr);
                     if (gr) cudaGraphDestroy(gr);
                     s = user;
                     throw;
                 }
+                c.capturing = false;
+                for (const auto& p : c.cap_ev) {  // profiled launches inside the PCG graph are not retargeted
+                    c.graph_events.push_back(p.a);
+                    c.graph_events.push_back(p.b);
+                }
+                c.cap_ev.clear();
                 CK(cudaStreamEndCapture(s, &gr));
                 s = user;
                 CK(cudaGraphInstantiate(&c.pcg_graph, gr, 0));
@@ -1601,6 +1643,117 @@ void dispatch(dr_ctx* c, F&& f) {
         f(im);
     }
 }
+template <typename F>
+void dispatch_on(dr_ctx* c, cudaStream_t st, F&& f) {  // the work issued on stream st
+    if (c->cfg.flags & DR_FP64) {
+        Impl<double> im(*c, c->g, st);
+        f(im);
+    } else {
+        Impl<float> im(*c, c->g, st);
+        f(im);
+    }
+}
+
+void destroy_graph(dr_ctx::CallGraph& e) {
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.graph) cudaGraphDestroy(e.graph);
+    for (cudaEvent_t ev : e.own) cudaEventDestroy(ev);
+    e = dr_ctx::CallGraph{};
+}
+
+std::string prof_signature(const dr_ctx* c) { return c->prof ? "on:" + c->prof_only : "off"; }
+
+// Run body(stream) as a cached CUDA graph keyed by (kind, a, b): captured on the internal stream c->hi
+// the first time, then replayed on the context stream.  Profiled launches (dr_profile_*) are event-
+// record nodes in the graph; every replay points them at fresh pool events, so the per-kernel
+// accounting is the same as in eager execution.  Loopback slabs (host barriers) run eagerly.
+template <typename F>
+void run_graph(dr_ctx* c, int kind, const void* a, const void* b, F&& body) {
+    if (!c->graphs || (c->dist() && !c->comm->capturable())) {
+        body(c->stream);
+        return;
+    }
+    const std::string sig = prof_signature(c);
+    dr_ctx::CallGraph* e = nullptr;
+    for (auto& x : c->call_graphs)
+        if (x.kind == kind && x.a == a && x.b == b && x.epoch == c->graph_epoch && x.prof_sig == sig) e = &x;
+    if (!e) {
+        // drop stale entries; cap the cache (distinct argument pointers each capture once)
+        std::vector<dr_ctx::CallGraph> keep;
+        for (auto& x : c->call_graphs) {
+            if (x.epoch == c->graph_epoch && x.prof_sig == sig && keep.size() < 31) keep.push_back(x);
+            else destroy_graph(x);
+        }
+        c->call_graphs.swap(keep);
+        dr_ctx::CallGraph ng;
+        ng.kind = kind;
+        ng.a = a;
+        ng.b = b;
+        ng.epoch = c->graph_epoch;
+        ng.prof_sig = sig;
+        const int64_t l0 = c->launches;
+        cudaStream_t cs = c->hi;
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        c->capturing = true;
+        c->cap_ev.clear();
+        try {
+            body(cs);
+        } catch (...) {
+            c->capturing = false;
+            cudaGraph_t gr = nullptr;
+            cudaStreamEndCapture(cs, &gr);
+            if (gr) cudaGraphDestroy(gr);
+            for (const auto& p : c->cap_ev) {
+                cudaEventDestroy(p.a);
+                cudaEventDestroy(p.b);
+            }
+            c->cap_ev.clear();
+            c->launches = l0;
+            throw;
+        }
+        c->capturing = false;
+        CK(cudaStreamEndCapture(cs, &ng.graph));
+        ng.launches = c->launches - l0;
+        c->launches = l0;
+        // map the profiler's events to their record nodes
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(ng.graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) CK(cudaGraphGetNodes(ng.graph, nodes.data(), &nn));
+        auto node_of = [&](cudaEvent_t ev) -> cudaGraphNode_t {
+            for (cudaGraphNode_t n : nodes) {
+                cudaGraphNodeType t;
+                CK(cudaGraphNodeGetType(n, &t));
+                if (t != cudaGraphNodeTypeEventRecord) continue;
+                cudaEvent_t x = nullptr;
+                CK(cudaGraphEventRecordNodeGetEvent(n, &x));
+                if (x == ev) return n;
+            }
+            fail(DR_ERR_CUDA, "profiler event node missing from the captured graph");
+        };
+        for (const auto& p : c->cap_ev) {
+            ng.ev.push_back(dr_ctx::CallGraph::EvNode{p.tag, node_of(p.a), node_of(p.b)});
+            ng.own.push_back(p.a);
+            ng.own.push_back(p.b);
+        }
+        c->cap_ev.clear();
+        CK(cudaGraphInstantiate(&ng.exec, ng.graph, 0));
+        c->call_graphs.push_back(ng);
+        e = &c->call_graphs.back();
+    }
+    for (const auto& en : e->ev) {
+        cudaEvent_t x = c->take_event(), y = c->take_event();
+        CK(cudaGraphExecEventRecordNodeSetEvent(e->exec, en.a, x));
+        CK(cudaGraphExecEventRecordNodeSetEvent(e->exec, en.b, y));
+        c->pending.push_back(dr_ctx::Pending{en.tag, x, y});
+    }
+    CK(cudaGraphLaunch(e->exec, c->stream));
+    c->launches += e->launches;
+}
+
+bool graphable(const void* a, const void* b) {  // device buffers the kernels use in place
+    return is_device_ptr(a) && aligned16(a) && is_device_ptr(b) && aligned16(b);
+}
 
 template <typename F>
 dr_status comm_run(F&& f) {
@@ -1823,6 +1976,8 @@ dr_status dr_destroy(dr_ctx* c) {
     }
     if (c->ev_hi) cudaEventDestroy(c->ev_hi);
     if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
+    for (auto& e : c->call_graphs) destroy_graph(e);
+    for (cudaEvent_t e : c->graph_events) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -1837,6 +1992,7 @@ dr_status dr_destroy(dr_ctx* c) {
 
 dr_status dr_set_images(dr_ctx* c, const void* rho_T, const void* rho_R) {
     return run(c, [&] {
+        ++c->graph_epoch;  // captured matvec / preconditioner graphs are stale
         if (!rho_T || !rho_R) fail(DR_ERR_ARG, "rho_T and rho_R must be non-NULL");
         dispatch(c, [&](auto& im) {
             const size_t F = c->g.M * elem_size(c);
@@ -1850,6 +2006,7 @@ dr_status dr_set_images(dr_ctx* c, const void* rho_T, const void* rho_R) {
 
 dr_status dr_set_velocity(dr_ctx* c, const void* v) {
     return run(c, [&] {
+        ++c->graph_epoch;  // captured matvec / preconditioner graphs are stale
         if (!v) fail(DR_ERR_ARG, "v must be non-NULL");
         c->have_velocity = false;
         c->have_state = c->have_adjoint = c->have_matvec = false;
@@ -1896,17 +2053,22 @@ dr_status dr_hessian_matvec(dr_ctx* c, const void* vt, void* Hvt) {
         if (vt == Hvt) fail(DR_ERR_ARG, "vt and Hvt must not alias");
         if (!c->have_state) fail(DR_ERR_ORDER, "hessian_matvec needs forward_solve");
         const size_t V = 3 * c->g.M * elem_size(c);
-        const void* in = stage_in(c, vt, V, c->ws + c->L.stin);
-        with_output(c, Hvt, V, c->ws + c->L.stout, [&](void* out) {
-            dispatch(c, [&](auto& im) {
+        if ((c->cfg.flags & DR_FULL_NEWTON) && !c->have_adjoint) {  // the lambda terms need the adjoint slices
+            dispatch(c, [&](auto& im) { im.adjoint_solve(); });
+            c->have_adjoint = true;
+        }
+        auto body = [&](const void* in, void* out, cudaStream_t st) {
+            dispatch_on(c, st, [&](auto& im) {
                 using T = std::remove_pointer_t<decltype(im.rhoR())>;
-                if (im.newton() && !c->have_adjoint) {  // the lambda terms need the adjoint slices
-                    im.adjoint_solve();
-                    c->have_adjoint = true;
-                }
                 im.hessian_matvec(static_cast<const T*>(in), static_cast<T*>(out));
             });
-        });
+        };
+        if (graphable(vt, Hvt)) {
+            run_graph(c, 1, vt, Hvt, [&](cudaStream_t st) { body(vt, Hvt, st); });
+        } else {
+            const void* in = stage_in(c, vt, V, c->ws + c->L.stin);
+            with_output(c, Hvt, V, c->ws + c->L.stout, [&](void* out) { body(in, out, c->stream); });
+        }
         c->have_matvec = true;
     });
 }
@@ -1915,14 +2077,19 @@ dr_status dr_precond_apply(dr_ctx* c, const void* r, void* z) {
     return run(c, [&] {
         if (!r || !z) fail(DR_ERR_ARG, "r and z must be non-NULL");
         const size_t V = 3 * c->g.M * elem_size(c);
-        const void* in = stage_in(c, r, V, c->ws + c->L.stin);
-        with_output(c, z, V, c->ws + c->L.stout, [&](void* out) {
-            dispatch(c, [&](auto& im) {
+        auto body = [&](const void* in, void* out, cudaStream_t st) {
+            dispatch_on(c, st, [&](auto& im) {
                 using T = std::remove_pointer_t<decltype(im.rhoR())>;
                 const T* i = static_cast<const T*>(in);
                 im.precond(cvec(vec(const_cast<T*>(i), (size_t)c->g.M)), vec(static_cast<T*>(out), (size_t)c->g.M));
             });
-        });
+        };
+        if (graphable(r, z)) {
+            run_graph(c, 2, r, z, [&](cudaStream_t st) { body(r, z, st); });
+        } else {
+            const void* in = stage_in(c, r, V, c->ws + c->L.stin);
+            with_output(c, z, V, c->ws + c->L.stout, [&](void* out) { body(in, out, c->stream); });
+        }
     });
 }
 dr_status dr_gradient(dr_ctx* c, void* gout) {

@@ -646,3 +646,46 @@ def test_window_gather_same_bits_as_pair_path(dr, monkeypatch):
                       ctx.hessian_matvec(vt), ctx.get_field(dr.DR_FIELD_BTILDE)]
         for a, b in zip(res["0"], res["1"]):
             assert torch.equal(a, b), name
+
+
+def test_call_graphs_match_eager(dr, monkeypatch):
+    """dr_hessian_matvec / dr_precond_apply replayed from the context's cached CUDA graphs (default) give
+    the bits of eager execution (DR_GRAPHS=0): the first call (capture + launch), replays, a second
+    argument pair, and a new velocity (stale graphs re-captured).  The profiler's per-kernel launch
+    counts agree (its events are record nodes retargeted at every replay)."""
+    name, n, nt, vgen, iso = CASES[2]
+    res, prof = {}, {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("DR_GRAPHS", mode)
+        ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+        ctx.forward_solve()
+        vts = [synth.round32(synth.smooth_vec(21 + i, n, kmax=5)).contiguous().cuda() for i in range(2)]
+        Hs = [torch.empty_like(vts[0]) for _ in range(2)]
+        Zs = [torch.empty_like(vts[0]) for _ in range(2)]
+        out = []
+        for rep in range(3):
+            for i in range(2):
+                ctx.hessian_matvec(vts[i], Hs[i])
+                ctx.precond_apply(Hs[i], Zs[i])
+                out += [Hs[i].clone(), Zs[i].clone()]
+        ctx.set_velocity(synth.round32(synth.smooth_vec(9, n, kmax=4, cells_per_step=1.0, nt=nt)).contiguous().cuda())
+        ctx.forward_solve()
+        for i in range(2):
+            ctx.hessian_matvec(vts[i], Hs[i])
+            ctx.precond_apply(Hs[i], Zs[i])
+            out += [Hs[i].clone(), Zs[i].clone()]
+        ctx.profile_reset()
+        ctx.profile_enable(True)
+        for i in range(2):
+            ctx.hessian_matvec(vts[i], Hs[i])
+            ctx.precond_apply(Hs[i], Zs[i])
+        torch.cuda.synchronize()
+        p, launches = ctx.profile()
+        ctx.profile_enable(False)
+        out += [Hs[0].clone(), Zs[1].clone()]
+        res[mode] = out
+        prof[mode] = ({t: k for t, (k, ms) in p.items()}, launches)
+        assert all(ms > 0 for t, (k, ms) in p.items()), p
+    for a, b in zip(res["0"], res["1"]):
+        assert torch.equal(a, b)
+    assert prof["0"] == prof["1"]
