@@ -24,6 +24,7 @@
 #include "fft.cuh"
 #include "pointwise.cuh"
 #include "sl.cuh"
+#include "plane2d.cuh"
 #include "comm.cuh"
 
 using namespace dr;
@@ -199,6 +200,9 @@ struct dr_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hi = nullptr;
     bool overlap = false;                     // DR_OVERLAP=1 in the environment at dr_create
     bool window = false;                      // DR_WINDOW=1: sliding-window fp32 gathers (sl.cuh k_sl_window)
+    bool pairs = false;                       // DR_PAIRS=1: x3-adjacent shared-plane pair gathers (sl.cuh k_sl_pairs)
+    bool plane2d = false;                     // DR_PLANE2D=1: fused x1/x2 cluster plane transforms (plane2d.cuh)
+    int ring = 0;                             // DR_RING=P: x1/x2 pass pairs per P planes through an L2-resident scratch
     bool tma_middle = true;                   // DR_TMA_MIDDLE=0 at dr_create: the unstaged fp32 middle pass
     bool graphs = true;                       // DR_GRAPHS=0 disables the CUDA-graph PCG iteration
     int chunk = 0;                            // DR_CHUNK=P: x1/x2 pass pairs run per P planes (L2 reuse)
@@ -555,6 +559,66 @@ struct Impl {
         stream(add ? "row_c2r_add" : "row_c2r", PT{g, sp, RowOut<T>{out, add}, twx(), csf, css}, row_tiles<PT::RB>(), nc);
     }
 
+    // Fused x1/x2 plane transforms (plane2d.cuh): one rank, fp32 fields, N1 = N2 = 256.  Persistent
+    // clusters of 8 CTAs (one per SM), as many as can be co-resident.
+    // scratch ring of 3 components x c.ring planes of half spectra (after the 3 batched spectrum slots;
+    // the forward (Tc) and inverse (T) rings share the same bytes, so the lines stay L2-resident)
+    bool ring_ok() const { return c.ring > 0 && !c.dist() && c.ring < g.n3 && g.n3 % c.ring == 0; }
+    template <typename U>
+    Cx<U>* ring_scratch() { return reinterpret_cast<Cx<U>*>(specD(3)); }
+    bool plane2d_ok(const void* a, const void* b) const {
+        return c.plane2d && !c.dist() && std::is_same<T, float>::value && g.n1 == 256 && g.n2 == 256 && al16(a) && al16(b);
+    }
+    template <class K>
+    int plane_clusters(K k, size_t smem, int nitems) {
+        set_smem(k, smem);
+        static std::atomic<int> cache[MAX_DEV];
+        const int d = c.dev < MAX_DEV ? c.dev : MAX_DEV - 1;
+        int n = cache[d].load(std::memory_order_relaxed);
+        if (n == 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(8 * 16);
+            cfg.blockDim = dim3(256);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 8;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CK(cudaOccupancyMaxActiveClusters(&n, k, &cfg));
+            n = std::max(n, 1);
+            cache[d].store(n, std::memory_order_relaxed);
+        }
+        return std::min(n, nitems);
+    }
+    template <typename Tc>
+    void fwd2d(const T* f, Cx<Tc>* sp, int nc, int64_t csf, int64_t css) {
+        if constexpr (std::is_same<T, float>::value) {
+            auto k = k_plane_fwd<float, Tc>;
+            constexpr size_t sm = plane_fwd_smem<float, Tc>();
+            const int nitems = nc * g.n3;
+            const int ncl = plane_clusters(k, sm, nitems);
+            const char* tag = tag_n(sizeof(Tc) == 8 ? "plane_fwd_f64" : "plane_fwd_f32", nc);
+            PB(tag);
+            k<<<8 * ncl, 256, sm, s>>>(f, sp, g.n3, nitems, csf, css, g.n1p, twx_t<Tc>(), twy_t<Tc>());
+            PE(tag);
+        }
+    }
+    void inv2d(const Cx<T>* sp, T* out, const T* add, int nc, int64_t csf, int64_t css) {
+        if constexpr (std::is_same<T, float>::value) {
+            auto k = k_plane_inv<float>;
+            constexpr size_t sm = plane_inv_smem<float>();
+            const int nitems = nc * g.n3;
+            const int ncl = plane_clusters(k, sm, nitems);
+            const char* tag = tag_n(add ? "plane_inv_add" : "plane_inv", nc);
+            PB(tag);
+            k<<<8 * ncl, 256, sm, s>>>(sp, out, add, g.n3, nitems, csf, css, g.n1p, twx(), twy());
+            PE(tag);
+        }
+    }
+
 #define DR_SWITCH_ROW(Lval, call)                          \
     switch (Lval) {                                        \
         case 2: call(2); break;                            \
@@ -644,27 +708,28 @@ struct Impl {
     }
 
     template <typename U, int L, int DIR, bool SI, bool SO>
-    void col_fft_LS(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs) {
+    void col_fft_LS(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs, int64_t csd) {
         using PT = ColFftPass<U, L, DIR, SI, SO>;
         const ColGeom cg = spec_geom();
         stream(DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32",
-               PT{cg, src, dst, tw, nb_in, nb_out, cs}, col_tiles<PT>(cg, g.n3), nc);
+               PT{cg, src, dst, tw, nb_in, nb_out, cs, csd}, col_tiles<PT>(cg, g.n3), nc);
     }
     template <typename U, int L, int DIR>
-    void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs) {
+    void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs, int64_t csd) {
         // the split layouts only occur on the side facing an all-to-all: out of the forward, into the inverse
-        if (DIR < 0 && nb_out) col_fft_LS<U, L, DIR, false, true>(src, dst, tw, nb_in, nb_out, nc, cs);
-        else if (DIR > 0 && nb_in) col_fft_LS<U, L, DIR, true, false>(src, dst, tw, nb_in, nb_out, nc, cs);
-        else col_fft_LS<U, L, DIR, false, false>(src, dst, tw, nb_in, nb_out, nc, cs);
+        if (DIR < 0 && nb_out) col_fft_LS<U, L, DIR, false, true>(src, dst, tw, nb_in, nb_out, nc, cs, csd);
+        else if (DIR > 0 && nb_in) col_fft_LS<U, L, DIR, true, false>(src, dst, tw, nb_in, nb_out, nc, cs, csd);
+        else col_fft_LS<U, L, DIR, false, false>(src, dst, tw, nb_in, nb_out, nc, cs, csd);
     }
+    // (csd: component stride of dst when it differs from src's cs)
     template <typename Tc>
-    void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out, int nc = 1, int64_t cs = 0) {  // forward along x2, in Tc
-#define CALL(LL) col_fft_L<Tc, LL, -1>(src, dst, twy_t<Tc>(), 0, nb_out, nc, cs)
+    void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out, int nc = 1, int64_t cs = 0, int64_t csd = -1) {  // forward along x2, in Tc
+#define CALL(LL) col_fft_L<Tc, LL, -1>(src, dst, twy_t<Tc>(), 0, nb_out, nc, cs, csd)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
-    void col_fft_inv(const Cx<T>* src, Cx<T>* dst, int nb_in, int nc = 1, int64_t cs = 0) {  // inverse along x2, in T
-#define CALL(LL) col_fft_L<T, LL, +1>(src, dst, twy(), nb_in, 0, nc, cs)
+    void col_fft_inv(const Cx<T>* src, Cx<T>* dst, int nb_in, int nc = 1, int64_t cs = 0, int64_t csd = -1) {  // inverse along x2, in T
+#define CALL(LL) col_fft_L<T, LL, +1>(src, dst, twy(), nb_in, 0, nc, cs, csd)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
@@ -698,6 +763,10 @@ struct Impl {
     template <typename Tc = double>
     void spec_forward(const T* f, int slot) {
         if (!c.dist()) {
+            if (plane2d_ok(f, specD_t<Tc>(slot))) {
+                fwd2d<Tc>(f, specD_t<Tc>(slot), 1, 0, 0);
+                return;
+            }
             row_r2c<Tc>(f, specD_t<Tc>(slot));
             col_fft_fwd<Tc>(specD_t<Tc>(slot), specD_t<Tc>(slot), 0);
             return;
@@ -709,6 +778,10 @@ struct Impl {
     // Back from the middle pass's output slot to a real slab field (+ add).
     void spec_inverse(int slot, T* out, const T* add) {
         if (!c.dist()) {
+            if (plane2d_ok(out, add)) {
+                inv2d(specF(slot), out, add, 1, 0, 0);
+                return;
+            }
             col_fft_inv(specF(slot), specF(slot), 0);
             row_c2r(specF(slot), out, add);
             return;
@@ -800,6 +873,21 @@ struct Impl {
                     sub.template row_r2c<Tc>(in.c[0] + (size_t)z * plane(), sp, 3, si, g.S);
                     sub.template col_fft_fwd<Tc>(sp, sp, 0, 3, g.S);
                 }
+            } else if (plane2d_ok(in.c[0], specD_t<Tc>(0))) {
+                fwd2d<Tc>(in.c[0], specD_t<Tc>(0), 3, si, g.S);
+            } else if (ring_ok()) {
+                // plane chunks through one scratch ring: the x1 half spectra of a chunk are written to the
+                // same (L2-resident) scratch lines every chunk and read back by the chunk's x2 pass
+                Grid gc = g;
+                gc.n3 = c.ring;
+                gc.M = (int64_t)g.n1 * g.n2 * gc.n3;
+                Impl sub(c, gc, s);
+                const int64_t rs = (int64_t)c.ring * g.n2 * g.n1p;
+                Cx<Tc>* sc = ring_scratch<Tc>();
+                for (int z = 0; z < g.n3; z += c.ring) {
+                    sub.template row_r2c<Tc>(in.c[0] + (size_t)z * plane(), sc, 3, si, rs);
+                    sub.template col_fft_fwd<Tc>(sc, specD_t<Tc>(0) + (size_t)z * g.n2 * g.n1p, 0, 3, rs, g.S);
+                }
             } else {
                 row_r2c<Tc>(in.c[0], specD_t<Tc>(0), 3, si, g.S);
                 col_fft_fwd<Tc>(specD_t<Tc>(0), specD_t<Tc>(0), 0, 3, g.S);
@@ -823,6 +911,24 @@ struct Impl {
                     const size_t off = (size_t)z * plane();
                     sub.col_fft_inv(sp, sp, 0, 3, g.S);
                     sub.row_c2r(sp, out.c[0] + off, add ? add->c[0] + off : nullptr, 3, so, g.S);
+                }
+                return;
+            }
+            if (plane2d_ok(out.c[0], add ? add->c[0] : nullptr)) {
+                inv2d(specF(0), out.c[0], add ? add->c[0] : nullptr, 3, so, g.S);
+                return;
+            }
+            if (ring_ok()) {
+                Grid gc = g;
+                gc.n3 = c.ring;
+                gc.M = (int64_t)g.n1 * g.n2 * gc.n3;
+                Impl sub(c, gc, s);
+                const int64_t rs = (int64_t)c.ring * g.n2 * g.n1p;
+                Cx<T>* sc = ring_scratch<T>();
+                for (int z = 0; z < g.n3; z += c.ring) {
+                    const size_t off = (size_t)z * plane();
+                    sub.col_fft_inv(specF(0) + (size_t)z * g.n2 * g.n1p, sc, 0, 3, g.S, rs);
+                    sub.row_c2r(sc, out.c[0] + off, add ? add->c[0] + off : nullptr, 3, so, rs);
                 }
                 return;
             }
@@ -985,6 +1091,15 @@ struct Impl {
             if (c.window) {  // sliding-window gather (sl.cuh k_sl_window)
                 constexpr size_t sm = win_box_bytes();
                 auto k = k_sl_window<Epi>;
+                set_smem(k, sm);
+                PB(tag);
+                k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
+                PE(tag);
+                goto launched;
+            }
+            if (c.pairs) {  // shared-plane pair gather (sl.cuh k_sl_pairs)
+                constexpr size_t sm = pairs_smem_bytes();
+                auto k = k_sl_pairs<Epi>;
                 set_smem(k, sm);
                 PB(tag);
                 k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
@@ -1940,6 +2055,12 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
         c->chunk = ch ? atoi(ch) : 0;
         const char* wi = getenv("DR_WINDOW");
         c->window = wi && wi[0] == '1';
+        const char* pa = getenv("DR_PAIRS");
+        c->pairs = pa && pa[0] == '1';
+        const char* p2 = getenv("DR_PLANE2D");
+        c->plane2d = p2 && p2[0] == '1';
+        const char* rg = getenv("DR_RING");
+        c->ring = rg ? atoi(rg) : 0;
     }
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);

@@ -742,7 +742,8 @@ struct ColFftPass {
     Cx<T>* dst;
     const Cx<T>* tw;
     int nb_in, nb_out;
-    int64_t cs = 0;  // component stride (blockIdx.y = component) of src and dst
+    int64_t cs = 0;    // component stride (blockIdx.y = component) of src (and of dst when csd < 0)
+    int64_t csd = -1;  // component stride of dst
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
         int x0, o0, xi, t, oi;
@@ -754,7 +755,7 @@ struct ColFftPass {
         const Cx<T>* tw = tw_smem<T, L, NT, TWS>(this->tw, reinterpret_cast<Cx<T>*>(smem + CC::SMEM));
         fft_line_io<T, L, DIR, false, false>(buf, t, tw, 1,
                                              col_acc<2, T, SPLIT_IN>(const_cast<Cx<T>*>(src) + blockIdx.y * cs, c, x, o, nb_in, on, 0),
-                                             col_acc<2, T, SPLIT_OUT>(dst + blockIdx.y * cs, c, x, o, nb_out, on, 0));
+                                             col_acc<2, T, SPLIT_OUT>(dst + blockIdx.y * (csd < 0 ? cs : csd), c, x, o, nb_out, on, 0));
     }
 };
 

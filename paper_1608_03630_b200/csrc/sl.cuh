@@ -806,6 +806,160 @@ __global__ void __launch_bounds__(SL_THREADS, WIN_MINB)
 }
 
 // ---------------------------------------------------------------------------------------------
+// Shared-plane pair gather (fp32, one component: every transport step of the hot path).  The pair path
+// of k_sl_gather is bound by the shared-memory datapath (64 stencil LDS per point at 1.3 wavefronts),
+// so this kernel reuses loaded values in registers ("Blocking, prefetching, and vectorization
+// can be used to improve the performance").  A thread pairs x3-adjacent points A = (x, y, z) and
+// B = (x, y, z + 1).  The velocity is smooth, so on the bench field 93 % of such pairs have equal
+// floor(-d) along all three axes (floors differ by a cell along any one axis in 3.3 % of pairs).
+// Their stencils then share the same 4 x 4 columns and B's four planes start one plane above A's
+// (the box holds that fifth plane: it is B's top stencil plane), so the pair reads the
+// 5 planes of the union once (80 LDS for two points instead of 128) and contracts each value with both
+// points' weights in one packed FFMA2 (the shared value broadcast).  x3 weights are padded to 5 slots
+// (A at slots 0-3, B at 1-4, zeros elsewhere): the zero products are exact zeros, and every
+// non-zero term is summed in the pair path's order, so both kernels give the same bits (up to the sign
+// of an exact zero).  Pairs that do not share (and the last point of an odd column) are deferred to a
+// shared-memory queue that the whole CTA drains after the main loop with the two-pointer pair
+// arithmetic (interp_box2), so a misaligned lane idles for one pair instead of making its warp run
+// both paths.  Deferred pairs are appended in source-lane order (a misalignment is a smooth surface,
+// so neighbouring lanes defer together) and a drain lane takes one pair: neighbouring drain lanes then
+// read neighbouring columns, as in the main loop, instead of colliding on random banks.
+constexpr int PQ_CAP = SL_THREADS * SL_TZ / 2;  // every pair of the tile (uint16 p * SL_THREADS + thread)
+constexpr size_t pairs_smem_bytes() { return box_bytes<float, 1>() + PQ_CAP * sizeof(uint16_t); }
+
+// finish two arbitrary points of the box (either may be invalid: ok = false) with the pair arithmetic
+template <class Epi>
+__device__ __forceinline__ void pair_any(const Grid& g, const TileCtx<float, 1>& c, const float* __restrict__ box,
+                                         const int iA[3], const int iB[3], uint32_t idA, uint32_t idB, bool okA,
+                                         bool okB, const float dA[3], const float dB[3],
+                                         const typename Epi::Late& lA, const typename Epi::Late& lB, const Epi& epi) {
+    constexpr int BX = BoxGeom<float, 1>::BX, BY = BoxGeom<float, 1>::BY;
+    int qA[3], qB[3];
+    float tA[3], tB[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        cell_of<float>(iA[a], dA[a], qA[a], tA[a]);
+        cell_of<float>(iB[a], dB[a], qB[a], tB[a]);
+        if (!okB) { qB[a] = qA[a]; tB[a] = tA[a]; }
+        if (!okA) { qA[a] = qB[a]; tA[a] = tB[a]; }
+    }
+    const float* bA = box + ((qA[2] - 1 - c.oz) * BY + (qA[1] - 1 - c.oy)) * BX + (qA[0] - 1 - c.ox);
+    const float* bB = box + ((qB[2] - 1 - c.oz) * BY + (qB[1] - 1 - c.oy)) * BX + (qB[0] - 1 - c.ox);
+    DR_ASSERT(qA[0] - 1 - c.ox >= 0 && qA[0] + 2 - c.ox < c.ex && qA[1] - 1 - c.oy >= 0 && qA[1] + 2 - c.oy < c.ey &&
+              qA[2] - 1 - c.oz >= 0 && qA[2] + 2 - c.oz < c.ez);
+    DR_ASSERT(qB[0] - 1 - c.ox >= 0 && qB[0] + 2 - c.ox < c.ex && qB[1] - 1 - c.oy >= 0 && qB[1] + 2 - c.oy < c.ey &&
+              qB[2] - 1 - c.oz >= 0 && qB[2] + 2 - c.oz < c.ez);
+    float2 w[3][4];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) lagrange4x2(make_float2(tA[a], tB[a]), w[a]);
+    const float2 r = interp_box2<BX, BY>(bA, bB, w[0], w[1], w[2]);
+    if (okA) epi.store(idA, &r.x, lA);
+    if (okB) epi.store(idB, &r.y, lB);
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(SL_THREADS, (EpiMinB<Epi>::V))
+    k_sl_pairs(Grid g, Src<float, 1> src, Disp<float> d, const int* __restrict__ plan, int ntiles, Epi epi) {
+    using T = float;
+    constexpr int BX = BoxGeom<T, 1>::BX, BY = BoxGeom<T, 1>::BY;
+    constexpr int NP = SL_TZ / 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* box = reinterpret_cast<T*>(smem_raw);
+    uint16_t* queue = reinterpret_cast<uint16_t*>(smem_raw + box_bytes<T, 1>());
+    __shared__ int qn;
+    const int tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    const TileCtx<T, 1> c = tile_ctx<T, 1>(g, plan, tile);
+    stage_box<T, 1>(g, src, c, box);
+    const int x = c.x0 + (threadIdx.x % SL_TX), y = c.y0 + threadIdx.x / SL_TX;
+    const bool xyok = x < g.n1 && y < g.n2;
+    const int kmax = min(SL_TZ, g.n3 - c.z0);
+    const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
+    const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
+    if (!c.fits) {  // global-memory fallback (uniform per tile; nothing staged, no barrier)
+        if (xyok) column_from_global<T, 1, Epi>(g, src, d, x, y, c.z0, kmax, id0, plane, epi);
+        return;
+    }
+    if (threadIdx.x == 0) qn = 0;
+    PairIn<T, Epi> cur;
+    if (xyok) load_pair<T, Epi>(d, epi, id0, id0 + plane, 0 < kmax, 1 < kmax, cur);
+    cp_async_wait_all();
+    __syncthreads();
+    if (xyok) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int kA = 2 * p;
+            if (kA >= kmax) break;
+            const bool okB = kA + 1 < kmax;
+            PairIn<T, Epi> nxt;
+            if (p + 1 < NP && kA + 2 < kmax)
+                load_pair<T, Epi>(d, epi, id0 + (kA + 2) * plane, id0 + (kA + 3) * plane, true, kA + 3 < kmax, nxt);
+            const uint32_t idA = id0 + kA * plane, idB = idA + plane;
+            const int zA = c.z0 + kA + g.z0;
+            int qA[3], qB[3];
+            T tA[3], tB[3];
+            const int iA[3] = {x, y, zA}, iB[3] = {x, y, zA + 1};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                cell_of<T>(iA[a], cur.dA[a], qA[a], tA[a]);
+                cell_of<T>(iB[a], cur.dB[a], qB[a], tB[a]);
+            }
+            if (okB && qA[0] == qB[0] && qA[1] == qB[1] && qB[2] == qA[2] + 1) {
+                const T* bA = box + ((qA[2] - 1 - c.oz) * BY + (qA[1] - 1 - c.oy)) * BX + (qA[0] - 1 - c.ox);
+                DR_ASSERT(qA[0] - 1 - c.ox >= 0 && qA[0] + 2 - c.ox < c.ex && qA[1] - 1 - c.oy >= 0 &&
+                          qA[1] + 2 - c.oy < c.ey && qA[2] - 1 - c.oz >= 0 && qA[2] + 3 - c.oz < c.ez);
+                float2 w1[4], w2[4], w3[4];
+                lagrange4x2(make_float2(tA[0], tB[0]), w1);
+                lagrange4x2(make_float2(tA[1], tB[1]), w2);
+                lagrange4x2(make_float2(tA[2], tB[2]), w3);
+                float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    float2 accb = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const T* r = bA + (j * BY + bb) * BX;
+                        const T r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3];
+                        float2 row = __fmul2_rn(w1[0], make_float2(r0, r0));
+                        row = __ffma2_rn(w1[1], make_float2(r1, r1), row);
+                        row = __ffma2_rn(w1[2], make_float2(r2, r2), row);
+                        row = __ffma2_rn(w1[3], make_float2(r3, r3), row);
+                        accb = (bb == 0) ? __fmul2_rn(w2[0], row) : __ffma2_rn(w2[bb], row, accb);
+                    }
+                    // plane j: A's weight j (j < 4), B's weight j - 1 (j > 0)
+                    const float2 W = make_float2(j < 4 ? w3[j & 3].x : 0.f, j > 0 ? w3[(j + 3) & 3].y : 0.f);
+                    acc = (j == 0) ? __fmul2_rn(W, accb) : __ffma2_rn(W, accb, acc);
+                }
+                epi.store(idA, &acc.x, cur.lA);
+                epi.store(idB, &acc.y, cur.lB);
+            } else {  // deferred: slot in source-lane order (warp-aggregated), so drain lanes stay x-adjacent
+                const unsigned m = __activemask();
+                const unsigned lt = m & ((1u << (threadIdx.x & 31)) - 1u);
+                int base = 0;
+                if (lt == 0) base = atomicAdd(&qn, __popc(m));
+                base = __shfl_sync(m, base, __ffs(m) - 1);
+                queue[base + __popc(lt)] = (uint16_t)(p * SL_THREADS + threadIdx.x);
+            }
+            cur = nxt;
+        }
+    }
+    __syncthreads();
+    // drain: one deferred pair per thread (a pair's two points share the thread's column)
+    const int n = qn;
+    for (int i = threadIdx.x; i < n; i += SL_THREADS) {
+        const int e = queue[i];
+        const int kA = 2 * (e / SL_THREADS), ts = e % SL_THREADS;
+        const bool okB = kA + 1 < kmax;
+        const int xs = c.x0 + ts % SL_TX, ys = c.y0 + ts / SL_TX;
+        const int iA[3] = {xs, ys, c.z0 + kA + g.z0}, iB[3] = {xs, ys, c.z0 + kA + 1 + g.z0};
+        const uint32_t idA = ((uint32_t)(c.z0 + kA) * g.n2 + ys) * g.n1 + xs, idB = idA + plane;
+        PairIn<T, Epi> in;
+        load_pair<T, Epi>(d, epi, idA, idB, true, okB, in);
+        pair_any<Epi>(g, c, box, iA, iB, idA, idB, true, okB, in.dA, in.dB, in.lA, in.lB, epi);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Off-rank departure points (slabs; the paper's Algorithm 1, on x3 slabs).  A point whose
 // stencil planes floor(s3)-1 .. floor(s3)+2 leave the rank's planes + ghosts is served by the rank
 // owning plane floor(s3): its cell (q, t) travels there once per velocity (the plan), and every gather

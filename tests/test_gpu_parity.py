@@ -689,3 +689,109 @@ def test_call_graphs_match_eager(dr, monkeypatch):
     for a, b in zip(res["0"], res["1"]):
         assert torch.equal(a, b)
     assert prof["0"] == prof["1"]
+
+
+# N1 = N2 = 256 planes take the fused x1/x2 cluster transforms (plane2d.cuh) in fp32 contexts; n3 = 32
+# (96 plane items) is not a multiple of the resident cluster count, so clusters finish on different planes
+PLANE_GRIDS = [(256, 256, 8), (256, 256, 32)]
+
+
+@pytest.mark.parametrize("n", PLANE_GRIDS, ids=["x".join(map(str, g)) for g in PLANE_GRIDS])
+def test_plane2d_spectral_ops(dr, n, monkeypatch):
+    """(DR_PLANE2D=1, opt-in: measured slower than the per-axis passes) grad, div, beta A (H1, H2), (beta A)^-1 (isochoric and not), Leray through the fused plane
+    transforms against the oracle, with modes up to |k| = 80 along x1/x2 (and n3/3 along x3) and white
+    noise with Nyquist content; the profiler shows the fused kernels ran."""
+    monkeypatch.setenv("DR_PLANE2D", "1")
+    tol = TOL32_OP
+    f, f64 = prep(synth.blobs(5, n, kcut=80), False)
+    u, u64 = prep(synth.smooth_vec(6, n, kmax=min(n) // 3), False)
+    f, u = f.cuda(), u.cuda()
+    for reg in (1, 2):
+        ctx = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37))
+        ctx.profile_reset()
+        ctx.profile_enable(True)
+        if reg == 1:
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_GRAD, f)), O.grad(f64)) < tol
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_DIV, u)), O.div(u64)) < tol
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, u)), O.leray(u64)) < tol
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_REG, u)), O.reg_apply(u64, reg, 0.37)) < tol
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, False)) < tol
+        torch.cuda.synchronize()
+        p, _ = ctx.profile()
+        assert any(t.startswith("plane_fwd") for t in p) and any(t.startswith("plane_inv") for t in p), p
+        ci = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37, isochoric=True))
+        assert rel(np64(ci.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, True)) < tol
+    w = torch.from_numpy(np.random.default_rng(3).standard_normal((3,) + tuple(n)[::-1]))
+    w, w64 = prep(w, False)
+    ctx = dr.Context(dr.Config(n=n, nt=2, reg=1, beta=0.37))
+    assert rel(np64(ctx.op_spectral(dr.DR_OP_PRECOND, w.cuda())), O.precond(w64, 1, 0.37, False)) < tol
+    assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, w.cuda())), O.leray(w64)) < tol
+
+
+@pytest.mark.parametrize("iso", [False, True])
+def test_plane2d_matvec(dr, iso, monkeypatch):
+    """(DR_PLANE2D=1) One GN matvec through the fused plane transforms (non-isochoric: the three components batched,
+    b~ added in the inverse kernel's epilogue; isochoric: the KIND-6 path per component)."""
+    monkeypatch.setenv("DR_PLANE2D", "1")
+    n, nt = (256, 256, 8), 2
+    ctx = dr.Context(dr.Config(n=n, nt=nt, reg=2, beta=1e-2, isochoric=iso))
+    rT, rT64 = prep(synth.blobs(11, n, kcut=2), False)
+    rR, rR64 = prep(synth.blobs(12, n, kcut=2), False)
+    v, v64 = prep(synth.smooth_vec(9, n, kmax=2, divfree=iso, cells_per_step=1.5, nt=nt), False)
+    ctx.set_images(rT.cuda(), rR.cuda())
+    ctx.set_velocity(v.cuda())
+    prob = O.Problem(rho_T=rT64, rho_R=rR64, nt=nt, reg=2, beta=1e-2, iso=iso)
+    vt, vt64 = prep(synth.smooth_vec(21, n, kmax=2, divfree=iso), False)
+    check_matvec(dr, ctx, prob, v64, vt, vt64, False, iso)
+
+
+def test_plane2d_close_to_axis_passes(dr, monkeypatch):
+    """The fused plane transforms against the per-axis passes (DR_PLANE2D=0) on the same inputs: the
+    same transforms up to the rounding of the two-real-in-one split of columns 0 and N1/2."""
+    n = (256, 256, 16)
+    u = synth.round32(synth.smooth_vec(6, n, kmax=40)).contiguous().cuda()
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("DR_PLANE2D", mode)  # (the per-axis passes are the default)
+        ctx = dr.Context(dr.Config(n=n, nt=2, reg=2, beta=0.37))
+        out[mode] = [np64(ctx.op_spectral(k, u)) for k in (dr.DR_OP_REG, dr.DR_OP_PRECOND, dr.DR_OP_LERAY)]
+    for a, b in zip(out["0"], out["1"]):
+        assert rel(a, b) < 2e-6
+
+
+@pytest.mark.parametrize("ring", ["4", "8"])
+def test_ring_chunks_same_bits(dr, monkeypatch, ring):
+    """x1/x2 pass pairs run per plane chunk through the scratch ring (DR_RING) give the bits of the
+    whole-field passes: the same line transforms, only their order and the intermediate's address change
+    (beta A, (beta A)^-1 and a matvec with b~ added in the c2r)."""
+    name, n, nt, vgen, iso = CASES[1]
+    out = {}
+    for mode in ("0", ring):
+        monkeypatch.setenv("DR_RING", mode)
+        ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+        ctx.forward_solve()
+        vt = synth.round32(synth.smooth_vec(21, n, kmax=5)).contiguous().cuda()
+        out[mode] = [ctx.op_spectral(dr.DR_OP_REG, vt), ctx.op_spectral(dr.DR_OP_PRECOND, vt), ctx.hessian_matvec(vt)]
+    for a, b in zip(out["0"], out[ring]):
+        assert torch.equal(a, b)
+
+
+def test_pairs_gather_same_bits_as_pair_path(dr, monkeypatch):
+    """The shared-plane pair gather (k_sl_pairs, DR_PAIRS=1, opt-in: measured slower)
+    against the default pair path on every transport of the hot path: the zero x3 weights add exact
+    zeros and the non-zero terms are summed in the same order, deferred pairs use the same two-pointer
+    arithmetic, so the bits agree.  The stress case mixes deferred pairs and global-memory tiles."""
+    for case in (CASES[1], CASES[2], CASES[3]):
+        name, n, nt, vgen, iso = case
+        res = {}
+        for w in ("0", "1"):
+            monkeypatch.setenv("DR_PAIRS", w)
+            ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+            ctx.forward_solve()
+            ctx.adjoint_solve()
+            vt = synth.round32(synth.smooth_vec(21, n, kmax=5)).contiguous().cuda()
+            res[w] = [ctx.get_departure(1), ctx.get_departure(-1), ctx.get_field(dr.DR_FIELD_MULTIPLIER),
+                      ctx.get_field(dr.DR_FIELD_STATE, nt), ctx.get_field(dr.DR_FIELD_ADJOINT, 0),
+                      ctx.hessian_matvec(vt), ctx.get_field(dr.DR_FIELD_BTILDE)]
+        for a, b in zip(res["0"], res["1"]):
+            assert torch.equal(a, b), name
