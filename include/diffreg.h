@@ -38,7 +38,11 @@
  * ENVIRONMENT (read by dr_create / dr_create_dist; A/B switches, defaults are the measured best):
  * DR_OVERLAP=1 transforms beta A vt on a second stream concurrently with the transport sweeps
  * (measured slower, off); DR_TMA_MIDDLE=0 replaces the tensor-map TMA fp32 x3 middle pass by the
- * one-tile-per-CTA pass.  Results are bit-identical either way.
+ * one-tile-per-CTA pass; DR_PEER_GHOSTS=1 (slabs) fuses the ghost exchange into the producing gathers
+ * (dr_peer_export).  Opt-in experiments (measured slower on one B200): DR_PAIRS=1
+ * (shared-plane pair gathers), DR_WINDOW=1 (sliding-window gathers), DR_PLANE2D=1 (x1/x2 plane
+ * transforms through cluster shared memory), DR_RING=P (plane chunks through an L2 scratch ring).
+ * Results are bit-identical either way (DR_PLANE2D: within rounding).
  *
  * OWNERSHIP.  The caller owns every input, output and the workspace.  Inputs are only read;
  * images and the velocity are copied into the workspace (retained).  Outputs are fully
@@ -152,6 +156,26 @@ size_t dr_workspace_bytes_dist(const dr_config* cfg, int nranks);
  * rules as dr_create. */
 dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, size_t workspace_bytes,
                          void* stream, dr_ctx** out);
+
+/* Fused ghost exchange (SURVEY §8(e) "fuse the collectives"; the ghost layers of P:L314 / Alg. 1
+ * P:L326-337).  With DR_PEER_GHOSTS=1 in the environment at dr_create_dist (P > 1), every
+ * semi-Lagrangian gather whose output is the next gather's source (state, adjoint, incremental
+ * state / adjoint, deformation steps) also stores the slab's boundary planes straight into the x3
+ * neighbours' ghost planes of the same workspace slot -- the transfer rides in the gather's epilogue
+ * instead of a send/recv before the next gather, which then only waits for its two neighbours (a
+ * stream-ordered barrier; host events for loopback ranks, an epoch flag in peer memory for one
+ * process per GPU).  Ghosts of fields produced by other kernels are still exchanged with send/recv.
+ * Results are bit-identical to the send/recv path and to one rank.  Loopback communicators map the
+ * other ranks' workspaces directly.  NCCL communicators need the neighbours' workspaces mapped:
+ *   dr_peer_export  -- this context's CUDA IPC handle (64 bytes, of the allocation holding the
+ *                      workspace) and the workspace's byte offset in that allocation;
+ *   dr_peer_import  -- all ranks' handles [nranks][64] and offsets [nranks] (gathered by the caller,
+ *                      e.g. torch.distributed.all_gather_object); opens the two neighbours'.
+ * Collective (import).  Errors: DR_ERR_ARG (NULL, or not an NCCL context for import), DR_ERR_CUDA
+ * (IPC failure: e.g. peers on different nodes or without peer access).  Until imported, an NCCL
+ * context keeps the send/recv exchange. */
+dr_status dr_peer_export(dr_ctx* ctx, uint8_t handle[64], uint64_t* offset);
+dr_status dr_peer_import(dr_ctx* ctx, const uint8_t* handles, const uint64_t* offsets);
 
 
 /* Template rho_T and reference rho_R images (scalar fields).  Copied.  Invalidates the

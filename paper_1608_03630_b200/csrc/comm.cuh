@@ -41,7 +41,36 @@ struct Comm {
     virtual void group(const std::vector<P2P>& ops, cudaStream_t s) = 0;
     virtual std::string check() { return ""; }  // asynchronous error, empty if none
     virtual bool capturable() const { return false; }  // group() may be recorded into a CUDA graph
+    // Peer memory (fused ghost exchange, EpiPeer): rank q's workspace mapped in this process, or null.
+    virtual char* peer_ws(int) { return nullptr; }
+    virtual void set_ws(char*) {}
+    // Stream-ordered neighbour barrier: work issued on s after peer_sync starts only when both x3
+    // neighbours (rank +- 1, periodic) have issued everything before their matching peer_sync -- i.e.
+    // their peer stores into this rank's ghosts are complete, and their reads of earlier fields are done.
+    // pflags: this rank's flag words in its workspace (NCCL backend).
+    virtual void peer_sync(cudaStream_t, uint64_t*) {}
 };
+
+// Flag protocol of peer_sync for one process per GPU: each rank keeps an epoch counter and two flag
+// words (written by its lower / upper neighbour) in its own workspace; one thread bumps the epoch,
+// publishes it into both neighbours' flags (release at system scope, after a system fence that orders
+// this rank's preceding peer stores) and waits until both of its own flags reach it (acquire).  The
+// epoch lives in device memory, so a CUDA graph that captured the kernel stays correct on replay.
+// pf: [0] epoch, [1] flag from the lower neighbour, [2] flag from the upper neighbour.
+__global__ void k_peer_sync(uint64_t* pf, uint64_t* dn_from_up, uint64_t* up_from_dn) {
+    if (threadIdx.x != 0) return;
+    const uint64_t e = pf[0] + 1;
+    pf[0] = e;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dn_from_up), "l"(e) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(up_from_dn), "l"(e) : "memory");
+    for (int w = 1; w <= 2; ++w) {
+        uint64_t v = 0;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(pf + w) : "memory");
+        } while (v < e);
+    }
+}
 
 // ----------------------------------------------------------------------------------------------- NCCL
 typedef struct ncclComm* ncclComm_t;
@@ -113,6 +142,7 @@ struct NcclComm : Comm {
         nccl_ck(A.CommInitRank(&comm, n, id, r), "ncclCommInitRank");
     }
     ~NcclComm() override {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
         if (comm) NcclApi::get().CommDestroy(comm);
     }
     void group(const std::vector<P2P>& ops, cudaStream_t s) override {
@@ -126,6 +156,18 @@ struct NcclComm : Comm {
         nccl_ck(A.GroupEnd(), "ncclGroupEnd");
     }
     bool capturable() const override { return true; }  // NCCL kernels under stream capture
+    // CUDA IPC mappings of the neighbours' workspaces (dr_peer_import); index = rank, null if unmapped
+    std::vector<char*> peers;
+    std::vector<void*> opened;
+    char* peer_ws(int q) override { return q >= 0 && q < (int)peers.size() ? peers[q] : nullptr; }
+    void peer_sync(cudaStream_t s, uint64_t* pf) override {
+        const int dn = (rank + size - 1) % size, up = (rank + 1) % size;
+        // my flag words sit at the same workspace offset in every rank
+        auto far = [&](int q, int w) {
+            return reinterpret_cast<uint64_t*>(peers[q] + ((char*)(pf + w) - peers[rank]));
+        };
+        k_peer_sync<<<1, 32, 0, s>>>(pf, far(dn, 2), far(up, 1));
+    }
     std::string check() override {
         int e = 0;
         NcclApi& A = NcclApi::get();
@@ -136,7 +178,7 @@ struct NcclComm : Comm {
 
 // ------------------------------------------------------------------------------------------ loopback
 struct Hub {
-    explicit Hub(int n) : size(n), posts(n), done(n), ready(n), fin(n) {
+    explicit Hub(int n) : size(n), posts(n), done(n), ready(n), fin(n), ws(n, nullptr) {
         for (int i = 0; i < n; ++i) {
             cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&fin[i], cudaEventDisableTiming);
@@ -167,6 +209,7 @@ struct Hub {
     std::vector<std::vector<P2P>> posts;
     std::vector<int> done;
     std::vector<cudaEvent_t> ready, fin;
+    std::vector<char*> ws;  // each rank's workspace (peer stores of the fused ghost exchange)
 };
 
 struct LoopbackComm : Comm {
@@ -211,6 +254,19 @@ struct LoopbackComm : Comm {
         for (int q = 0; q < size; ++q)
             if (q != rank) cudaStreamWaitEvent(s, H.fin[q], 0);
         H.barrier();  // posts may be overwritten by the next group
+    }
+    char* peer_ws(int q) override { return hub->ws[q]; }
+    void set_ws(char* w) override { hub->ws[rank] = w; }
+    // every rank records the point its stream has reached; each waits for its neighbours' (all ranks
+    // here: the host barrier is global anyway) -- events only, no kernel waits on another rank's kernel
+    void peer_sync(cudaStream_t s, uint64_t*) override {
+        Hub& H = *hub;
+        if (cudaEventRecord(H.ready[rank], s) != cudaSuccess) throw std::runtime_error("loopback: event record");
+        H.barrier();
+        const int dn = (rank + size - 1) % size, up = (rank + 1) % size;
+        cudaStreamWaitEvent(s, H.ready[dn], 0);
+        if (up != dn) cudaStreamWaitEvent(s, H.ready[up], 0);
+        H.barrier();  // the events may be re-recorded by the next sync
     }
 };
 

@@ -113,7 +113,7 @@ struct Layout {
     int64_t rcap = 0;
     size_t rem = 0;
     size_t kry, sN, bN, sc, rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
-        plan_m, plan_t, maxext, red, twx, twy, twz, twxd, twyd, twzd, total;
+        plan_m, plan_t, maxext, red, pflags, twx, twy, twz, twxd, twyd, twzd, total;
 };
 
 Layout layout(const dr_config* c, int nranks = 1) {
@@ -171,6 +171,7 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.plan_t = take(pb);
     L.maxext = take(16 * sizeof(int));
     L.red = take(4096 * sizeof(double));  // reduction partials + per-rank gather slots
+    L.pflags = take(256);                 // peer_sync epoch + neighbour flags (fused ghost exchange)
     L.twx = take((size_t)g.n1 * 2 * es);
     L.twy = take((size_t)g.n2 * 2 * es);
     L.twz = take((size_t)g.n3g * 2 * es);
@@ -203,6 +204,9 @@ struct dr_ctx {
     bool pairs = false;                       // DR_PAIRS=1: x3-adjacent shared-plane pair gathers (sl.cuh k_sl_pairs)
     bool plane2d = false;                     // DR_PLANE2D=1: fused x1/x2 cluster plane transforms (plane2d.cuh)
     int ring = 0;                             // DR_RING=P: x1/x2 pass pairs per P planes through an L2-resident scratch
+    bool peer_ghosts = false;                 // DR_PEER_GHOSTS=1 (slabs): gathers store boundary planes into the
+                                              // neighbours' ghosts (EpiPeer); consumers peer_sync instead of exchanging
+    const void* last_peer_out = nullptr;      // the field whose ghosts the last peer-storing gather filled
     bool tma_middle = true;                   // DR_TMA_MIDDLE=0 at dr_create: the unstaged fp32 middle pass
     bool graphs = true;                       // DR_GRAPHS=0 disables the CUDA-graph PCG iteration
     int chunk = 0;                            // DR_CHUNK=P: x1/x2 pass pairs run per P planes (L2 reuse)
@@ -416,8 +420,26 @@ struct Impl {
     }
     // ghost planes of a ghosted scalar field (interior pointer f): my top zg planes go to rank + 1 (its
     // lower ghosts), my bottom zgh planes to rank - 1 (its upper ghosts); periodic in rank.
+    // fused ghost exchange: every rank's peer-storing gathers run in the same order, so all ranks agree
+    // on whether a field's ghosts were filled by its producer (then only the neighbour barrier remains)
+    bool peer_on() const {
+        if (!c.dist() || !c.peer_ghosts) return false;
+        const int P = c.nranks;
+        return c.comm->peer_ws((c.rank + 1) % P) && c.comm->peer_ws((c.rank + P - 1) % P);
+    }
+    void peer_sync() {
+        PB("peer_sync");
+        c.comm->peer_sync(s, c.at<uint64_t>(c.L.pflags));
+        PE("peer_sync");
+    }
     void ghosts(T* f) {
         if (!c.dist()) return;
+        if (f == c.last_peer_out) {  // the producing gather already stored them (EpiPeer)
+            c.last_peer_out = nullptr;
+            peer_sync();
+            return;
+        }
+        c.last_peer_out = nullptr;
         const int P = c.nranks, up = (c.rank + 1) % P, dn = (c.rank + P - 1) % P;
         const size_t pl = plane() * sizeof(T);
         std::vector<P2P> ops = {
@@ -1075,19 +1097,40 @@ struct Impl {
         exchange(ops);
     }
 
-    // gather sources are ghosted fields: the kernel indexes x3 from the slot base (zg planes below)
+    // gather sources are ghosted fields: the kernel indexes x3 from the slot base (zg planes below).
+    // pout: the ghosted output slot when the next gather reads it -- with the fused ghost exchange the
+    // epilogue also stores the boundary planes into the neighbours' ghosts (EpiPeer).
     template <int NC, class Epi>
-    void gather(const char* tag, Src<T, NC> src, const T* d, const int* plan_buf, Epi epi) {
+    void gather(const char* tag, Src<T, NC> src, const T* d, const int* plan_buf, Epi epi, T* pout = nullptr) {
         for (int cc = 0; cc < NC; ++cc) {
             ghosts(const_cast<T*>(src.p[cc]));
             src.p[cc] -= (size_t)g.zg * plane();
         }
+        if (pout && peer_on()) {
+            const int P = c.nranks, up = (c.rank + 1) % P, dn = (c.rank + P - 1) % P;
+            const size_t off = (size_t)((char*)pout - c.ws);
+            const int64_t pl = (int64_t)plane();
+            EpiPeer<T, Epi> pe{epi, reinterpret_cast<T*>(c.comm->peer_ws(dn) + off) + g.n3 * pl,
+                               reinterpret_cast<T*>(c.comm->peer_ws(up) + off) - g.n3 * pl, (uint32_t)(g.zgh * pl),
+                               (uint32_t)((g.n3 - g.zg) * pl)};
+            launch_gather<NC>(tag, src, d, plan_buf, pe);
+            c.last_peer_out = pout;
+            return;
+        }
+        launch_gather<NC>(tag, src, d, plan_buf, epi);
+    }
+    template <class Epi>
+    struct IsPeer : std::false_type {};
+    template <class E>
+    struct IsPeer<EpiPeer<T, E>> : std::true_type {};
+    template <int NC, class Epi>
+    void launch_gather(const char* tag, const Src<T, NC>& src, const T* d, const int* plan_buf, const Epi& epi) {
         const int f = field_of(plan_buf);
         const bool remote = c.dist() && c.rp[f].any;
         if (remote) remote_serve<NC>(f, src);
         const Disp<T> dp{{d, d + g.M, d + 2 * g.M}};
         const int nt = (int)n_tiles(g);  // one CTA per tile
-        if constexpr (std::is_same<T, float>::value && NC == 1) {
+        if constexpr (std::is_same<T, float>::value && NC == 1 && !IsPeer<Epi>::value) {
             if (c.window) {  // sliding-window gather (sl.cuh k_sl_window)
                 constexpr size_t sm = win_box_bytes();
                 auto k = k_sl_window<Epi>;
@@ -1127,8 +1170,8 @@ struct Impl {
     int* plan_m() { return c.at<int>(c.L.plan_m); }
     int* plan_t() { return c.at<int>(c.L.plan_t); }
 
-    void gather_scalar_p(T* f, T* out) {
-        gather<1>("sl_state", Src<T, 1>{{f}}, dplus(), plan_p(), EpiStore<T>{out});
+    void gather_scalar_p(T* f, T* out, bool next_gathered = false) {
+        gather<1>("sl_state", Src<T, 1>{{f}}, dplus(), plan_p(), EpiStore<T>{out}, next_gathered ? out : nullptr);
     }
 
     // -------------------------------------------------------------------- API steps
@@ -1164,7 +1207,7 @@ struct Impl {
         }
     }
     void forward_solve() {
-        for (int j = 0; j < c.cfg.nt; ++j) gather_scalar_p(rho(j), rho(j + 1));
+        for (int j = 0; j < c.cfg.nt; ++j) gather_scalar_p(rho(j), rho(j + 1), j + 1 < c.cfg.nt);
         for (int j = 0; j <= c.cfg.nt; ++j) grad(rho(j), G3(j));
     }
 
@@ -1174,7 +1217,8 @@ struct Impl {
         k_sub<T><<<grid_1d(g.M), 256, 0, s>>>(g.M, rhoR(), rho(nt), lam(nt));
         PE("sub");
         for (int k = nt; k >= 1; --k)
-            gather<1>("sl_adjoint", Src<T, 1>{{lam(k)}}, dminus(), plan_m(), EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)});
+            gather<1>("sl_adjoint", Src<T, 1>{{lam(k)}}, dminus(), plan_m(), EpiAdjoint<T>{lam(k - 1), mult_or_null(), T(1)},
+                      k > 1 ? lam(k - 1) : nullptr);
     }
 
     // out = beta A u + P b (P = Leray when isochoric, else I): the tail of Eq. 5e and of Eq. 4
@@ -1473,7 +1517,7 @@ struct Impl {
                 const bool last = (j == nt - 1);
                 T* out = last ? u.c[a] : w[(j + 1) & 1];
                 gather<1>("sl_deform", Src<T, 1>{{w[j & 1]}}, dplus(), plan_p(),
-                          EpiAddScaled<T>{out, vc(a), last ? T(-0.5) * dtt : -dtt});
+                          EpiAddScaled<T>{out, vc(a), last ? T(-0.5) * dtt : -dtt}, last ? nullptr : out);
             }
         }
     }
@@ -1650,9 +1694,9 @@ struct Impl {
             if (last && !newton()) {  // GN: the last step also writes b~'s k = nt term (EpiIncState WB)
                 EpiIncState<T, true> eb{e.out, e.vt0, e.vt1, e.vt2, e.G0, e.G1, e.G2, e.c,
                                         bt(), bt() + g.M, bt() + 2 * g.M, T(0.5) * dtt * T(-1)};
-                gather<1>("sl_inc_state_b", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), eb);
+                gather<1>("sl_inc_state_b", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), eb, e.out);
             } else {
-                gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), e);
+                gather<1>("sl_inc_state", Src<T, 1>{{lt(j)}}, dplus(), plan_p(), e, e.out);
             }
         }
         if (newton()) newton_terms(vt);
@@ -1665,7 +1709,7 @@ struct Impl {
             if (k == nt && !newton()) {  // b~ already holds the k = nt term (sl_inc_state_b)
                 auto e = adjoint_epi<2>(k, Gk, wk, dtt);
                 e.scale = T(-1);
-                gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+                gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e, k > 1 ? e.out : nullptr);
             } else if (k == nt) {
                 auto e = adjoint_epi<1>(k, Gk, wk, dtt);
                 e.scale = T(-1);
@@ -1673,12 +1717,14 @@ struct Impl {
                 const T* Gn = G(nt);
                 e.H0 = Gn; e.H1 = Gn + g.M; e.H2 = Gn + 2 * g.M;
                 e.wn = T(0.5) * dtt;
-                gather<2>("sl_inc_adjoint_n1", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt));
+                gather<2>("sl_inc_adjoint_n1", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt),
+                          k > 1 ? e.out : nullptr);
             } else {
                 auto e = adjoint_epi<2>(k, Gk, wk, dtt);
                 e.scale = T(1);
-                if (newton()) gather<2>("sl_inc_adjoint_n2", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt));
-                else gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e);
+                if (newton()) gather<2>("sl_inc_adjoint_n2", Src<T, 2>{{src, sN(k)}}, dminus(), plan_m(), to_newton(e, k, dtt),
+                                        k > 1 ? e.out : nullptr);
+                else gather<1>("sl_inc_adjoint_q2", Src<T, 1>{{src}}, dminus(), plan_m(), e, k > 1 ? e.out : nullptr);
             }
         }
         if (newton()) axpby(1.0, bN(), 1.0, bt());  // b~ += int lam grad rho~ dt
@@ -1927,6 +1973,50 @@ dr_status dr_comm_create_nccl(const uint8_t uid[128], int rank, int nranks, dr_c
     });
 }
 
+dr_status dr_peer_export(dr_ctx* c, uint8_t handle[64], uint64_t* offset) {
+    if (!c || !handle || !offset) return DR_ERR_ARG;
+    return run(c, [&] {
+        static const auto range = [] {
+            cudaDriverEntryPointQueryResult q;
+            void* fn = nullptr;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess) {
+                cudaGetLastError();
+                fn = nullptr;
+            }
+            return reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(fn);
+        }();
+        if (!range) fail(DR_ERR_CUDA, "cuMemGetAddressRange unavailable");
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (range(&base, &size, (CUdeviceptr)c->ws) != CUDA_SUCCESS) fail(DR_ERR_CUDA, "cuMemGetAddressRange failed");
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, (void*)base));
+        static_assert(sizeof(h) == 64, "IPC handle size");
+        std::memcpy(handle, &h, 64);
+        *offset = (uint64_t)((CUdeviceptr)c->ws - base);
+    });
+}
+
+dr_status dr_peer_import(dr_ctx* c, const uint8_t* handles, const uint64_t* offsets) {
+    if (!c || !handles || !offsets) return DR_ERR_ARG;
+    auto* nc = dynamic_cast<NcclComm*>(c->comm);
+    if (!nc) return DR_ERR_ARG;
+    return run(c, [&] {
+        const int P = nc->size, r = nc->rank;
+        nc->peers.assign(P, nullptr);
+        nc->peers[r] = c->ws;
+        for (int q : {(r + P - 1) % P, (r + 1) % P}) {
+            if (q == r || nc->peers[q]) continue;
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handles + (size_t)q * 64, 64);
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            nc->opened.push_back(p);
+            nc->peers[q] = static_cast<char*>(p) + offsets[q];
+        }
+    });
+}
+
 dr_status dr_hub_create(int nranks, dr_hub** out) {
     if (!out || nranks < 1) return DR_ERR_ARG;
     auto* h = new dr_hub();
@@ -2061,6 +2151,15 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
         c->plane2d = p2 && p2[0] == '1';
         const char* rg = getenv("DR_RING");
         c->ring = rg ? atoi(rg) : 0;
+        const char* pg = getenv("DR_PEER_GHOSTS");
+        c->peer_ghosts = pg && pg[0] == '1' && nranks > 1;
+    }
+    if (c->comm) c->comm->set_ws(c->ws);
+    if (cudaMemsetAsync(c->ws + c->L.pflags, 0, 256, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        if (c->own_ws) cudaFree(c->ws);
+        delete c;
+        return DR_ERR_CUDA;
     }
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
@@ -2096,6 +2195,7 @@ dr_status dr_destroy(dr_ctx* c) {
         cudaStreamDestroy(c->hi);
     }
     if (c->ev_hi) cudaEventDestroy(c->ev_hi);
+    if (c->comm) c->comm->set_ws(nullptr);
     if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
     for (auto& e : c->call_graphs) destroy_graph(e);
     for (cudaEvent_t e : c->graph_events) cudaEventDestroy(e);

@@ -648,13 +648,17 @@ __device__ __forceinline__ ColAcc<T, SPLIT> col_acc(Cx<T>* a, const ColGeom& c, 
 
 // CTA shape of a column pass: XC columns (one 128-byte segment: 16 complex64 / 8 complex128) x OL
 // transverse lines, TPL threads per line, capped so NC components of the CTA's lines fit in ~96 KB.
-template <int L, typename T, int NC = 1>
+// MAXNT > 0 caps the CTA at MAXNT threads by narrowing XC (the fp64 x3 middle pass at L >= 512: 32
+// threads per line x 8 columns made 256-thread CTAs of ~200 registers, one per SM -- 8 warps, latency
+// bound at 2 TB/s; 4 columns x 32 threads keep 2-3 CTAs per SM).
+template <int L, typename T, int NC = 1, int MAXNT = 0>
 struct ColCfg {
     static constexpr int ES = (int)sizeof(Cx<T>);
     static constexpr int TPL = Tpl<L, T>::V;
     static constexpr int LPB = (L + L / 16 + 1 + WaveLanes<T>::V) * ES;  // bytes per line (bound, for sizing)
-    static constexpr int XC0 = 128 / ES;
-    static constexpr int XC = (NC * XC0 * LPB <= 96 * 1024) ? XC0 : (NC * (XC0 / 2) * LPB <= 96 * 1024) ? XC0 / 2 : XC0 / 4;
+    static constexpr int XCN = (MAXNT > 0 && MAXNT / TPL >= 1 && MAXNT / TPL < 128 / ES) ? MAXNT / TPL : 128 / ES;
+    static constexpr int XC0 = XCN;
+    static constexpr int XC = (NC * XC0 * LPB <= 96 * 1024) ? XC0 : (NC * (XC0 / 2) * LPB <= 96 * 1024) ? (XC0 / 2 > 0 ? XC0 / 2 : 1) : (XC0 / 4 > 0 ? XC0 / 4 : 1);
     static constexpr int OLT = (XC * TPL >= CtaThreads<T>::V) ? 1 : CtaThreads<T>::V / (XC * TPL);
     static constexpr int MAXL = (96 * 1024) / (NC * LPB);
     static constexpr int OLS = (MAXL / XC) >= 1 ? MAXL / XC : 1;
@@ -879,7 +883,7 @@ template <typename Ti, typename To, int L, int KIND>
 struct MiddlePass {
     using T = Ti;
     static constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
-    using CC = ColCfg<L, T, NCI>;
+    using CC = ColCfg<L, T, NCI, (sizeof(T) == 8 && L >= 512) ? 128 : 0>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
     static constexpr int LPO = ColLP<L, To, XC>::V;  // stride of the To lines of the inverse
     static constexpr int TPLO = Tpl<L, To>::V;  // threads per inverse line (fp32: fewer than fp64)

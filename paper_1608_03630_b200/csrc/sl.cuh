@@ -16,7 +16,15 @@
 
 namespace dr {
 
-constexpr int SL_TX = 32, SL_TY = 8, SL_TZ = 8, SL_THREADS = SL_TX * SL_TY;
+// A warp is one x1 row of the tile (lane = x1).  SL_TX <= 32 columns per tile: with 31 (DR_TX=31) the
+// 32 lanes' stencil columns never span 33 words, so the two end lanes of a warp whose departure floor
+// steps up along x1 cannot collide in one bank (tools/bank_sim.py: 1.30 -> 1.05 wavefronts per LDS);
+// lane 31 idles.
+#ifndef DR_TX
+#define DR_TX 32
+#endif
+constexpr int SL_TX = DR_TX, SL_LANES = 32, SL_TY = 8, SL_TZ = 8, SL_THREADS = SL_LANES * SL_TY;
+static_assert(SL_TX <= SL_LANES, "tile width");
 constexpr int PLAN_INTS = 8;  // ox, oy, oz, ex, ey, ez, pad, pad
 
 // Lagrange weights for nodes -1, 0, 1, 2 at t in [0, 1) (reading A6)
@@ -110,9 +118,9 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restr
     __syncthreads();
     int x0, y0, z0;
     tile_coords(g, blockIdx.x, x0, y0, z0);
-    const int x = x0 + (threadIdx.x % SL_TX), y = y0 + threadIdx.x / SL_TX;
+    const int x = x0 + (threadIdx.x % SL_LANES), y = y0 + threadIdx.x / SL_LANES;
     int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
-    if (x < g.n1 && y < g.n2) {
+    if ((int)(threadIdx.x % SL_LANES) < SL_TX && x < g.n1 && y < g.n2) {
         for (int k = 0; k < SL_TZ; ++k) {
             const int z = z0 + k;
             if (z >= g.n3) break;
@@ -168,7 +176,10 @@ struct EpiStore {  // state solve: rho_{j+1} = I[rho_j](X+)   (Eq. 7 with f = 0)
     T* out;
     using Late = NoLate;
     __device__ __forceinline__ Late late(uint32_t) const { return Late{}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late&) const { out[id] = val[0]; }
+    __device__ __forceinline__ T store(uint32_t id, const T* val, const Late&) const {
+        out[id] = val[0];
+        return val[0];
+    }
 };
 
 // Adjoint-like step: nu_{k-1} = scale * m * I[nu_k](X-)  (Eq. 7 with f = nu div v; D7).
@@ -223,7 +234,7 @@ struct EpiAdjoint {
         }
         return l;
     }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
+    __device__ __forceinline__ T store(uint32_t id, const T* val, const Late& l) const {
         const T mm = m ? scale * l.m : scale;
         T r = mm * val[0];
         if constexpr (NEWTON) r += hdt * (T(1) + dtt * l.Dx) * val[1] + hdt * l.sn;
@@ -241,6 +252,7 @@ struct EpiAdjoint {
             b1[id] = b[1] + wr * l.g[1];
             b2[id] = b[2] + wr * l.g[2];
         }
+        return r;
     }
 };
 
@@ -251,7 +263,11 @@ struct EpiAddScaled {  // out = I[w](X) + c f(x): the merged-source step of the 
     T c;
     struct Late { T f; };
     __device__ __forceinline__ Late late(uint32_t id) const { return Late{__ldg(f + id)}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const { out[id] = val[0] + c * l.f; }
+    __device__ __forceinline__ T store(uint32_t id, const T* val, const Late& l) const {
+        const T r = val[0] + c * l.f;
+        out[id] = r;
+        return r;
+    }
 };
 
 // WB (last step, j + 1 = nt): also starts the b~ quadrature with its k = nt term
@@ -270,7 +286,7 @@ struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+
     __device__ __forceinline__ Late late(uint32_t id) const {
         return Late{{__ldg(vt0 + id), __ldg(vt1 + id), __ldg(vt2 + id)}, {__ldg(G0 + id), __ldg(G1 + id), __ldg(G2 + id)}};
     }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
+    __device__ __forceinline__ T store(uint32_t id, const T* val, const Late& l) const {
         const T f = l.v[0] * l.g[0] + l.v[1] * l.g[1] + l.v[2] * l.g[2];
         const T r = val[0] - c * f;
         out[id] = r;
@@ -280,6 +296,7 @@ struct EpiIncState {  // Algorithm 2 with the merged gather: g_{j+1} = I[g_j](X+
             b1[id] = ln * l.g[1];
             b2[id] = ln * l.g[2];
         }
+        return r;
     }
 };
 
@@ -290,9 +307,11 @@ struct EpiMultiplier {  // m = 1 + dt/2 (Dbar + D + dt Dbar D), Dbar = I[div v](
     T dt;
     struct Late { T D; };
     __device__ __forceinline__ Late late(uint32_t id) const { return Late{__ldg(D + id)}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const {
+    __device__ __forceinline__ T store(uint32_t id, const T* val, const Late& l) const {
         const T Db = val[0];
-        m[id] = T(1) + T(0.5) * dt * (Db + l.D + dt * Db * l.D);
+        const T r = T(1) + T(0.5) * dt * (Db + l.D + dt * Db * l.D);
+        m[id] = r;
+        return r;
     }
 };
 
@@ -304,7 +323,33 @@ struct EpiDeparture1 {  // d_a = sigma dt/2 (v_a(x) + I[v_a](X*)) / h_a  (Eq. 6,
     T c;
     struct Late { T v; };
     __device__ __forceinline__ Late late(uint32_t id) const { return Late{__ldg(v + id)}; }
-    __device__ __forceinline__ void store(uint32_t id, const T* val, const Late& l) const { d[id] = c * (l.v + val[0]); }
+    __device__ __forceinline__ T store(uint32_t id, const T* val, const Late& l) const {
+        const T r = c * (l.v + val[0]);
+        d[id] = r;
+        return r;
+    }
+};
+
+// Fused ghost exchange (multi-GPU x3 slabs): the gather that produces a field which the
+// next gather reads also stores the slab's boundary planes straight into the x3 neighbours' ghost planes
+// of the same slot (peer memory: NVLink stores to a CUDA-IPC-mapped workspace with one process per GPU,
+// the other contexts' workspaces with loopback ranks).  Planes z < zgh go to the lower neighbour's upper
+// ghosts, planes z >= n3 - zg to the upper neighbour's lower ghosts; the consumer then only waits for its
+// neighbours (Impl::peer_sync) instead of exchanging ghost planes before its gather.
+template <typename T, class Epi>
+struct EpiPeer {
+    Epi e;
+    T* lo;              // lo[id] = lower neighbour's upper ghost of my voxel id (id < lo_end)
+    T* hi;              // hi[id] = upper neighbour's lower ghost of my voxel id (id >= hi_begin)
+    uint32_t lo_end, hi_begin;
+    using Late = typename Epi::Late;
+    __device__ __forceinline__ Late late(uint32_t id) const { return e.late(id); }
+    __device__ __forceinline__ T store(uint32_t id, const T* val, const Late& l) const {
+        const T r = e.store(id, val, l);
+        if (id < lo_end) lo[id] = r;
+        if (id >= hi_begin) hi[id] = r;
+        return r;
+    }
 };
 
 template <typename T, int NC>
@@ -552,6 +597,10 @@ template <typename T, bool N>
 struct EpiMinB<EpiAdjoint<T, 2, N>> {
     static constexpr int V = 3;
 };
+template <typename T, class Epi>
+struct EpiMinB<EpiPeer<T, Epi>> {
+    static constexpr int V = EpiMinB<Epi>::V;
+};
 template <typename T, int NC, class Epi>
 struct GatherMinB {
     static constexpr int V = (sizeof(T) == 4 && NC == 1) ? EpiMinB<Epi>::V : BoxGeom<T, NC>::MINB;
@@ -593,8 +642,8 @@ __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
     if (tile >= ntiles) return;
     const TileCtx<T, NC> c = tile_ctx<T, NC>(g, plan, tile);
     stage_box<T, NC>(g, src, c, box);
-    const int x = c.x0 + (threadIdx.x % SL_TX), y = c.y0 + threadIdx.x / SL_TX;
-    const bool xyok = x < g.n1 && y < g.n2;
+    const int x = c.x0 + (threadIdx.x % SL_LANES), y = c.y0 + threadIdx.x / SL_LANES;
+    const bool xyok = (int)(threadIdx.x % SL_LANES) < SL_TX && x < g.n1 && y < g.n2;
     const int kmax = min(SL_TZ, g.n3 - c.z0);
     const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
     const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
@@ -688,8 +737,8 @@ __global__ void __launch_bounds__(SL_THREADS, WIN_MINB)
     if (tile >= ntiles) return;
     const TileCtx<T, 1> c = tile_ctx<T, 1, WinGeom, true>(g, plan, tile);
     stage_box<T, 1, WinGeom>(g, src, c, box);
-    const int x = c.x0 + (threadIdx.x % SL_TX), y = c.y0 + threadIdx.x / SL_TX;
-    const bool xyok = x < g.n1 && y < g.n2;
+    const int x = c.x0 + (threadIdx.x % SL_LANES), y = c.y0 + threadIdx.x / SL_LANES;
+    const bool xyok = (int)(threadIdx.x % SL_LANES) < SL_TX && x < g.n1 && y < g.n2;
     const int kmax = min(SL_TZ, g.n3 - c.z0);
     const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
     const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
@@ -698,7 +747,7 @@ __global__ void __launch_bounds__(SL_THREADS, WIN_MINB)
         return;
     }
     // the column's displacements (idle lanes of a narrow grid read a valid column and store nothing)
-    const int xc = min(x, g.n1 - 1), yc = min(y, g.n2 - 1);
+    const int xc = min((int)(threadIdx.x % SL_LANES) < SL_TX ? x : c.x0, g.n1 - 1), yc = min(y, g.n2 - 1);
     const uint32_t idc = ((uint32_t)c.z0 * g.n2 + yc) * g.n1 + xc;
     bool ok = kmax == SL_TZ;
     float t[3][SL_TZ];
@@ -871,8 +920,8 @@ __global__ void __launch_bounds__(SL_THREADS, (EpiMinB<Epi>::V))
     if (tile >= ntiles) return;
     const TileCtx<T, 1> c = tile_ctx<T, 1>(g, plan, tile);
     stage_box<T, 1>(g, src, c, box);
-    const int x = c.x0 + (threadIdx.x % SL_TX), y = c.y0 + threadIdx.x / SL_TX;
-    const bool xyok = x < g.n1 && y < g.n2;
+    const int x = c.x0 + (threadIdx.x % SL_LANES), y = c.y0 + threadIdx.x / SL_LANES;
+    const bool xyok = (int)(threadIdx.x % SL_LANES) < SL_TX && x < g.n1 && y < g.n2;
     const int kmax = min(SL_TZ, g.n3 - c.z0);
     const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
     const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
@@ -950,7 +999,7 @@ __global__ void __launch_bounds__(SL_THREADS, (EpiMinB<Epi>::V))
         const int e = queue[i];
         const int kA = 2 * (e / SL_THREADS), ts = e % SL_THREADS;
         const bool okB = kA + 1 < kmax;
-        const int xs = c.x0 + ts % SL_TX, ys = c.y0 + ts / SL_TX;
+        const int xs = c.x0 + ts % SL_LANES, ys = c.y0 + ts / SL_LANES;
         const int iA[3] = {xs, ys, c.z0 + kA + g.z0}, iB[3] = {xs, ys, c.z0 + kA + 1 + g.z0};
         const uint32_t idA = ((uint32_t)(c.z0 + kA) * g.n2 + ys) * g.n1 + xs, idB = idA + plane;
         PairIn<T, Epi> in;

@@ -35,7 +35,8 @@ EXPORTS = ["dr_workspace_bytes", "dr_create", "dr_destroy", "dr_set_images", "dr
            "dr_get_field", "dr_profile_enable", "dr_profile_reset", "dr_profile_only", "dr_profile_count", "dr_profile_entry",
            "dr_nccl_get_unique_id", "dr_comm_create_nccl", "dr_hub_create", "dr_hub_destroy",
            "dr_comm_create_loopback", "dr_comm_destroy", "dr_slab", "dr_workspace_bytes_dist", "dr_create_dist",
-           "dr_gradient", "dr_objective", "dr_pcg", "dr_deformation", "dr_solve", "dr_comm_selftest"]
+           "dr_gradient", "dr_objective", "dr_pcg", "dr_deformation", "dr_solve", "dr_comm_selftest",
+           "dr_peer_export", "dr_peer_import"]
 
 
 class dr_config(ctypes.Structure):
@@ -103,6 +104,8 @@ def lib():
                            ("dr_pcg", [vp, vp, vp, ctypes.c_double, i32, ctypes.POINTER(i32),
                                        ctypes.POINTER(ctypes.c_double)]),
                            ("dr_gradient", [vp, vp]),
+                           ("dr_peer_export", [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64)]),
+                           ("dr_peer_import", [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64)]),
                            ("dr_objective", [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
                            ("dr_nccl_get_unique_id", [ctypes.c_char_p]),
                            ("dr_comm_create_nccl", [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]),
@@ -274,6 +277,19 @@ class Context:
     def _check(self, st):
         if st != DR_OK:
             raise DiffRegError(st, lib().dr_last_error(self.h).decode())
+
+    # fused ghost exchange (DR_PEER_GHOSTS=1, include/diffreg.h dr_peer_export): the CUDA IPC mapping of
+    # the neighbours' workspaces for one process per GPU; loopback ranks need nothing
+    def peer_export(self) -> tuple[bytes, int]:
+        buf = ctypes.create_string_buffer(64)
+        off = ctypes.c_uint64()
+        self._check(lib().dr_peer_export(self.h, buf, ctypes.byref(off)))
+        return buf.raw, off.value
+
+    def peer_import(self, handles: list[bytes], offsets: list[int]):
+        assert len(handles) == len(offsets) == self.nranks and all(len(h) == 64 for h in handles)
+        arr = (ctypes.c_uint64 * self.nranks)(*offsets)
+        self._check(lib().dr_peer_import(self.h, b"".join(handles), arr))
 
     def close(self):
         if getattr(self, "h", None):

@@ -45,3 +45,14 @@ def slab_of(x: torch.Tensor, cfg: Config, nranks: int, rank: int) -> torch.Tenso
 def assemble(slabs: list[torch.Tensor]) -> torch.Tensor:
     """Inverse of slab_of over all ranks (concatenation along x3)."""
     return torch.cat(slabs, dim=slabs[0].dim() - 3)
+
+
+def map_peers(ctx) -> None:
+    """Fused ghost exchange across processes (DR_PEER_GHOSTS=1): every rank exports its workspace's
+    CUDA IPC handle, the handles are all-gathered over the default torch.distributed group, and each
+    rank maps its two x3 neighbours' workspaces (dr_peer_import).  Collective."""
+    import torch.distributed as dist
+    mine = ctx.peer_export()
+    allh = [None] * ctx.nranks
+    dist.all_gather_object(allh, mine)
+    ctx.peer_import([h for h, _ in allh], [o for _, o in allh])
