@@ -360,6 +360,8 @@ def run_ours(args, ws, rank, local):
     # the library's NCCL communicator is bootstrapped from a unique id broadcast over torch.distributed
     comm = dr.dist.make_comm(rank, ws) if ws > 1 else None
     ctx = dr.Context(cfg, device=dev, comm=comm)
+    if ws > 1 and os.environ.get("DR_PEER_GHOSTS") == "1":  # fused ghosts / transposes over peer memory
+        dr.dist.map_peers(ctx)
     rT, rR, v, vts = make_inputs(n, dev)
     if ws > 1:
         sl = lambda x: dr.dist.slab_of(x, cfg, ws, rank)  # noqa: E731

@@ -165,12 +165,16 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
  * instead of a send/recv before the next gather, which then only waits for its two neighbours (a
  * stream-ordered barrier; host events for loopback ranks, an epoch flag in peer memory for one
  * process per GPU).  Ghosts of fields produced by other kernels are still exchanged with send/recv.
+ * The same switch fuses the all-to-all transposes of the spectral operators with one output
+ * component: the forward x2 pass stores each rank's chunk straight into that rank's spectrum slot and
+ * the x3 middle pass stores its planes straight into the owning ranks' receive buffer (P <= 64), each
+ * between two all-rank stream barriers instead of a send/recv all-to-all.
  * Results are bit-identical to the send/recv path and to one rank.  Loopback communicators map the
  * other ranks' workspaces directly.  NCCL communicators need the neighbours' workspaces mapped:
  *   dr_peer_export  -- this context's CUDA IPC handle (64 bytes, of the allocation holding the
  *                      workspace) and the workspace's byte offset in that allocation;
  *   dr_peer_import  -- all ranks' handles [nranks][64] and offsets [nranks] (gathered by the caller,
- *                      e.g. torch.distributed.all_gather_object); opens the two neighbours'.
+ *                      e.g. torch.distributed.all_gather_object); opens every other rank's.
  * Collective (import).  Errors: DR_ERR_ARG (NULL, or not an NCCL context for import), DR_ERR_CUDA
  * (IPC failure: e.g. peers on different nodes or without peer access).  Until imported, an NCCL
  * context keeps the send/recv exchange. */

@@ -49,7 +49,29 @@ struct Comm {
     // their peer stores into this rank's ghosts are complete, and their reads of earlier fields are done.
     // pflags: this rank's flag words in its workspace (NCCL backend).
     virtual void peer_sync(cudaStream_t, uint64_t*) {}
+    // Stream-ordered barrier of all ranks (the fused all-to-all transposes): work after it starts only
+    // when every rank has issued everything before its matching call.  pws: device table of every rank's
+    // mapped workspace (NCCL backend), pf_off: byte offset of the flag words in a workspace.
+    virtual void peer_barrier_all(cudaStream_t, uint64_t*, char* const*, int64_t) {}
 };
+
+// pf[3]: epoch of the all-rank barrier; pf[8 + q]: flag written by rank q.
+__global__ void k_peer_sync_all(uint64_t* pf, char* const* pws, int64_t pf_off, int rank, int P) {
+    if (threadIdx.x != 0) return;
+    const uint64_t e = pf[3] + 1;
+    pf[3] = e;
+    __threadfence_system();
+    for (int q = 0; q < P; ++q) {
+        uint64_t* f = reinterpret_cast<uint64_t*>(pws[q] + pf_off) + 8 + rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+    }
+    for (int q = 0; q < P; ++q) {
+        uint64_t v = 0;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(pf + 8 + q) : "memory");
+        } while (v < e);
+    }
+}
 
 // Flag protocol of peer_sync for one process per GPU: each rank keeps an epoch counter and two flag
 // words (written by its lower / upper neighbour) in its own workspace; one thread bumps the epoch,
@@ -168,6 +190,9 @@ struct NcclComm : Comm {
         };
         k_peer_sync<<<1, 32, 0, s>>>(pf, far(dn, 2), far(up, 1));
     }
+    void peer_barrier_all(cudaStream_t s, uint64_t* pf, char* const* pws, int64_t pf_off) override {
+        k_peer_sync_all<<<1, 32, 0, s>>>(pf, pws, pf_off, rank, size);
+    }
     std::string check() override {
         int e = 0;
         NcclApi& A = NcclApi::get();
@@ -267,6 +292,14 @@ struct LoopbackComm : Comm {
         cudaStreamWaitEvent(s, H.ready[dn], 0);
         if (up != dn) cudaStreamWaitEvent(s, H.ready[up], 0);
         H.barrier();  // the events may be re-recorded by the next sync
+    }
+    void peer_barrier_all(cudaStream_t s, uint64_t*, char* const*, int64_t) override {
+        Hub& H = *hub;
+        if (cudaEventRecord(H.ready[rank], s) != cudaSuccess) throw std::runtime_error("loopback: event record");
+        H.barrier();
+        for (int q = 0; q < size; ++q)
+            if (q != rank) cudaStreamWaitEvent(s, H.ready[q], 0);
+        H.barrier();
     }
 };
 

@@ -171,7 +171,7 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.plan_t = take(pb);
     L.maxext = take(16 * sizeof(int));
     L.red = take(4096 * sizeof(double));  // reduction partials + per-rank gather slots
-    L.pflags = take(256);                 // peer_sync epoch + neighbour flags (fused ghost exchange)
+    L.pflags = take(2048);                // peer barriers: epochs + flags (bytes 0..1023), rank workspace table (1024..)
     L.twx = take((size_t)g.n1 * 2 * es);
     L.twy = take((size_t)g.n2 * 2 * es);
     L.twz = take((size_t)g.n3g * 2 * es);
@@ -207,6 +207,8 @@ struct dr_ctx {
     bool peer_ghosts = false;                 // DR_PEER_GHOSTS=1 (slabs): gathers store boundary planes into the
                                               // neighbours' ghosts (EpiPeer); consumers peer_sync instead of exchanging
     const void* last_peer_out = nullptr;      // the field whose ghosts the last peer-storing gather filled
+    bool peer_inv_fresh = false;              // the last middle pass stored its transpose chunks into the ranks' specF(3)
+    bool pws_ready = false;                   // the device table of mapped rank workspaces is filled
     bool tma_middle = true;                   // DR_TMA_MIDDLE=0 at dr_create: the unstaged fp32 middle pass
     bool graphs = true;                       // DR_GRAPHS=0 disables the CUDA-graph PCG iteration
     int chunk = 0;                            // DR_CHUNK=P: x1/x2 pass pairs run per P planes (L2 reuse)
@@ -431,6 +433,27 @@ struct Impl {
         PB("peer_sync");
         c.comm->peer_sync(s, c.at<uint64_t>(c.L.pflags));
         PE("peer_sync");
+    }
+    // fused all-to-all transposes: every rank's workspace mapped (loopback: all contexts; NCCL: all IPC
+    // handles imported), at most 64 ranks
+    bool peer_a2a_on() {
+        if (!c.dist() || !c.peer_ghosts || c.nranks > 64) return false;
+        for (int q = 0; q < c.nranks; ++q)
+            if (!c.comm->peer_ws(q)) return false;
+        if (!c.pws_ready) {  // the device table of rank workspaces, read by the peer-storing passes
+            std::vector<char*> h(c.nranks);
+            for (int q = 0; q < c.nranks; ++q) h[q] = c.comm->peer_ws(q);
+            CK(cudaMemcpyAsync(pws(), h.data(), h.size() * sizeof(char*), cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+            c.pws_ready = true;
+        }
+        return true;
+    }
+    char** pws() { return reinterpret_cast<char**>(c.ws + c.L.pflags + 1024); }
+    void peer_barrier_all() {
+        PB("peer_barrier");
+        c.comm->peer_barrier_all(s, c.at<uint64_t>(c.L.pflags), pws(), (int64_t)c.L.pflags);
+        PE("peer_barrier");
     }
     void ghosts(T* f) {
         if (!c.dist()) return;
@@ -750,6 +773,14 @@ struct Impl {
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
     }
+    template <typename Tc, int L>
+    void col_fft_fwd_peer(const Cx<Tc>* src, const PeerDst& pd) {
+        using PT = ColFftPass<Tc, L, -1, false, true, true>;
+        const ColGeom cg = spec_geom();
+        PT pt{cg, src, nullptr, twy_t<Tc>(), 0, nb(), 0, -1};
+        pt.pd = pd;
+        stream(sizeof(Tc) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32", pt, col_tiles<PT>(cg, g.n3), 1);
+    }
     void col_fft_inv(const Cx<T>* src, Cx<T>* dst, int nb_in, int nc = 1, int64_t cs = 0, int64_t csd = -1) {  // inverse along x2, in T
 #define CALL(LL) col_fft_L<T, LL, +1>(src, dst, twy(), nb_in, 0, nc, cs, csd)
         DR_SWITCH_COL(g.n2, CALL)
@@ -758,6 +789,25 @@ struct Impl {
 
     template <int L, int KIND, typename Tc>
     void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out, int comp, int nc, int64_t cs) {
+        if constexpr (MiddlePass<Tc, T, L, KIND>::NCO == 1) {
+            if (c.dist() && nc == 1 && peer_a2a_on()) {  // store the transpose chunks into the ranks' specF(3)
+                using PQ = MiddlePass<Tc, T, L, KIND, true>;
+                PQ pt;
+                pt.c = cg;
+                for (int i = 0; i < PQ::NCI; ++i) pt.in.p[i] = in[i];
+                pt.out.p[0] = out[0];
+                pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), comp};
+                pt.tw = twz_t<Tc>();
+                pt.two = twz();
+                pt.cs = cs;
+                const size_t chunk = (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<T>);
+                pt.pd = PeerDst{pws(), (int64_t)((char*)specF(3) - c.ws) + (int64_t)(c.rank * chunk), ilog2c(g.n3)};
+                peer_barrier_all();  // every rank finished reading its specF(3)
+                stream(sizeof(Tc) == 8 ? "col_middle_f64" : "col_middle_f32", pt, col_tiles<PQ>(cg, cg.n2), nc);
+                c.peer_inv_fresh = true;
+                return;
+            }
+        }
         using PT = MiddlePass<Tc, T, L, KIND>;
         PT pt;
         pt.c = cg;
@@ -794,6 +844,15 @@ struct Impl {
             return;
         }
         row_r2c<Tc>(f, specD_t<Tc>(6));
+        if (peer_a2a_on()) {  // the x2 pass stores each rank's chunk straight into its spectrum slot
+            const size_t chunk = (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<Tc>);
+            peer_barrier_all();  // every rank finished reading the slot (its previous middle pass)
+#define CALL(LL) col_fft_fwd_peer<Tc, LL>(specD_t<Tc>(6), PeerDst{pws(), (int64_t)((char*)specD_t<Tc>(slot) - c.ws) + (int64_t)(c.rank * chunk), ilog2c(nb())})
+            DR_SWITCH_COL(g.n2, CALL)
+#undef CALL
+            peer_barrier_all();  // every chunk arrived
+            return;
+        }
         col_fft_fwd<Tc>(specD_t<Tc>(6), specD_t<Tc>(7), nb());  // the split layout: one contiguous chunk per rank
         alltoall(specD_t<Tc>(7), specD_t<Tc>(slot), (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<Tc>));
     }
@@ -808,7 +867,12 @@ struct Impl {
             row_c2r(specF(slot), out, add);
             return;
         }
-        alltoall(specF(slot), specF(3), (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<T>));
+        if (c.peer_inv_fresh) {  // the middle pass stored the chunks into every rank's specF(3)
+            c.peer_inv_fresh = false;
+            peer_barrier_all();
+        } else {
+            alltoall(specF(slot), specF(3), (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<T>));
+        }
         col_fft_inv(specF(3), specF(4), nb());
         row_c2r(specF(4), out, add);
     }
@@ -2005,14 +2069,20 @@ dr_status dr_peer_import(dr_ctx* c, const uint8_t* handles, const uint64_t* offs
         const int P = nc->size, r = nc->rank;
         nc->peers.assign(P, nullptr);
         nc->peers[r] = c->ws;
-        for (int q : {(r + P - 1) % P, (r + 1) % P}) {
-            if (q == r || nc->peers[q]) continue;
+        for (int q = 0; q < P; ++q) {  // every rank: neighbours for the ghosts, all for the transposes
+            if (q == r) continue;
             cudaIpcMemHandle_t h;
             std::memcpy(&h, handles + (size_t)q * 64, 64);
             void* p = nullptr;
             CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
             nc->opened.push_back(p);
             nc->peers[q] = static_cast<char*>(p) + offsets[q];
+        }
+        if (P <= 64) {  // the device table of rank workspaces (filled here, outside any graph capture)
+            CK(cudaMemcpyAsync(c->ws + c->L.pflags + 1024, nc->peers.data(), P * sizeof(char*), cudaMemcpyHostToDevice,
+                               c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            c->pws_ready = true;
         }
     });
 }
@@ -2155,7 +2225,7 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
         c->peer_ghosts = pg && pg[0] == '1' && nranks > 1;
     }
     if (c->comm) c->comm->set_ws(c->ws);
-    if (cudaMemsetAsync(c->ws + c->L.pflags, 0, 256, c->stream) != cudaSuccess) {
+    if (cudaMemsetAsync(c->ws + c->L.pflags, 0, 2048, c->stream) != cudaSuccess) {
         cudaGetLastError();
         if (c->own_ws) cudaFree(c->ws);
         delete c;

@@ -646,6 +646,31 @@ __device__ __forceinline__ ColAcc<T, SPLIT> col_acc(Cx<T>* a, const ColGeom& c, 
     return r;
 }
 
+// Fused all-to-all transposes (multi-GPU x3 slabs, SURVEY §8(e) "FFT pass epilogues ... store straight
+// into peer buffers"): the last stage of the pass that produces a transpose's send data stores each
+// element straight into the receive buffer of the rank that owns it (peer memory), in the layout the
+// all-to-all would have delivered.  pws[q]: rank q's workspace as mapped here (a device array), boff:
+// byte offset of the receive buffer plus this rank's chunk.  Element p of the line goes to rank
+// q = p >> sh at pws[q] + boff + (ofs + (p & mk) * lo) elements.
+template <typename T>
+struct PeerAcc {
+    char* const* pws;
+    int64_t boff, ofs;
+    int64_t lo;
+    int sh, mk;
+    bool on;
+    __device__ __forceinline__ void st(int p, const Cx<T>& v) const {
+        if (!on) return;
+        reinterpret_cast<Cx<T>*>(pws[p >> sh] + boff)[ofs + (int64_t)(p & mk) * lo] = v;
+    }
+};
+struct PeerDst {  // host-filled description of a peer destination (nullptr pws: plain stores)
+    char* const* pws = nullptr;
+    int64_t boff = 0;
+    int sh = 0;
+};
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
 // CTA shape of a column pass: XC columns (one 128-byte segment: 16 complex64 / 8 complex128) x OL
 // transverse lines, TPL threads per line, capped so NC components of the CTA's lines fit in ~96 KB.
 // MAXNT > 0 caps the CTA at MAXNT threads by narrowing XC (the fp64 x3 middle pass at L >= 512: 32
@@ -734,7 +759,7 @@ struct ColDerivPass {
 // when both layouts are plain: every element is read by its own CTA before that CTA writes it).
 // nb_in / nb_out != 0 select the split layout on that side (the all-to-all chunks of the multi-GPU
 // transposes), fusing the pack / unpack into this pass.
-template <typename T, int L, int DIR, bool SPLIT_IN = false, bool SPLIT_OUT = false>
+template <typename T, int L, int DIR, bool SPLIT_IN = false, bool SPLIT_OUT = false, bool PEER = false>
 struct ColFftPass {
     using CC = ColCfg<L, T>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
@@ -748,6 +773,7 @@ struct ColFftPass {
     int nb_in, nb_out;
     int64_t cs = 0;    // component stride (blockIdx.y = component) of src (and of dst when csd < 0)
     int64_t csd = -1;  // component stride of dst
+    PeerDst pd;        // PEER: the split-layout chunks go straight to their ranks' receive buffers
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
         int x0, o0, xi, t, oi;
@@ -757,6 +783,13 @@ struct ColFftPass {
         const bool on = x < c.nx && o < c.n3;
         Cx<T>* buf = sm + (oi * XC + xi) * LP;
         const Cx<T>* tw = tw_smem<T, L, NT, TWS>(this->tw, reinterpret_cast<Cx<T>*>(smem + CC::SMEM));
+        if constexpr (PEER) {  // chunk of rank q = x2 block q: [i3][i2 % nb][x] in q's receive buffer
+            const int nb = nb_out;
+            PeerAcc<T> pa{pd.pws, pd.boff, ((int64_t)o * nb) * c.W + x, c.W, pd.sh, nb - 1, on};
+            fft_line_io<T, L, DIR, false, false>(
+                buf, t, tw, 1, col_acc<2, T, SPLIT_IN>(const_cast<Cx<T>*>(src) + blockIdx.y * cs, c, x, o, nb_in, on, 0), pa);
+            return;
+        }
         fft_line_io<T, L, DIR, false, false>(buf, t, tw, 1,
                                              col_acc<2, T, SPLIT_IN>(const_cast<Cx<T>*>(src) + blockIdx.y * cs, c, x, o, nb_in, on, 0),
                                              col_acc<2, T, SPLIT_OUT>(dst + blockIdx.y * (csd < 0 ? cs : csd), c, x, o, nb_out, on, 0));
@@ -879,7 +912,7 @@ struct SpecPtrs {
 // x3 middle pass: forward FFT of NCI spectra along x3 in Ti, symbol in Ti, then the NCO results are
 // narrowed to To in a second shared-memory region and transformed back in To (the inverse passes after
 // the symbol may run in the I/O precision: their rounding is relative to the already-amplified signal).
-template <typename Ti, typename To, int L, int KIND>
+template <typename Ti, typename To, int L, int KIND, bool PEER = false>
 struct MiddlePass {
     using T = Ti;
     static constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
@@ -899,6 +932,7 @@ struct MiddlePass {
     const Cx<Ti>* tw;
     const Cx<To>* two;  // inverse twiddles in To
     int64_t cs = 0;     // component stride of in / out (blockIdx.y = component; one-component symbols)
+    PeerDst pd;         // PEER (one output): plane p goes to rank p >> pd.sh's receive buffer
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
         Cx<To>* so = reinterpret_cast<Cx<To>*>(smem + BUFI);
@@ -965,8 +999,14 @@ struct MiddlePass {
                 const bool act = ln < LINES;
                 const bool lon = act && x0 + lxi < c.nx && o0 + loi < c.n2;
                 Cx<To>* buf = so + co * LINES * LPO + (act ? ln : 0) * LPO;
-                fft_line_io<To, L, +1, true, false>(buf, lt, two, 1, SmemLine<To>{buf},
-                                                    col_acc<3>(out.p[co] + blockIdx.y * cs, c, x0 + lxi, o0 + loi, 0, lon, 0));
+                if constexpr (PEER) {  // rank q's chunk: [i3 - q n3][line][x] (the split layout of the inverse x2 pass)
+                    const int mk = (1 << pd.sh) - 1;
+                    PeerAcc<To> pa{pd.pws, pd.boff, (int64_t)(o0 + loi) * c.W + x0 + lxi, (int64_t)c.n2 * c.W, pd.sh, mk, lon};
+                    fft_line_io<To, L, +1, true, false>(buf, lt, two, 1, SmemLine<To>{buf}, pa);
+                } else {
+                    fft_line_io<To, L, +1, true, false>(buf, lt, two, 1, SmemLine<To>{buf},
+                                                        col_acc<3>(out.p[co] + blockIdx.y * cs, c, x0 + lxi, o0 + loi, 0, lon, 0));
+                }
             }
         }
     }

@@ -1,6 +1,7 @@
 """Host-side logic of the slab-decomposed path on CPU (no GPU): the library's slab partition, the NCCL
-unique-id broadcast over torch.distributed and the slab slicing / reassembly bench.py and the tests
-use, exercised by world_size-2 gloo process groups."""
+unique-id broadcast over torch.distributed, the slab slicing / reassembly bench.py and the tests use,
+and the peer-mapping exchange of the fused ghost / transpose path, exercised by world_size-2 gloo
+process groups."""
 import os
 import socket
 
@@ -51,6 +52,21 @@ def _worker(rank, world, port, q):
         parts = [torch.empty_like(mine) for _ in range(world)]
         dist.all_gather(parts, mine)
         assert torch.equal(D.assemble(parts), v)
+        # 3. peer mapping for the fused ghost exchange / transposes (dr_peer_export / dr_peer_import):
+        #    every rank receives every rank's (handle, offset) in rank order (a stub context stands in
+        #    for the CUDA IPC calls)
+        class Stub:
+            nranks = world
+
+            def peer_export(self):
+                return bytes([rank]) * 64, 4096 * (rank + 1)
+
+            def peer_import(self, handles, offsets):
+                self.got = (handles, offsets)
+
+        st = Stub()
+        D.map_peers(st)
+        assert st.got == ([bytes([r]) * 64 for r in range(world)], [4096 * (r + 1) for r in range(world)])
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))

@@ -275,7 +275,8 @@ def run_slabs(dr, cfg, P, ins_full, profile=False):
 def test_peer_ghosts_match_single_rank(dr, monkeypatch, P, case):
     """Fused ghost exchange (DR_PEER_GHOSTS=1, include/diffreg.h dr_peer_export): the producing gathers
     store their boundary planes into the neighbours' ghosts through peer pointers (the other loopback
-    contexts' workspaces) and the consumers only wait for their neighbours -- every observable of the
+    contexts' workspaces) and the consumers only wait for their neighbours; the x2 forward pass and the
+    x3 middle pass store their transpose chunks into the owning ranks' buffers -- every observable of the
     pipeline (state, adjoint, GN / full-Newton matvec, gradient, deformation map) stays bit-identical to
     one rank, and the profiler shows the neighbour barriers that replaced the ghost exchanges."""
     n, nt, iso, vgen = CASES[case][:4]
@@ -290,8 +291,8 @@ def test_peer_ghosts_match_single_rank(dr, monkeypatch, P, case):
     ref = pipeline(dr.Context(cfg), rT, rR, v, vt)
     monkeypatch.setenv("DR_PEER_GHOSTS", "1")
     outs = run_slabs(dr, cfg, P, (rT, rR, v, vt), profile=True)
-    for o in outs:
-        assert "peer_sync" in o["_prof"], sorted(o["_prof"])
+    for o in outs:  # neighbour barriers replaced ghost exchanges, all-rank barriers the transposes
+        assert "peer_sync" in o["_prof"] and "peer_barrier" in o["_prof"], sorted(o["_prof"])
     for k, full in ref.items():
         if k in ("_J", "_prof"):
             continue
