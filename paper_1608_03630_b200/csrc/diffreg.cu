@@ -1293,6 +1293,21 @@ struct Impl {
             // beta a(k) u_c + i k'_c D/|k'|^2 and the c2r adds b_c
             T* D = Dv();  // isochoric contexts have no div v: the slot is free
             div(b, D);
+            const int64_t su = uniform_stride(u.c), sb = uniform_stride(b.c), so = uniform_stride(out.c);
+            if (!c.dist() && su && sb == so && so) {
+                // one rank: the three components' forward passes batched, D transformed once, one 4 -> 3
+                // middle pass (KIND 7: D's x3 transform and spectrum read once instead of per component),
+                // the inverse passes batched with b~ added
+                row_r2c<double>(u.c[0], specD(0), 3, su, g.S);
+                col_fft_fwd<double>(specD(0), specD(0), 0, 3, g.S);
+                spec_forward(D, 3);
+                Cx<double>* sd[4] = {specD(0), specD(1), specD(2), specD(3)};
+                Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
+                middle<7>(sd, sf);
+                col_fft_inv(specF(0), specF(0), 0, 3, g.S);
+                row_c2r(specF(0), out.c[0], b.c[0], 3, so, g.S);
+                return;
+            }
             spec_forward(D, 1);
             for (int cc = 0; cc < 3; ++cc) {
                 spec_forward(u.c[cc], 0);

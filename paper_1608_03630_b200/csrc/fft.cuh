@@ -706,6 +706,14 @@ __device__ __forceinline__ const Cx<T>* tw_smem(const Cx<T>* __restrict__ tw, Cx
     return sm;
 }
 
+// CTA-size cap of the fp32 derivative / x2 column passes at L >= 512 (16 columns x 32 threads made
+// 512-thread CTAs, one or two per SM; 8 columns: the x3 derivative 1.38 -> 0.92 ms, the inverse x2 pass
+// 854 -> 697 us at 512^3; the fp64 x2 pass measured slower capped, 1200 -> 1375 us, and is not)
+template <int L, typename T>
+struct ColCap {
+    static constexpr int V = (L >= 512 && sizeof(T) == 4) ? CtaThreads<T>::V : 0;
+};
+
 // thread -> (column xi, thread-in-line t, transverse line oi); line index oi * XC + xi
 template <int XC, int TPL>
 __device__ __forceinline__ void col_thread(int& xi, int& t, int& oi) {
@@ -725,7 +733,7 @@ __device__ __forceinline__ void col_origin(const ColGeom& c, int tile, int& x0, 
 // Derivative along x2 / x3 of a real field (viewed as complex pairs): out (+)= d f / dx_AX.
 template <typename T, int L, int AX>
 struct ColDerivPass {
-    using CC = ColCfg<L, T>;
+    using CC = ColCfg<L, T, 1, ColCap<L, T>::V>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr bool TWS = sizeof(T) == 4;
@@ -761,7 +769,7 @@ struct ColDerivPass {
 // transposes), fusing the pack / unpack into this pass.
 template <typename T, int L, int DIR, bool SPLIT_IN = false, bool SPLIT_OUT = false, bool PEER = false>
 struct ColFftPass {
-    using CC = ColCfg<L, T>;
+    using CC = ColCfg<L, T, 1, ColCap<L, T>::V>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
     static constexpr int MINB = MinB<T, NT>::V;
     static constexpr bool TWS = sizeof(T) == 4;
@@ -817,9 +825,11 @@ __device__ __forceinline__ T sym_a(const SymInfo& s, T kk) { return s.reg == 1 ?
 // kind 5: Y = norm * L_hat (beta a(k) V + B)      (isochoric gradient from the unprojected v, 6 -> 3)
 // kind 6: Y = norm * (beta a(k) V_c + i k'_c D / |k'|^2)   (isochoric matvec tail per component c, 2 -> 1;
 //         D = F[div b~]: L b~ = b~ - grad Lap^-1 div b~, whose b~ part is added in real space)
+// kind 7: kind 6 for the three components in one pass (4 -> 3: V_0, V_1, V_2, D; MiddlePass::run7 reads
+//         and transforms D once, then each V_c in turn through one input and one output line buffer)
 template <typename T, int KIND>
 struct Sym {
-    static constexpr int NCI = (KIND <= 1) ? 1 : (KIND == 6 ? 2 : (KIND >= 4 ? 6 : 3));
+    static constexpr int NCI = (KIND <= 1) ? 1 : (KIND == 6 ? 2 : (KIND == 7 ? 4 : (KIND >= 4 ? 6 : 3)));
     static constexpr int NCO = (KIND <= 1 || KIND == 6) ? 1 : 3;
     static __device__ __forceinline__ void apply(const SymInfo& s, Cx<T>* x, int k1, int k2, int k3, int kp1, int kp2,
                                                  int kp3) {
@@ -916,13 +926,14 @@ template <typename Ti, typename To, int L, int KIND, bool PEER = false>
 struct MiddlePass {
     using T = Ti;
     static constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
-    using CC = ColCfg<L, T, NCI, (sizeof(T) == 8 && L >= 512) ? 128 : 0>;
+    static constexpr int NCIS = KIND == 7 ? 2 : NCI, NCOS = KIND == 7 ? 1 : NCO;  // line buffers in shared memory
+    using CC = ColCfg<L, T, NCIS, (sizeof(T) == 8 && L >= 512) ? 128 : 0>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
     static constexpr int LPO = ColLP<L, To, XC>::V;  // stride of the To lines of the inverse
     static constexpr int TPLO = Tpl<L, To>::V;  // threads per inverse line (fp32: fewer than fp64)
     static constexpr int MINB = MinBMiddle<T, NT>::V;
     static constexpr size_t BUFI = CC::SMEM;
-    static constexpr size_t BUFO = BUFI + (size_t)NCO * LINES * LPO * sizeof(Cx<To>);
+    static constexpr size_t BUFO = BUFI + (size_t)NCOS * LINES * LPO * sizeof(Cx<To>);
     static constexpr bool TWS = sizeof(T) == 4;
     static constexpr size_t BUF = BUFO + (TWS ? L * (sizeof(Cx<T>) + sizeof(Cx<To>)) : 0);  // + both twiddle tables
     ColGeom c;
@@ -943,6 +954,10 @@ struct MiddlePass {
         const bool on = x0 + xi < c.nx && o0 + oi < c.n2;
         const Cx<T>* tw = tw_smem<T, L, NT, TWS>(this->tw, reinterpret_cast<Cx<T>*>(smem + BUFO));
         const Cx<To>* two = tw_smem<To, L, NT, TWS>(this->two, reinterpret_cast<Cx<To>*>(smem + BUFO + L * sizeof(Cx<T>)));
+        if constexpr (KIND == 7) {
+            run7(x0, o0, xi, t, oi, line, on, tw, two, sm, so);
+            return;
+        }
         if constexpr (KIND <= 1) {  // scalar symbol fused into the last forward stage
             const int og = o0 + oi + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
             const T k1 = (T)(x0 + xi), k2 = (T)wavenum(og, n2g);
@@ -983,12 +998,47 @@ struct MiddlePass {
         }
         __syncthreads();
     }
+    // kind 7: D's x3 spectrum once, then per component c: V_c forward, the kind-6 symbol of component c
+    // (Sym<T, 6>::apply with comp = c: the same arithmetic, so the same bits), inverse to out.p[c]
+    __device__ __forceinline__ void run7(int x0, int o0, int xi, int t, int oi, int line, bool on, const Cx<T>* tw,
+                                         const Cx<To>* two, Cx<T>* sm, Cx<To>* so) const {
+        Cx<T>* bV = sm;
+        Cx<T>* bD = sm + LINES * LP;
+        fft_line_io<T, L, -1, false, true>(bD + line * LP, t, tw, 1, col_acc<3>(in.p[3], c, x0 + xi, o0 + oi, 0, on, 0),
+                                           SmemLine<T>{bD + line * LP});
+        const int n1 = 2 * (c.nx - 1);
+        for (int cc = 0; cc < 3; ++cc) {
+            fft_line_io<T, L, -1, false, true>(bV + line * LP, t, tw, 1, col_acc<3>(in.p[cc], c, x0 + xi, o0 + oi, 0, on, 0),
+                                               SmemLine<T>{bV + line * LP});
+            SymInfo sc = s;
+            sc.comp = cc;
+            for (int e = threadIdx.x; e < LINES * L; e += NT) {
+                const int ln = e / L, p = e % L;
+                const int lxi = ln % XC, loi = ln / XC;
+                const int x = x0 + lxi, o = o0 + loi;
+                Cx<T> v[2] = {bV[ln * LP + P(p)], bD[ln * LP + P(p)]};
+                if (x < c.nx && o < c.n2) {
+                    const int og = o + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
+                    const int k1 = x, k2 = wavenum(og, n2g), k3 = wavenum(p, L);
+                    const int kp1 = (x == n1 / 2) ? 0 : x, kp2 = wavenum_odd(og, n2g), kp3 = wavenum_odd(p, L);
+                    Sym<T, 6>::apply(sc, v, k1, k2, k3, kp1, kp2, kp3);
+                }
+                so[ln * LPO + P(p)] = cx<To>((To)v[0].re, (To)v[0].im);
+            }
+            __syncthreads();
+            inverse_one(cc, 0, x0, o0, two, so);
+        }
+    }
     __device__ __forceinline__ void inverse(int x0, int o0, const Cx<To>* two, Cx<To>* so) const {
+#pragma unroll
+        for (int co = 0; co < NCO; ++co) inverse_one(co, co, x0, o0, two, so);
+    }
+    // inverse of line buffer set `cb` to output co
+    __device__ __forceinline__ void inverse_one(int co, int cb, int x0, int o0, const Cx<To>* two, Cx<To>* so) const {
         // inverse lines: the CTA's NT threads cover LINES lines of TPLO threads in NT / (LINES * TPLO) rounds
         static_assert(NT % TPLO == 0, "inverse thread mapping");
         constexpr int PER = NT / TPLO;  // lines per round
-#pragma unroll
-        for (int co = 0; co < NCO; ++co) {
+        {
 #pragma unroll
             for (int l0 = 0; l0 < LINES; l0 += PER) {
                 // thread -> (column, t, line) with columns fastest, as in col_thread
@@ -998,7 +1048,7 @@ struct MiddlePass {
                 const int ln = loi * XC + lxi;
                 const bool act = ln < LINES;
                 const bool lon = act && x0 + lxi < c.nx && o0 + loi < c.n2;
-                Cx<To>* buf = so + co * LINES * LPO + (act ? ln : 0) * LPO;
+                Cx<To>* buf = so + cb * LINES * LPO + (act ? ln : 0) * LPO;
                 if constexpr (PEER) {  // rank q's chunk: [i3 - q n3][line][x] (the split layout of the inverse x2 pass)
                     const int mk = (1 << pd.sh) - 1;
                     PeerAcc<To> pa{pd.pws, pd.boff, (int64_t)(o0 + loi) * c.W + x0 + lxi, (int64_t)c.n2 * c.W, pd.sh, mk, lon};
@@ -1055,7 +1105,7 @@ struct StgLine {
 template <typename Ti, int L, int KIND>
 struct MiddleTma {
     using T = Ti;
-    using CC = ColCfg<L, T>;
+    using CC = ColCfg<L, T, 1, ColCap<L, T>::V>;
     static constexpr int TPL = CC::TPL, XC = CC::XC, NT = CC::NT;
     static_assert(CC::OL == 1 && XC * sizeof(Cx<T>) == 128, "one 128-byte row per plane");
     static_assert(Tpl<L, float>::V == TPL, "the fp32 inverse keeps the thread -> (column, t) map");
