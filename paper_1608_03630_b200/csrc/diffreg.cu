@@ -2298,7 +2298,7 @@ dr_status dr_destroy(dr_ctx* c) {
 
 dr_status dr_set_images(dr_ctx* c, const void* rho_T, const void* rho_R) {
     return run(c, [&] {
-        ++c->graph_epoch;  // captured matvec / preconditioner graphs are stale
+        // (captured matvec / preconditioner graphs stay valid: they read the images' fixed workspace slots)
         if (!rho_T || !rho_R) fail(DR_ERR_ARG, "rho_T and rho_R must be non-NULL");
         dispatch(c, [&](auto& im) {
             const size_t F = c->g.M * elem_size(c);
@@ -2312,7 +2312,10 @@ dr_status dr_set_images(dr_ctx* c, const void* rho_T, const void* rho_R) {
 
 dr_status dr_set_velocity(dr_ctx* c, const void* v) {
     return run(c, [&] {
-        ++c->graph_epoch;  // captured matvec / preconditioner graphs are stale
+        // One rank: the captured matvec / preconditioner graphs read the velocity's products (displacements,
+        // tile plans, multiplier, state gradients) from fixed workspace slots and take no host-side decision
+        // on them, so they stay valid.  Slabs: the off-rank plans' host counts are baked into the launches.
+        if (c->dist()) ++c->graph_epoch;
         if (!v) fail(DR_ERR_ARG, "v must be non-NULL");
         c->have_velocity = false;
         c->have_state = c->have_adjoint = c->have_matvec = false;

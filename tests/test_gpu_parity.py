@@ -651,8 +651,9 @@ def test_window_gather_same_bits_as_pair_path(dr, monkeypatch):
 def test_call_graphs_match_eager(dr, monkeypatch):
     """dr_hessian_matvec / dr_precond_apply replayed from the context's cached CUDA graphs (default) give
     the bits of eager execution (DR_GRAPHS=0): the first call (capture + launch), replays, a second
-    argument pair, and a new velocity (stale graphs re-captured).  The profiler's per-kernel launch
-    counts agree (its events are record nodes retargeted at every replay)."""
+    argument pair, and a new velocity (one rank: the same graphs replayed -- they read the velocity's
+    products from fixed workspace slots).  The profiler's per-kernel launch counts agree (its events are
+    record nodes retargeted at every replay)."""
     name, n, nt, vgen, iso = CASES[2]
     res, prof = {}, {}
     for mode in ("0", "1"):
