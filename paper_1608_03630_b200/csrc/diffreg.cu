@@ -754,10 +754,15 @@ struct Impl {
 
     template <typename U, int L, int DIR, bool SI, bool SO>
     void col_fft_LS(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs, int64_t csd) {
-        using PT = ColFftPass<U, L, DIR, SI, SO>;
         const ColGeom cg = spec_geom();
-        stream(DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32",
-               PT{cg, src, dst, tw, nb_in, nb_out, cs, csd}, col_tiles<PT>(cg, g.n3), nc);
+        const char* tag = DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32";
+        if (csd >= 0 && csd != cs && !SI && !SO) {
+            using PT = ColFftPass<U, L, DIR, false, false, false, true>;
+            stream(tag, PT{cg, src, dst, tw, nb_in, nb_out, cs, csd}, col_tiles<PT>(cg, g.n3), nc);
+            return;
+        }
+        using PT = ColFftPass<U, L, DIR, SI, SO>;
+        stream(tag, PT{cg, src, dst, tw, nb_in, nb_out, cs, csd}, col_tiles<PT>(cg, g.n3), nc);
     }
     template <typename U, int L, int DIR>
     void col_fft_L(const Cx<U>* src, Cx<U>* dst, const Cx<U>* tw, int nb_in, int nb_out, int nc, int64_t cs, int64_t csd) {

@@ -767,7 +767,9 @@ struct ColDerivPass {
 // when both layouts are plain: every element is read by its own CTA before that CTA writes it).
 // nb_in / nb_out != 0 select the split layout on that side (the all-to-all chunks of the multi-GPU
 // transposes), fusing the pack / unpack into this pass.
-template <typename T, int L, int DIR, bool SPLIT_IN = false, bool SPLIT_OUT = false, bool PEER = false>
+// DCS: dst has its own component stride csd (the scratch ring); a template flag because the runtime
+// choice cost the plain passes 8 % (fp32 x2: 83 -> 90 us at 256^3)
+template <typename T, int L, int DIR, bool SPLIT_IN = false, bool SPLIT_OUT = false, bool PEER = false, bool DCS = false>
 struct ColFftPass {
     using CC = ColCfg<L, T, 1, ColCap<L, T>::V>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
@@ -800,7 +802,7 @@ struct ColFftPass {
         }
         fft_line_io<T, L, DIR, false, false>(buf, t, tw, 1,
                                              col_acc<2, T, SPLIT_IN>(const_cast<Cx<T>*>(src) + blockIdx.y * cs, c, x, o, nb_in, on, 0),
-                                             col_acc<2, T, SPLIT_OUT>(dst + blockIdx.y * (csd < 0 ? cs : csd), c, x, o, nb_out, on, 0));
+                                             col_acc<2, T, SPLIT_OUT>(dst + blockIdx.y * (DCS ? csd : cs), c, x, o, nb_out, on, 0));
     }
 };
 
