@@ -39,7 +39,9 @@
  * DR_OVERLAP=1 transforms beta A vt on a second stream concurrently with the transport sweeps
  * (measured slower, off); DR_TMA_MIDDLE=0 replaces the tensor-map TMA fp32 x3 middle pass by the
  * one-tile-per-CTA pass; DR_PEER_GHOSTS=1 (slabs) fuses the ghost exchange into the producing gathers
- * (dr_peer_export).  Opt-in experiments (measured slower on one B200): DR_PAIRS=1
+ * (dr_peer_export); DR_GRAPHS=0 runs matvec / preconditioner calls eagerly instead of replaying the
+ * context's captured CUDA graphs; DR_NCCL_GRAPHS=1 also captures NCCL contexts' calls (default eager);
+ * DR_NCCL_LIB names the libnccl.so.2 to dlopen (the Python binding sets torch's bundled one).  Opt-in experiments (measured slower on one B200): DR_PAIRS=1
  * (shared-plane pair gathers), DR_WINDOW=1 (sliding-window gathers), DR_PLANE2D=1 (x1/x2 plane
  * transforms through cluster shared memory), DR_RING=P (plane chunks through an L2 scratch ring).
  * Results are bit-identical either way (DR_PLANE2D: within rounding).

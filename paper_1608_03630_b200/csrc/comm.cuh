@@ -119,9 +119,10 @@ struct NcclApi {
         return api;
     }
     void load() {
+        // DR_NCCL_LIB (the Python binding points it at torch's bundled libnccl.so.2 when unset), then the
+        // dynamic loader's search path
         const char* env = getenv("DR_NCCL_LIB");
-        const char* cands[] = {env, "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
-                               "libnccl.so.2", "libnccl.so"};
+        const char* cands[] = {env, "libnccl.so.2", "libnccl.so"};
         for (const char* c : cands) {
             if (!c) continue;
             h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
@@ -177,7 +178,13 @@ struct NcclComm : Comm {
         }
         nccl_ck(A.GroupEnd(), "ncclGroupEnd");
     }
-    bool capturable() const override { return true; }  // NCCL kernels under stream capture
+    // NCCL kernels under stream capture (the matvec / preconditioner call graphs): opt-in with
+    // DR_NCCL_GRAPHS=1 -- never exercised with more than one GPU in this build's tests, so the eager
+    // path stays the default for multi-process runs
+    bool capturable() const override {
+        const char* e = getenv("DR_NCCL_GRAPHS");
+        return e && e[0] == '1';
+    }
     // CUDA IPC mappings of the neighbours' workspaces (dr_peer_import); index = rank, null if unmapped
     std::vector<char*> peers;
     std::vector<void*> opened;

@@ -74,6 +74,14 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() or paper_1608_03630_b200/build.py")
+        if "DR_NCCL_LIB" not in os.environ:  # torch's bundled NCCL for the multi-GPU communicator (dlopen'ed lazily)
+            try:
+                import nvidia.nccl as _nccl
+                cand = os.path.join(list(_nccl.__path__)[0], "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["DR_NCCL_LIB"] = cand
+            except ImportError:
+                pass
         L = ctypes.CDLL(LIB_PATH)
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
         L.dr_workspace_bytes.argtypes = [ctypes.POINTER(dr_config)]
