@@ -202,6 +202,7 @@ struct dr_ctx {
     bool overlap = false;                     // DR_OVERLAP=1 in the environment at dr_create
     bool window = false;                      // DR_WINDOW=1: sliding-window fp32 gathers (sl.cuh k_sl_window)
     bool pairs = false;                       // DR_PAIRS=1: x3-adjacent shared-plane pair gathers (sl.cuh k_sl_pairs)
+    bool gather_tma = true;                   // DR_GATHER_TMA=0: gather boxes staged by cp.async only
     bool plane2d = false;                     // DR_PLANE2D=1: fused x1/x2 cluster plane transforms (plane2d.cuh)
     int ring = 0;                             // DR_RING=P: x1/x2 pass pairs per P planes through an L2-resident scratch
     bool peer_ghosts = false;                 // DR_PEER_GHOSTS=1 (slabs): gathers store boundary planes into the
@@ -901,8 +902,7 @@ struct Impl {
     }
     // Tensor-map TMA tiles (fft.cuh MiddleTma): a 4-D map (2 W scalars, n2, n3, components)
     // over spectrum slots `base` .. (component stride S); false if the driver entry point is missing.
-    template <typename U>
-    bool tensor_map(CUtensorMap* tm, const void* base, int nc, cuuint32_t box0, cuuint32_t box1, cuuint32_t box2) {
+    static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
         static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
             cudaDriverEntryPointQueryResult q;
             void* fn = nullptr;
@@ -912,6 +912,30 @@ struct Impl {
             }
             return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
         }();
+        return encode;
+    }
+    // 3-D map over a gather source's slot (x1, x2, slot planes) with the staged box's extents
+    GatherTma gather_tma(const T* slot_base) {
+        GatherTma gt;
+        std::memset(&gt, 0, sizeof(gt));
+        if constexpr (std::is_same<T, float>::value) {
+            const auto encode = tma_encoder();
+            if (!c.gather_tma || !encode || ((uintptr_t)slot_base & 15)) return gt;
+            using BG = BoxGeom<float, 1>;
+            const cuuint64_t dims[3] = {(cuuint64_t)g.n1, (cuuint64_t)g.n2, (cuuint64_t)(g.n3 + g.zg + g.zgh)};
+            const cuuint64_t strides[2] = {(cuuint64_t)g.n1 * 4, (cuuint64_t)g.n1 * g.n2 * 4};
+            const cuuint32_t box[3] = {(cuuint32_t)BG::BX, (cuuint32_t)BG::BY, (cuuint32_t)BG::BZ};
+            const cuuint32_t el[3] = {1, 1, 1};
+            if (box[0] > 256 || box[1] > 256 || box[2] > 256) return gt;
+            gt.use = encode(&gt.tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<T*>(slot_base), dims, strides, box, el,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        return gt;
+    }
+    template <typename U>
+    bool tensor_map(CUtensorMap* tm, const void* base, int nc, cuuint32_t box0, cuuint32_t box1, cuuint32_t box2) {
+        const auto encode = tma_encoder();
         if (!encode) return false;
         const ColGeom cg = spec_geom();
         const cuuint64_t es = sizeof(U);
@@ -1215,6 +1239,18 @@ struct Impl {
                 set_smem(k, sm);
                 PB(tag);
                 k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi);
+                PE(tag);
+                goto launched;
+            }
+        }
+        if constexpr (std::is_same<T, float>::value && NC == 1) {
+            const GatherTma gt = gather_tma(src.p[0]);
+            if (gt.use) {  // box staged by the TMA engine (sl.cuh k_sl_gather_tma)
+                constexpr size_t sm = box_bytes<T, NC>();
+                auto k = k_sl_gather_tma<Epi>;
+                set_smem(k, sm);
+                PB(tag);
+                k<<<(unsigned)nt, SL_THREADS, sm, s>>>(g, src, dp, plan_buf, nt, epi, gt);
                 PE(tag);
                 goto launched;
             }
@@ -2235,6 +2271,8 @@ dr_status dr_create_dist(const dr_config* cfg, dr_comm* comm, void* workspace, s
         c->chunk = ch ? atoi(ch) : 0;
         const char* wi = getenv("DR_WINDOW");
         c->window = wi && wi[0] == '1';
+        const char* gtm = getenv("DR_GATHER_TMA");
+        c->gather_tma = !(gtm && gtm[0] == '0');
         const char* pa = getenv("DR_PAIRS");
         c->pairs = pa && pa[0] == '1';
         const char* p2 = getenv("DR_PLANE2D");

@@ -13,6 +13,7 @@
 // for the launch fall back to gathering straight from global memory (same arithmetic).
 #pragma once
 #include "common.cuh"
+#include "fft.cuh"  // mbarrier / bulk-copy helpers (the TMA box staging)
 
 namespace dr {
 
@@ -632,6 +633,32 @@ __device__ __forceinline__ void column_from_global(const Grid& g, const Src<T, N
     }
 }
 
+// Box staging by the tensor-map TMA engine (fp32, one component): a 3-D map over the source's ghosted
+// slot (x1, x2, slot planes) with the box's compile-time extents (BoxGeom: 64 x 15 x 14) lands the box
+// exactly in the gather's shared-memory layout (row stride 64 words) with one cp.async.bulk.tensor
+// issued by one thread and completed on an mbarrier -- no per-chunk address arithmetic or LDGSTS on
+// the LSU path the stencil loads saturate.  Only tiles whose planned box does not wrap periodically
+// (the map cannot wrap; columns past the field are zero-filled and never read) use it; the others
+// stage with cp.async as before.  tm: a zeroed map disables it (use = 0).
+struct GatherTma {
+    CUtensorMap tm;
+    int use;
+};
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+// the planned box [ox, ox + ex) x [oy, oy + ey) x [oz, oz + ez) lies inside the source slot (no wrap)
+template <typename T, int NC>
+__device__ __forceinline__ bool box_inside(const Grid& g, const TileCtx<T, NC>& c) {
+    const int zs = g.ghost ? c.oz - g.z0 + g.zg : c.oz;
+    const int nzs = g.ghost ? g.n3 + g.zg + g.zgh : g.n3;
+    return c.fits && c.ox >= 0 && c.ox + c.ex <= g.n1 && c.oy >= 0 && c.oy + c.ey <= g.n2 && zs >= 0 && zs + c.ez <= nzs;
+}
+
 template <typename T, int NC, class Epi>
 __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
     k_sl_gather(Grid g, Src<T, NC> src, Disp<T> d, const int* __restrict__ plan, int ntiles, Epi epi) {
@@ -655,6 +682,65 @@ __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
     if (xyok) load_pair<T, Epi>(d, epi, id0, id0 + H * plane, 0 < kmax, H < kmax, cur);
     cp_async_wait_all();
     __syncthreads();
+    if (!xyok) return;
+#pragma unroll
+    for (int p = 0; p < H; ++p) {
+        if (p >= kmax) break;
+        PairIn<T, Epi> nxt;
+        if (p + 1 < H && p + 1 < kmax)
+            load_pair<T, Epi>(d, epi, id0 + (p + 1) * plane, id0 + (p + 1 + H) * plane, true, p + 1 + H < kmax, nxt);
+        pair_from_box<T, NC, Epi>(g, c, box, x, y, c.z0 + p, id0 + p * plane, id0 + (p + H) * plane, p + H < kmax,
+                                  cur, epi);
+        cur = nxt;
+    }
+}
+
+// The same gather with the box staged by the TMA engine where the planned box does not wrap (fp32, one
+// component; GatherTma above).
+template <class Epi>
+__global__ void __launch_bounds__(SL_THREADS, (GatherMinB<float, 1, Epi>::V))
+    k_sl_gather_tma(Grid g, Src<float, 1> src, Disp<float> d, const int* __restrict__ plan, int ntiles, Epi epi,
+                const __grid_constant__ GatherTma gt) {
+    using T = float;
+    constexpr int NC = 1;
+    constexpr int H = SL_TZ / 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t tbar;
+    T* box = reinterpret_cast<T*>(smem_raw);
+    const int tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    const TileCtx<T, NC> c = tile_ctx<T, NC>(g, plan, tile);
+    bool tma = false;
+    {
+        tma = box_inside<T, NC>(g, c);  // uniform per CTA
+        if (tma) {
+            if (threadIdx.x == 0) {
+                mbar_init(&tbar, 1);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                mbar_expect(&tbar, (unsigned)box_bytes<T, NC>());
+                tma_load_3d(box, &gt.tm, c.ox, c.oy, g.ghost ? c.oz - g.z0 + g.zg : c.oz, &tbar);
+            }
+        }
+    }
+    if (!tma) stage_box<T, NC>(g, src, c, box);
+    const int x = c.x0 + (threadIdx.x % SL_LANES), y = c.y0 + threadIdx.x / SL_LANES;
+    const bool xyok = (int)(threadIdx.x % SL_LANES) < SL_TX && x < g.n1 && y < g.n2;
+    const int kmax = min(SL_TZ, g.n3 - c.z0);
+    const uint32_t plane = (uint32_t)g.n1 * (uint32_t)g.n2;
+    const uint32_t id0 = ((uint32_t)c.z0 * g.n2 + y) * g.n1 + x;
+    if (!c.fits) {  // global-memory fallback (no barrier needed: nothing was staged)
+        if (xyok) column_from_global<T, NC, Epi>(g, src, d, x, y, c.z0, kmax, id0, plane, epi);
+        return;
+    }
+    PairIn<T, Epi> cur;
+    if (xyok) load_pair<T, Epi>(d, epi, id0, id0 + H * plane, 0 < kmax, H < kmax, cur);
+    if (tma) {
+        __syncthreads();  // the mbarrier's initialisation is visible before anyone waits on it
+        mbar_wait(&tbar, 0);
+    } else {
+        cp_async_wait_all();
+        __syncthreads();
+    }
     if (!xyok) return;
 #pragma unroll
     for (int p = 0; p < H; ++p) {

@@ -796,3 +796,24 @@ def test_pairs_gather_same_bits_as_pair_path(dr, monkeypatch):
                       ctx.hessian_matvec(vt), ctx.get_field(dr.DR_FIELD_BTILDE)]
         for a, b in zip(res["0"], res["1"]):
             assert torch.equal(a, b), name
+
+
+def test_gather_tma_staging_same_bits(dr, monkeypatch):
+    """Gather boxes staged by the TMA engine (default: k_sl_gather_tma, tiles whose planned box does not
+    wrap) against cp.async staging only (DR_GATHER_TMA=0): the same values land in the same shared-memory
+    layout, so every transport of the hot path gives the same bits (the stress case mixes TMA tiles,
+    wrapping cp.async tiles and global-memory tiles)."""
+    for case in (CASES[1], CASES[2], CASES[3]):
+        name, n, nt, vgen, iso = case
+        res = {}
+        for w in ("0", "1"):
+            monkeypatch.setenv("DR_GATHER_TMA", w)
+            ctx, prob, v64 = setup_case(dr, name, n, nt, vgen, iso, False)
+            ctx.forward_solve()
+            ctx.adjoint_solve()
+            vt = synth.round32(synth.smooth_vec(21, n, kmax=5)).contiguous().cuda()
+            res[w] = [ctx.get_departure(1), ctx.get_departure(-1), ctx.get_field(dr.DR_FIELD_MULTIPLIER),
+                      ctx.get_field(dr.DR_FIELD_STATE, nt), ctx.get_field(dr.DR_FIELD_ADJOINT, 0),
+                      ctx.hessian_matvec(vt), ctx.get_field(dr.DR_FIELD_BTILDE)]
+        for a, b in zip(res["0"], res["1"]):
+            assert torch.equal(a, b), name
