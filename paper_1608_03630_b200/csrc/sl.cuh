@@ -586,9 +586,15 @@ template <class Epi>
 struct EpiMinB {
     static constexpr int V = 4;
 };
+#ifndef DR_MINB_INC
+#define DR_MINB_INC 3
+#endif
+#ifndef DR_MINB_Q2
+#define DR_MINB_Q2 3
+#endif
 template <typename T, bool WB>
 struct EpiMinB<EpiIncState<T, WB>> {
-    static constexpr int V = 3;
+    static constexpr int V = DR_MINB_INC;
 };
 template <typename T, bool N>
 struct EpiMinB<EpiAdjoint<T, 1, N>> {
@@ -596,7 +602,7 @@ struct EpiMinB<EpiAdjoint<T, 1, N>> {
 };
 template <typename T, bool N>
 struct EpiMinB<EpiAdjoint<T, 2, N>> {
-    static constexpr int V = 3;
+    static constexpr int V = DR_MINB_Q2;
 };
 template <typename T, class Epi>
 struct EpiMinB<EpiPeer<T, Epi>> {
