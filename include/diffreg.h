@@ -75,7 +75,7 @@ typedef enum dr_status {
     DR_ERR_CUDA = 5,       /* CUDA runtime error (message in dr_last_error)                      */
     DR_ERR_NCCL = 6,       /* multi-GPU communicator error (NCCL, or libnccl.so.2 not loadable)   */
     DR_ERR_OOM = 7,        /* workspace smaller than dr_workspace_bytes / cudaMalloc failed       */
-    DR_ERR_NONFINITE = 8,  /* reserved                                                           */
+    DR_ERR_NONFINITE = 8,  /* DR_CHECK_FINITE contexts: an input field holds NaN / Inf  */
     DR_ERR_PLAN = 9        /* multi-GPU: off-rank departure points exceed the scatter capacity    */
 } dr_status;
 
@@ -84,14 +84,19 @@ enum { DR_REG_H1 = 1,      /* A = -Laplacian   (H1 seminorm, beta/2 |grad v|^2),
 
 enum { DR_ISOCHORIC = 1u,  /* incompressible variant: v Leray-projected, P = Leray  */
        DR_FP64 = 2u,       /* all fields are double instead of float                             */
-       DR_FULL_NEWTON = 4u };  /* NEXT-3: dr_hessian_matvec keeps the two lambda terms of Eq. 5c /
+       DR_FULL_NEWTON = 4u,  /* NEXT-3: dr_hessian_matvec keeps the two lambda terms of Eq. 5c /
                                   b~; default is Gauss-Newton          */
+       DR_CHECK_FINITE = 8u };  /* dr_set_images, dr_set_velocity, dr_hessian_matvec and
+                                  dr_precond_apply scan their inputs first and return
+                                  DR_ERR_NONFINITE (on every rank) if any value is NaN or Inf; the
+                                  scan synchronises the stream (one pass over the input), so these
+                                  calls are no longer asynchronous and are not graph-replayed faster */
 
 typedef struct dr_config {
     int32_t n[3];   /* N1 (x1, fastest), N2, N3                                                   */
     int32_t nt;     /* number of time steps n_t, dt = 1/n_t; 1 <= nt <= 64          */
     int32_t reg;    /* DR_REG_H1 or DR_REG_H2                                                     */
-    uint32_t flags; /* DR_ISOCHORIC | DR_FP64 | DR_FULL_NEWTON                                    */
+    uint32_t flags; /* DR_ISOCHORIC | DR_FP64 | DR_FULL_NEWTON | DR_CHECK_FINITE                  */
     double beta;    /* regularisation parameter beta > 0 (Eq. 2a)                      */
     int32_t ghost_lo, ghost_hi; /* slab ghost planes below / above (multi-GPU only; 0 -> 4 / 5).  A
                                    gather stencil spans floor(s3)-1 .. floor(s3)+2, so (g, g+1) planes

@@ -68,7 +68,7 @@ dr_status validate(const dr_config* c, int nranks = 1) {
     if (c->nt < 1 || c->nt > 64) return DR_ERR_PARAM;
     if (c->reg != DR_REG_H1 && c->reg != DR_REG_H2) return DR_ERR_PARAM;
     if (!(c->beta > 0.0) || !std::isfinite(c->beta)) return DR_ERR_PARAM;
-    if (c->flags & ~(uint32_t)(DR_ISOCHORIC | DR_FP64 | DR_FULL_NEWTON)) return DR_ERR_PARAM;
+    if (c->flags & ~(uint32_t)(DR_ISOCHORIC | DR_FP64 | DR_FULL_NEWTON | DR_CHECK_FINITE)) return DR_ERR_PARAM;
     if (nranks < 1) return DR_ERR_ARG;
     if (nranks > 1) {  // slabs: P | N3 and P | N2 (x2 blocks of the transposes), slab >= ghost width
         if (c->n[2] % nranks || c->n[1] % nranks) return DR_ERR_GRID;
@@ -100,6 +100,8 @@ Grid make_grid(const dr_config* c, int rank = 0, int nranks = 1) {
     g.zgh = g.ghost ? ghost_hi(c) : 0;
     return g;
 }
+
+bool is_device_ptr(const void* p);  // (defined with the C ABI below)
 
 int64_t n_tiles(const Grid& g) {
     return (int64_t)((g.n1 + SL_TX - 1) / SL_TX) * ((g.n2 + SL_TY - 1) / SL_TY) * ((g.n3 + SL_TZ - 1) / SL_TZ);
@@ -1384,6 +1386,25 @@ struct Impl {
     }
 
     // sum over all ranks of one double per rank (device scalar at `val`), identical on every rank
+    // DR_CHECK_FINITE: any NaN / Inf among n values of p (device or host) on any rank -> DR_ERR_NONFINITE
+    // (every rank takes the same decision: the flags are summed over ranks)
+    void check_finite(const void* p, int64_t n, const char* what) {
+        double* flag = c.at<double>(c.L.red) + 4001;
+        double bad = 0.0;
+        if (is_device_ptr(p)) {
+            CK(cudaMemsetAsync(flag, 0, sizeof(double), s));
+            PB("nonfinite");
+            k_nonfinite<T><<<grid_1d(n), 256, 0, s>>>(n, static_cast<const T*>(p), flag);
+            PE("nonfinite");
+        } else {
+            CK(cudaStreamSynchronize(s));
+            const T* h = static_cast<const T*>(p);
+            for (int64_t i = 0; i < n; ++i)
+                if (!std::isfinite(h[i])) { bad = 1.0; break; }
+            CK(cudaMemcpyAsync(flag, &bad, sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        if (allsum(flag) > 0) fail(DR_ERR_NONFINITE, std::string(what) + " holds NaN or Inf values");
+    }
     double allsum(double* val) {
         double* slots = c.at<double>(c.L.red) + 3072;
         const int P = c.nranks;
@@ -2344,6 +2365,10 @@ dr_status dr_set_images(dr_ctx* c, const void* rho_T, const void* rho_R) {
         // (captured matvec / preconditioner graphs stay valid: they read the images' fixed workspace slots)
         if (!rho_T || !rho_R) fail(DR_ERR_ARG, "rho_T and rho_R must be non-NULL");
         dispatch(c, [&](auto& im) {
+            if (c->cfg.flags & DR_CHECK_FINITE) {
+                im.check_finite(rho_T, c->g.M, "rho_T");
+                im.check_finite(rho_R, c->g.M, "rho_R");
+            }
             const size_t F = c->g.M * elem_size(c);
             CK(cudaMemcpyAsync(im.rhoT(), rho_T, F, cudaMemcpyDefault, c->stream));
             CK(cudaMemcpyAsync(im.rhoR(), rho_R, F, cudaMemcpyDefault, c->stream));
@@ -2364,6 +2389,7 @@ dr_status dr_set_velocity(dr_ctx* c, const void* v) {
         c->have_state = c->have_adjoint = c->have_matvec = false;
         dispatch(c, [&](auto& im) {
             using T = std::remove_pointer_t<decltype(im.rhoR())>;
+            if (c->cfg.flags & DR_CHECK_FINITE) im.check_finite(v, 3 * c->g.M, "v");
             im.set_velocity(static_cast<const T*>(v));
         });
         c->have_velocity = true;
@@ -2405,6 +2431,7 @@ dr_status dr_hessian_matvec(dr_ctx* c, const void* vt, void* Hvt) {
         if (vt == Hvt) fail(DR_ERR_ARG, "vt and Hvt must not alias");
         if (!c->have_state) fail(DR_ERR_ORDER, "hessian_matvec needs forward_solve");
         const size_t V = 3 * c->g.M * elem_size(c);
+        if (c->cfg.flags & DR_CHECK_FINITE) dispatch(c, [&](auto& im) { im.check_finite(vt, 3 * c->g.M, "vt"); });
         if ((c->cfg.flags & DR_FULL_NEWTON) && !c->have_adjoint) {  // the lambda terms need the adjoint slices
             dispatch(c, [&](auto& im) { im.adjoint_solve(); });
             c->have_adjoint = true;
@@ -2429,6 +2456,7 @@ dr_status dr_precond_apply(dr_ctx* c, const void* r, void* z) {
     return run(c, [&] {
         if (!r || !z) fail(DR_ERR_ARG, "r and z must be non-NULL");
         const size_t V = 3 * c->g.M * elem_size(c);
+        if (c->cfg.flags & DR_CHECK_FINITE) dispatch(c, [&](auto& im) { im.check_finite(r, 3 * c->g.M, "r"); });
         auto body = [&](const void* in, void* out, cudaStream_t st) {
             dispatch_on(c, st, [&](auto& im) {
                 using T = std::remove_pointer_t<decltype(im.rhoR())>;

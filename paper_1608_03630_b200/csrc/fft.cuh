@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(MiddleTma<Ti, L, KIND>::NT, MiddleTma<Ti, L, K
 // One CTA per tile of a pass.
 template <class PassT>
 __global__ void __launch_bounds__(PassT::NT, PassT::MINB) k_stream(PassT pass) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     pass.run(blockIdx.x, smem_raw);
 }
 

@@ -14,6 +14,16 @@ __global__ void k_inc_init(int64_t M, const T* __restrict__ vt, const T* __restr
     }
 }
 
+// DR_CHECK_FINITE: *flag = 1.0 if any of the n values is NaN or infinite (the input check of the
+// main-path calls, SURVEY §8(b) DR_ERR_NONFINITE)
+template <typename T>
+__global__ void k_nonfinite(int64_t n, const T* __restrict__ x, double* __restrict__ flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1.0;
+}
+
 // lambda(1) = rho_R - rho(1)   (Eq. 3)
 template <typename T>
 __global__ void k_sub(int64_t M, const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out) {

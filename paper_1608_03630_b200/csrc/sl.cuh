@@ -669,7 +669,7 @@ template <typename T, int NC, class Epi>
 __global__ void __launch_bounds__(SL_THREADS, (GatherMinB<T, NC, Epi>::V))
     k_sl_gather(Grid g, Src<T, NC> src, Disp<T> d, const int* __restrict__ plan, int ntiles, Epi epi) {
     constexpr int H = SL_TZ / 2;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     T* box = reinterpret_cast<T*>(smem_raw);
     const int tile = blockIdx.x;
     if (tile >= ntiles) return;
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(SL_THREADS, WIN_MINB)
     using T = float;
     constexpr int BX = WinGeom::BX, BY = WinGeom::BY;
     constexpr int H = SL_TZ / 2, NP = SL_TZ / 2, NJ = SL_TZ + 4;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     T* box = reinterpret_cast<T*>(smem_raw);
     const int tile = blockIdx.x;
     if (tile >= ntiles) return;
@@ -1004,7 +1004,7 @@ __global__ void __launch_bounds__(SL_THREADS, (EpiMinB<Epi>::V))
     using T = float;
     constexpr int BX = BoxGeom<T, 1>::BX, BY = BoxGeom<T, 1>::BY;
     constexpr int NP = SL_TZ / 2;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     T* box = reinterpret_cast<T*>(smem_raw);
     uint16_t* queue = reinterpret_cast<uint16_t*>(smem_raw + box_bytes<T, 1>());
     __shared__ int qn;

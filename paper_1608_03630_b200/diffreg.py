@@ -23,7 +23,7 @@ if os.environ.get("DR_LIB_VARIANT"):  # A/B builds of the same sources (build.py
 DR_OK, DR_ERR_ARG, DR_ERR_GRID, DR_ERR_PARAM, DR_ERR_ORDER, DR_ERR_CUDA, DR_ERR_NCCL, DR_ERR_OOM, \
     DR_ERR_NONFINITE, DR_ERR_PLAN = range(10)
 DR_REG_H1, DR_REG_H2 = 1, 2
-DR_ISOCHORIC, DR_FP64, DR_FULL_NEWTON = 1, 2, 4
+DR_ISOCHORIC, DR_FP64, DR_FULL_NEWTON, DR_CHECK_FINITE = 1, 2, 4, 8
 DR_OP_GRAD, DR_OP_DIV, DR_OP_REG, DR_OP_PRECOND, DR_OP_LERAY = range(5)
 (DR_FIELD_STATE, DR_FIELD_STATE_GRAD, DR_FIELD_ADJOINT, DR_FIELD_INC_STATE, DR_FIELD_INC_ADJOINT,
  DR_FIELD_BTILDE, DR_FIELD_MULTIPLIER, DR_FIELD_VELOCITY) = range(8)
@@ -146,11 +146,12 @@ class Config:
     newton: bool = False  # NEXT-3: full-Newton Hessian (default Gauss-Newton)
     ghost_lo: int = 0  # slab ghost planes (multi-GPU; 0 -> library default 4 / 5)
     ghost_hi: int = 0
+    check_finite: bool = False  # DR_CHECK_FINITE: NaN / Inf inputs -> DR_ERR_NONFINITE (synchronising scan)
 
     def c(self) -> dr_config:
         n = (self.n,) * 3 if isinstance(self.n, int) else tuple(self.n)
         flags = (DR_ISOCHORIC if self.isochoric else 0) | (DR_FP64 if self.fp64 else 0) | \
-            (DR_FULL_NEWTON if self.newton else 0)
+            (DR_FULL_NEWTON if self.newton else 0) | (DR_CHECK_FINITE if self.check_finite else 0)
         cfg = dr_config()
         cfg.n[:] = list(n)
         cfg.nt, cfg.reg, cfg.flags, cfg.beta = self.nt, self.reg, flags, self.beta

@@ -817,3 +817,44 @@ def test_gather_tma_staging_same_bits(dr, monkeypatch):
                       ctx.hessian_matvec(vt), ctx.get_field(dr.DR_FIELD_BTILDE)]
         for a, b in zip(res["0"], res["1"]):
             assert torch.equal(a, b), name
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_nonfinite_inputs_rejected(dr, fp64):
+    """DR_CHECK_FINITE (SURVEY §8(b) DR_ERR_NONFINITE): a NaN or Inf in an image, the velocity, a matvec
+    probe or a preconditioner input -- device or host buffer -- returns DR_ERR_NONFINITE before any
+    work; finite inputs give the bits of an unchecked context."""
+    n = 16
+    cfg = dr.Config(n=n, nt=2, fp64=fp64, check_finite=True)
+    dt = torch.float64 if fp64 else torch.float32
+    ctx = dr.Context(cfg)
+    ref = dr.Context(dr.Config(n=n, nt=2, fp64=fp64))
+    f = synth.blobs(1, n, kcut=4).to(dt).cuda()
+    v = synth.smooth_vec(2, n, kmax=3, cells_per_step=1.0, nt=2).to(dt).cuda()
+    vt = synth.smooth_vec(3, n, kmax=3).to(dt).cuda()
+
+    def bad(x, val, host=False):
+        y = x.clone()
+        y.view(-1)[y.numel() // 3] = val
+        return y.cpu() if host else y
+
+    for val in (float("nan"), float("inf")):
+        for host in (False, True):
+            with pytest.raises(dr.DiffRegError) as e:
+                ctx.set_images(bad(f, val, host), f.cpu() if host else f)
+            assert e.value.status == dr.DR_ERR_NONFINITE
+            with pytest.raises(dr.DiffRegError) as e:
+                ctx.set_velocity(bad(v, val, host))
+            assert e.value.status == dr.DR_ERR_NONFINITE
+    for c in (ctx, ref):
+        c.set_images(f, f)
+        c.set_velocity(v)
+        c.forward_solve()
+    with pytest.raises(dr.DiffRegError) as e:
+        ctx.hessian_matvec(bad(vt, float("nan")))
+    assert e.value.status == dr.DR_ERR_NONFINITE
+    with pytest.raises(dr.DiffRegError) as e:
+        ctx.precond_apply(bad(vt, float("-inf")))
+    assert e.value.status == dr.DR_ERR_NONFINITE
+    assert torch.equal(ctx.hessian_matvec(vt), ref.hessian_matvec(vt))
+    assert torch.equal(ctx.precond_apply(vt), ref.precond_apply(vt))
