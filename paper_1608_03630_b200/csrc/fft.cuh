@@ -130,10 +130,30 @@ struct SmemLine {
     __device__ __forceinline__ void st(int i, const Cx<T>& v) const { b[P(i)] = v; }
 };
 
+// Stage-major twiddle table (tws < 0 in stage_io): for every stage with Ns > 1 and radix Rs, the
+// entries w(r, k) = e^{DIR 2 pi i r k / (Ns Rs)} for r = 1..Rs-1, k = 0..Ns-1 stored as [r - 1][k], so
+// the lanes of a line (consecutive k) read consecutive entries.  The natural table indexed by
+// m = r k L / (Ns Rs) put those lanes r * L / (Ns Rs) entries apart: up to 8-way shared-memory bank
+// conflicts on 16-byte complex128 entries (ncu: the fp64 staged r2c pass at 1.61 wavefronts per LDS).
+// Offset of stage Ns in the table of a radix-R plan of length L (R = 16, last radix L / Ns):
+template <int L, int R>
+__host__ __device__ constexpr int stage_tw_off(int Ns) {
+    int off = 0;
+    for (int n = R; n < Ns; n *= R) off += ((L / n < R ? L / n : R) - 1) * n;
+    return off;
+}
+template <int L, int R>
+__host__ __device__ constexpr int stage_tw_count() {
+    int n = R;
+    while (n < L) n *= R;
+    return stage_tw_off<L, R>(n);
+}
+
 // One Stockham autosort stage of radix R (Ns = product of the previous radices) on a line of length L.
 // Each of the TPL threads of the line owns NB = L/R/TPL butterflies; operands come from src.ld, results
 // go to dst.st (shared memory or global).  SYNC: the stage is in place in shared memory, so all reads
-// must finish (barrier) before the writes.  tw: table of e^{-2 pi i m / (L*tws)}, m < L*tws.
+// must finish (barrier) before the writes.  tw: table of e^{-2 pi i m / (L*tws)}, m < L*tws; tws < 0:
+// the stage-major table above (of the line's radix-16 plan).
 template <typename T, int L, int R, int Ns, int DIR, int TPL, bool SYNC, class Src, class Dst>
 __device__ __forceinline__ void stage_io(int t, const Cx<T>* __restrict__ tw, int tws, const Src& src, const Dst& dst) {
     constexpr int NB = (L / R) / TPL;
@@ -153,7 +173,7 @@ __device__ __forceinline__ void stage_io(int t, const Cx<T>* __restrict__ tw, in
 #pragma unroll
             for (int r = 1; r < R; ++r) {
                 const int m = r * k * (L / (Ns * R));
-                Cx<T> w = tw[m * tws];
+                Cx<T> w = tws < 0 ? tw[stage_tw_off<L, 16>(Ns) + (r - 1) * Ns + k] : tw[m * tws];
                 if (DIR > 0) w.im = -w.im;
                 x[b][r] = cmul(x[b][r], w);
             }
@@ -440,8 +460,9 @@ struct RowR2cStaged {
     static constexpr int SI = staged_stride<Ti, TPL>(L) * (int)sizeof(Cx<Ti>);  // staged row stride, bytes
     static constexpr size_t STG = (size_t)RB * SI, EPB = 0;
     static constexpr int NTW = 2 * L;  // twiddles e^{-2 pi i m / 2L} in shared memory
+    static constexpr int NST = stage_tw_count<L, 16>();  // + the stage-major table of the L-point FFT
     using TW = Cx<Tc>;
-    static constexpr size_t BUF = 128 + 2 * STG + EPB + RC::LINES + NTW * sizeof(TW);
+    static constexpr size_t BUF = 128 + 2 * STG + EPB + RC::LINES + (NTW + NST) * sizeof(TW);
     Grid g;
     const Ti* f;
     Cx<Tc>* spec;
@@ -462,7 +483,7 @@ struct RowR2cStaged {
         const bool ok = row < nrows();
         Cx<Tc>* buf = reinterpret_cast<Cx<Tc>*>(lines) + line * LP;
         const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(stg + line * SI);
-        fft_line_io<Tc, L, -1, false, true>(buf, t, twN, 2, RowLd<Ti, Tc>{src}, SmemLine<Tc>{buf});
+        fft_line_io<Tc, L, -1, false, true>(buf, t, twN + NTW, -1, RowLd<Ti, Tc>{src}, SmemLine<Tc>{buf});
         if (!ok) return;
         Cx<Tc>* out = spec + blockIdx.y * css + row * g.n1p;
         for (int k = t; k <= L / 2; k += TPL) {
@@ -485,8 +506,9 @@ struct RowC2rStaged {
     static constexpr int SA = staged_stride<T, TPL>(L) * (int)sizeof(Cx<T>);
     static constexpr size_t STG = (size_t)RB * SI, EPB = ADD ? (size_t)RB * SA : 0;
     static constexpr int NTW = 2 * L;
+    static constexpr int NST = stage_tw_count<L, 16>();
     using TW = Cx<T>;
-    static constexpr size_t BUF = 128 + 2 * STG + EPB + RC::LINES + NTW * sizeof(TW);
+    static constexpr size_t BUF = 128 + 2 * STG + EPB + RC::LINES + (NTW + NST) * sizeof(TW);
     Grid g;
     const Cx<T>* spec;
     RowOut<T> epi;
@@ -527,7 +549,7 @@ struct RowC2rStaged {
             add = reinterpret_cast<const Cx<T>*>(ep + line * SA);
         }
         Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out + blockIdx.y * csf) + row * L;
-        fft_line_io<T, L, +1, true, false>(buf, t, twN, 2, SmemLine<T>{buf}, RowSt<T>{dst, add, 0, ok});
+        fft_line_io<T, L, +1, true, false>(buf, t, twN + NTW, -1, SmemLine<T>{buf}, RowSt<T>{dst, add, 0, ok});
     }
 };
 
@@ -551,6 +573,18 @@ __global__ void __launch_bounds__(PassT::NT, PassT::MINB) k_rows(PassT pass, int
         mbar_fence_init();
     }
     for (int i = threadIdx.x; i < PassT::NTW; i += PassT::NT) tw[i] = pass.twN[i];
+    // stage-major table (stage_tw_off): entry (Ns, r, k) = twN[2 r k L / (Ns Rs)] of the L-point plan
+    constexpr int L = PassT::NTW / 2;
+    for (int i = threadIdx.x; i < PassT::NST; i += PassT::NT) {
+        int Ns = 16, e = i;
+        while (e >= ((L / Ns < 16 ? L / Ns : 16) - 1) * Ns) {
+            e -= ((L / Ns < 16 ? L / Ns : 16) - 1) * Ns;
+            Ns *= 16;
+        }
+        const int Rs = L / Ns < 16 ? L / Ns : 16;
+        const int r = 1 + e / Ns, k = e % Ns;
+        tw[PassT::NTW + i] = pass.twN[2 * r * k * (L / (Ns * Rs))];
+    }
     __syncthreads();
     int tile = blockIdx.x;
     if (warp == 0 && tile < ntiles) pass.issue_in(tile, stg, &bar[0], lane);
