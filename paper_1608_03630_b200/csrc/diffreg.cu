@@ -795,8 +795,23 @@ struct Impl {
 #undef CALL
     }
 
+    // isochoric data term, x2 stage (fft.cuh ColDivPass): Q = i (k1' F2 P1 + k2' F2 P2), R = F2 P3 from the x1
+    // half spectra P_a of b~'s components; nb_out != 0: the split layout of the slab transposes
+    template <int L, bool SO>
+    void col_div_L(const Cx<T>* p1, const Cx<T>* p2, const Cx<T>* p3, Cx<T>* q, Cx<T>* r, int nb_out) {
+        using PT = ColDivPass<T, L, SO>;
+        const ColGeom cg = spec_geom();
+        stream("col_div", PT{cg, p1, p2, p3, q, r, twy_t<T>(), nb_out, g.n1}, col_tiles<PT>(cg, g.n3));
+    }
+    void col_div(const Cx<T>* p1, const Cx<T>* p2, const Cx<T>* p3, Cx<T>* q, Cx<T>* r, int nb_out) {
+#define CALL(LL) (nb_out ? col_div_L<LL, true>(p1, p2, p3, q, r, nb_out) : col_div_L<LL, false>(p1, p2, p3, q, r, 0))
+        DR_SWITCH_COL(g.n2, CALL)
+#undef CALL
+    }
+
     template <int L, int KIND, typename Tc>
-    void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out, int comp, int nc, int64_t cs) {
+    void middle_L(const ColGeom& cg, Cx<Tc>* const* in, Cx<T>* const* out, int comp, int nc, int64_t cs,
+                  Cx<T>* const* inq) {
         if constexpr (MiddlePass<Tc, T, L, KIND>::NCO == 1) {
             if (c.dist() && nc == 1 && peer_a2a_on()) {  // store the transpose chunks into the ranks' specF(3)
                 using PQ = MiddlePass<Tc, T, L, KIND, true>;
@@ -804,6 +819,7 @@ struct Impl {
                 pt.c = cg;
                 for (int i = 0; i < PQ::NCI; ++i) pt.in.p[i] = in[i];
                 pt.out.p[0] = out[0];
+                if (inq) pt.inq = SpecPtrs<T, 2>{{inq[0], inq[1]}};
                 pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), comp};
                 pt.tw = twz_t<Tc>();
                 pt.two = twz();
@@ -821,6 +837,7 @@ struct Impl {
         pt.c = cg;
         for (int i = 0; i < PT::NCI; ++i) pt.in.p[i] = in[i];
         for (int i = 0; i < PT::NCO; ++i) pt.out.p[i] = out[i];
+        if (inq) pt.inq = SpecPtrs<T, 2>{{inq[0], inq[1]}};
         pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), comp};
         pt.tw = twz_t<Tc>();
         pt.two = twz();
@@ -828,9 +845,10 @@ struct Impl {
         stream(sizeof(Tc) == 8 ? "col_middle_f64" : "col_middle_f32", pt, col_tiles<PT>(cg, cg.n2), nc);
     }
     template <int KIND, typename Tc = double>
-    void middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0, int nc = 1, int64_t cs = 0) {
+    void middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0, int nc = 1, int64_t cs = 0,
+                Cx<T>* const* inq = nullptr) {
         const ColGeom cg = c.dist() ? spec_geom_t() : spec_geom();
-#define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out, comp, nc, cs)
+#define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out, comp, nc, cs, inq)
         DR_SWITCH_COL(g.n3g, CALL)
 #undef CALL
     }
@@ -1331,32 +1349,42 @@ struct Impl {
     // out = beta A u + P b (P = Leray when isochoric, else I): the tail of Eq. 5e and of Eq. 4
     void reg_plus_data(V3<const T> u, V3<const T> b, V3<T> out) {
         if (c.cfg.flags & DR_ISOCHORIC) {
-            // L b = b - grad Lap^-1 div b: D = div b by the per-axis derivative passes (its rounding is
-            // damped by k'/|k'|^2), one forward transform of D, then per component a 2 -> 1 middle pass
-            // beta a(k) u_c + i k'_c D/|k'|^2 and the c2r adds b_c
-            T* D = Dv();  // isochoric contexts have no div v: the slot is free
-            div(b, D);
+            // L b = b - grad Lap^-1 div b with F[div b] = F3 Q + i k3' F3 R formed in the x3 middle pass from
+            // b's x1 half spectra (r2c in T: the projection damps their rounding) through the x2 stage
+            // ColDivPass -- no real-space derivative passes, no transform of div b; then per component the
+            // kind-6 symbol beta a(k) u_c + i k'_c D/|k'|^2 (middle kind 8 / 9) and the c2r adds b_c
+            constexpr int F = (int)(sizeof(Cx<double>) / sizeof(Cx<T>));  // T spectrum slots per complex128 slot
             const int64_t su = uniform_stride(u.c), sb = uniform_stride(b.c), so = uniform_stride(out.c);
             if (!c.dist() && su && sb == so && so) {
-                // one rank: the three components' forward passes batched, D transformed once, one 4 -> 3
-                // middle pass (KIND 7: D's x3 transform and spectrum read once instead of per component),
-                // the inverse passes batched with b~ added
+                // one rank: the components batched per pass, D formed once per line (kind 8), Q / R in
+                // place of P1 / P3 (T slots of complex128 slots 3..5; u's spectra fill slots 0..2)
                 row_r2c<double>(u.c[0], specD(0), 3, su, g.S);
                 col_fft_fwd<double>(specD(0), specD(0), 0, 3, g.S);
-                spec_forward(D, 3);
-                Cx<double>* sd[4] = {specD(0), specD(1), specD(2), specD(3)};
+                Cx<T>* P0 = specD_t<T>(3 * F);
+                row_r2c<T>(b.c[0], P0, 3, sb, g.S);
+                col_div(P0, P0 + g.S, P0 + 2 * g.S, P0, P0 + 2 * g.S, 0);
+                Cx<double>* sd[3] = {specD(0), specD(1), specD(2)};
                 Cx<T>* sf[3] = {specF(0), specF(1), specF(2)};
-                middle<7>(sd, sf);
+                Cx<T>* sq[2] = {P0, P0 + 2 * g.S};
+                middle<8>(sd, sf, 0, 1, 0, sq);
                 col_fft_inv(specF(0), specF(0), 0, 3, g.S);
                 row_c2r(specF(0), out.c[0], b.c[0], 3, so, g.S);
                 return;
             }
-            spec_forward(D, 1);
+            // slabs: P_a in T slots from complex128 slot 1 (spec_forward keeps slot 0 and scratch slots 6, 7),
+            // Q / R in the split layout, transposed into P1 / P2's slots; kind 9 per component (same bits)
+            Cx<T>* P0 = specD_t<T>(1 * F);
+            for (int cc = 0; cc < 3; ++cc) row_r2c<T>(b.c[cc], P0 + (size_t)cc * g.S);
+            col_div(P0, P0 + g.S, P0 + 2 * g.S, P0 + 3 * g.S, P0 + 4 * g.S, nb());
+            const size_t chunk = (size_t)g.n3 * nb() * g.n1p * sizeof(Cx<T>);
+            alltoall(P0 + 3 * g.S, P0, chunk);
+            alltoall(P0 + 4 * g.S, P0 + g.S, chunk);
+            Cx<T>* sq[2] = {P0, P0 + g.S};
             for (int cc = 0; cc < 3; ++cc) {
                 spec_forward(u.c[cc], 0);
-                Cx<double>* sd[2] = {specD(0), specD(1)};
+                Cx<double>* sd[1] = {specD(0)};
                 Cx<T>* sf = specF(0);
-                middle<6>(sd, &sf, cc);
+                middle<9>(sd, &sf, cc, 1, 0, sq);
                 spec_inverse(0, out.c[cc], b.c[cc]);
             }
         } else {

@@ -840,6 +840,54 @@ struct ColFftPass {
     }
 };
 
+// Isochoric data term, x2 stage (L b~ = b~ - grad Lap^-1 div b~, Eq. 4): from the x1 half
+// spectra P_a = F1 b~_a of the three components it forms Q = i (k1' F2 P_1 + k2' F2 P_2) and R = F2 P_3,
+// so that the x3 middle pass obtains F[div b~] = F3 Q + i k3' F3 R (the spectral divergence with the
+// Nyquist wavenumbers zeroed, as the derivative passes take it) -- no real-space derivative passes and
+// no forward transform of div b~.  Q may alias P_1 and R alias P_3 in the plain layout (every element is
+// read by its own CTA before that CTA writes it); SPLIT_OUT writes the all-to-all split layout (slabs).
+template <typename T, int L, bool SPLIT_OUT = false>
+struct ColDivPass {
+    using CC = ColCfg<L, T, 2, ColCap<L, T>::V>;
+    static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT, LINES = CC::LINES;
+    static constexpr int MINB = MinB<T, NT>::V;
+    static constexpr bool TWS = sizeof(T) == 4;
+    static constexpr size_t BUF = CC::SMEM + (TWS ? L * sizeof(Cx<T>) : 0);  // + twiddles
+    ColGeom c;
+    const Cx<T>* p1;
+    const Cx<T>* p2;
+    const Cx<T>* p3;
+    Cx<T>* q;
+    Cx<T>* r;
+    const Cx<T>* tw;
+    int nb_out;
+    int n1;  // real x1 extent: column n1 / 2 is the x1 Nyquist
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int x = x0 + xi, o = o0 + oi;
+        const bool on = x < c.nx && o < c.n3;
+        Cx<T>* bA = sm + (oi * XC + xi) * LP;
+        Cx<T>* bB = bA + LINES * LP;
+        const Cx<T>* tw = tw_smem<T, L, NT, TWS>(this->tw, reinterpret_cast<Cx<T>*>(smem + CC::SMEM));
+        fft_line_io<T, L, -1, false, true>(bA, t, tw, 1, col_acc<2>(const_cast<Cx<T>*>(p1), c, x, o, 0, on, 0),
+                                           SmemLine<T>{bA});
+        fft_line_io<T, L, -1, false, true>(bB, t, tw, 1, col_acc<2>(const_cast<Cx<T>*>(p2), c, x, o, 0, on, 0),
+                                           SmemLine<T>{bB});
+        const T k1 = (T)((x == n1 / 2) ? 0 : x);
+        const auto qa = col_acc<2, T, SPLIT_OUT>(q, c, x, o, nb_out, on, 0);
+        for (int p = t; p < L; p += TPL) {
+            const T k2 = (T)wavenum_odd(p, L);
+            qa.st(p, mul_i(scale(bA[P(p)], k1) + scale(bB[P(p)], k2), T(1)));
+        }
+        __syncthreads();  // bA is the next transform's line buffer
+        fft_line_io<T, L, -1, false, false>(bA, t, tw, 1, col_acc<2>(const_cast<Cx<T>*>(p3), c, x, o, 0, on, 0),
+                                            col_acc<2, T, SPLIT_OUT>(r, c, x, o, nb_out, on, 0));
+    }
+};
+
 // ---------------------------------------------------------------------------------------------
 // Spectral symbols applied in the x3 middle pass.  k = (k1, k2, k3) signed wavenumbers,
 // kp = (k1', k2', k3') with the Nyquist zeroed.  `norm` = full inverse normalisation 2/M.
@@ -863,10 +911,13 @@ __device__ __forceinline__ T sym_a(const SymInfo& s, T kk) { return s.reg == 1 ?
 //         D = F[div b~]: L b~ = b~ - grad Lap^-1 div b~, whose b~ part is added in real space)
 // kind 7: kind 6 for the three components in one pass (4 -> 3: V_0, V_1, V_2, D; MiddlePass::run7 reads
 //         and transforms D once, then each V_c in turn through one input and one output line buffer)
+// kind 8: kind 6 for the three components with D formed in the pass from the x2 stage of the data term
+//         (ColDivPass): D = F3 Q + i k3' F3 R, Q and R in the I/O precision (MiddlePass::run_div; 3 -> 3 plus
+//         the two spectra inq); kind 9: the same for one component (comp = SymInfo::comp; slabs)
 template <typename T, int KIND>
 struct Sym {
-    static constexpr int NCI = (KIND <= 1) ? 1 : (KIND == 6 ? 2 : (KIND == 7 ? 4 : (KIND >= 4 ? 6 : 3)));
-    static constexpr int NCO = (KIND <= 1 || KIND == 6) ? 1 : 3;
+    static constexpr int NCI = (KIND <= 1 || KIND == 9) ? 1 : (KIND == 6 ? 2 : (KIND == 7 ? 4 : (KIND == 8 ? 3 : (KIND >= 4 ? 6 : 3))));
+    static constexpr int NCO = (KIND <= 1 || KIND == 6 || KIND == 9) ? 1 : 3;
     static __device__ __forceinline__ void apply(const SymInfo& s, Cx<T>* x, int k1, int k2, int k3, int kp1, int kp2,
                                                  int kp3) {
         const T kk = T(k1) * T(k1) + T(k2) * T(k2) + T(k3) * T(k3);
@@ -962,7 +1013,8 @@ template <typename Ti, typename To, int L, int KIND, bool PEER = false>
 struct MiddlePass {
     using T = Ti;
     static constexpr int NCI = Sym<T, KIND>::NCI, NCO = Sym<T, KIND>::NCO;
-    static constexpr int NCIS = KIND == 7 ? 2 : NCI, NCOS = KIND == 7 ? 1 : NCO;  // line buffers in shared memory
+    // line buffers in shared memory (kinds 8 / 9: one Ti buffer for V_c, two To buffers for Q / D and R / output)
+    static constexpr int NCIS = KIND == 7 ? 2 : (KIND >= 8 ? 1 : NCI), NCOS = KIND == 7 ? 1 : (KIND >= 8 ? 2 : NCO);
     using CC = ColCfg<L, T, NCIS, (sizeof(T) == 8 && L >= 512) ? 128 : 0>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, LINES = CC::LINES, NT = CC::NT;
     static constexpr int LPO = ColLP<L, To, XC>::V;  // stride of the To lines of the inverse
@@ -975,6 +1027,7 @@ struct MiddlePass {
     ColGeom c;
     SpecPtrs<Ti, NCI> in;
     SpecPtrs<To, NCO> out;
+    SpecPtrs<To, 2> inq;  // kinds 8 / 9: Q, R of ColDivPass
     SymInfo s;
     const Cx<Ti>* tw;
     const Cx<To>* two;  // inverse twiddles in To
@@ -992,19 +1045,21 @@ struct MiddlePass {
         const Cx<To>* two = tw_smem<To, L, NT, TWS>(this->two, reinterpret_cast<Cx<To>*>(smem + BUFO + L * sizeof(Cx<T>)));
         if constexpr (KIND == 7) {
             run7(x0, o0, xi, t, oi, line, on, tw, two, sm, so);
-            return;
-        }
-        if constexpr (KIND <= 1) {  // scalar symbol fused into the last forward stage
-            const int og = o0 + oi + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
-            const T k1 = (T)(x0 + xi), k2 = (T)wavenum(og, n2g);
-            Cx<T>* buf = sm + line * LP;
-            fft_line_io<T, L, -1, false, true>(
-                buf, t, tw, 1, col_acc<3>(in.p[0] + blockIdx.y * cs, c, x0 + xi, o0 + oi, 0, on, 0),
-                SymSt<T, To, L, KIND>{so + line * LPO, k1 * k1 + k2 * k2, (T)s.norm, (T)s.beta, s.reg, on});
+        } else if constexpr (KIND >= 8) {
+            run_div(x0, o0, xi, t, oi, line, on, tw, two, sm, so);
         } else {
-            forward_and_symbol(x0, o0, xi, t, oi, line, on, tw, sm, so);
+            if constexpr (KIND <= 1) {  // scalar symbol fused into the last forward stage
+                const int og = o0 + oi + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
+                const T k1 = (T)(x0 + xi), k2 = (T)wavenum(og, n2g);
+                Cx<T>* buf = sm + line * LP;
+                fft_line_io<T, L, -1, false, true>(
+                    buf, t, tw, 1, col_acc<3>(in.p[0] + blockIdx.y * cs, c, x0 + xi, o0 + oi, 0, on, 0),
+                    SymSt<T, To, L, KIND>{so + line * LPO, k1 * k1 + k2 * k2, (T)s.norm, (T)s.beta, s.reg, on});
+            } else {
+                forward_and_symbol(x0, o0, xi, t, oi, line, on, tw, sm, so);
+            }
+            inverse(x0, o0, two, so);
         }
-        inverse(x0, o0, two, so);
     }
     __device__ __forceinline__ void forward_and_symbol(int x0, int o0, int xi, int t, int oi, int line, bool on,
                                                        const Cx<T>* tw, Cx<T>* sm, Cx<To>* so) const {
@@ -1063,6 +1118,64 @@ struct MiddlePass {
             }
             __syncthreads();
             inverse_one(cc, 0, x0, o0, two, so);
+        }
+    }
+    // forward x3 transform in To of a To spectrum into line buffer set sb (the inverse's thread mapping)
+    __device__ __forceinline__ void forward_o(const Cx<To>* src, Cx<To>* sb, int x0, int o0, const Cx<To>* two) const {
+        constexpr int PER = NT / TPLO;  // lines per round
+        static_assert(NT % TPLO == 0 && LINES % PER == 0, "forward_o thread mapping");
+#pragma unroll
+        for (int l0 = 0; l0 < LINES; l0 += PER) {
+            const int lxi = threadIdx.x % XC;
+            const int rr = threadIdx.x / XC;
+            const int lt = rr % TPLO, loi = l0 / XC + rr / TPLO;
+            const int ln = loi * XC + lxi;
+            const bool lon = x0 + lxi < c.nx && o0 + loi < c.n2;
+            Cx<To>* buf = sb + ln * LPO;
+            fft_line_io<To, L, -1, false, true>(buf, lt, two, 1,
+                                                col_acc<3>(const_cast<Cx<To>*>(src), c, x0 + lxi, o0 + loi, 0, lon, 0),
+                                                SmemLine<To>{buf});
+        }
+    }
+    // kinds 8 / 9: D = F3 Q + i k3' F3 R once (To), then per component c: V_c forward (Ti), the kind-6 symbol
+    // of component c with D widened to Ti, narrowed into R's buffer, inverse to the output
+    __device__ __forceinline__ void run_div(int x0, int o0, int xi, int t, int oi, int line, bool on, const Cx<T>* tw,
+                                            const Cx<To>* two, Cx<T>* sm, Cx<To>* so) const {
+        Cx<To>* bQ = so;
+        Cx<To>* bR = so + LINES * LPO;
+        forward_o(inq.p[0], bQ, x0, o0, two);
+        forward_o(inq.p[1], bR, x0, o0, two);
+        for (int e = threadIdx.x; e < LINES * L; e += NT) {
+            const int ln = e / L, p = e % L;
+            const To k3 = (To)wavenum_odd(p, L);
+            bQ[ln * LPO + P(p)] = bQ[ln * LPO + P(p)] + mul_i(bR[ln * LPO + P(p)], k3);
+        }
+        __syncthreads();
+        const int n1 = 2 * (c.nx - 1);
+        constexpr int NCC = KIND == 8 ? 3 : 1;
+        for (int ci = 0; ci < NCC; ++ci) {
+            const Cx<T>* vin = KIND == 8 ? in.p[ci] : in.p[0] + blockIdx.y * cs;
+            fft_line_io<T, L, -1, false, true>(sm + line * LP, t, tw, 1,
+                                               col_acc<3>(const_cast<Cx<T>*>(vin), c, x0 + xi, o0 + oi, 0, on, 0),
+                                               SmemLine<T>{sm + line * LP});
+            SymInfo sc = s;
+            sc.comp = KIND == 8 ? ci : s.comp;
+            for (int e = threadIdx.x; e < LINES * L; e += NT) {
+                const int ln = e / L, p = e % L;
+                const int lxi = ln % XC, loi = ln / XC;
+                const int x = x0 + lxi, o = o0 + loi;
+                const Cx<To> d = bQ[ln * LPO + P(p)];
+                Cx<T> v[2] = {sm[ln * LP + P(p)], cx<T>((T)d.re, (T)d.im)};
+                if (x < c.nx && o < c.n2) {
+                    const int og = o + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
+                    const int k1 = x, k2 = wavenum(og, n2g), k3 = wavenum(p, L);
+                    const int kp1 = (x == n1 / 2) ? 0 : x, kp2 = wavenum_odd(og, n2g), kp3 = wavenum_odd(p, L);
+                    Sym<T, 6>::apply(sc, v, k1, k2, k3, kp1, kp2, kp3);
+                }
+                bR[ln * LPO + P(p)] = cx<To>((To)v[0].re, (To)v[0].im);
+            }
+            __syncthreads();
+            inverse_one(KIND == 8 ? ci : 0, 1, x0, o0, two, so);
         }
     }
     __device__ __forceinline__ void inverse(int x0, int o0, const Cx<To>* two, Cx<To>* so) const {

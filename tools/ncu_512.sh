@@ -1,0 +1,17 @@
+#!/bin/bash
+# ncu --set full of the 512^3 column passes (x2 fp64 forward, KIND-7 middle, x3 derivative) in one isochoric matvec
+set -u
+TAG=$1
+mkdir -p gpurun_out
+for spec in "ColFftPass<double, .int.512, .int.-1:0" "MiddlePass<double, float, .int.512, .int.7:0" "ColDerivPass<float, .int.512, .int.3:0" "ColFftPass<float, .int.512, .int.1:0"; do
+  K=${spec%:*}; S=${spec##*:}; N=$(echo "$K" | tr -c 'A-Za-z0-9' '_')
+  timeout 900 ncu --set full --metrics lts__t_sectors_srcunit_tex_op_read.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --import-source on --kernel-name-base demangled \
+    -k "regex:${K}" -s $S -c 1 -o gpurun_out/prof_${TAG}_$N python tools/prof_config4b.py > gpurun_out/ncu_${TAG}_$N.log 2>&1
+  R=gpurun_out/prof_${TAG}_$N.ncu-rep
+  if [ -f $R ]; then
+    python tools/ncu_summary.py $R > gpurun_out/summary_${TAG}_$N.txt 2>&1; head -24 gpurun_out/summary_${TAG}_$N.txt
+    ncu -i $R --page raw --csv > gpurun_out/raw_${TAG}_$N.csv 2>/dev/null
+    ncu -i $R --page details > gpurun_out/details_${TAG}_$N.txt 2>/dev/null
+    rm -f $R
+  else grep -i "warn\|error" gpurun_out/ncu_${TAG}_$N.log | head -3; fi
+done
