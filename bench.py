@@ -109,12 +109,15 @@ def algo_bytes(tag, n, nt, es=4):
         "col_middle_f64": 2, "col_middle_f32": 2, "row_c2r": 2,
         "row_c2r_add": 3,                  # + the b~ read
         "row_deriv": 2, "col_deriv": 2,
+        "col_div": 5,                      # isochoric data term x2 stage: P_1..P_3 read, Q and R written
         "sub": 3, "dstar": 6,
     }
-    base = tag[:-3] if tag.endswith("_x3") else tag
+    import re
+    m = re.match(r"(.*)_x(\d+)$", tag)  # batched launches: "_xK" = K components / fields in one launch
+    base, k = (m.group(1), int(m.group(2))) if m else (tag, 1)
     if base not in v:
         return None
-    return int(round((3 if tag.endswith("_x3") else 1) * v[base] * es * M))
+    return int(round(k * v[base] * es * M))
 
 
 MATVEC_VALUES = lambda nt: 21 * nt + 47  # noqa: E731  §8(d) matvec total, non-isochoric (131 at n_t = 4)

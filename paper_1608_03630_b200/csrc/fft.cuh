@@ -282,8 +282,11 @@ struct RowDerivPass {
     T* out;
     int accumulate;
     const Cx<T>* twN;
+    int64_t cs = 0, cso = 0;  // element strides of f / out between the fields of a batch (blockIdx.y)
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        const T* f = this->f + blockIdx.y * cs;
+        T* out = this->out + blockIdx.y * cso;
         const int64_t nrows = (int64_t)g.n2 * g.n3;
         const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
         int64_t row = (int64_t)tile * RB + line;
@@ -777,8 +780,11 @@ struct ColDerivPass {
     Cx<T>* dst;
     int accumulate;
     const Cx<T>* tw;
+    int64_t cs = 0, cso = 0;  // complex-element strides of src / dst between the fields of a batch (blockIdx.y)
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         Cx<T>* sm = reinterpret_cast<Cx<T>*>(smem);
+        const Cx<T>* src = this->src + blockIdx.y * cs;
+        Cx<T>* dst = this->dst + blockIdx.y * cso;
         int x0, o0, xi, t, oi;
         col_origin<XC, OL>(c, tile, x0, o0);
         col_thread<XC, TPL>(xi, t, oi);
