@@ -1,9 +1,9 @@
 #!/bin/bash
-# ncu --set full of the 512^3 column passes (x2 fp64 forward, KIND-7 middle, x3 derivative) in one isochoric matvec
+# ncu --set full of the 512^3 column passes (isochoric kind-8 middle, ColDivPass, non-isochoric kind-0 middle)
 set -u
 TAG=$1
 mkdir -p gpurun_out
-for spec in "ColFftPass<double, .int.512, .int.-1:0" "MiddlePass<double, float, .int.512, .int.7:0" "ColDerivPass<float, .int.512, .int.3:0" "ColFftPass<float, .int.512, .int.1:0"; do
+for spec in "MiddlePass<double, float, .int.512, .int.8:0" "ColDivPass<float, .int.512:0" "MiddlePass<double, float, .int.512, .int.0:0"; do
   K=${spec%:*}; S=${spec##*:}; N=$(echo "$K" | tr -c 'A-Za-z0-9' '_')
   timeout 900 ncu --set full --metrics lts__t_sectors_srcunit_tex_op_read.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:${K}" -s $S -c 1 -o gpurun_out/prof_${TAG}_$N python tools/prof_config4b.py > gpurun_out/ncu_${TAG}_$N.log 2>&1
