@@ -110,7 +110,7 @@ def algo_bytes(tag, n, nt, es=4):
         "row_c2r_add": 3,                  # + the b~ read
         "row_deriv": 2, "col_deriv": 2,
         "col_div": 5,                      # isochoric data term x2 stage: P_1..P_3 read, Q and R written
-        "sub": 3, "dstar": 6,
+        "sub": 3, "dstar": 6, "dstar_plan": 6,  # d* = c v written while its tile plan is taken
     }
     import re
     m = re.match(r"(.*)_x(\d+)$", tag)  # batched launches: "_xK" = K components / fields in one launch

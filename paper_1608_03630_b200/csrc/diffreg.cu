@@ -1122,6 +1122,14 @@ struct Impl {
         k_sl_plan<T><<<(unsigned)n_tiles(g), SL_THREADS, 0, s>>>(g, d, plan_buf, mx);
         PE("sl_plan");
     }
+    // d = (c0 v0, c1 v1, c2 v2) written while its plan is taken (the first stage of Eq. 6)
+    void dstar_plan(T* d, int* plan_buf, T c0, T c1, T c2) {
+        int* mx = c.at<int>(c.L.maxext);
+        PB("dstar_plan");
+        k_sl_plan<T, true><<<(unsigned)n_tiles(g), SL_THREADS, 0, s>>>(g, d, plan_buf, mx,
+                                                                        DstarIn<T>{{vc(0), vc(1), vc(2)}, {c0, c1, c2}});
+        PE("dstar_plan");
+    }
 
     // ---------------------------------------------------------------- off-rank departure points
     // device arrays of remote plan f (0: d*, 1: d+, 2: d-): [ids_out][ids_in][rec_out][rec_in][val_out][val_in]
@@ -1331,11 +1339,7 @@ struct Impl {
         const double dtt = 1.0 / c.cfg.nt;
         for (int sg = 1; sg >= -1; sg -= 2) {
             T* dout = sg > 0 ? dplus() : dminus();
-            PB("dstar");
-            k_dstar<T><<<grid_1d(g.M), 256, 0, s>>>(g, vc(0), vc(1), vc(2), tmp3(), (T)(sg * dtt / h[0]),
-                                                    (T)(sg * dtt / h[1]), (T)(sg * dtt / h[2]));
-            PE("dstar");
-            plan(tmp3(), plan_t());
+            dstar_plan(tmp3(), plan_t(), (T)(sg * dtt / h[0]), (T)(sg * dtt / h[1]), (T)(sg * dtt / h[2]));
             remote_plan(0, tmp3());
             for (int a = 0; a < 3; ++a) {
                 EpiDeparture1<T> e{dout + (size_t)a * g.M, vc(a), (T)(sg * 0.5 * dtt / h[a])};

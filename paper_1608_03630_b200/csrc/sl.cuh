@@ -111,9 +111,17 @@ __device__ __forceinline__ void tile_coords(const Grid& g, int tile, int& x0, in
 // points, and the running maximum extents over all tiles (for sizing shared memory).
 // maxext[0..2]: running maximum box extents; maxext[3] is set to 1 when, in slab mode, a tile's box
 // leaves the rank's planes plus ghosts (the displacement exceeds the ghost width: DR_ERR_PLAN).
+// DSTAR: d is written here, d_a = c_a v_a (the first-stage displacement of Eq. 6, c_a = sigma dt / h_a),
+// while its plan is taken -- one pass over v instead of a separate d pass and a plan pass over d.
 template <typename T>
-__global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restrict__ d, int* __restrict__ plan,
-                                                        int* __restrict__ maxext) {
+struct DstarIn {
+    const T* v[3];
+    T c[3];
+};
+template <typename T, bool DSTAR = false>
+__global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restrict__ d_in, int* __restrict__ plan,
+                                                        int* __restrict__ maxext, DstarIn<T> ds = DstarIn<T>{}) {
+    T* d = const_cast<T*>(d_in);
     __shared__ int red[6];
     if (threadIdx.x < 6) red[threadIdx.x] = (threadIdx.x < 3) ? INT_MAX : INT_MIN;
     __syncthreads();
@@ -129,9 +137,16 @@ __global__ void __launch_bounds__(SL_THREADS) k_sl_plan(Grid g, const T* __restr
             const int ii[3] = {x, y, z + g.z0};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
+                T da;
+                if constexpr (DSTAR) {
+                    da = ds.c[a] * ds.v[a][id];
+                    d[a * g.M + id] = da;
+                } else {
+                    da = d[a * g.M + id];
+                }
                 int q;
                 T t;
-                cell_of<T>(ii[a], d[a * g.M + id], q, t);
+                cell_of<T>(ii[a], da, q, t);
                 mn[a] = min(mn[a], q);
                 mx[a] = max(mx[a], q);
             }
@@ -1178,18 +1193,6 @@ __global__ void k_remote_fixup(const int* __restrict__ ids, const T* __restrict_
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = val[(size_t)i * NC + c];
         epi.store(id, v, epi.late(id));
-    }
-}
-
-// First-stage displacement of Eq. 6: d* = sigma dt v / h (cells), X* = x - h d*.  v: component pointers
-// (slab interiors), dstar: [3][M].
-template <typename T>
-__global__ void k_dstar(Grid g, const T* __restrict__ v0, const T* __restrict__ v1, const T* __restrict__ v2,
-                        T* __restrict__ dstar, T c0, T c1, T c2) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.M; e += (int64_t)gridDim.x * blockDim.x) {
-        dstar[e] = c0 * v0[e];
-        dstar[g.M + e] = c1 * v1[e];
-        dstar[2 * g.M + e] = c2 * v2[e];
     }
 }
 
