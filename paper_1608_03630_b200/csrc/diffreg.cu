@@ -54,6 +54,14 @@ int ilog2(int n) {
     return l;
 }
 bool pow2_in_range(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
+// x2 extents that are not powers of two (one rank): even, 6 .. 510, transformed by Bluestein's chirp-z
+// form through power-of-two FFTs of length M >= 2 N2 - 1 <= 1024 (fft.cuh ColBlue*)
+bool blue_len(int n) { return n >= 6 && n <= 510 && n % 2 == 0 && (n & (n - 1)) != 0; }
+int blue_m(int n) {
+    int m = 1;
+    while (m < 2 * n - 1) m <<= 1;
+    return m;
+}
 
 // Ghost planes of a slab: the stencil of a departure point s3 spans floor(s3)-1 ..
 // floor(s3)+2, so (g, g + 1) planes cover x3 displacements |d3| <= g - 1 cells.  Default (4, 5).
@@ -64,7 +72,7 @@ int ghost_hi(const dr_config* c) { return c->ghost_hi > 0 ? c->ghost_hi : GHOST_
 dr_status validate(const dr_config* c, int nranks = 1) {
     if (!c) return DR_ERR_ARG;
     for (int a = 0; a < 3; ++a)
-        if (!pow2_in_range(c->n[a])) return DR_ERR_GRID;
+        if (!pow2_in_range(c->n[a]) && !(a == 1 && nranks == 1 && blue_len(c->n[a]))) return DR_ERR_GRID;
     if (c->nt < 1 || c->nt > 64) return DR_ERR_PARAM;
     if (c->reg != DR_REG_H1 && c->reg != DR_REG_H2) return DR_ERR_PARAM;
     if (!(c->beta > 0.0) || !std::isfinite(c->beta)) return DR_ERR_PARAM;
@@ -115,7 +123,7 @@ struct Layout {
     int64_t rcap = 0;
     size_t rem = 0;
     size_t kry, sN, bN, sc, rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
-        plan_m, plan_t, maxext, red, pflags, twx, twy, twz, twxd, twyd, twzd, total;
+        plan_m, plan_t, maxext, red, pflags, twx, twy, twz, twxd, twyd, twzd, blue, total;
 };
 
 Layout layout(const dr_config* c, int nranks = 1) {
@@ -180,6 +188,9 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.twxd = take((size_t)g.n1 * 16);
     L.twyd = take((size_t)g.n2 * 16);
     L.twzd = take((size_t)g.n3g * 16);
+    // Bluestein tables of a non-power-of-two x2 extent (fp64): twM[M], w_fwd[N], w_inv[N], bhat_fwd[M],
+    // bhat_inv[M]
+    L.blue = blue_len(g.n2) ? take((size_t)(3 * blue_m(g.n2) + 2 * g.n2) * 16) : 0;
     L.total = off;
     return L;
 }
@@ -499,7 +510,58 @@ struct Impl {
         CK(cudaMemcpyAsync(c.ws + off, h.data(), sizeof(Cx<U>) * n, cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
     }
+    // Bluestein tables (fft.cuh ColBlue*, fp64), from long double: w_j = e^{D i pi (j^2 mod 2N) / N},
+    // b_j = conj(w_j) for |j| < N placed circularly in M, bhat = DFT_M(b) / M (direct sum: M <= 1024)
+    void fill_blue(size_t off) {
+        const int n = g.n2, M = blue_m(n);
+        const long double pi = 3.141592653589793238462643383279502884L;
+        std::vector<Cx<double>> h((size_t)3 * M + 2 * n);
+        for (int m = 0; m < M; ++m) {
+            const long double a = -2.0L * pi * (long double)m / (long double)M;
+            h[m] = Cx<double>{(double)std::cos(a), (double)std::sin(a)};
+        }
+        for (int d = 0; d < 2; ++d) {
+            const long double sg = d == 0 ? -1.0L : 1.0L;
+            std::vector<long double> wr(n), wi(n);
+            for (int j = 0; j < n; ++j) {
+                const long long q = ((long long)j * j) % (2LL * n);
+                const long double a = sg * pi * (long double)q / (long double)n;
+                wr[j] = std::cos(a);
+                wi[j] = std::sin(a);
+                h[(size_t)M + (size_t)d * n + j] = Cx<double>{(double)wr[j], (double)wi[j]};
+            }
+            std::vector<long double> br(M, 0.0L), bi(M, 0.0L);
+            for (int j = 0; j < n; ++j) {
+                br[j] = wr[j];
+                bi[j] = -wi[j];
+                if (j > 0) {
+                    br[M - j] = wr[j];
+                    bi[M - j] = -wi[j];
+                }
+            }
+            for (int k = 0; k < M; ++k) {
+                long double sr = 0.0L, si = 0.0L;
+                for (int j = 0; j < M; ++j) {
+                    if (br[j] == 0.0L && bi[j] == 0.0L) continue;
+                    const long double a = -2.0L * pi * (long double)(((long long)j * k) % M) / (long double)M;
+                    const long double cr = std::cos(a), ci = std::sin(a);
+                    sr += br[j] * cr - bi[j] * ci;
+                    si += br[j] * ci + bi[j] * cr;
+                }
+                h[(size_t)M + 2 * n + (size_t)d * M + k] = Cx<double>{(double)(sr / M), (double)(si / M)};
+            }
+        }
+        CK(cudaMemcpyAsync(c.ws + off, h.data(), h.size() * sizeof(Cx<double>), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    BlueTab bluetab() {
+        const int n = g.n2, M = blue_m(n);
+        const Cx<double>* t = reinterpret_cast<const Cx<double>*>(c.ws + c.L.blue);
+        return BlueTab{t, {t + M, t + M + n}, {t + M + 2 * n, t + 2 * M + 2 * n}, n};
+    }
+    bool blue2() const { return blue_len(g.n2); }
     void init_twiddles() {
+        if (blue2()) fill_blue(c.L.blue);
         fill_twiddles<T>(g.n1, c.L.twx);
         fill_twiddles<T>(g.n2, c.L.twy);
         fill_twiddles<T>(g.n3g, c.L.twz);
@@ -721,6 +783,51 @@ struct Impl {
     ColGeom spec_geom_t() const { return ColGeom{g.n1p, g.n1c, nb(), g.n3g, c.rank * nb(), g.n2}; }
     ColGeom pair_geom_t() const { return ColGeom{g.n1 / 2, g.n1 / 2, nb(), g.n3g, c.rank * nb(), g.n2}; }
 
+    // ---- x2 passes of a non-power-of-two extent (Bluestein, fft.cuh ColBlue*; one rank)
+#define DR_SWITCH_BLUE(Mval, call)                          \
+    switch (Mval) {                                         \
+        case 16: call(16); break;                           \
+        case 32: call(32); break;                           \
+        case 64: call(64); break;                           \
+        case 128: call(128); break;                         \
+        case 256: call(256); break;                         \
+        case 512: call(512); break;                         \
+        case 1024: call(1024); break;                       \
+        default: fail(DR_ERR_GRID, "unsupported x2 length"); \
+    }
+    template <typename U, int M, int DIR>
+    void blue_fft_M(const Cx<U>* src, Cx<U>* dst, int nc, int64_t cs, int64_t csd) {
+        using PT = ColBlueFftPass<U, M, DIR>;
+        const ColGeom cg = spec_geom();
+        const char* tag = DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32";
+        stream(tag, PT{cg, src, dst, bluetab(), cs, csd}, col_tiles<PT>(cg, g.n3), nc);
+    }
+    template <typename U, int DIR>
+    void blue_fft(const Cx<U>* src, Cx<U>* dst, int nc, int64_t cs, int64_t csd) {
+#define CALL(MM) blue_fft_M<U, MM, DIR>(src, dst, nc, cs, csd)
+        DR_SWITCH_BLUE(blue_m(g.n2), CALL)
+#undef CALL
+    }
+    template <int M>
+    void blue_deriv_M(const T* f, T* out, int acc, int nf, int64_t fs, int64_t os) {
+        using PT = ColBlueDerivPass<T, M>;
+        const ColGeom cg = pair_geom();
+        stream("col_deriv", PT{cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, bluetab(),
+                               fs / 2, os / 2},
+               col_tiles<PT>(cg, cg.n3), nf);
+    }
+    void blue_deriv(const T* f, T* out, int acc, int nf = 1, int64_t fs = 0, int64_t os = 0) {
+#define CALL(MM) blue_deriv_M<MM>(f, out, acc, nf, fs, os)
+        DR_SWITCH_BLUE(blue_m(g.n2), CALL)
+#undef CALL
+    }
+    template <int M>
+    void blue_div_M(const Cx<T>* p1, const Cx<T>* p2, const Cx<T>* p3, Cx<T>* q, Cx<T>* r) {
+        using PT = ColBlueDivPass<T, M>;
+        const ColGeom cg = spec_geom();
+        stream("col_div", PT{cg, p1, p2, p3, q, r, bluetab(), g.n1}, col_tiles<PT>(cg, g.n3));
+    }
+
     template <int L, int AX>
     void col_deriv_L(const ColGeom& cg, const T* f, T* out, int acc, int nf = 1, int64_t fs = 0, int64_t os = 0) {
         using PT = ColDerivPass<T, L, AX>;
@@ -730,6 +837,10 @@ struct Impl {
     }
     // out (+)= d f / dx_ax (1-D transforms along the axis only); x3 on slabs transposes first
     void col_deriv(int ax, const T* f, T* out, int acc) {
+        if (ax == 2 && blue2()) {
+            blue_deriv(f, out, acc);
+            return;
+        }
         if (ax == 2) {
 #define CALL(LL) col_deriv_L<LL, 2>(pair_geom(), f, out, acc)
             DR_SWITCH_COL(g.n2, CALL)
@@ -778,6 +889,10 @@ struct Impl {
     // (csd: component stride of dst when it differs from src's cs)
     template <typename Tc>
     void col_fft_fwd(const Cx<Tc>* src, Cx<Tc>* dst, int nb_out, int nc = 1, int64_t cs = 0, int64_t csd = -1) {  // forward along x2, in Tc
+        if (blue2()) {  // one rank: nb_out == 0
+            blue_fft<Tc, -1>(src, dst, nc, cs, csd);
+            return;
+        }
 #define CALL(LL) col_fft_L<Tc, LL, -1>(src, dst, twy_t<Tc>(), 0, nb_out, nc, cs, csd)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
@@ -791,6 +906,10 @@ struct Impl {
         stream(sizeof(Tc) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32", pt, col_tiles<PT>(cg, g.n3), 1);
     }
     void col_fft_inv(const Cx<T>* src, Cx<T>* dst, int nb_in, int nc = 1, int64_t cs = 0, int64_t csd = -1) {  // inverse along x2, in T
+        if (blue2()) {  // one rank: nb_in == 0
+            blue_fft<T, +1>(src, dst, nc, cs, csd);
+            return;
+        }
 #define CALL(LL) col_fft_L<T, LL, +1>(src, dst, twy(), nb_in, 0, nc, cs, csd)
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
@@ -805,6 +924,12 @@ struct Impl {
         stream("col_div", PT{cg, p1, p2, p3, q, r, twy_t<T>(), nb_out, g.n1}, col_tiles<PT>(cg, g.n3));
     }
     void col_div(const Cx<T>* p1, const Cx<T>* p2, const Cx<T>* p3, Cx<T>* q, Cx<T>* r, int nb_out) {
+        if (blue2()) {  // one rank
+#define CALL(MM) blue_div_M<MM>(p1, p2, p3, q, r)
+            DR_SWITCH_BLUE(blue_m(g.n2), CALL)
+#undef CALL
+            return;
+        }
 #define CALL(LL) (nb_out ? col_div_L<LL, true>(p1, p2, p3, q, r, nb_out) : col_div_L<LL, false>(p1, p2, p3, q, r, 0))
         DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
@@ -914,9 +1039,13 @@ struct Impl {
 #define CALL(LL) row_deriv_L<LL>(f, out, 0, nf, fs, os)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
+        if (blue2()) {
+            blue_deriv(f, out + g.M, 0, nf, fs, os);
+        } else {
 #define CALL(LL) col_deriv_L<LL, 2>(pair_geom(), f, out + g.M, 0, nf, fs, os)
-        DR_SWITCH_COL(g.n2, CALL)
+            DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
+        }
 #define CALL(LL) col_deriv_L<LL, 3>(pair_geom(), f, out + 2 * g.M, 0, nf, fs, os)
         DR_SWITCH_COL(g.n3, CALL)
 #undef CALL

@@ -895,6 +895,154 @@ struct ColDivPass {
 };
 
 // ---------------------------------------------------------------------------------------------
+// x2 lines of a length N that is not a power of two (the paper's 256 x 300 x 256 grid; SURVEY
+// §8(b) admits any even N >= 4): Bluestein's chirp-z form of the length-N DFT, X_k = w_k sum_n (x_n w_n)
+// conj(w_{k-n}) with w_j = e^{DIR i pi j^2 / N} (nk = (n^2 + k^2 - (k - n)^2) / 2), i.e. a circular
+// convolution evaluated with two radix-16 FFTs of the power of two M >= 2N - 1 and the precomputed
+// transform bhat = FFT_M(b) / M of the chirp b_j = conj(w_j), j in (-N, N).  chirp[n] = w_n per direction.
+// The arithmetic is fp64 whatever the I/O type: an fp32 convolution of length M ~ 2N leaves a white
+// rounding floor that odd symbols (k' / N up to N / 2) amplify past the 1e-5 operator bar.
+template <typename Ti>
+struct AccD {  // a column accessor in the I/O type, seen in double
+    ColAcc<Ti> a;
+    __device__ __forceinline__ Cx<double> ld(int i) const {
+        const Cx<Ti> v = a.ld(i);
+        return cx<double>((double)v.re, (double)v.im);
+    }
+    __device__ __forceinline__ void st(int i, const Cx<double>& v) const { a.st(i, cx<Ti>((Ti)v.re, (Ti)v.im)); }
+};
+template <class Src>
+struct ChirpLd {  // a_j = w_j x_j (j < n), zero padding up to M
+    Src s;
+    const Cx<double>* w;
+    int n;
+    __device__ __forceinline__ Cx<double> ld(int j) const { return j < n ? cmul(s.ld(j), w[j]) : cx(0.0, 0.0); }
+};
+template <class Dst>
+struct ChirpSt {  // X_k = w_k c_k (k < n); the padding outputs are dropped
+    Dst d;
+    const Cx<double>* w;
+    int n;
+    __device__ __forceinline__ void st(int k, const Cx<double>& v) const {
+        if (k < n) d.st(k, cmul(v, w[k]));
+    }
+};
+struct BlueTab {  // fp64: twM[M], then for the forward (0) / inverse (1) direction w[N], bhat[M]
+    const Cx<double>* twM;
+    const Cx<double>* w[2];
+    const Cx<double>* bhat[2];
+    int n;
+};
+template <int M, int D, class Src, class Dst>
+__device__ __forceinline__ void blue_line(Cx<double>* buf, int t, const BlueTab& bt, const Src& src, const Dst& dst) {
+    constexpr int TPL = Tpl<M, double>::V;
+    fft_line_io<double, M, -1, false, true>(buf, t, bt.twM, 1, ChirpLd<Src>{src, bt.w[D], bt.n}, SmemLine<double>{buf});
+    for (int j = t; j < M; j += TPL) buf[P(j)] = cmul(buf[P(j)], bt.bhat[D][j]);
+    __syncthreads();
+    fft_line_io<double, M, +1, true, false>(buf, t, bt.twM, 1, SmemLine<double>{buf}, ChirpSt<Dst>{dst, bt.w[D], bt.n});
+}
+
+// x2 FFT (DIR) of length N = bt.n, src -> dst (may alias: a CTA loads its lines before it stores them)
+template <typename Ti, int M, int DIR>
+struct ColBlueFftPass {
+    using CC = ColCfg<M, double, 1>;
+    static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
+    static constexpr int MINB = MinB<double, NT>::V;
+    static constexpr size_t BUF = CC::SMEM;
+    ColGeom c;
+    const Cx<Ti>* src;
+    Cx<Ti>* dst;
+    BlueTab bt;
+    int64_t cs = 0, csd = -1;
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int x = x0 + xi, o = o0 + oi;
+        const bool on = x < c.nx && o < c.n3;
+        blue_line<M, DIR < 0 ? 0 : 1>(reinterpret_cast<Cx<double>*>(smem) + (oi * XC + xi) * LP, t, bt,
+                                      AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0)},
+                                      AccD<Ti>{col_acc<2>(dst + blockIdx.y * (csd >= 0 ? csd : cs), c, x, o, 0, on, 0)});
+    }
+};
+
+// x2 derivative of a real field viewed as complex pairs (ColDerivPass with Bluestein transforms):
+// out (+)= F2^-1[i k2' / N F2 f]; nf fields per launch (blockIdx.y)
+template <typename Ti, int M>
+struct ColBlueDerivPass {
+    using CC = ColCfg<M, double, 2>;
+    static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT, LINES = CC::LINES;
+    static constexpr int MINB = MinB<double, NT>::V;
+    static constexpr size_t BUF = CC::SMEM;
+    ColGeom c;
+    const Cx<Ti>* src;
+    Cx<Ti>* dst;
+    int accumulate;
+    BlueTab bt;
+    int64_t cs = 0, cso = 0;
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int x = x0 + xi, o = o0 + oi;
+        const bool on = x < c.nx && o < c.n3;
+        Cx<double>* bA = reinterpret_cast<Cx<double>*>(smem) + (oi * XC + xi) * LP;
+        Cx<double>* bB = bA + LINES * LP;
+        const int n = bt.n;
+        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0)},
+                        SmemLine<double>{bB});
+        __syncthreads();
+        for (int k = t; k < n; k += TPL) bB[P(k)] = mul_i(bB[P(k)], (double)wavenum_odd(k, n) / (double)n);
+        __syncthreads();
+        blue_line<M, 1>(bA, t, bt, SmemLine<double>{bB}, AccD<Ti>{col_acc<2>(dst + blockIdx.y * cso, c, x, o, 0, on, accumulate)});
+    }
+};
+
+// ColDivPass with Bluestein x2 transforms: Q = i (k1' F2 P1 + k2' F2 P2), R = F2 P3 (one rank)
+template <typename Ti>
+struct DivCombineSt {  // Q_k = i (k1' B_k + k2'(k) v)
+    Cx<double>* b;
+    AccD<Ti> q;
+    double k1;
+    int n;
+    __device__ __forceinline__ void st(int k, const Cx<double>& v) const {
+        q.st(k, mul_i(scale(b[P(k)], k1) + scale(v, (double)wavenum_odd(k, n)), 1.0));
+    }
+};
+template <typename Ti, int M>
+struct ColBlueDivPass {
+    using CC = ColCfg<M, double, 2>;
+    static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT, LINES = CC::LINES;
+    static constexpr int MINB = MinB<double, NT>::V;
+    static constexpr size_t BUF = CC::SMEM;
+    ColGeom c;
+    const Cx<Ti>* p1;
+    const Cx<Ti>* p2;
+    const Cx<Ti>* p3;
+    Cx<Ti>* q;
+    Cx<Ti>* r;
+    BlueTab bt;
+    int n1;
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int x = x0 + xi, o = o0 + oi;
+        const bool on = x < c.nx && o < c.n3;
+        Cx<double>* bA = reinterpret_cast<Cx<double>*>(smem) + (oi * XC + xi) * LP;
+        Cx<double>* bB = bA + LINES * LP;
+        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p1), c, x, o, 0, on, 0)}, SmemLine<double>{bB});
+        __syncthreads();
+        const double k1 = (double)((x == n1 / 2) ? 0 : x);
+        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p2), c, x, o, 0, on, 0)},
+                        DivCombineSt<Ti>{bB, AccD<Ti>{col_acc<2>(q, c, x, o, 0, on, 0)}, k1, bt.n});
+        __syncthreads();
+        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p3), c, x, o, 0, on, 0)},
+                        AccD<Ti>{col_acc<2>(r, c, x, o, 0, on, 0)});
+    }
+};
+
+// ---------------------------------------------------------------------------------------------
 // Spectral symbols applied in the x3 middle pass.  k = (k1, k2, k3) signed wavenumbers,
 // kp = (k1', k2', k3') with the Nyquist zeroed.  `norm` = full inverse normalisation 2/M.
 struct SymInfo {

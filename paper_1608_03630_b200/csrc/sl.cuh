@@ -87,7 +87,7 @@ __device__ __forceinline__ T interp_global(const T* __restrict__ f, const Grid& 
         T accb = T(0);
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
-            const int j2 = wrapi(q2 + bb - 1, g.n2);
+            const int j2 = wrap2(q2 + bb - 1, g.n2);
             const T* r = f + ((int64_t)j3 * g.n2 + j2) * g.n1;
             T row = T(0);
 #pragma unroll
@@ -502,7 +502,7 @@ __device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, 
     while (yy >= c.ey) { yy -= c.ey; ++zz; }
     const int gx = wrapi(c.ox + ch * VEC, g.n1);
     while (zz < c.ez) {
-        const int gy = wrapi(c.oy + yy, g.n2);
+        const int gy = wrap2(c.oy + yy, g.n2);
         const int gz = g.ghost ? c.oz + zz - g.z0 + g.zg : wrapi(c.oz + zz, g.n3);
         const uint32_t gofs = ((uint32_t)gz * g.n2 + gy) * g.n1 + gx;
         T* dst = box + (zz * BY + yy) * BX + ch * VEC;

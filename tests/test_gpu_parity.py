@@ -130,6 +130,53 @@ def test_matvec_long_lines(dr, n, iso, fp64):
     check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, iso)
 
 
+# x2 extents that are not powers of two (one rank; Bluestein x2 passes, M = 16 .. 1024): the paper's own
+# grid is 256 x 300 x 256; SURVEY §8(b) admits any even N >= 4
+BLUE_GRIDS = [(8, 6, 8), (16, 12, 8), (32, 24, 16), (16, 300, 16), (32, 510, 8)]
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("n", BLUE_GRIDS, ids=["x".join(map(str, g)) for g in BLUE_GRIDS])
+def test_spectral_ops_non_pow2_x2(dr, n, fp64):
+    """grad, div, beta A (H1, H2), (beta A)^-1 (isochoric and not) and the Leray projection on grids whose
+    N2 is not a power of two, against the oracle (whose non-power-of-two lines are plain DFT sums)."""
+    tol = tols(fp64)[0]
+    kc = max(1, min(n) // 3)
+    f, f64 = prep(synth.blobs(5, n, kcut=kc), fp64)
+    u, u64 = prep(synth.smooth_vec(6, n, kmax=kc), fp64)
+    f, u = f.cuda(), u.cuda()
+    for reg in (1, 2):
+        ctx = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37, fp64=fp64))
+        if reg == 1:
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_GRAD, f)), O.grad(f64)) < tol
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_DIV, u)), O.div(u64)) < tol
+            assert rel(np64(ctx.op_spectral(dr.DR_OP_LERAY, u)), O.leray(u64)) < tol
+        Au = O.reg_apply(u64, reg, 0.37)
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_REG, u)), Au) < amp_tol(tol, u64.shape[1:], reg, 0.37, u64, Au, fp64)
+        assert rel(np64(ctx.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, False)) < tol
+        ci = dr.Context(dr.Config(n=n, nt=2, reg=reg, beta=0.37, fp64=fp64, isochoric=True))
+        assert rel(np64(ci.op_spectral(dr.DR_OP_PRECOND, u)), O.precond(u64, reg, 0.37, True)) < tol
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("iso", [False, True])
+@pytest.mark.parametrize("n", BLUE_GRIDS[1:4], ids=["x".join(map(str, g)) for g in BLUE_GRIDS[1:4]])
+def test_matvec_non_pow2_x2(dr, n, iso, fp64):
+    """Setup, forward solve and one GN matvec per mode with a non-power-of-two N2 (ragged x2 gather
+    tiles, periodic wrap by remainder, Bluestein x2 passes in the gradients, the tail and the data term)."""
+    kc = max(1, min(n) // 3)
+    nt = 2
+    ctx = dr.Context(dr.Config(n=n, nt=nt, reg=2, beta=1e-2, isochoric=iso, fp64=fp64))
+    rT, rT64 = prep(synth.blobs(11, n, kcut=kc), fp64)
+    rR, rR64 = prep(synth.blobs(12, n, kcut=kc), fp64)
+    v, v64 = prep(synth.smooth_vec(9, n, kmax=min(kc, 3), divfree=iso, cells_per_step=1.5, nt=nt), fp64)
+    ctx.set_images(rT.cuda(), rR.cuda())
+    ctx.set_velocity(v.cuda())
+    prob = O.Problem(rho_T=rT64, rho_R=rR64, nt=nt, reg=2, beta=1e-2, iso=iso)
+    vt, vt64 = prep(synth.smooth_vec(21, n, kmax=min(kc, 3), divfree=iso), fp64)
+    check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, iso)
+
+
 @pytest.mark.parametrize("fp64", [False, True])
 def test_spectral_white_noise_nyquist(dr, fp64):
     """White noise carries Nyquist content: both sides must zero it in odd symbols (reading A2)."""
