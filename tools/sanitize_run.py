@@ -41,9 +41,15 @@ for iso in (False, True):
         ctx = dr.Context(dr.Config(n=n, nt=2, isochoric=iso, newton=newton))
         run(ctx, *pipeline(ctx, n, 1.5, 10))
         ctx.close()
-# slabs with scatter
+# x2 extents that are not powers of two (Bluestein x2 passes, ragged x2 tiles)
+for nb in ((16, 12, 16), (8, 20, 8)):
+    for iso in (False, True):
+        ctx = dr.Context(dr.Config(n=nb, nt=2, isochoric=iso))
+        run(ctx, *pipeline(ctx, nb, 1.5, 30))
+        ctx.close()
+# slabs with scatter (isochoric with DR_SANITIZE_ISO=1: the split-layout ColDivPass and kind 9)
 P, n2 = 2, (16, 16, 32)
-cfg = dr.Config(n=n2, nt=2)
+cfg = dr.Config(n=n2, nt=2, isochoric=os.environ.get("DR_SANITIZE_ISO") == "1")
 hub = dr.diffreg.Hub(P)
 comms = [hub.comm(r) for r in range(P)]
 streams = [torch.cuda.Stream() for _ in range(P)]
