@@ -188,9 +188,9 @@ Layout layout(const dr_config* c, int nranks = 1) {
     L.twxd = take((size_t)g.n1 * 16);
     L.twyd = take((size_t)g.n2 * 16);
     L.twzd = take((size_t)g.n3g * 16);
-    // Bluestein tables of a non-power-of-two x2 extent (fp64): twM[M], w_fwd[N], w_inv[N], bhat_fwd[M],
-    // bhat_inv[M]
-    L.blue = blue_len(g.n2) ? take((size_t)(3 * blue_m(g.n2) + 2 * g.n2) * 16) : 0;
+    // Bluestein tables of a non-power-of-two x2 extent, fp32 then fp64: twM[M], w_fwd[N], w_inv[N],
+    // bhat_fwd[M], bhat_inv[M]
+    L.blue = blue_len(g.n2) ? take((size_t)(3 * blue_m(g.n2) + 2 * g.n2) * (8 + 16)) : 0;
     L.total = off;
     return L;
 }
@@ -510,33 +510,31 @@ struct Impl {
         CK(cudaMemcpyAsync(c.ws + off, h.data(), sizeof(Cx<U>) * n, cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
     }
-    // Bluestein tables (fft.cuh ColBlue*, fp64), from long double: w_j = e^{D i pi (j^2 mod 2N) / N},
+    // Bluestein tables (fft.cuh ColBlue*), fp32 then fp64, from long double: w_j = e^{D i pi (j^2 mod 2N) / N},
     // b_j = conj(w_j) for |j| < N placed circularly in M, bhat = DFT_M(b) / M (direct sum: M <= 1024)
+    size_t blue_bytes_f() const { return (size_t)(3 * blue_m(g.n2) + 2 * g.n2) * sizeof(Cx<float>); }
     void fill_blue(size_t off) {
         const int n = g.n2, M = blue_m(n);
         const long double pi = 3.141592653589793238462643383279502884L;
-        std::vector<Cx<double>> h((size_t)3 * M + 2 * n);
+        std::vector<long double> re((size_t)3 * M + 2 * n), im((size_t)3 * M + 2 * n);
         for (int m = 0; m < M; ++m) {
             const long double a = -2.0L * pi * (long double)m / (long double)M;
-            h[m] = Cx<double>{(double)std::cos(a), (double)std::sin(a)};
+            re[m] = std::cos(a);
+            im[m] = std::sin(a);
         }
         for (int d = 0; d < 2; ++d) {
             const long double sg = d == 0 ? -1.0L : 1.0L;
-            std::vector<long double> wr(n), wi(n);
+            std::vector<long double> br(M, 0.0L), bi(M, 0.0L);
             for (int j = 0; j < n; ++j) {
                 const long long q = ((long long)j * j) % (2LL * n);
                 const long double a = sg * pi * (long double)q / (long double)n;
-                wr[j] = std::cos(a);
-                wi[j] = std::sin(a);
-                h[(size_t)M + (size_t)d * n + j] = Cx<double>{(double)wr[j], (double)wi[j]};
-            }
-            std::vector<long double> br(M, 0.0L), bi(M, 0.0L);
-            for (int j = 0; j < n; ++j) {
-                br[j] = wr[j];
-                bi[j] = -wi[j];
+                re[(size_t)M + (size_t)d * n + j] = std::cos(a);
+                im[(size_t)M + (size_t)d * n + j] = std::sin(a);
+                br[j] = std::cos(a);
+                bi[j] = -std::sin(a);
                 if (j > 0) {
-                    br[M - j] = wr[j];
-                    bi[M - j] = -wi[j];
+                    br[M - j] = br[j];
+                    bi[M - j] = bi[j];
                 }
             }
             for (int k = 0; k < M; ++k) {
@@ -548,16 +546,25 @@ struct Impl {
                     sr += br[j] * cr - bi[j] * ci;
                     si += br[j] * ci + bi[j] * cr;
                 }
-                h[(size_t)M + 2 * n + (size_t)d * M + k] = Cx<double>{(double)(sr / M), (double)(si / M)};
+                re[(size_t)M + 2 * n + (size_t)d * M + k] = sr / M;
+                im[(size_t)M + 2 * n + (size_t)d * M + k] = si / M;
             }
         }
-        CK(cudaMemcpyAsync(c.ws + off, h.data(), h.size() * sizeof(Cx<double>), cudaMemcpyHostToDevice, s));
+        std::vector<Cx<float>> hf(re.size());
+        std::vector<Cx<double>> hd(re.size());
+        for (size_t i = 0; i < re.size(); ++i) {
+            hf[i] = Cx<float>{(float)re[i], (float)im[i]};
+            hd[i] = Cx<double>{(double)re[i], (double)im[i]};
+        }
+        CK(cudaMemcpyAsync(c.ws + off, hf.data(), hf.size() * sizeof(Cx<float>), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c.ws + off + blue_bytes_f(), hd.data(), hd.size() * sizeof(Cx<double>), cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
     }
-    BlueTab bluetab() {
+    template <typename U>
+    BlueTab<U> bluetab() {
         const int n = g.n2, M = blue_m(n);
-        const Cx<double>* t = reinterpret_cast<const Cx<double>*>(c.ws + c.L.blue);
-        return BlueTab{t, {t + M, t + M + n}, {t + M + 2 * n, t + 2 * M + 2 * n}, n};
+        const Cx<U>* t = reinterpret_cast<const Cx<U>*>(c.ws + c.L.blue + (sizeof(U) == 8 ? blue_bytes_f() : 0));
+        return BlueTab<U>{t, {t + M, t + M + n}, {t + M + 2 * n, t + 2 * M + 2 * n}, n};
     }
     bool blue2() const { return blue_len(g.n2); }
     void init_twiddles() {
@@ -800,7 +807,7 @@ struct Impl {
         using PT = ColBlueFftPass<U, M, DIR>;
         const ColGeom cg = spec_geom();
         const char* tag = DIR > 0 ? "col_fft_inv" : sizeof(U) == 8 ? "col_fft_fwd_f64" : "col_fft_fwd_f32";
-        stream(tag, PT{cg, src, dst, bluetab(), cs, csd}, col_tiles<PT>(cg, g.n3), nc);
+        stream(tag, PT{cg, src, dst, bluetab<U>(), cs, csd}, col_tiles<PT>(cg, g.n3), nc);
     }
     template <typename U, int DIR>
     void blue_fft(const Cx<U>* src, Cx<U>* dst, int nc, int64_t cs, int64_t csd) {
@@ -812,7 +819,7 @@ struct Impl {
     void blue_deriv_M(const T* f, T* out, int acc, int nf, int64_t fs, int64_t os) {
         using PT = ColBlueDerivPass<T, M>;
         const ColGeom cg = pair_geom();
-        stream("col_deriv", PT{cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, bluetab(),
+        stream("col_deriv", PT{cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, bluetab<double>(),
                                fs / 2, os / 2},
                col_tiles<PT>(cg, cg.n3), nf);
     }
@@ -825,7 +832,7 @@ struct Impl {
     void blue_div_M(const Cx<T>* p1, const Cx<T>* p2, const Cx<T>* p3, Cx<T>* q, Cx<T>* r) {
         using PT = ColBlueDivPass<T, M>;
         const ColGeom cg = spec_geom();
-        stream("col_div", PT{cg, p1, p2, p3, q, r, bluetab(), g.n1}, col_tiles<PT>(cg, g.n3));
+        stream("col_div", PT{cg, p1, p2, p3, q, r, bluetab<double>(), g.n1}, col_tiles<PT>(cg, g.n3));
     }
 
     template <int L, int AX>

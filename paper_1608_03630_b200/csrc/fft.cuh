@@ -900,59 +900,65 @@ struct ColDivPass {
 // conj(w_{k-n}) with w_j = e^{DIR i pi j^2 / N} (nk = (n^2 + k^2 - (k - n)^2) / 2), i.e. a circular
 // convolution evaluated with two radix-16 FFTs of the power of two M >= 2N - 1 and the precomputed
 // transform bhat = FFT_M(b) / M of the chirp b_j = conj(w_j), j in (-N, N).  chirp[n] = w_n per direction.
-// The arithmetic is fp64 whatever the I/O type: an fp32 convolution of length M ~ 2N leaves a white
-// rounding floor that odd symbols (k' / N up to N / 2) amplify past the 1e-5 operator bar.
-template <typename Ti>
-struct AccD {  // a column accessor in the I/O type, seen in double
+// Plain x2 transforms compute in their I/O precision (the forward of the amplifying symbols is fp64 by
+// type, reading A20; an fp32 inverse after a symbol rounds relative to the already-shaped signal); the
+// derivative and divergence stages compute in fp64 whatever the I/O type: an fp32 convolution of length
+// M ~ 2N leaves a white rounding floor that the odd symbol (k' / N up to N / 2) lifts past the 1e-5
+// operator bar.
+template <typename Ti, typename Tc>
+struct AccC {  // a column accessor in the I/O type, seen in the compute type
     ColAcc<Ti> a;
-    __device__ __forceinline__ Cx<double> ld(int i) const {
+    __device__ __forceinline__ Cx<Tc> ld(int i) const {
         const Cx<Ti> v = a.ld(i);
-        return cx<double>((double)v.re, (double)v.im);
+        return cx<Tc>((Tc)v.re, (Tc)v.im);
     }
-    __device__ __forceinline__ void st(int i, const Cx<double>& v) const { a.st(i, cx<Ti>((Ti)v.re, (Ti)v.im)); }
+    __device__ __forceinline__ void st(int i, const Cx<Tc>& v) const { a.st(i, cx<Ti>((Ti)v.re, (Ti)v.im)); }
 };
-template <class Src>
+template <typename Ti>
+using AccD = AccC<Ti, double>;
+template <typename Tc, class Src>
 struct ChirpLd {  // a_j = w_j x_j (j < n), zero padding up to M
     Src s;
-    const Cx<double>* w;
+    const Cx<Tc>* w;
     int n;
-    __device__ __forceinline__ Cx<double> ld(int j) const { return j < n ? cmul(s.ld(j), w[j]) : cx(0.0, 0.0); }
+    __device__ __forceinline__ Cx<Tc> ld(int j) const { return j < n ? cmul(s.ld(j), w[j]) : cx(Tc(0), Tc(0)); }
 };
-template <class Dst>
+template <typename Tc, class Dst>
 struct ChirpSt {  // X_k = w_k c_k (k < n); the padding outputs are dropped
     Dst d;
-    const Cx<double>* w;
+    const Cx<Tc>* w;
     int n;
-    __device__ __forceinline__ void st(int k, const Cx<double>& v) const {
+    __device__ __forceinline__ void st(int k, const Cx<Tc>& v) const {
         if (k < n) d.st(k, cmul(v, w[k]));
     }
 };
-struct BlueTab {  // fp64: twM[M], then for the forward (0) / inverse (1) direction w[N], bhat[M]
-    const Cx<double>* twM;
-    const Cx<double>* w[2];
-    const Cx<double>* bhat[2];
+template <typename Tc>
+struct BlueTab {  // twM[M], then for the forward (0) / inverse (1) direction w[N], bhat[M]
+    const Cx<Tc>* twM;
+    const Cx<Tc>* w[2];
+    const Cx<Tc>* bhat[2];
     int n;
 };
-template <int M, int D, class Src, class Dst>
-__device__ __forceinline__ void blue_line(Cx<double>* buf, int t, const BlueTab& bt, const Src& src, const Dst& dst) {
-    constexpr int TPL = Tpl<M, double>::V;
-    fft_line_io<double, M, -1, false, true>(buf, t, bt.twM, 1, ChirpLd<Src>{src, bt.w[D], bt.n}, SmemLine<double>{buf});
+template <typename Tc, int M, int D, class Src, class Dst>
+__device__ __forceinline__ void blue_line(Cx<Tc>* buf, int t, const BlueTab<Tc>& bt, const Src& src, const Dst& dst) {
+    constexpr int TPL = Tpl<M, Tc>::V;
+    fft_line_io<Tc, M, -1, false, true>(buf, t, bt.twM, 1, ChirpLd<Tc, Src>{src, bt.w[D], bt.n}, SmemLine<Tc>{buf});
     for (int j = t; j < M; j += TPL) buf[P(j)] = cmul(buf[P(j)], bt.bhat[D][j]);
     __syncthreads();
-    fft_line_io<double, M, +1, true, false>(buf, t, bt.twM, 1, SmemLine<double>{buf}, ChirpSt<Dst>{dst, bt.w[D], bt.n});
+    fft_line_io<Tc, M, +1, true, false>(buf, t, bt.twM, 1, SmemLine<Tc>{buf}, ChirpSt<Tc, Dst>{dst, bt.w[D], bt.n});
 }
 
-// x2 FFT (DIR) of length N = bt.n, src -> dst (may alias: a CTA loads its lines before it stores them)
-template <typename Ti, int M, int DIR>
+// x2 FFT (DIR) of length N = bt.n in T, src -> dst (may alias: a CTA loads its lines before it stores them)
+template <typename T, int M, int DIR>
 struct ColBlueFftPass {
-    using CC = ColCfg<M, double, 1>;
+    using CC = ColCfg<M, T, 1, ColCap<M, T>::V>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT;
-    static constexpr int MINB = MinB<double, NT>::V;
+    static constexpr int MINB = MinB<T, NT>::V;
     static constexpr size_t BUF = CC::SMEM;
     ColGeom c;
-    const Cx<Ti>* src;
-    Cx<Ti>* dst;
-    BlueTab bt;
+    const Cx<T>* src;
+    Cx<T>* dst;
+    BlueTab<T> bt;
     int64_t cs = 0, csd = -1;
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         int x0, o0, xi, t, oi;
@@ -960,9 +966,9 @@ struct ColBlueFftPass {
         col_thread<XC, TPL>(xi, t, oi);
         const int x = x0 + xi, o = o0 + oi;
         const bool on = x < c.nx && o < c.n3;
-        blue_line<M, DIR < 0 ? 0 : 1>(reinterpret_cast<Cx<double>*>(smem) + (oi * XC + xi) * LP, t, bt,
-                                      AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0)},
-                                      AccD<Ti>{col_acc<2>(dst + blockIdx.y * (csd >= 0 ? csd : cs), c, x, o, 0, on, 0)});
+        blue_line<T, M, DIR < 0 ? 0 : 1>(reinterpret_cast<Cx<T>*>(smem) + (oi * XC + xi) * LP, t, bt,
+                                         col_acc<2>(const_cast<Cx<T>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0),
+                                         col_acc<2>(dst + blockIdx.y * (csd >= 0 ? csd : cs), c, x, o, 0, on, 0));
     }
 };
 
@@ -978,7 +984,7 @@ struct ColBlueDerivPass {
     const Cx<Ti>* src;
     Cx<Ti>* dst;
     int accumulate;
-    BlueTab bt;
+    BlueTab<double> bt;
     int64_t cs = 0, cso = 0;
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         int x0, o0, xi, t, oi;
@@ -989,12 +995,12 @@ struct ColBlueDerivPass {
         Cx<double>* bA = reinterpret_cast<Cx<double>*>(smem) + (oi * XC + xi) * LP;
         Cx<double>* bB = bA + LINES * LP;
         const int n = bt.n;
-        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0)},
+        blue_line<double, M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0)},
                         SmemLine<double>{bB});
         __syncthreads();
         for (int k = t; k < n; k += TPL) bB[P(k)] = mul_i(bB[P(k)], (double)wavenum_odd(k, n) / (double)n);
         __syncthreads();
-        blue_line<M, 1>(bA, t, bt, SmemLine<double>{bB}, AccD<Ti>{col_acc<2>(dst + blockIdx.y * cso, c, x, o, 0, on, accumulate)});
+        blue_line<double, M, 1>(bA, t, bt, SmemLine<double>{bB}, AccD<Ti>{col_acc<2>(dst + blockIdx.y * cso, c, x, o, 0, on, accumulate)});
     }
 };
 
@@ -1021,7 +1027,7 @@ struct ColBlueDivPass {
     const Cx<Ti>* p3;
     Cx<Ti>* q;
     Cx<Ti>* r;
-    BlueTab bt;
+    BlueTab<double> bt;
     int n1;
     __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
         int x0, o0, xi, t, oi;
@@ -1031,13 +1037,13 @@ struct ColBlueDivPass {
         const bool on = x < c.nx && o < c.n3;
         Cx<double>* bA = reinterpret_cast<Cx<double>*>(smem) + (oi * XC + xi) * LP;
         Cx<double>* bB = bA + LINES * LP;
-        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p1), c, x, o, 0, on, 0)}, SmemLine<double>{bB});
+        blue_line<double, M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p1), c, x, o, 0, on, 0)}, SmemLine<double>{bB});
         __syncthreads();
         const double k1 = (double)((x == n1 / 2) ? 0 : x);
-        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p2), c, x, o, 0, on, 0)},
+        blue_line<double, M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p2), c, x, o, 0, on, 0)},
                         DivCombineSt<Ti>{bB, AccD<Ti>{col_acc<2>(q, c, x, o, 0, on, 0)}, k1, bt.n});
         __syncthreads();
-        blue_line<M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p3), c, x, o, 0, on, 0)},
+        blue_line<double, M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(p3), c, x, o, 0, on, 0)},
                         AccD<Ti>{col_acc<2>(r, c, x, o, 0, on, 0)});
     }
 };
