@@ -72,7 +72,7 @@ int ghost_hi(const dr_config* c) { return c->ghost_hi > 0 ? c->ghost_hi : GHOST_
 dr_status validate(const dr_config* c, int nranks = 1) {
     if (!c) return DR_ERR_ARG;
     for (int a = 0; a < 3; ++a)
-        if (!pow2_in_range(c->n[a]) && !(a == 1 && nranks == 1 && blue_len(c->n[a]))) return DR_ERR_GRID;
+        if (!pow2_in_range(c->n[a]) && !(a >= 1 && nranks == 1 && blue_len(c->n[a]))) return DR_ERR_GRID;
     if (c->nt < 1 || c->nt > 64) return DR_ERR_PARAM;
     if (c->reg != DR_REG_H1 && c->reg != DR_REG_H2) return DR_ERR_PARAM;
     if (!(c->beta > 0.0) || !std::isfinite(c->beta)) return DR_ERR_PARAM;
@@ -123,7 +123,7 @@ struct Layout {
     int64_t rcap = 0;
     size_t rem = 0;
     size_t kry, sN, bN, sc, rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
-        plan_m, plan_t, maxext, red, pflags, twx, twy, twz, twxd, twyd, twzd, blue, total;
+        plan_m, plan_t, maxext, red, pflags, twx, twy, twz, twxd, twyd, twzd, blue, blue3, total;
 };
 
 Layout layout(const dr_config* c, int nranks = 1) {
@@ -191,6 +191,7 @@ Layout layout(const dr_config* c, int nranks = 1) {
     // Bluestein tables of a non-power-of-two x2 extent, fp32 then fp64: twM[M], w_fwd[N], w_inv[N],
     // bhat_fwd[M], bhat_inv[M]
     L.blue = blue_len(g.n2) ? take((size_t)(3 * blue_m(g.n2) + 2 * g.n2) * (8 + 16)) : 0;
+    L.blue3 = blue_len(g.n3g) ? take((size_t)(3 * blue_m(g.n3g) + 2 * g.n3g) * (8 + 16)) : 0;  // the same for x3
     L.total = off;
     return L;
 }
@@ -512,9 +513,9 @@ struct Impl {
     }
     // Bluestein tables (fft.cuh ColBlue*), fp32 then fp64, from long double: w_j = e^{D i pi (j^2 mod 2N) / N},
     // b_j = conj(w_j) for |j| < N placed circularly in M, bhat = DFT_M(b) / M (direct sum: M <= 1024)
-    size_t blue_bytes_f() const { return (size_t)(3 * blue_m(g.n2) + 2 * g.n2) * sizeof(Cx<float>); }
-    void fill_blue(size_t off) {
-        const int n = g.n2, M = blue_m(n);
+    static size_t blue_bytes_f(int n) { return (size_t)(3 * blue_m(n) + 2 * n) * sizeof(Cx<float>); }
+    void fill_blue(size_t off, int n) {
+        const int M = blue_m(n);
         const long double pi = 3.141592653589793238462643383279502884L;
         std::vector<long double> re((size_t)3 * M + 2 * n), im((size_t)3 * M + 2 * n);
         for (int m = 0; m < M; ++m) {
@@ -557,18 +558,23 @@ struct Impl {
             hd[i] = Cx<double>{(double)re[i], (double)im[i]};
         }
         CK(cudaMemcpyAsync(c.ws + off, hf.data(), hf.size() * sizeof(Cx<float>), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(c.ws + off + blue_bytes_f(), hd.data(), hd.size() * sizeof(Cx<double>), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c.ws + off + blue_bytes_f(n), hd.data(), hd.size() * sizeof(Cx<double>), cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
     }
     template <typename U>
-    BlueTab<U> bluetab() {
-        const int n = g.n2, M = blue_m(n);
-        const Cx<U>* t = reinterpret_cast<const Cx<U>*>(c.ws + c.L.blue + (sizeof(U) == 8 ? blue_bytes_f() : 0));
+    BlueTab<U> bluetab_at(size_t base, int n) {
+        const int M = blue_m(n);
+        const Cx<U>* t = reinterpret_cast<const Cx<U>*>(c.ws + base + (sizeof(U) == 8 ? blue_bytes_f(n) : 0));
         return BlueTab<U>{t, {t + M, t + M + n}, {t + M + 2 * n, t + 2 * M + 2 * n}, n};
     }
+    template <typename U>
+    BlueTab<U> bluetab() { return bluetab_at<U>(c.L.blue, g.n2); }
+    BlueTab<double> bluetab3() { return bluetab_at<double>(c.L.blue3, g.n3g); }
+    bool blue3() const { return blue_len(g.n3g); }
     bool blue2() const { return blue_len(g.n2); }
     void init_twiddles() {
-        if (blue2()) fill_blue(c.L.blue);
+        if (blue2()) fill_blue(c.L.blue, g.n2);
+        if (blue3()) fill_blue(c.L.blue3, g.n3g);
         fill_twiddles<T>(g.n1, c.L.twx);
         fill_twiddles<T>(g.n2, c.L.twy);
         fill_twiddles<T>(g.n3g, c.L.twz);
@@ -823,6 +829,43 @@ struct Impl {
                                fs / 2, os / 2},
                col_tiles<PT>(cg, cg.n3), nf);
     }
+    template <int M>
+    void blue_deriv3_M(const T* f, T* out, int acc, int nf, int64_t fs, int64_t os) {
+        using PT = ColBlueDerivPass<T, M, 3>;
+        const ColGeom cg = pair_geom();
+        stream("col_deriv", PT{cg, reinterpret_cast<const Cx<T>*>(f), reinterpret_cast<Cx<T>*>(out), acc, bluetab3(),
+                               fs / 2, os / 2},
+               col_tiles<PT>(cg, cg.n2), nf);
+    }
+    void blue_deriv3(const T* f, T* out, int acc, int nf = 1, int64_t fs = 0, int64_t os = 0) {
+#define CALL(MM) blue_deriv3_M<MM>(f, out, acc, nf, fs, os)
+        DR_SWITCH_BLUE(blue_m(g.n3g), CALL)
+#undef CALL
+    }
+    // x3 middle pass of a non-power-of-two x3 extent (fft.cuh BlueMiddlePass; one rank)
+    template <int KIND, typename Tc, int M>
+    void blue_middle_M(Cx<Tc>* const* in, Cx<T>* const* out, int comp, int nc, int64_t cs, Cx<T>* const* inq) {
+        using PT = BlueMiddlePass<Tc, T, M, KIND>;
+        PT pt;
+        pt.c = spec_geom();
+        for (int i = 0; i < PT::NCI; ++i) pt.in.p[i] = in[i];
+        for (int i = 0; i < PT::NCO; ++i) pt.out.p[i] = out[i];
+        if (inq) pt.inq = SpecPtrs<T, 2>{{inq[0], inq[1]}};
+        pt.s = SymInfo{c.cfg.reg, c.cfg.beta, 2.0 / ((double)g.n1 * g.n2 * g.n3g), comp};
+        pt.bt = bluetab3();
+        pt.cs = cs;
+        stream(sizeof(Tc) == 8 ? "col_middle_f64" : "col_middle_f32", pt, col_tiles<PT>(pt.c, pt.c.n2), nc);
+    }
+    template <int KIND, typename Tc>
+    void blue_middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp, int nc, int64_t cs, Cx<T>* const* inq) {
+        if constexpr (KIND == 6 || KIND == 7 || KIND == 9) {
+            fail(DR_ERR_GRID, "non-power-of-two x3 extents run on one rank only");
+        } else {
+#define CALL(MM) blue_middle_M<KIND, Tc, MM>(in, out, comp, nc, cs, inq)
+            DR_SWITCH_BLUE(blue_m(g.n3g), CALL)
+#undef CALL
+        }
+    }
     void blue_deriv(const T* f, T* out, int acc, int nf = 1, int64_t fs = 0, int64_t os = 0) {
 #define CALL(MM) blue_deriv_M<MM>(f, out, acc, nf, fs, os)
         DR_SWITCH_BLUE(blue_m(g.n2), CALL)
@@ -852,6 +895,10 @@ struct Impl {
 #define CALL(LL) col_deriv_L<LL, 2>(pair_geom(), f, out, acc)
             DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
+            return;
+        }
+        if (!c.dist() && blue3()) {
+            blue_deriv3(f, out, acc);
             return;
         }
         if (!c.dist()) {
@@ -980,6 +1027,10 @@ struct Impl {
     template <int KIND, typename Tc = double>
     void middle(Cx<Tc>* const* in, Cx<T>* const* out, int comp = 0, int nc = 1, int64_t cs = 0,
                 Cx<T>* const* inq = nullptr) {
+        if (blue3()) {
+            blue_middle<KIND, Tc>(in, out, comp, nc, cs, inq);
+            return;
+        }
         const ColGeom cg = c.dist() ? spec_geom_t() : spec_geom();
 #define CALL(LL) middle_L<LL, KIND, Tc>(cg, in, out, comp, nc, cs, inq)
         DR_SWITCH_COL(g.n3g, CALL)
@@ -1053,9 +1104,13 @@ struct Impl {
             DR_SWITCH_COL(g.n2, CALL)
 #undef CALL
         }
+        if (blue3()) {
+            blue_deriv3(f, out + 2 * g.M, 0, nf, fs, os);
+        } else {
 #define CALL(LL) col_deriv_L<LL, 3>(pair_geom(), f, out + 2 * g.M, 0, nf, fs, os)
-        DR_SWITCH_COL(g.n3, CALL)
+            DR_SWITCH_COL(g.n3, CALL)
 #undef CALL
+        }
     }
     void grad(const T* f, V3<T> out) {
         row_deriv(f, out.c[0], 0);

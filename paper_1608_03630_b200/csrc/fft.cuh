@@ -974,7 +974,7 @@ struct ColBlueFftPass {
 
 // x2 derivative of a real field viewed as complex pairs (ColDerivPass with Bluestein transforms):
 // out (+)= F2^-1[i k2' / N F2 f]; nf fields per launch (blockIdx.y)
-template <typename Ti, int M>
+template <typename Ti, int M, int AX = 2>
 struct ColBlueDerivPass {
     using CC = ColCfg<M, double, 2>;
     static constexpr int TPL = CC::TPL, LP = CC::LP, XC = CC::XC, OL = CC::OL, NT = CC::NT, LINES = CC::LINES;
@@ -991,16 +991,16 @@ struct ColBlueDerivPass {
         col_origin<XC, OL>(c, tile, x0, o0);
         col_thread<XC, TPL>(xi, t, oi);
         const int x = x0 + xi, o = o0 + oi;
-        const bool on = x < c.nx && o < c.n3;
+        const bool on = x < c.nx && o < (AX == 2 ? c.n3 : c.n2);
         Cx<double>* bA = reinterpret_cast<Cx<double>*>(smem) + (oi * XC + xi) * LP;
         Cx<double>* bB = bA + LINES * LP;
         const int n = bt.n;
-        blue_line<double, M, 0>(bA, t, bt, AccD<Ti>{col_acc<2>(const_cast<Cx<Ti>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0)},
+        blue_line<double, M, 0>(bA, t, bt, AccD<Ti>{col_acc<AX>(const_cast<Cx<Ti>*>(src) + blockIdx.y * cs, c, x, o, 0, on, 0)},
                         SmemLine<double>{bB});
         __syncthreads();
         for (int k = t; k < n; k += TPL) bB[P(k)] = mul_i(bB[P(k)], (double)wavenum_odd(k, n) / (double)n);
         __syncthreads();
-        blue_line<double, M, 1>(bA, t, bt, SmemLine<double>{bB}, AccD<Ti>{col_acc<2>(dst + blockIdx.y * cso, c, x, o, 0, on, accumulate)});
+        blue_line<double, M, 1>(bA, t, bt, SmemLine<double>{bB}, AccD<Ti>{col_acc<AX>(dst + blockIdx.y * cso, c, x, o, 0, on, accumulate)});
     }
 };
 
@@ -1367,6 +1367,100 @@ struct MiddlePass {
                                                         col_acc<3>(out.p[co] + blockIdx.y * cs, c, x0 + lxi, o0 + loi, 0, lon, 0));
                 }
             }
+        }
+    }
+};
+
+// x3 middle pass of an x3 extent that is not a power of two (one rank): every line of every input goes
+// through a Bluestein forward transform (fp64) into its own shared-memory line, the symbol is applied
+// there (Sym<double, KIND>, the same expressions as MiddlePass), and every output line goes back through
+// a Bluestein inverse; I/O in the spectra's types.  Kinds 0 / 1 (scalar, components by blockIdx.y),
+// 2 / 3 / 5 (coupled) and 8 (the isochoric data term from ColDivPass's Q, R: D = F3 Q + i k3' F3 R).
+template <int M, int NB>
+struct BlueMidCfg {
+    static constexpr int TPL = Tpl<M, double>::V;
+    static constexpr int XC = NB <= 2 ? 4 : 2;
+    static constexpr int LW = ColLP<M, double, XC>::V;       // work line (M points)
+    static constexpr int LD = M / 2 + M / 32 + 2;              // data line: n3 <= M / 2 points, padded by P()
+    static constexpr size_t PER = (size_t)(NB * LD + LW) * sizeof(Cx<double>);
+    static constexpr int OLT = (128 / (XC * TPL)) > 0 ? 128 / (XC * TPL) : 1;
+    static constexpr int OLS = (int)((96 * 1024) / (XC * PER)) > 0 ? (int)((96 * 1024) / (XC * PER)) : 1;
+    static constexpr int OL = OLT < OLS ? OLT : OLS;
+    static constexpr int LINES = XC * OL, NT = XC * OL * TPL;
+    static constexpr size_t SMEM = LINES * PER;
+};
+template <typename Ti, typename To, int M, int KIND>
+struct BlueMiddlePass {
+    static constexpr int NCI = Sym<double, KIND>::NCI, NCO = Sym<double, KIND>::NCO;
+    static constexpr int NB = KIND == 8 ? 5 : NCI;  // data lines per transverse line
+    using CC = BlueMidCfg<M, NB>;
+    static constexpr int TPL = CC::TPL, XC = CC::XC, OL = CC::OL, NT = CC::NT, LINES = CC::LINES;
+    static constexpr int MINB = 1;
+    static constexpr size_t BUF = CC::SMEM;
+    ColGeom c;
+    SpecPtrs<Ti, NCI> in;
+    SpecPtrs<To, NCO> out;
+    SpecPtrs<To, 2> inq;
+    SymInfo s;
+    BlueTab<double> bt;
+    int64_t cs = 0;
+    __device__ __forceinline__ Cx<double>* dline(unsigned char* smem, int b, int ln) const {
+        return reinterpret_cast<Cx<double>*>(smem) + (size_t)LINES * CC::LW + ((size_t)b * LINES + ln) * CC::LD;
+    }
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        int x0, o0, xi, t, oi;
+        col_origin<XC, OL>(c, tile, x0, o0);
+        col_thread<XC, TPL>(xi, t, oi);
+        const int x = x0 + xi, o = o0 + oi, ln = oi * XC + xi;
+        const bool on = x < c.nx && o < c.n2;
+        const int n = bt.n;
+        Cx<double>* work = reinterpret_cast<Cx<double>*>(smem) + (size_t)ln * CC::LW;
+        const int64_t off = (KIND <= 1) ? blockIdx.y * cs : 0;
+#pragma unroll 1
+        for (int b = 0; b < NB; ++b) {
+            if (b < NCI) {
+                blue_line<double, M, 0>(work, t, bt, AccD<Ti>{col_acc<3>(in.p[b] + off, c, x, o, 0, on, 0)},
+                                        SmemLine<double>{dline(smem, b, ln)});
+            } else {
+                blue_line<double, M, 0>(work, t, bt, AccD<To>{col_acc<3>(inq.p[b - NCI], c, x, o, 0, on, 0)},
+                                        SmemLine<double>{dline(smem, b, ln)});
+            }
+            __syncthreads();
+        }
+        const int n1 = 2 * (c.nx - 1);
+        for (int e = threadIdx.x; e < LINES * n; e += NT) {
+            const int l = e / n, p = e % n;
+            const int lx = x0 + l % XC, lo = o0 + l / XC;
+            Cx<double> v[NB];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) v[b] = dline(smem, b, l)[P(p)];
+            if (lx < c.nx && lo < c.n2) {
+                const int og = lo + c.k2off, n2g = c.n2g ? c.n2g : c.n2;
+                const int k1 = lx, k2 = wavenum(og, n2g), k3 = wavenum(p, n);
+                const int kp1 = (lx == n1 / 2) ? 0 : lx, kp2 = wavenum_odd(og, n2g), kp3 = wavenum_odd(p, n);
+                if constexpr (KIND == 8) {
+                    const Cx<double> d = v[3] + mul_i(v[4], (double)kp3);
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) {
+                        SymInfo sc = s;
+                        sc.comp = cc;
+                        Cx<double> w2[2] = {v[cc], d};
+                        Sym<double, 6>::apply(sc, w2, k1, k2, k3, kp1, kp2, kp3);
+                        v[cc] = w2[0];
+                    }
+                } else {
+                    Sym<double, KIND>::apply(s, v, k1, k2, k3, kp1, kp2, kp3);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < NCO; ++b) dline(smem, b, l)[P(p)] = v[b];
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int b = 0; b < NCO; ++b) {
+            blue_line<double, M, 1>(work, t, bt, SmemLine<double>{dline(smem, b, ln)},
+                                    AccD<To>{col_acc<3>(out.p[b] + off, c, x, o, 0, on, 0)});
+            __syncthreads();
         }
     }
 };

@@ -82,7 +82,7 @@ __device__ __forceinline__ T interp_global(const T* __restrict__ f, const Grid& 
     T acc = T(0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        const int j3 = g.ghost ? q3 + c - 1 - g.z0 + g.zg : wrapi(q3 + c - 1, g.n3);
+        const int j3 = g.ghost ? q3 + c - 1 - g.z0 + g.zg : wrap2(q3 + c - 1, g.n3);
         DR_ASSERT(j3 >= 0 && j3 < g.n3 + g.zg + g.zgh);
         T accb = T(0);
 #pragma unroll
@@ -503,7 +503,7 @@ __device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, 
     const int gx = wrapi(c.ox + ch * VEC, g.n1);
     while (zz < c.ez) {
         const int gy = wrap2(c.oy + yy, g.n2);
-        const int gz = g.ghost ? c.oz + zz - g.z0 + g.zg : wrapi(c.oz + zz, g.n3);
+        const int gz = g.ghost ? c.oz + zz - g.z0 + g.zg : wrap2(c.oz + zz, g.n3);
         const uint32_t gofs = ((uint32_t)gz * g.n2 + gy) * g.n1 + gx;
         T* dst = box + (zz * BY + yy) * BX + ch * VEC;
         DR_ASSERT(zz < BZ && yy < BY && ch * VEC + VEC <= BX && gz >= 0 && gz < g.n3 + g.zg + g.zgh);

@@ -44,14 +44,16 @@ def test_invalid_configs_rejected_without_gpu(L):
     assert L.dr_create(ctypes.byref(c), None, 0, None, ctypes.byref(h)) == dr.DR_ERR_GRID
     c = dr.Config(n=16, beta=0.0).c()
     assert L.dr_create(ctypes.byref(c), None, 0, None, ctypes.byref(h)) == dr.DR_ERR_PARAM
-    # N2 may be any even extent in [6, 510] on one rank (Bluestein x2 passes; the paper's 256 x 300 x 256,
-    # P:L583); N1 / N3 stay powers of two, odd N2 and slabs with such an N2 are rejected
+    # N2 / N3 may be any even extent in [6, 510] on one rank (Bluestein passes; the paper's 256 x 300 x 256,
+    # P:L583); N1 stays a power of two, odd extents and slabs with such an extent are rejected
     assert dr.dr_workspace_bytes(dr.Config(n=(256, 300, 256), nt=4)) > 0
     assert dr.dr_workspace_bytes(dr.Config(n=(16, 6, 16), nt=4)) > 0
+    assert dr.dr_workspace_bytes(dr.Config(n=(16, 12, 300), nt=4)) > 0
     for bad in (dr.Config(n=(16, 301, 16)), dr.Config(n=(16, 512 + 8, 16)),
-                dr.Config(n=(300, 16, 16)), dr.Config(n=(16, 16, 300))):
+                dr.Config(n=(300, 16, 16)), dr.Config(n=(16, 16, 301))):
         assert dr.dr_workspace_bytes(bad) == 0, bad
     assert dr.diffreg.dr_workspace_bytes_dist(dr.Config(n=(16, 300, 16), nt=4), 2) == 0
+    assert dr.diffreg.dr_workspace_bytes_dist(dr.Config(n=(16, 16, 24), nt=4), 2) == 0
     c = dr.Config(n=16).c()
     assert L.dr_create(ctypes.byref(c), None, 0, None, None) == dr.DR_ERR_ARG
     assert L.dr_status_string(dr.DR_ERR_ORDER) == b"DR_ERR_ORDER"
