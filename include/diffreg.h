@@ -22,10 +22,10 @@
  *   scalar field : N3*N2*N1 values, index i1 + N1*(i2 + N2*i3)  (x1 fastest)
  *   vector field : 3 consecutive scalar fields (SoA): component a at offset a*N1*N2*N3
  *   value type   : float, or double when the context was created with DR_FP64.
- * GPU grid restriction (this build): N1 is a power of two in [4, 1024]; N2 and N3 are powers of two
- * in [4, 1024] or, on one rank, any even extent in [6, 510] (the paper's 256 x 300 x 256 grid,
- * P:L583): those lines are transformed by Bluestein's chirp-z form through power-of-two FFTs of
- * length M >= 2 N - 1 (slower: two M-point FFTs per N-point DFT).
+ * GPU grid restriction (this build): every N_a is a power of two in [4, 1024] or, on one rank, N2 and
+ * N3 any even extent in [6, 510] and N1 any multiple of 4 in [12, 1020] (the paper's 256 x 300 x 256
+ * grid): those lines are transformed by Bluestein's chirp-z form through power-of-two FFTs
+ * of length M >= 2 N - 1 (x1: of the half-length complex row; slower: two M-point FFTs per DFT).
  *
  * POINTERS.  Every field pointer of the main path (set_images, set_velocity, forward_solve,
  * adjoint_solve, hessian_matvec, precond_apply) may be a device pointer or a host pointer
@@ -72,8 +72,8 @@ extern "C" {
 typedef enum dr_status {
     DR_OK = 0,
     DR_ERR_ARG = 1,        /* NULL / aliasing / bad enum argument                                */
-    DR_ERR_GRID = 2,       /* N1 not a power of two in [4, 1024]; N2 / N3 neither that nor (one  */
-                           /* rank) even in [6, 510]; slabs: P must divide N2 and N3              */
+    DR_ERR_GRID = 2,       /* N_a neither a power of two in [4, 1024] nor (one rank) N2 / N3 even */
+                           /* in [6, 510], N1 % 4 == 0 in [12, 1020]; slabs: P | N2, P | N3       */
     DR_ERR_PARAM = 3,      /* beta <= 0, nt < 1 or nt > 64, reg not H1/H2                        */
     DR_ERR_ORDER = 4,      /* call sequence violated (see each function)                         */
     DR_ERR_CUDA = 5,       /* CUDA runtime error (message in dr_last_error)                      */

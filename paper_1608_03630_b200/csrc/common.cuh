@@ -53,8 +53,8 @@ struct Grid {
     int ghost;             // 1: slab mode (gathers index x3 through the ghosts, no wrap)
 };
 
-__device__ __forceinline__ int wrapi(int i, int n) { return i & (n - 1); }  // n is a power of two (N1)
-// x2 / x3 may also be even extents that are not powers of two (Bluestein passes, one rank): a remainder then
+__device__ __forceinline__ int wrapi(int i, int n) { return i & (n - 1); }  // n is a power of two
+// extents that are not powers of two (Bluestein passes, one rank): a remainder then
 __device__ __forceinline__ int wrap2(int i, int n) { return (n & (n - 1)) ? ((i % n) + n) % n : (i & (n - 1)); }
 
 // Signed wavenumber of index i on an axis of length n: k in {-n/2+1, ..., n/2}.

@@ -57,6 +57,9 @@ bool pow2_in_range(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
 // x2 extents that are not powers of two (one rank): even, 6 .. 510, transformed by Bluestein's chirp-z
 // form through power-of-two FFTs of length M >= 2 N2 - 1 <= 1024 (fft.cuh ColBlue*)
 bool blue_len(int n) { return n >= 6 && n <= 510 && n % 2 == 0 && (n & (n - 1)) != 0; }
+// x1 (one rank): N1 = 2L with L not a power of two, N1 % 4 == 0 (16-byte box chunks and TMA row strides
+// of the gathers), L <= 510; the half-length complex row transforms run in Bluestein form
+bool blue1_len(int n) { return n >= 12 && n <= 1020 && n % 4 == 0 && ((n / 2) & (n / 2 - 1)) != 0; }
 int blue_m(int n) {
     int m = 1;
     while (m < 2 * n - 1) m <<= 1;
@@ -72,7 +75,8 @@ int ghost_hi(const dr_config* c) { return c->ghost_hi > 0 ? c->ghost_hi : GHOST_
 dr_status validate(const dr_config* c, int nranks = 1) {
     if (!c) return DR_ERR_ARG;
     for (int a = 0; a < 3; ++a)
-        if (!pow2_in_range(c->n[a]) && !(a >= 1 && nranks == 1 && blue_len(c->n[a]))) return DR_ERR_GRID;
+        if (!pow2_in_range(c->n[a]) && !(nranks == 1 && (a >= 1 ? blue_len(c->n[a]) : blue1_len(c->n[a]))))
+            return DR_ERR_GRID;
     if (c->nt < 1 || c->nt > 64) return DR_ERR_PARAM;
     if (c->reg != DR_REG_H1 && c->reg != DR_REG_H2) return DR_ERR_PARAM;
     if (!(c->beta > 0.0) || !std::isfinite(c->beta)) return DR_ERR_PARAM;
@@ -123,7 +127,7 @@ struct Layout {
     int64_t rcap = 0;
     size_t rem = 0;
     size_t kry, sN, bN, sc, rhoT, rhoR, v, vin, dp, dm, m, D, rho, G, lam, lt, rt1, bt, tmp3, stin, stout, specD, specF, xs, xr, plan_p,
-        plan_m, plan_t, maxext, red, pflags, twx, twy, twz, twxd, twyd, twzd, blue, blue3, total;
+        plan_m, plan_t, maxext, red, pflags, twx, twy, twz, twxd, twyd, twzd, blue, blue3, blue1, total;
 };
 
 Layout layout(const dr_config* c, int nranks = 1) {
@@ -192,6 +196,7 @@ Layout layout(const dr_config* c, int nranks = 1) {
     // bhat_fwd[M], bhat_inv[M]
     L.blue = blue_len(g.n2) ? take((size_t)(3 * blue_m(g.n2) + 2 * g.n2) * (8 + 16)) : 0;
     L.blue3 = blue_len(g.n3g) ? take((size_t)(3 * blue_m(g.n3g) + 2 * g.n3g) * (8 + 16)) : 0;  // the same for x3
+    L.blue1 = blue1_len(g.n1) ? take((size_t)(3 * blue_m(g.n1 / 2) + g.n1) * (8 + 16)) : 0;  // x1 rows: L = N1 / 2
     L.total = off;
     return L;
 }
@@ -570,11 +575,15 @@ struct Impl {
     template <typename U>
     BlueTab<U> bluetab() { return bluetab_at<U>(c.L.blue, g.n2); }
     BlueTab<double> bluetab3() { return bluetab_at<double>(c.L.blue3, g.n3g); }
+    template <typename U>
+    BlueTab<U> bluetab1() { return bluetab_at<U>(c.L.blue1, g.n1 / 2); }
+    bool blue1() const { return blue1_len(g.n1); }
     bool blue3() const { return blue_len(g.n3g); }
     bool blue2() const { return blue_len(g.n2); }
     void init_twiddles() {
         if (blue2()) fill_blue(c.L.blue, g.n2);
         if (blue3()) fill_blue(c.L.blue3, g.n3g);
+        if (blue1()) fill_blue(c.L.blue1, g.n1 / 2);
         fill_twiddles<T>(g.n1, c.L.twx);
         fill_twiddles<T>(g.n2, c.L.twy);
         fill_twiddles<T>(g.n3g, c.L.twz);
@@ -755,6 +764,18 @@ struct Impl {
         case 512: call(512); break;                        \
         default: fail(DR_ERR_GRID, "unsupported row length"); \
     }
+// Bluestein convolution lengths M (non-power-of-two extents, one rank)
+#define DR_SWITCH_BLUE(Mval, call)                          \
+    switch (Mval) {                                         \
+        case 16: call(16); break;                           \
+        case 32: call(32); break;                           \
+        case 64: call(64); break;                           \
+        case 128: call(128); break;                         \
+        case 256: call(256); break;                         \
+        case 512: call(512); break;                         \
+        case 1024: call(1024); break;                       \
+        default: fail(DR_ERR_GRID, "unsupported Bluestein length"); \
+    }
 #define DR_SWITCH_COL(Lval, call)                          \
     switch (Lval) {                                        \
         case 4: call(4); break;                            \
@@ -769,18 +790,57 @@ struct Impl {
         default: fail(DR_ERR_GRID, "unsupported column length"); \
     }
 
+    // ---- x1 rows of a non-power-of-two extent (Bluestein, fft.cuh RowBlue*; one rank)
+    template <int M>
+    void blue_row_deriv_M(const T* f, T* out, int acc, int nf, int64_t fs, int64_t os) {
+        using PT = RowBlueDerivPass<T, M>;
+        stream("row_deriv", PT{g, f, out, acc, twxd(), bluetab1<double>(), fs, os}, row_tiles<PT::RB>(), nf);
+    }
+    void blue_row_deriv(const T* f, T* out, int acc, int nf = 1, int64_t fs = 0, int64_t os = 0) {
+#define CALL(MM) blue_row_deriv_M<MM>(f, out, acc, nf, fs, os)
+        DR_SWITCH_BLUE(blue_m(g.n1 / 2), CALL)
+#undef CALL
+    }
+    template <typename Tc, int M>
+    void blue_row_r2c_M(const T* f, Cx<Tc>* sp, int nc, int64_t csf, int64_t css) {
+        using PT = RowBlueR2cPass<T, Tc, M>;
+        stream(sizeof(Tc) == 8 ? "row_r2c_f64" : "row_r2c_f32", PT{g, f, sp, twx_t<Tc>(), bluetab1<Tc>(), csf, css},
+               row_tiles<PT::RB>(), nc);
+    }
+    template <int M>
+    void blue_row_c2r_M(const Cx<T>* sp, T* out, const T* add, int nc, int64_t csf, int64_t css) {
+        using PT = RowBlueC2rPass<T, M>;
+        stream(add ? "row_c2r_add" : "row_c2r", PT{g, sp, RowOut<T>{out, add}, twx(), bluetab1<T>(), csf, css},
+               row_tiles<PT::RB>(), nc);
+    }
     void row_deriv(const T* f, T* out, int acc) {
+        if (blue1()) {
+            blue_row_deriv(f, out, acc);
+            return;
+        }
 #define CALL(LL) row_deriv_L<LL>(f, out, acc)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
     }
     template <typename Tc>
     void row_r2c(const T* f, Cx<Tc>* sp, int nc = 1, int64_t csf = 0, int64_t css = 0) {
+        if (blue1()) {
+#define CALL(MM) blue_row_r2c_M<Tc, MM>(f, sp, nc, csf, css)
+            DR_SWITCH_BLUE(blue_m(g.n1 / 2), CALL)
+#undef CALL
+            return;
+        }
 #define CALL(LL) row_r2c_L<LL, Tc>(f, sp, nc, csf, css)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
     }
     void row_c2r(const Cx<T>* sp, T* out, const T* add, int nc = 1, int64_t csf = 0, int64_t css = 0) {
+        if (blue1()) {
+#define CALL(MM) blue_row_c2r_M<MM>(sp, out, add, nc, csf, css)
+            DR_SWITCH_BLUE(blue_m(g.n1 / 2), CALL)
+#undef CALL
+            return;
+        }
 #define CALL(LL) row_c2r_L<LL>(sp, out, add, nc, csf, css)
         DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
@@ -797,17 +857,6 @@ struct Impl {
     ColGeom pair_geom_t() const { return ColGeom{g.n1 / 2, g.n1 / 2, nb(), g.n3g, c.rank * nb(), g.n2}; }
 
     // ---- x2 passes of a non-power-of-two extent (Bluestein, fft.cuh ColBlue*; one rank)
-#define DR_SWITCH_BLUE(Mval, call)                          \
-    switch (Mval) {                                         \
-        case 16: call(16); break;                           \
-        case 32: call(32); break;                           \
-        case 64: call(64); break;                           \
-        case 128: call(128); break;                         \
-        case 256: call(256); break;                         \
-        case 512: call(512); break;                         \
-        case 1024: call(1024); break;                       \
-        default: fail(DR_ERR_GRID, "unsupported x2 length"); \
-    }
     template <typename U, int M, int DIR>
     void blue_fft_M(const Cx<U>* src, Cx<U>* dst, int nc, int64_t cs, int64_t csd) {
         using PT = ColBlueFftPass<U, M, DIR>;
@@ -1094,9 +1143,13 @@ struct Impl {
             for (int i = 0; i < nf; ++i) grad(f + i * fs, vec(out + i * os, (size_t)g.M));
             return;
         }
+        if (blue1()) {
+            blue_row_deriv(f, out, 0, nf, fs, os);
+        } else {
 #define CALL(LL) row_deriv_L<LL>(f, out, 0, nf, fs, os)
-        DR_SWITCH_ROW(g.n1 / 2, CALL)
+            DR_SWITCH_ROW(g.n1 / 2, CALL)
 #undef CALL
+        }
         if (blue2()) {
             blue_deriv(f, out + g.M, 0, nf, fs, os);
         } else {

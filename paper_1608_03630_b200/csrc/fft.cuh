@@ -972,6 +972,139 @@ struct ColBlueFftPass {
     }
 };
 
+// x1 rows of an extent N1 = 2L that is not a power of two (one rank, N1 % 4 == 0): the half-length
+// complex transform of the packed row (z_n = x_2n + i x_2n+1, r2c_pair / c2r_pair as the radix passes)
+// runs in Bluestein form with M >= 2L - 1.  RB rows per CTA, one M-point work line and one L-point line
+// each; every row is processed by TPL = Tpl<M, Tc> threads.
+template <int M, typename Tc>
+struct RowBlueCfg {
+    static constexpr int TPL = Tpl<M, Tc>::V;
+    static constexpr int RB = (128 / TPL) > 0 ? 128 / TPL : 1;
+    static constexpr int NT = RB * TPL;
+    static constexpr int LW = PadLP<M, 1, 0>::V;          // work line
+    static constexpr int LZ = M / 2 + M / 32 + 2;           // L <= M / 2 points, padded by P()
+    static constexpr size_t SMEM = (size_t)RB * (LW + LZ) * sizeof(Cx<Tc>);
+};
+template <typename Ti, typename Tc>
+struct RowStC {  // a RowSt in the I/O type fed in the compute type
+    RowSt<Ti> r;
+    __device__ __forceinline__ void st(int i, const Cx<Tc>& v) const { r.st(i, cx<Ti>((Ti)v.re, (Ti)v.im)); }
+};
+// r2c: real rows (Ti) -> half spectra (Tc), row stride g.n1p
+template <typename Ti, typename Tc, int M>
+struct RowBlueR2cPass {
+    using RC = RowBlueCfg<M, Tc>;
+    static constexpr int TPL = RC::TPL, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = 1;
+    static constexpr size_t BUF = RC::SMEM;
+    Grid g;
+    const Ti* f;
+    Cx<Tc>* spec;
+    const Cx<Tc>* twN;  // e^{-2 pi i m / N1}
+    BlueTab<Tc> bt;     // length L = N1 / 2
+    int64_t csf = 0, css = 0;
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        const int L = bt.n;
+        const int64_t nrows = (int64_t)g.n2 * g.n3;
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows;
+        if (!ok) row = nrows - 1;
+        Cx<Tc>* work = reinterpret_cast<Cx<Tc>*>(smem) + line * RC::LW;
+        Cx<Tc>* z = reinterpret_cast<Cx<Tc>*>(smem) + RB * RC::LW + line * RC::LZ;
+        const Cx<Ti>* src = reinterpret_cast<const Cx<Ti>*>(f + blockIdx.y * csf) + row * L;
+        blue_line<Tc, M, 0>(work, t, bt, RowLd<Ti, Tc>{src}, SmemLine<Tc>{z});
+        __syncthreads();
+        if (!ok) return;
+        Cx<Tc>* out = spec + blockIdx.y * css + row * g.n1p;
+        for (int k = t; k <= L / 2; k += TPL) {
+            Cx<Tc> Xk, Xl;
+            r2c_pair(z[P(k)], z[P(k == 0 ? 0 : L - k)], twN[k], Xk, Xl);
+            out[k] = Xk;
+            out[L - k] = Xl;
+        }
+    }
+};
+// c2r: half spectra -> real rows (+ add), in T
+template <typename T, int M>
+struct RowBlueC2rPass {
+    using RC = RowBlueCfg<M, T>;
+    static constexpr int TPL = RC::TPL, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = 1;
+    static constexpr size_t BUF = RC::SMEM;
+    Grid g;
+    const Cx<T>* spec;
+    RowOut<T> epi;
+    const Cx<T>* twN;
+    BlueTab<T> bt;
+    int64_t csf = 0, css = 0;
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        const int L = bt.n;
+        const int64_t nrows = (int64_t)g.n2 * g.n3;
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows;
+        if (!ok) row = nrows - 1;
+        Cx<T>* work = reinterpret_cast<Cx<T>*>(smem) + line * RC::LW;
+        Cx<T>* z = reinterpret_cast<Cx<T>*>(smem) + RB * RC::LW + line * RC::LZ;
+        const Cx<T>* in = spec + blockIdx.y * css + row * g.n1p;
+        for (int k = t; k <= L / 2; k += TPL) {
+            Cx<T> Zk, Zl;
+            c2r_pair(in[k], in[L - k], twN[k], Zk, Zl);
+            z[P(k)] = Zk;
+            if (k != 0 && 2 * k != L) z[P(L - k)] = Zl;
+        }
+        __syncthreads();
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(epi.out + blockIdx.y * csf) + row * L;
+        const Cx<T>* add = epi.add ? reinterpret_cast<const Cx<T>*>(epi.add + blockIdx.y * csf) + row * L : nullptr;
+        blue_line<T, M, 1>(work, t, bt, SmemLine<T>{z}, RowSt<T>{dst, add, 0, ok});
+    }
+};
+// x1 derivative (RowDerivPass with Bluestein transforms, fp64 arithmetic: the odd symbol lifts an fp32
+// convolution's rounding floor), out = acc * out + d f / dx1; nf fields per launch (blockIdx.y)
+template <typename T, int M>
+struct RowBlueDerivPass {
+    using RC = RowBlueCfg<M, double>;
+    static constexpr int TPL = RC::TPL, RB = RC::RB, NT = RC::NT;
+    static constexpr int MINB = 1;
+    static constexpr size_t BUF = RC::SMEM;
+    Grid g;
+    const T* f;
+    T* out;
+    int accumulate;
+    const Cx<double>* twN;
+    BlueTab<double> bt;
+    int64_t cs = 0, cso = 0;
+    __device__ __forceinline__ void run(int tile, unsigned char* smem) const {
+        const int L = bt.n;
+        const int64_t nrows = (int64_t)g.n2 * g.n3;
+        const int line = threadIdx.x / TPL, t = threadIdx.x % TPL;
+        int64_t row = (int64_t)tile * RB + line;
+        const bool ok = row < nrows;
+        if (!ok) row = nrows - 1;
+        Cx<double>* work = reinterpret_cast<Cx<double>*>(smem) + line * RC::LW;
+        Cx<double>* z = reinterpret_cast<Cx<double>*>(smem) + RB * RC::LW + line * RC::LZ;
+        const Cx<T>* src = reinterpret_cast<const Cx<T>*>(f + blockIdx.y * cs) + row * L;
+        blue_line<double, M, 0>(work, t, bt, RowLd<T, double>{src}, SmemLine<double>{z});
+        __syncthreads();
+        for (int k = t; k <= L / 2; k += TPL) {  // RowDerivPass's pair arithmetic
+            const int l = (k == 0) ? 0 : L - k;
+            Cx<double> Xk, Xl;
+            r2c_pair(z[P(k)], z[P(l)], twN[k], Xk, Xl);
+            Xk = mul_i(Xk, double(k) / double(L));
+            Xl = (k == 0) ? cx(0.0, 0.0) : mul_i(Xl, double(L - k) / double(L));
+            if (k == L / 2 && L > 1 && 2 * k == L) Xl = Xk;
+            Cx<double> Zk, Zl;
+            c2r_pair(Xk, (k == 0) ? cx(0.0, 0.0) : Xl, twN[k], Zk, Zl);
+            z[P(k)] = Zk;
+            if (k != 0 && 2 * k != L) z[P(L - k)] = Zl;
+        }
+        __syncthreads();
+        Cx<T>* dst = reinterpret_cast<Cx<T>*>(out + blockIdx.y * cso) + row * L;
+        blue_line<double, M, 1>(work, t, bt, SmemLine<double>{z}, RowStC<T, double>{RowSt<T>{dst, nullptr, accumulate, ok}});
+    }
+};
+
 // x2 derivative of a real field viewed as complex pairs (ColDerivPass with Bluestein transforms):
 // out (+)= F2^-1[i k2' / N F2 f]; nf fields per launch (blockIdx.y)
 template <typename Ti, int M, int AX = 2>

@@ -91,7 +91,7 @@ __device__ __forceinline__ T interp_global(const T* __restrict__ f, const Grid& 
             const T* r = f + ((int64_t)j3 * g.n2 + j2) * g.n1;
             T row = T(0);
 #pragma unroll
-            for (int a = 0; a < 4; ++a) row += w1[a] * __ldg(r + wrapi(q1 + a - 1, g.n1));
+            for (int a = 0; a < 4; ++a) row += w1[a] * __ldg(r + wrap2(q1 + a - 1, g.n1));
             accb += w2[bb] * row;
         }
         acc += w3[c] * accb;
@@ -500,7 +500,7 @@ __device__ __forceinline__ void stage_box(const Grid& g, const Src<T, NC>& src, 
     if (ch >= nch || r0 >= RSTEP) return;
     int yy = r0, zz = 0;
     while (yy >= c.ey) { yy -= c.ey; ++zz; }
-    const int gx = wrapi(c.ox + ch * VEC, g.n1);
+    const int gx = wrap2(c.ox + ch * VEC, g.n1);  // N1 % VEC == 0: a chunk never straddles the wrap
     while (zz < c.ez) {
         const int gy = wrap2(c.oy + yy, g.n2);
         const int gz = g.ghost ? c.oz + zz - g.z0 + g.zg : wrap2(c.oz + zz, g.n3);

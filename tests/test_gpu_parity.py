@@ -130,19 +130,21 @@ def test_matvec_long_lines(dr, n, iso, fp64):
     check_matvec(dr, ctx, prob, v64, vt, vt64, fp64, iso)
 
 
-# x2 / x3 extents that are not powers of two (one rank; Bluestein passes, M = 16 .. 1024): the paper's own
+# extents that are not powers of two (one rank; Bluestein passes, M = 16 .. 1024): the paper's own
 # grid is 256 x 300 x 256; SURVEY §8(b) admits any even N >= 4
 BLUE_GRIDS = [(8, 6, 8), (16, 12, 8), (32, 24, 16), (16, 300, 16), (32, 510, 8),
               # x3 (Bluestein middle passes and x3 derivatives), and both axes at once
-              (8, 8, 6), (16, 8, 12), (16, 16, 24), (8, 16, 300), (16, 12, 20)]
+              (8, 8, 6), (16, 8, 12), (16, 16, 24), (8, 16, 300), (16, 12, 20),
+              # x1 (Bluestein half-length row transforms, N1 % 4 == 0), and all three axes
+              (12, 8, 8), (20, 16, 8), (300, 8, 16), (12, 12, 20)]
 
 
 @pytest.mark.parametrize("fp64", [False, True])
 @pytest.mark.parametrize("n", BLUE_GRIDS, ids=["x".join(map(str, g)) for g in BLUE_GRIDS])
 def test_spectral_ops_non_pow2_x2(dr, n, fp64):
     """grad, div, beta A (H1, H2), (beta A)^-1 (isochoric and not) and the Leray projection on grids whose
-    N2 and / or N3 is not a power of two, against the oracle (whose non-power-of-two lines are plain DFT
-    sums)."""
+    N1, N2 and / or N3 is not a power of two, against the oracle (whose non-power-of-two lines are plain
+    DFT sums)."""
     tol = tols(fp64)[0]
     kc = max(1, min(n) // 3)
     f, f64 = prep(synth.blobs(5, n, kcut=kc), fp64)
@@ -165,7 +167,7 @@ def test_spectral_ops_non_pow2_x2(dr, n, fp64):
 @pytest.mark.parametrize("iso", [False, True])
 @pytest.mark.parametrize("n", BLUE_GRIDS[1:4] + BLUE_GRIDS[6:], ids=["x".join(map(str, g)) for g in BLUE_GRIDS[1:4] + BLUE_GRIDS[6:]])
 def test_matvec_non_pow2_x2(dr, n, iso, fp64):
-    """Setup, forward solve and one GN matvec per mode with a non-power-of-two N2 and / or N3 (ragged
+    """Setup, forward solve and one GN matvec per mode with non-power-of-two extents (ragged
     gather tiles, periodic wrap by remainder, Bluestein x2 / x3 passes in the gradients, the tail, the
     data term and the preconditioner)."""
     kc = max(1, min(n) // 3)
