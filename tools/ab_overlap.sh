@@ -1,5 +1,7 @@
 #!/bin/bash
 # A/B of the spectral-overlap experiment (DR_OVERLAP 1/2, DR_GATHER_PAD) on one box: tools/ab_overlap.sh TAG
+# (the DR_OVERLAP=2 and DR_GATHER_PAD knobs were experiment builds, removed after the measurement in
+# profiles/ab_overlap_r2s.txt; DR_OVERLAP=1 remains)
 set -u
 TAG=$1
 cd ${GRAFT_REPO_ROOT:-.}
