@@ -57,5 +57,33 @@ def main(n=256, nwarps=20000, seed=0):
         print(f"{name:20s} mean wavefronts/LDS {degs.mean():.3f}  (P(deg>1) = {(degs > 1).mean():.3f})")
 
 
+
+
+def rotated(n=256, nwarps=20000, seed=0):
+    """Per-lane tap rotation: at the a-th x1 load of each stencil row, a lane reads tap (a - s) mod 4,
+    s = floor(-d1) mod 4 (a per-point rule, so every path could sum in the same order).  Lanes whose x1
+    floors differ by one then read the same column offset from their own x in 3 of the 4 loads instead
+    of none, so the end-lane collision of a 33-column warp span hits one load in four."""
+    v = synth.smooth_vec(3, n, kmax=8, cells_per_step=2.0, nt=4).double().numpy()
+    d = v * (1.0 / 4) / (2 * np.pi / n)
+    rng = np.random.default_rng(seed)
+    ys, zs = rng.integers(0, n, nwarps), rng.integers(0, n, nwarps)
+    x0 = rng.integers(0, n // 32, nwarps) * 32
+    X = (x0[:, None] + np.arange(32)[None, :]) % n
+    Y, Z = np.broadcast_to(ys[:, None], X.shape), np.broadcast_to(zs[:, None], X.shape)
+    f = [np.floor(-d[a][Z, Y, X]).astype(np.int64) for a in range(3)]
+    q1, q2, q3 = X + f[0], Y + f[1], Z + f[2]
+    s = np.mod(f[0], 4)
+    for name, rot in (("natural order", np.zeros_like(s)), ("rotated by floor mod 4", s)):
+        degs = []
+        for c in range(4):
+            for b in range(4):
+                for a in range(4):
+                    tap = np.mod(a - rot, 4)
+                    degs.append(degree((q3 + c) * 64 * 15 + (q2 + b) * 64 + (q1 + tap) + 10 ** 6))
+        degs = np.stack(degs)
+        print(f"{name:24s} mean wavefronts/LDS {degs.mean():.3f}  (P(deg>1) = {(degs > 1).mean():.3f})")
+
+
 if __name__ == "__main__":
-    main()
+    rotated() if "--rotated" in sys.argv else main()
