@@ -74,7 +74,10 @@ def rotated(n=256, nwarps=20000, seed=0):
     f = [np.floor(-d[a][Z, Y, X]).astype(np.int64) for a in range(3)]
     q1, q2, q3 = X + f[0], Y + f[1], Z + f[2]
     s = np.mod(f[0], 4)
-    for name, rot in (("natural order", np.zeros_like(s)), ("rotated by floor mod 4", s)):
+    # "by node column mod 4": at load a read the tap whose box column is congruent to a (mod 4) — a rule
+    # of the stencil's lowest node q1 alone, so the box, global-memory and owner-side paths can all use it.
+    for name, rot in (("natural order", np.zeros_like(s)), ("rotated by floor mod 4", s),
+                      ("by node column mod 4", np.mod(q1, 4))):
         degs = []
         for c in range(4):
             for b in range(4):
