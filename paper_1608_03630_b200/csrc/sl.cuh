@@ -454,6 +454,38 @@ __device__ __forceinline__ float2 interp_box2(const float* __restrict__ bA, cons
     return acc;
 }
 
+#ifdef DR_TAPROT
+// A/B experiment only (tools/bank_sim.py --rotated; never the product build): each lane reads the four
+// x1 taps of a stencil row rotated by floor(-d1) mod 4, so lanes whose x1 floors differ by one read
+// the same column offset from their own x in 3 of the 4 loads.  Sums in the rotated order.
+__device__ __forceinline__ float pick4(const float2 w[4], int i, bool y) {
+    const float v0 = y ? w[0].y : w[0].x, v1 = y ? w[1].y : w[1].x, v2 = y ? w[2].y : w[2].x,
+                v3 = y ? w[3].y : w[3].x;
+    const float lo = (i & 1) ? v1 : v0, hi = (i & 1) ? v3 : v2;
+    return (i & 2) ? hi : lo;
+}
+template <int BX, int BY>
+__device__ __forceinline__ float2 interp_box2_rot(const float* const pA[4], const float* const pB[4],
+                                                  const float2 w1[4], const float2 w2[4], const float2 w3[4]) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        float2 accb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            const int o = (c * BY + bb) * BX;
+            float2 row = __fmul2_rn(w1[0], make_float2(pA[0][o], pB[0][o]));
+            row = __ffma2_rn(w1[1], make_float2(pA[1][o], pB[1][o]), row);
+            row = __ffma2_rn(w1[2], make_float2(pA[2][o], pB[2][o]), row);
+            row = __ffma2_rn(w1[3], make_float2(pA[3][o], pB[3][o]), row);
+            accb = (bb == 0) ? __fmul2_rn(w2[0], row) : __ffma2_rn(w2[bb], row, accb);
+        }
+        acc = (c == 0) ? __fmul2_rn(w3[0], accb) : __ffma2_rn(w3[c], accb, acc);
+    }
+    return acc;
+}
+#endif
+
 // Tile context: origin of the tile and the planned box (x origin aligned down to VEC = 16 B /
 // sizeof(T) so rows stage as 16-byte cp.async chunks; N1 is a multiple of VEC, so a chunk never
 // straddles the periodic wrap).
@@ -563,12 +595,34 @@ __device__ __forceinline__ void pair_from_box(const Grid& g, const TileCtx<T, NC
         float2 w[3][4];
 #pragma unroll
         for (int a = 0; a < 3; ++a) lagrange4x2(make_float2(tA[a], tB[a]), w[a]);
+#ifdef DR_TAPROT
+        const int sA = (qA[0] - x) & 3, sB = (qB[0] - x) & 3;
+        const float* pA[4];
+        const float* pB[4];
+        float2 w1r[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int oA = (a - sA) & 3, oB = (a - sB) & 3;
+            pA[a] = bA + oA;
+            pB[a] = bB + oB;
+            w1r[a] = make_float2(pick4(w[0], oA, false), pick4(w[0], oB, true));
+        }
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+            const float* qa[4] = {pA[0] + cc * SC, pA[1] + cc * SC, pA[2] + cc * SC, pA[3] + cc * SC};
+            const float* qb[4] = {pB[0] + cc * SC, pB[1] + cc * SC, pB[2] + cc * SC, pB[3] + cc * SC};
+            const float2 r = interp_box2_rot<BX, BY>(qa, qb, w1r, w[1], w[2]);
+            vA[cc] = r.x;
+            vB[cc] = r.y;
+        }
+#else
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) {
             const float2 r = interp_box2<BX, BY>(bA + cc * SC, bB + cc * SC, w[0], w[1], w[2]);
             vA[cc] = r.x;
             vB[cc] = r.y;
         }
+#endif
     } else {
         T w1[4], w2[4], w3[4];
         lagrange4(tA[0], w1);
